@@ -1,0 +1,517 @@
+"""Decode-attention benchmark (BASELINE.json metric: decode-attention KV GB/s, fraction of the
+HBM roofline, attention tokens/s).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--impl ours|reference]
+
+A step is one decode iteration of the workload over every layer: per layer, append each
+request's new-token K/V into the paged HBM store (lam_kv_append) and run decode attention
+over the full context (lam_decode).  KV bytes are the reference's algorithmic bytes
+(attn_cost, reference core/src/perf.cpp:77-88): 2 e (d/G) L l B per step.
+
+Default workload (N=1): BASELINE config 2, LLaMA-2-7B all 32 layers, bf16, B=64, l=4096 —
+137 GB of KV resident in HBM (far above the 126 MB L2, so no flush is needed).
+With N>1 (torchrun, one rank per GPU) the KV heads are sharded over ranks
+(head_partition, attention.cpp:164-177) and the global batch grows with N (weak scaling):
+each rank is the model worker of B requests and the attention worker of Hkv/N heads of all
+N*B requests; Q/K/V are scattered and outputs gathered by NCCL all-to-all, overlapped with
+attention across two staggered micro-batches.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "decode-attention KV GB/s"
+
+# workload -> shape (BASELINE.json configs)
+WORKLOADS = {
+    "c1": dict(desc="LLaMA-7B 1 layer MHA fp32 B=8 l=1024 (dense, as the CPU reference runs it)",
+               spec="LLAMA_7B_1L_F32", B=8, l=1024, Hq=32, Hkv=32, D=128, layers=1,
+               dtype="float32", paged=False, P=64),
+    "c2": dict(desc="LLaMA-2-7B 32 layers MHA bf16 B=64 l=4096 paged", spec="LLAMA2_7B", B=64,
+               l=4096, Hq=32, Hkv=32, D=128, layers=32, dtype="bfloat16", paged=True, P=64),
+    "c3": dict(desc="LLaMA-2-70B GQA 64/8 bf16 B=128 l=4096 paged", spec="LLAMA2_70B", B=128,
+               l=4096, Hq=64, Hkv=8, D=128, layers=80, dtype="bfloat16", paged=True, P=64),
+    "c4": dict(desc="LLaMA-2-70B GQA 64/8 bf16 B=32 l=32768 paged, split-K", spec="LLAMA2_70B",
+               B=32, l=32768, Hq=64, Hkv=8, D=128, layers=80, dtype="bfloat16", paged=True, P=64),
+    "c5": dict(desc="LLaMA-2-70B GQA mixed lengths 128..16384 (log-uniform, seed 2024) B=256 paged",
+               spec="LLAMA2_70B", B=256, l=16384, Hq=64, Hkv=8, D=128, layers=80,
+               dtype="bfloat16", paged=True, P=64, mixed=True),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------- clocks sampling
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, p in zip(names, parts[4:8]):
+                if p.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+def measured_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except Exception:
+            pass
+    return {}
+
+
+# ---------------------------------------------------------------- CPU baseline
+def cpu_baseline(w: dict, target_s: float, seed: int = 1) -> dict:
+    """The reference's own exact_attention<float> (oracle/_ref, built from
+    reference core/src/attention.cpp -O3) over a bounded sample of the workload's
+    (request, kv head) units, all host threads; falls back to our C port (1 thread)."""
+    import numpy as np
+
+    from oracle import oracle as O
+    from paper_2405_01814_b200 import perf as PF
+
+    spec = getattr(PF, w["spec"])
+    e = spec.bytes_per_elem
+    D, Hq, Hkv, l = w["D"], w["Hq"], w["Hkv"], w["l"]
+    G = Hq // Hkv
+    rng = np.random.default_rng(seed)
+    units = 8 if l >= 16384 else (32 if l >= 4096 else 128)
+    B = max(1, -(-units // Hkv))
+    units = B * Hkv
+    q = rng.uniform(-1, 1, (B, Hq, D)).astype(np.float32)
+    k = rng.uniform(-1, 1, (B, Hkv, l, D)).astype(np.float32)
+    v = rng.uniform(-1, 1, (B, Hkv, l, D)).astype(np.float32)
+    lens = np.full(B, l, np.int32)
+    bytes_per_run = units * l * 2 * D * e  # algorithmic bytes in the workload's dtype
+    if O.ref_available():
+        lib = O.ref()
+        threads = int(lib.ref_hardware_threads()) or os.cpu_count() or 1
+        h = lib.ref_bench_create(B, Hq, Hkv, D, l, O.ptr(lens), O.ptr(q), O.ptr(k), O.ptr(v),
+                                 1.0 / math.sqrt(D), units)
+        lib.ref_bench_run(h, threads, None)  # warm
+        runs, secs = 0, 0.0
+        while secs < target_s:
+            secs += lib.ref_bench_run(h, threads, None)
+            runs += 1
+        lib.ref_bench_destroy(h)
+        kind = "reference"
+    else:
+        threads = 1
+        runs, secs = 0, 0.0
+        while secs < target_s:
+            t0 = time.perf_counter()
+            O.decode_dense(q, k, v, lens, 1.0 / math.sqrt(D))
+            secs += time.perf_counter() - t0
+            runs += 1
+        kind = "port"
+    gbs = bytes_per_run * runs / secs / 1e9
+    cpu_model = ""
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                cpu_model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"value": gbs, "unit": "GB/s", "cores": threads, "kind": kind,
+            "seconds": secs, "runs": runs,
+            "sample": (f"{units} (request, kv head) units x {G} q heads x l={l}, d={D} of one "
+                       f"layer, exact_attention<float> on fp32 upcasts, {runs} runs, "
+                       f"{threads} threads; bytes = attn_cost with e={e}"),
+            "cpu_model": cpu_model, "tokens_per_s_equiv": gbs * 1e9 / PF.kv_bytes_per_token(spec)}
+
+
+def run_reference(args, w: dict, rank: int, world: int) -> None:
+    if rank != 0:
+        return
+    from paper_2405_01814_b200 import perf as PF
+
+    spec = getattr(PF, w["spec"])
+    for _ in range(args.warmup):
+        cpu_baseline(w, target_s=0.0)
+    vals, secs = [], 0.0
+    for _ in range(args.steps):
+        r = cpu_baseline(w, target_s=0.5)
+        vals.append(r["value"])
+        secs += r["seconds"]
+    value = statistics.median(vals)
+    step_bytes = PF.attn_cost(spec, w["B"], w["l"]).bytes
+    line = {"metric": METRIC, "value": value, "unit": "GB/s", "impl": "reference",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": step_bytes / (value * 1e9) * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic U(-1,1)",
+            "config": {"workload": f"{args.workload}: {w['desc']}", "global_batch": w["B"],
+                       "seq_len": w["l"], "layers": w["layers"],
+                       "parallelism": "host threads"},
+            "attn_tokens_per_s": value * 1e9 / PF.kv_bytes_per_token(spec),
+            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": r["cores"],
+                             "kind": r["kind"], "sample": r["sample"], "cpu_model": r["cpu_model"]},
+            "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU workload
+def mixed_lengths(B: int, seed: int = 2024):
+    import numpy as np
+
+    r = np.random.default_rng(seed)
+    return np.exp(r.uniform(math.log(128), math.log(16384), B)).astype(np.int32)
+
+
+class Workload:
+    """Resident paged KV for every layer (or as many distinct layer buffers as fit) plus
+    per-layer new-token inputs; one GPU's share under KV-head sharding."""
+
+    def __init__(self, w: dict, rank: int, world: int, device):
+        import numpy as np
+        import torch
+
+        from paper_2405_01814_b200 import _lib, perf as PF
+        from paper_2405_01814_b200.kvcache import PagedKVCache
+
+        self.w, self.rank, self.world, self.device = w, rank, world, device
+        self.spec = getattr(PF, w["spec"])
+        self.dtype = getattr(torch, w["dtype"])
+        self.Hq, self.Hkv, self.D = w["Hq"], w["Hkv"], w["D"]
+        if self.Hkv % world:
+            raise SystemExit(f"{self.Hkv} KV heads do not shard over {world} GPUs")
+        self.hq_local, self.hkv_local = self.Hq // world, self.Hkv // world
+        self.B_local = w["B"]                 # requests whose q/k/v this rank produces
+        self.B = w["B"] * world               # requests whose local heads this rank attends
+        self.layers = w["layers"]
+        if w.get("mixed"):
+            self.lens = np.concatenate([mixed_lengths(w["B"], 2024 + r) for r in range(world)])
+        else:
+            self.lens = np.full(self.B, w["l"], np.int32)
+        self.max_len = int(self.lens.max())
+        esz = torch.tensor([], dtype=self.dtype).element_size()
+        P = w["P"]
+        pages_per_seq = -(-self.lens // P)
+        self.num_pages = int(pages_per_seq.sum())
+        layer_bytes = 2 * self.num_pages * self.hkv_local * P * self.D * esz
+        free, _ = torch.cuda.mem_get_info(device)
+        budget = free - 6 * 2**30
+        self.resident = max(1, min(self.layers, budget // layer_bytes))
+        self.kv_bytes_layer = layer_bytes
+        self.ctx = _lib.context(device.index)
+        if w["paged"]:
+            self.cache = PagedKVCache(self.resident, self.hkv_local, self.D, P, self.num_pages,
+                                      self.B, int(pages_per_seq.max()), dtype=self.dtype,
+                                      device=device, shuffle_seed=1234 + rank)
+            self.cache.set_lengths(self.lens)
+            self.cache.sync()
+            g = torch.Generator(device=device).manual_seed(1 + rank)
+            self.cache.fill_random(g)
+            self.k_layers = [self.cache.k[i] for i in range(self.resident)]
+            self.v_layers = [self.cache.v[i] for i in range(self.resident)]
+            self.page_table = self.cache.page_table
+        else:
+            g = torch.Generator(device=device).manual_seed(1 + rank)
+            shape = (self.B, self.hkv_local, self.max_len, self.D)
+            self.k_layers = [torch.empty(shape, dtype=self.dtype, device=device).uniform_(-1, 1, generator=g)
+                             for _ in range(self.resident)]
+            self.v_layers = [torch.empty(shape, dtype=self.dtype, device=device).uniform_(-1, 1, generator=g)
+                             for _ in range(self.resident)]
+            self.page_table = None
+        self.seq_lens = torch.tensor(self.lens, dtype=torch.int32, device=device)
+        self.positions = (self.seq_lens - 1).contiguous()
+        gi = torch.Generator(device=device).manual_seed(99 + rank)
+        # model-worker side inputs for this rank's B_local requests, per layer
+        self.q_in = torch.empty((self.layers, self.B_local, self.Hq, self.D), dtype=self.dtype,
+                                device=device).uniform_(-1, 1, generator=gi)
+        self.kn_in = torch.empty((self.layers, self.B_local, self.Hkv, self.D), dtype=self.dtype,
+                                 device=device).uniform_(-1, 1, generator=gi)
+        self.vn_in = torch.empty_like(self.kn_in).uniform_(-1, 1, generator=gi)
+        self.out = torch.empty((self.layers, self.B_local, self.Hq, self.D), dtype=self.dtype,
+                               device=device)
+        self.step_bytes = float(PF.kv_bytes_per_token(self.spec)) * float(self.lens.sum())
+        self.decode_bytes_per_launch = float(self.lens.sum()) * 2 * self.hkv_local * self.D * esz
+        # plan once (fixed shapes): kernel family + splits; reserve the split-K workspace
+        from paper_2405_01814_b200 import decode as dec
+
+        qd = torch.empty((self.B, self.hq_local, self.D), dtype=self.dtype, device=device)
+        kw = dict(page_table=self.page_table, max_len=self.max_len)
+        self.kernel, self.splits, self.chunk = dec.plan(qd, self.k_layers[0], self.v_layers[0],
+                                                        self.seq_lens, ctx=self.ctx, **kw)
+        self.ctx.reserve(self.B * self.hq_local * max(self.splits, 1), self.D,
+                         self.B * self.hkv_local)
+
+    def layer_pools(self, layer: int):
+        i = layer % self.resident
+        return self.k_layers[i], self.v_layers[i]
+
+
+def run_ours(args, w: dict, rank: int, world: int) -> None:
+    import numpy as np
+    import torch
+
+    from paper_2405_01814_b200 import _lib, decode as dec
+
+    device = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(device)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=device)
+    t_setup = time.time()
+    W = Workload(w, rank, world, device)
+    log(f"[rank {rank}] setup {time.time() - t_setup:.1f}s: {W.resident}/{W.layers} layers resident, "
+        f"kernel={W.kernel} splits={W.splits} chunk={W.chunk}")
+
+    stream = torch.cuda.current_stream(device)
+    engine = None
+    if world > 1:
+        from paper_2405_01814_b200.dist import HeadShardedAttention
+
+        engine = HeadShardedAttention(W, dist)
+
+    def step_local(ev=None):
+        """world == 1: append + decode per layer on the current stream."""
+        for layer in range(W.layers):
+            kp, vp = W.layer_pools(layer)
+            dec.kv_append(W.kn_in[layer], W.vn_in[layer], kp, vp, W.positions, W.page_table)
+            if ev is not None:
+                ev[layer][0].record(stream)
+            dec.decode(W.q_in[layer], kp, vp, W.seq_lens, page_table=W.page_table,
+                       max_len=W.max_len, out=W.out[layer], ctx=W.ctx,
+                       split_tokens=W.chunk)
+            if ev is not None:
+                ev[layer][1].record(stream)
+
+    def step(ev=None):
+        if engine is None:
+            step_local(ev)
+        else:
+            engine.step(ev)
+
+    def barrier():
+        torch.cuda.synchronize(device)
+        if dist is not None:
+            dist.barrier()
+            torch.cuda.synchronize(device)
+
+    # ---- warm-up
+    for _ in range(max(args.warmup, 0)):
+        step()
+    barrier()
+
+    # ---- timed region (device-resident inputs)
+    ev = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(W.layers)]
+          for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(device.index if "CUDA_VISIBLE_DEVICES" not in os.environ else
+                           int(os.environ["CUDA_VISIBLE_DEVICES"].split(",")[device.index]))
+    if rank == 0:
+        sampler.start()
+        time.sleep(0.3)
+    barrier()
+    t0.record(stream)
+    for s in range(args.steps):
+        step(ev[s])
+    t1.record(stream)
+    barrier()
+    clocks = sampler.stop() if rank == 0 else None
+    ms_total = t0.elapsed_time(t1)
+    kern_ms = [ev[s][l][0].elapsed_time(ev[s][l][1]) for s in range(args.steps)
+               for l in range(W.layers)]
+    ms_step = ms_total / max(args.steps, 1)
+    if dist is not None:
+        t = torch.tensor([ms_step, statistics.mean(kern_ms)], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step, kern_avg = float(t[0]), float(t[1])
+    else:
+        kern_avg = statistics.mean(kern_ms)
+    launches = args.steps * W.layers * 2
+
+    # ---- end-to-end through the C-ABI host-buffer entry point (pinned host buffers)
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, W, engine, dist, device, stream)
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    peaks = measured_peaks()
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    total_bytes = W.step_bytes * world
+    value = total_bytes / (ms_step / 1e3) / 1e9
+    achieved = W.decode_bytes_per_launch / (kern_avg / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": {"bfloat16": "bf16", "float32": "f32", "float16": "f16"}[w["dtype"]],
+        "data": "synthetic: q, k, v ~ U(-1,1) (bench_attention.cpp:11-27 law), shuffled page placement",
+        "config": {"workload": f"{args.workload}: {w['desc']}", "global_batch": W.B,
+                   "seq_len": int(W.max_len), "sum_seq_len": int(W.lens.sum()) ,
+                   "layers": W.layers, "kv_layers_resident": W.resident,
+                   "q_heads": W.Hq, "kv_heads": W.Hkv, "head_dim": W.D, "page_size": w["P"],
+                   "parallelism": f"kv-head sharded x{world}" if world > 1 else "single GPU",
+                   "l2": f"inputs {W.kv_bytes_layer * W.resident / 2**30:.0f} GiB of KV >> 126 MB L2; no flush needed",
+                   "kernel": W.kernel, "splits": W.splits, "split_tokens": W.chunk},
+        "attn_tokens_per_s": W.B / (ms_step / 1e3),
+        "frac_of_hbm_roofline": value / world / peak,
+        "frac_of_hbm_spec_8tbs": value / world / 8000.0,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650",
+                     "kernel": f"decode_{W.kernel}", "bytes_per_launch": W.decode_bytes_per_launch,
+                     "avg_launch_ms": kern_avg, "traffic": None},
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    if e2e is not None:
+        line["e2e"] = e2e
+    if not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline(w, target_s=args.cpu_seconds)
+        except Exception as exc:  # the CPU baseline is reported, never required
+            line["cpu_baseline"] = {"error": repr(exc)}
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, W, engine, dist, device, stream):
+    """Same step through lam_decode_step_host: q / k_new / v_new copied from pinned host
+    memory every layer, output copied back to pinned host memory, inside the timed region."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2405_01814_b200 import _lib, decode as dec
+
+    lib = _lib.load()
+    L = W.layers
+    h_q = W.q_in.cpu().pin_memory()
+    h_kn = W.kn_in.cpu().pin_memory()
+    h_vn = W.vn_in.cpu().pin_memory()
+    h_out = torch.empty(W.out.shape, dtype=W.out.dtype).pin_memory()
+    if engine is not None:
+        return engine.e2e(args, h_q, h_kn, h_vn, h_out)
+    d_q = torch.empty_like(W.q_in[0])
+    d_kn = torch.empty_like(W.kn_in[0])
+    d_vn = torch.empty_like(W.vn_in[0])
+    d_out = torch.empty_like(W.out[0])
+    args_l = []
+    for layer in range(L):
+        kp, vp = W.layer_pools(layer)
+        a, _ = dec.make_args(d_q, kp, vp, W.seq_lens, page_table=W.page_table, max_len=W.max_len,
+                             out=d_out, split_tokens=W.chunk)
+        args_l.append(a)
+    sp = stream.cuda_stream
+
+    def step():
+        for layer in range(L):
+            _lib.check(lib.lam_decode_step_host(
+                W.ctx.handle, args_l[layer], h_q[layer].data_ptr(), h_kn[layer].data_ptr(),
+                h_vn[layer].data_ptr(), h_out[layer].data_ptr(), d_kn.data_ptr(),
+                d_vn.data_ptr(), W.positions.data_ptr(), sp))
+
+    for _ in range(max(1, args.warmup)):
+        step()
+    torch.cuda.synchronize(device)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize(device)
+    ms = t0.elapsed_time(t1) / max(args.steps, 1)
+    h2d = (h_q.numel() + h_kn.numel() + h_vn.numel()) * h_q.element_size()
+    d2h = h_out.numel() * h_out.element_size()
+    return {"value": W.step_bytes / (ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "api": "lam_decode_step_host (C-ABI, host buffers)"}
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawTextHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", 1)))
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=3.0)
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if args.gpus != world and world == 1 and args.gpus > 1:
+        log(f"--gpus {args.gpus} requested without torchrun: running one rank")
+        args.gpus = 1
+    w = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference(args, w, rank, world)
+    else:
+        run_ours(args, w, rank, world)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,199 @@
+/*
+ * lamina_attn.h — C-ABI of the B200 (sm_100a) decode-attention operator.
+ *
+ * This is the drop-in boundary below the reference's C++ operator API
+ * (/root/reference/proj/core/include/disagg/attention.hpp:1-114).  Every entry
+ * point takes plain pointers, sizes and an opaque cudaStream_t (passed as void*);
+ * no C++ or torch types cross it.  The C++ wrapper that keeps the reference
+ * signatures unchanged lives in paper_2405_01814_b200/dropin/attention.cpp and
+ * maps the status codes below onto the reference exception hierarchy
+ * (model.hpp:25-40):
+ *
+ *   LAM_OK               0  success
+ *   LAM_ERR_ERROR        1  -> disagg::Error            (empty key set, index out of range,
+ *                                                         finalize of an empty partial, bad split)
+ *   LAM_ERR_VALIDATION   2  -> disagg::ValidationError  (dims, divisibility, unsupported shape)
+ *   LAM_ERR_CUDA         3  CUDA runtime / driver failure (message in lam_last_error())
+ *
+ * Ownership: the caller owns every buffer; the library owns lam_ctx / lam_plan handles.
+ * Threading: lam_ctx is not shared between concurrently running host threads; the
+ * *_host entry points use a per-thread staging area and are reentrant.
+ * There is no CPU fallback: every attention entry point runs on the GPU.
+ */
+#ifndef LAMINA_ATTN_H
+#define LAMINA_ATTN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LAM_OK 0
+#define LAM_ERR_ERROR 1
+#define LAM_ERR_VALIDATION 2
+#define LAM_ERR_CUDA 3
+
+/* element types */
+#define LAM_F32 0
+#define LAM_F64 1
+#define LAM_BF16 2
+#define LAM_F16 3
+
+/* kernel families (lam_decode `kernel` argument / lam_plan_kernel result) */
+#define LAM_KERNEL_AUTO 0
+#define LAM_KERNEL_SIMT 1     /* warp-shuffle online softmax, CUDA cores (MHA) */
+#define LAM_KERNEL_GQA_MMA 2  /* tensor-core m16n8k16 over a GQA group of 8 q heads */
+
+typedef struct lam_ctx lam_ctx;
+
+/* ---- library / context -------------------------------------------------- */
+
+int lam_version(void);
+/* Thread-local message for the last non-zero status returned on this thread. */
+const char* lam_last_error(void);
+
+/* A context binds one CUDA device and owns the split-K workspace + counters. */
+int lam_ctx_create(int device, lam_ctx** out);
+int lam_ctx_destroy(lam_ctx* ctx);
+/* Pre-size the split-K workspace so no allocation happens inside lam_decode. */
+int lam_ctx_reserve(lam_ctx* ctx, int64_t partial_rows, int32_t head_dim, int64_t counters);
+/* Number of SMs of the context's device (148 on B200). */
+int lam_ctx_num_sms(const lam_ctx* ctx);
+
+/* ---- reference operator API, device pointers -----------------------------
+ * One "instance" is one AttnInstance (attention.hpp:20-30): a query vector of d
+ * elements and its key/value rows.  Keys/values of all instances live in two row
+ * pools k_rows/v_rows of shape [rows][d]; instance i owns rows
+ * [kv_row0[i], kv_row0[i] + kv_len[i]).  Several instances may share rows
+ * (multi_head_attention's GQA mapping, attention.cpp:141-150) — nothing is copied.
+ * dtype is LAM_F32 or LAM_F64 (the reference's two instantiations,
+ * attention.cpp:205-230); scale points to n_inst values of that dtype.
+ */
+
+/* exact_attention (attention.cpp:48-70).  LAM_ERR_ERROR if any kv_len == 0. */
+int lam_exact_attention(lam_ctx* ctx, int dtype, int64_t n_inst, int32_t d, const void* q,
+                        const void* k_rows, const void* v_rows, const int64_t* kv_row0,
+                        const int64_t* kv_len, const void* scale, void* out, void* stream);
+
+/* partial_attention over index subsets (attention.cpp:72-98).  Instance i uses
+ * indices idx[idx_off[i] .. idx_off[i+1]) into its own rows; an empty subset yields
+ * the identity partial (acc = 0, max_logit = log_denom = -inf, count = 0).
+ * LAM_ERR_ERROR ("token index out of range") if any index is outside [0, kv_len[i]). */
+int lam_partial_attention(lam_ctx* ctx, int dtype, int64_t n_inst, int32_t d, const void* q,
+                          const void* k_rows, const void* v_rows, const int64_t* kv_row0,
+                          const int64_t* kv_len, const int64_t* idx, const int64_t* idx_off,
+                          const void* scale, void* acc, void* max_logit, void* log_denom,
+                          int64_t* token_count, void* stream);
+
+/* merge (attention.cpp:100-118), n pairs elementwise; identity early-outs are bitwise. */
+int lam_merge(lam_ctx* ctx, int dtype, int64_t n, int32_t d, const void* a_acc,
+              const void* a_max, const void* a_log_denom, const int64_t* a_count,
+              const void* b_acc, const void* b_max, const void* b_log_denom,
+              const int64_t* b_count, void* o_acc, void* o_max, void* o_log_denom,
+              int64_t* o_count, void* stream);
+
+/* finalize (attention.cpp:120-127).  LAM_ERR_ERROR if any partial is empty. */
+int lam_finalize(lam_ctx* ctx, int dtype, int64_t n, int32_t d, const void* acc,
+                 const void* log_denom, const int64_t* count, void* out, void* stream);
+
+/* ---- reference operator API, host pointers --------------------------------
+ * Same semantics as above, but every array lives in host memory; the library stages
+ * it through a per-thread device buffer, runs the kernel and copies results back
+ * before returning.  These are what the C++ drop-in calls. */
+int lam_exact_attention_host(int dtype, int64_t n_inst, int32_t d, const void* q,
+                             int64_t n_rows, const void* k_rows, const void* v_rows,
+                             const int64_t* kv_row0, const int64_t* kv_len, const void* scale,
+                             void* out);
+int lam_partial_attention_host(int dtype, int64_t n_inst, int32_t d, const void* q,
+                               int64_t n_rows, const void* k_rows, const void* v_rows,
+                               const int64_t* kv_row0, const int64_t* kv_len,
+                               const int64_t* idx, const int64_t* idx_off, const void* scale,
+                               void* acc, void* max_logit, void* log_denom,
+                               int64_t* token_count);
+int lam_merge_host(int dtype, int64_t n, int32_t d, const void* a_acc, const void* a_max,
+                   const void* a_log_denom, const int64_t* a_count, const void* b_acc,
+                   const void* b_max, const void* b_log_denom, const int64_t* b_count,
+                   void* o_acc, void* o_max, void* o_log_denom, int64_t* o_count);
+int lam_finalize_host(int dtype, int64_t n, int32_t d, const void* acc, const void* log_denom,
+                      const int64_t* count, void* out);
+
+/* ---- work partitioning (host logic, attention.cpp:164-203) ---------------- */
+
+/* ranges[2*i], ranges[2*i+1] = [begin, end) of device i.  LAM_ERR_VALIDATION with a
+ * message containing "divisible" unless num_kv_heads % num_devices == 0. */
+int lam_head_partition(int64_t num_kv_heads, int64_t num_devices, int64_t* ranges);
+/* Greedy longest-first bin packing; ties to the lower device index. */
+int lam_request_partition(const double* kv_sizes, int64_t n, int64_t num_devices,
+                          int64_t* device_of, double* device_load, double* imbalance);
+
+/* ---- production decode path (paged HBM KV store) --------------------------
+ * KV layout, per layer, per K and V pool:
+ *   paged  (page_table != NULL): pool[num_pages][Hkv][page_size][D]; token t of request b
+ *          lives in physical page page_table[b*pt_stride + t/page_size], row t%page_size.
+ *   dense  (page_table == NULL): pool[B][Hkv][page_size][D], i.e. page_size is the row
+ *          capacity l_max of each (request, kv head).
+ * Rows are D contiguous elements (256 B for bf16 D=128): every 16-byte vector is aligned.
+ * q: [B][Hq][D] in kv_dtype.  out: [B][Hq][D] in out_dtype (kv_dtype or LAM_F32).
+ * lse (nullable): [B][Hq] fp32 natural-log sum-exp of the scaled logits.
+ * seq_lens: [B] int32 device array; max_len is a host upper bound used for grid sizing.
+ * kernel: LAM_KERNEL_AUTO picks GQA_MMA for 16-bit KV with Hq/Hkv == 8 (or 4, 2), SIMT
+ *         otherwise.  split_tokens: tokens per split-K chunk (0 = auto). */
+typedef struct lam_decode_args {
+  int32_t kv_dtype;
+  int32_t out_dtype;
+  int32_t batch;
+  int32_t num_q_heads;
+  int32_t num_kv_heads;
+  int32_t head_dim;
+  float scale;
+  int32_t page_size;
+  int32_t pt_stride;
+  int32_t max_len;
+  int32_t split_tokens;
+  int32_t kernel;
+  int64_t num_pages; /* paged: pages in the pool (tensor-map extent); dense: ignored */
+  const void* q;
+  const void* k_pool;
+  const void* v_pool;
+  const int32_t* page_table;
+  const int32_t* seq_lens;
+  void* out;
+  float* lse;
+} lam_decode_args;
+
+int lam_decode(lam_ctx* ctx, const lam_decode_args* args, void* stream);
+/* Kernel family and split count lam_decode would use for these arguments. */
+int lam_decode_plan(lam_ctx* ctx, const lam_decode_args* args, int32_t* kernel,
+                    int32_t* num_splits, int32_t* split_tokens);
+
+/* Write the new token of every request into the paged pools (bit-exact copy):
+ *   k_pool[page_table[b][pos/P]][h][pos%P][:] = k_new[b][h][:], same for V,
+ *   pos = positions[b].  Dense layout when page_table == NULL (pos < page_size). */
+int lam_kv_append(int32_t dtype, int32_t batch, int32_t num_kv_heads, int32_t head_dim,
+                  int32_t page_size, int32_t pt_stride, const int32_t* page_table,
+                  const int32_t* positions, const void* k_new, const void* v_new,
+                  void* k_pool, void* v_pool, void* stream);
+
+/* Gather tokens [0, len_b) of every request from the paged pool into a dense
+ * [B][Hkv][l_max][D] buffer (inverse of the paging; used to prove bit-exactness). */
+int lam_kv_gather(int32_t dtype, int32_t batch, int32_t num_kv_heads, int32_t head_dim,
+                  int32_t page_size, int32_t pt_stride, const int32_t* page_table,
+                  const int32_t* seq_lens, int32_t l_max, const void* pool, void* dense,
+                  void* stream);
+
+/* Host-buffer decode step (the reference-facing end-to-end call, one layer): copies q,
+ * k_new, v_new from host memory (pinned for overlap) into args->q / d_k_new / d_v_new,
+ * appends the new token of request b at d_positions[b] (lam_kv_append), runs lam_decode
+ * into args->out and copies it back to h_out.  Everything is enqueued on `stream`; the
+ * caller synchronises.  args->k_pool / args->v_pool must be writable. */
+int lam_decode_step_host(lam_ctx* ctx, const lam_decode_args* args, const void* h_q,
+                         const void* h_k_new, const void* h_v_new, void* h_out, void* d_k_new,
+                         void* d_v_new, const int32_t* d_positions, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LAMINA_ATTN_H */

@@ -1,0 +1,711 @@
+// capi.cu — the extern "C" boundary (include/lamina_attn.h): contexts, workspace, planning,
+// tensor maps, status codes, and the host-buffer entry points used by the C++ drop-in.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/lamina_attn.h"
+#include "decode_common.cuh"
+#include "lam_internal.h"
+
+struct lam_ctx {
+  int device = 0;
+  int num_sms = 0;
+  float* ws_acc = nullptr;
+  int64_t ws_acc_cap = 0;  // floats
+  float* ws_ml = nullptr;
+  int64_t ws_ml_cap = 0;   // floats
+  int32_t* counters = nullptr;
+  int64_t counters_cap = 0;
+  int32_t* err = nullptr;  // device error word for the instance API
+  void* scratch = nullptr; // instance API: logits workspace
+  int64_t scratch_cap = 0; // bytes
+  int64_t* offs = nullptr; // instance API: logit offsets
+  int64_t offs_cap = 0;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(LAM_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define LAM_CUDA(call)                                     \
+  do {                                                     \
+    cudaError_t e_ = (call);                               \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);    \
+  } while (0)
+
+int elem_bytes(int dtype) {
+  switch (dtype) {
+    case LAM_F32: return 4;
+    case LAM_F64: return 8;
+    case LAM_BF16: return 2;
+    case LAM_F16: return 2;
+    default: return 0;
+  }
+}
+
+template <typename T>
+cudaError_t grow(T** ptr, int64_t* cap, int64_t need, bool zero) {
+  if (need <= *cap) return cudaSuccess;
+  if (*ptr) cudaFree(*ptr);
+  *ptr = nullptr;
+  *cap = 0;
+  const int64_t n = std::max<int64_t>(need, 1);
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(ptr), n * sizeof(T));
+  if (e != cudaSuccess) return e;
+  if (zero) {
+    e = cudaMemset(*ptr, 0, n * sizeof(T));
+    if (e != cudaSuccess) return e;
+  }
+  *cap = n;
+  return cudaSuccess;
+}
+
+// ---- driver entry point for tensor maps (no -lcuda link dependency) ----
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D view [rows][D] of a 16-bit pool, 64x64 boxes, 128-byte swizzle.
+int make_pool_map(CUtensorMap* map, int dtype, const void* base, int64_t rows, int D) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return fail(LAM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(D) * 2};
+  const cuuint32_t box[2] = {64, 64};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUtensorMapDataType dt =
+      dtype == LAM_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  CUresult r = enc(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(LAM_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+  return LAM_OK;
+}
+
+struct Plan {
+  int kernel = 0;  // LAM_KERNEL_SIMT / LAM_KERNEL_GQA_MMA
+  int GQ = 1;      // q heads per CTA
+  int QG = 1;      // q-head groups per kv head
+  int tile = 32;
+  int chunk = 0;
+  int S = 1;
+};
+
+// Pick the split count that minimises (waves x per-CTA tiles) with a fixed per-CTA cost.
+void choose_splits(Plan& pl, int64_t units, int max_len, int slots, int split_tokens) {
+  const int tiles_total = std::max(1, (max_len + pl.tile - 1) / pl.tile);
+  if (split_tokens > 0) {
+    const int ct = std::max(1, (split_tokens + pl.tile - 1) / pl.tile);
+    pl.chunk = ct * pl.tile;
+    pl.S = (tiles_total + ct - 1) / ct;
+    return;
+  }
+  const double kOverheadTiles = 2.0;
+  double best = 1e300;
+  int best_ct = tiles_total;
+  const int max_s = std::min(tiles_total, 256);
+  for (int s = 1; s <= max_s; ++s) {
+    const int ct = (tiles_total + s - 1) / s;
+    const int s_eff = (tiles_total + ct - 1) / ct;
+    if (s_eff != s) continue;
+    const double ctas = static_cast<double>(units) * s_eff;
+    const double waves = std::ceil(ctas / std::max(1, slots));
+    const double cost = waves * (ct + kOverheadTiles) + (s_eff > 1 ? 0.5 : 0.0);
+    if (cost < best - 1e-9) {
+      best = cost;
+      best_ct = ct;
+    }
+  }
+  pl.chunk = best_ct * pl.tile;
+  pl.S = (tiles_total + best_ct - 1) / best_ct;
+}
+
+int plan_decode(lam_ctx* ctx, const lam_decode_args* a, Plan* pl) {
+  if (!a) return fail(LAM_ERR_VALIDATION, "null decode args");
+  const int kvd = a->kv_dtype;
+  if (kvd != LAM_F32 && kvd != LAM_BF16 && kvd != LAM_F16)
+    return fail(LAM_ERR_VALIDATION, "kv_dtype must be f32, bf16 or f16");
+  if (a->out_dtype != kvd && a->out_dtype != LAM_F32)
+    return fail(LAM_ERR_VALIDATION, "out_dtype must equal kv_dtype or be f32");
+  if (a->batch < 0 || a->num_q_heads < 1 || a->num_kv_heads < 1)
+    return fail(LAM_ERR_VALIDATION, "need batch >= 0 and at least one q and kv head");
+  if (a->num_q_heads % a->num_kv_heads != 0)
+    return fail(LAM_ERR_VALIDATION, "query heads must be a multiple of KV heads");
+  if (a->head_dim != 64 && a->head_dim != 128)
+    return fail(LAM_ERR_VALIDATION, "head_dim must be 64 or 128 on the decode path");
+  if (a->page_size < 1) return fail(LAM_ERR_VALIDATION, "page_size must be >= 1");
+  if (a->max_len < 0) return fail(LAM_ERR_VALIDATION, "max_len must be >= 0");
+  const int G = a->num_q_heads / a->num_kv_heads;
+  const bool paged = a->page_table != nullptr;
+  if (!paged && a->max_len > a->page_size)
+    return fail(LAM_ERR_VALIDATION, "dense layout: max_len exceeds the row capacity page_size");
+
+  const bool mma_ok = (kvd == LAM_BF16 || kvd == LAM_F16) && a->head_dim == 128 && G >= 2 &&
+                      G <= 8 && (!paged || a->page_size % 64 == 0);
+  int kernel = a->kernel;
+  if (kernel == LAM_KERNEL_AUTO) kernel = mma_ok ? LAM_KERNEL_GQA_MMA : LAM_KERNEL_SIMT;
+  if (kernel == LAM_KERNEL_GQA_MMA) {
+    if (!mma_ok)
+      return fail(LAM_ERR_VALIDATION,
+                  "GQA MMA kernel needs 16-bit KV, head_dim 128, 2 <= G <= 8 and page_size % 64 == 0");
+    pl->kernel = kernel;
+    pl->GQ = 8;
+    pl->QG = 1;
+    pl->tile = 64;
+  } else if (kernel == LAM_KERNEL_SIMT) {
+    if (paged && a->page_size % 32 != 0)
+      return fail(LAM_ERR_VALIDATION, "paged layout needs page_size % 32 == 0");
+    pl->kernel = kernel;
+    pl->GQ = G % 4 == 0 ? 4 : (G % 2 == 0 ? 2 : 1);
+    pl->QG = G / pl->GQ;
+    pl->tile = 32;
+  } else {
+    return fail(LAM_ERR_VALIDATION, "unknown kernel family");
+  }
+  const int occ = pl->kernel == LAM_KERNEL_GQA_MMA ? lam::occupancy_mma(kvd)
+                                                   : lam::occupancy_simt(kvd, a->head_dim, pl->GQ);
+  if (occ <= 0) return fail(LAM_ERR_CUDA, "decode kernel cannot be resident on this device");
+  const int64_t units = static_cast<int64_t>(a->batch) * a->num_kv_heads * pl->QG;
+  choose_splits(*pl, units, a->max_len, occ * ctx->num_sms, a->split_tokens);
+  if (pl->S > 65535) return fail(LAM_ERR_VALIDATION, "too many splits");
+  return LAM_OK;
+}
+
+// per-thread context + staging for the host-buffer entry points
+struct HostStage {
+  lam_ctx* ctx = nullptr;
+  cudaStream_t stream = nullptr;
+  std::vector<void*> bufs;
+  std::vector<int64_t> caps;
+  ~HostStage() {
+    for (void* p : bufs)
+      if (p) cudaFree(p);
+    if (stream) cudaStreamDestroy(stream);
+    if (ctx) lam_ctx_destroy(ctx);
+  }
+  int init() {
+    if (ctx) return LAM_OK;
+    int dev = 0;
+    LAM_CUDA(cudaGetDevice(&dev));
+    int rc = lam_ctx_create(dev, &ctx);
+    if (rc != LAM_OK) return rc;
+    LAM_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    return LAM_OK;
+  }
+  // buffer slot i with at least `bytes`
+  int get(size_t i, int64_t bytes, void** out) {
+    if (bufs.size() <= i) {
+      bufs.resize(i + 1, nullptr);
+      caps.resize(i + 1, 0);
+    }
+    if (caps[i] < bytes) {
+      if (bufs[i]) cudaFree(bufs[i]);
+      bufs[i] = nullptr;
+      caps[i] = 0;
+      LAM_CUDA(cudaMalloc(&bufs[i], std::max<int64_t>(bytes, 16)));
+      caps[i] = std::max<int64_t>(bytes, 16);
+    }
+    *out = bufs[i];
+    return LAM_OK;
+  }
+};
+
+thread_local HostStage g_stage;
+
+int check_err_word(lam_ctx* ctx, cudaStream_t stream, const char* empty_msg) {
+  int32_t h = 0;
+  LAM_CUDA(cudaMemcpyAsync(&h, ctx->err, sizeof(h), cudaMemcpyDeviceToHost, stream));
+  LAM_CUDA(cudaStreamSynchronize(stream));
+  if (h == 2) return fail(LAM_ERR_ERROR, "token index out of range");
+  if (h == 1) return fail(LAM_ERR_ERROR, empty_msg);
+  return LAM_OK;
+}
+
+int run_instances(lam_ctx* ctx, int dtype, int64_t n_inst, int32_t d, const void* q,
+                  const void* k, const void* v, const int64_t* kv_row0, const int64_t* kv_len,
+                  const int64_t* idx, const int64_t* idx_off, const void* scale, void* acc,
+                  void* max_logit, void* log_denom, int64_t* count, int exact,
+                  cudaStream_t stream) {
+  if (!ctx) return fail(LAM_ERR_VALIDATION, "null context");
+  if (dtype != LAM_F32 && dtype != LAM_F64)
+    return fail(LAM_ERR_VALIDATION, "instance API supports f32 and f64");
+  if (d < 1) return fail(LAM_ERR_VALIDATION, "query must be non-empty");
+  if (n_inst < 0) return fail(LAM_ERR_VALIDATION, "negative instance count");
+  if (n_inst == 0) return LAM_OK;
+  LAM_CUDA(cudaSetDevice(ctx->device));
+  LAM_CUDA(grow(&ctx->offs, &ctx->offs_cap, n_inst + 1, false));
+  LAM_CUDA(lam::launch_count_scan(n_inst, kv_len, exact ? nullptr : idx_off, ctx->offs, stream));
+  int64_t total = 0;
+  LAM_CUDA(cudaMemcpyAsync(&total, ctx->offs + n_inst, sizeof(total), cudaMemcpyDeviceToHost,
+                           stream));
+  LAM_CUDA(cudaStreamSynchronize(stream));
+  const int64_t need = std::max<int64_t>(total, 1) * elem_bytes(dtype);
+  if (ctx->scratch_cap < need) {
+    if (ctx->scratch) cudaFree(ctx->scratch);
+    ctx->scratch = nullptr;
+    ctx->scratch_cap = 0;
+    LAM_CUDA(cudaMalloc(&ctx->scratch, need));
+    ctx->scratch_cap = need;
+  }
+  LAM_CUDA(cudaMemsetAsync(ctx->err, 0, sizeof(int32_t), stream));
+  LAM_CUDA(lam::launch_instances(dtype, n_inst, d, q, k, v, kv_row0, kv_len, exact ? nullptr : idx,
+                                 exact ? nullptr : idx_off, scale, ctx->scratch, ctx->offs, acc,
+                                 max_logit, log_denom, count, exact, ctx->err, stream));
+  return check_err_word(ctx, stream, "exact_attention requires a non-empty key set");
+}
+
+}  // namespace
+
+extern "C" {
+
+int lam_version(void) { return 1; }
+
+const char* lam_last_error(void) { return g_last_error.c_str(); }
+
+int lam_ctx_create(int device, lam_ctx** out) {
+  if (!out) return fail(LAM_ERR_VALIDATION, "null output pointer");
+  *out = nullptr;
+  int n = 0;
+  LAM_CUDA(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n) return fail(LAM_ERR_VALIDATION, "no such CUDA device");
+  LAM_CUDA(cudaSetDevice(device));
+  int major = 0;
+  LAM_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+  if (major < 10) return fail(LAM_ERR_CUDA, "liblamina_attn is built for sm_100a (B200) only");
+  auto* c = new lam_ctx();
+  c->device = device;
+  cudaError_t e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (e == cudaSuccess) e = cudaMalloc(&c->err, sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMemset(c->err, 0, sizeof(int32_t));
+  if (e != cudaSuccess) {
+    delete c;
+    return cuda_fail(e, "lam_ctx_create");
+  }
+  *out = c;
+  return LAM_OK;
+}
+
+int lam_ctx_destroy(lam_ctx* c) {
+  if (!c) return LAM_OK;
+  cudaSetDevice(c->device);
+  cudaFree(c->ws_acc);
+  cudaFree(c->ws_ml);
+  cudaFree(c->counters);
+  cudaFree(c->err);
+  cudaFree(c->scratch);
+  cudaFree(c->offs);
+  delete c;
+  return LAM_OK;
+}
+
+int lam_ctx_num_sms(const lam_ctx* c) { return c ? c->num_sms : 0; }
+
+int lam_ctx_reserve(lam_ctx* c, int64_t partial_rows, int32_t head_dim, int64_t counters) {
+  if (!c) return fail(LAM_ERR_VALIDATION, "null context");
+  LAM_CUDA(cudaSetDevice(c->device));
+  LAM_CUDA(grow(&c->ws_acc, &c->ws_acc_cap, partial_rows * head_dim, false));
+  LAM_CUDA(grow(&c->ws_ml, &c->ws_ml_cap, partial_rows * 2, false));
+  LAM_CUDA(grow(&c->counters, &c->counters_cap, counters, true));
+  return LAM_OK;
+}
+
+// ---------------- instance API (device pointers) ----------------
+
+int lam_exact_attention(lam_ctx* ctx, int dtype, int64_t n_inst, int32_t d, const void* q,
+                        const void* k_rows, const void* v_rows, const int64_t* kv_row0,
+                        const int64_t* kv_len, const void* scale, void* out, void* stream) {
+  return run_instances(ctx, dtype, n_inst, d, q, k_rows, v_rows, kv_row0, kv_len, nullptr,
+                       nullptr, scale, out, nullptr, nullptr, nullptr, 1,
+                       static_cast<cudaStream_t>(stream));
+}
+
+int lam_partial_attention(lam_ctx* ctx, int dtype, int64_t n_inst, int32_t d, const void* q,
+                          const void* k_rows, const void* v_rows, const int64_t* kv_row0,
+                          const int64_t* kv_len, const int64_t* idx, const int64_t* idx_off,
+                          const void* scale, void* acc, void* max_logit, void* log_denom,
+                          int64_t* token_count, void* stream) {
+  if (!idx_off) return fail(LAM_ERR_VALIDATION, "partial_attention needs idx_off");
+  return run_instances(ctx, dtype, n_inst, d, q, k_rows, v_rows, kv_row0, kv_len, idx, idx_off,
+                       scale, acc, max_logit, log_denom, token_count, 0,
+                       static_cast<cudaStream_t>(stream));
+}
+
+int lam_merge(lam_ctx* ctx, int dtype, int64_t n, int32_t d, const void* a_acc,
+              const void* a_max, const void* a_log_denom, const int64_t* a_count,
+              const void* b_acc, const void* b_max, const void* b_log_denom,
+              const int64_t* b_count, void* o_acc, void* o_max, void* o_log_denom,
+              int64_t* o_count, void* stream) {
+  if (!ctx) return fail(LAM_ERR_VALIDATION, "null context");
+  if (dtype != LAM_F32 && dtype != LAM_F64)
+    return fail(LAM_ERR_VALIDATION, "merge supports f32 and f64");
+  if (d < 0 || n < 0) return fail(LAM_ERR_VALIDATION, "negative size");
+  LAM_CUDA(cudaSetDevice(ctx->device));
+  auto s = static_cast<cudaStream_t>(stream);
+  LAM_CUDA(lam::launch_merge(dtype, n, d, a_acc, a_max, a_log_denom, a_count, b_acc, b_max,
+                             b_log_denom, b_count, o_acc, o_max, o_log_denom, o_count, ctx->err,
+                             s));
+  return LAM_OK;
+}
+
+int lam_finalize(lam_ctx* ctx, int dtype, int64_t n, int32_t d, const void* acc,
+                 const void* log_denom, const int64_t* count, void* out, void* stream) {
+  if (!ctx) return fail(LAM_ERR_VALIDATION, "null context");
+  if (dtype != LAM_F32 && dtype != LAM_F64)
+    return fail(LAM_ERR_VALIDATION, "finalize supports f32 and f64");
+  LAM_CUDA(cudaSetDevice(ctx->device));
+  auto s = static_cast<cudaStream_t>(stream);
+  LAM_CUDA(cudaMemsetAsync(ctx->err, 0, sizeof(int32_t), s));
+  LAM_CUDA(lam::launch_finalize(dtype, n, d, acc, log_denom, count, out, ctx->err, s));
+  return check_err_word(ctx, s, "cannot finalize an empty partial");
+}
+
+// ---------------- instance API (host pointers) ----------------
+
+namespace {
+struct HostCopy {
+  const void* host;
+  int64_t bytes;
+};
+// Stage `n` host arrays into per-thread device slots starting at `slot0`.
+int stage_in(int slot0, std::initializer_list<HostCopy> items, std::vector<void*>& dev) {
+  int i = slot0;
+  for (const auto& it : items) {
+    void* d = nullptr;
+    int rc = g_stage.get(i++, it.bytes, &d);
+    if (rc != LAM_OK) return rc;
+    if (it.host && it.bytes > 0)
+      LAM_CUDA(cudaMemcpyAsync(d, it.host, it.bytes, cudaMemcpyHostToDevice, g_stage.stream));
+    dev.push_back(d);
+  }
+  return LAM_OK;
+}
+}  // namespace
+
+int lam_exact_attention_host(int dtype, int64_t n_inst, int32_t d, const void* q, int64_t n_rows,
+                             const void* k_rows, const void* v_rows, const int64_t* kv_row0,
+                             const int64_t* kv_len, const void* scale, void* out) {
+  int rc = g_stage.init();
+  if (rc != LAM_OK) return rc;
+  const int e = elem_bytes(dtype);
+  if (e == 0) return fail(LAM_ERR_VALIDATION, "bad dtype");
+  if (n_inst <= 0) return LAM_OK;
+  std::vector<void*> dv;
+  rc = stage_in(0,
+                {{q, n_inst * d * e},
+                 {k_rows, n_rows * d * e},
+                 {v_rows, n_rows * d * e},
+                 {kv_row0, n_inst * 8},
+                 {kv_len, n_inst * 8},
+                 {scale, n_inst * e},
+                 {nullptr, n_inst * d * e}},
+                dv);
+  if (rc != LAM_OK) return rc;
+  rc = lam_exact_attention(g_stage.ctx, dtype, n_inst, d, dv[0], dv[1], dv[2],
+                           static_cast<int64_t*>(dv[3]), static_cast<int64_t*>(dv[4]), dv[5], dv[6],
+                           g_stage.stream);
+  if (rc != LAM_OK) return rc;
+  LAM_CUDA(cudaMemcpyAsync(out, dv[6], n_inst * d * e, cudaMemcpyDeviceToHost, g_stage.stream));
+  LAM_CUDA(cudaStreamSynchronize(g_stage.stream));
+  return LAM_OK;
+}
+
+int lam_partial_attention_host(int dtype, int64_t n_inst, int32_t d, const void* q,
+                               int64_t n_rows, const void* k_rows, const void* v_rows,
+                               const int64_t* kv_row0, const int64_t* kv_len,
+                               const int64_t* idx, const int64_t* idx_off, const void* scale,
+                               void* acc, void* max_logit, void* log_denom,
+                               int64_t* token_count) {
+  int rc = g_stage.init();
+  if (rc != LAM_OK) return rc;
+  const int e = elem_bytes(dtype);
+  if (e == 0) return fail(LAM_ERR_VALIDATION, "bad dtype");
+  if (n_inst <= 0) return LAM_OK;
+  const int64_t n_idx = idx_off[n_inst];
+  std::vector<void*> dv;
+  rc = stage_in(0,
+                {{q, n_inst * d * e},
+                 {k_rows, n_rows * d * e},
+                 {v_rows, n_rows * d * e},
+                 {kv_row0, n_inst * 8},
+                 {kv_len, n_inst * 8},
+                 {idx, n_idx * 8},
+                 {idx_off, (n_inst + 1) * 8},
+                 {scale, n_inst * e},
+                 {nullptr, n_inst * d * e},
+                 {nullptr, n_inst * e},
+                 {nullptr, n_inst * e},
+                 {nullptr, n_inst * 8}},
+                dv);
+  if (rc != LAM_OK) return rc;
+  rc = lam_partial_attention(g_stage.ctx, dtype, n_inst, d, dv[0], dv[1], dv[2],
+                             static_cast<int64_t*>(dv[3]), static_cast<int64_t*>(dv[4]),
+                             static_cast<int64_t*>(dv[5]), static_cast<int64_t*>(dv[6]), dv[7],
+                             dv[8], dv[9], dv[10], static_cast<int64_t*>(dv[11]), g_stage.stream);
+  if (rc != LAM_OK) return rc;
+  auto s = g_stage.stream;
+  LAM_CUDA(cudaMemcpyAsync(acc, dv[8], n_inst * d * e, cudaMemcpyDeviceToHost, s));
+  LAM_CUDA(cudaMemcpyAsync(max_logit, dv[9], n_inst * e, cudaMemcpyDeviceToHost, s));
+  LAM_CUDA(cudaMemcpyAsync(log_denom, dv[10], n_inst * e, cudaMemcpyDeviceToHost, s));
+  LAM_CUDA(cudaMemcpyAsync(token_count, dv[11], n_inst * 8, cudaMemcpyDeviceToHost, s));
+  LAM_CUDA(cudaStreamSynchronize(s));
+  return LAM_OK;
+}
+
+int lam_merge_host(int dtype, int64_t n, int32_t d, const void* a_acc, const void* a_max,
+                   const void* a_log_denom, const int64_t* a_count, const void* b_acc,
+                   const void* b_max, const void* b_log_denom, const int64_t* b_count,
+                   void* o_acc, void* o_max, void* o_log_denom, int64_t* o_count) {
+  int rc = g_stage.init();
+  if (rc != LAM_OK) return rc;
+  const int e = elem_bytes(dtype);
+  if (e == 0) return fail(LAM_ERR_VALIDATION, "bad dtype");
+  if (n <= 0) return LAM_OK;
+  std::vector<void*> dv;
+  rc = stage_in(0,
+                {{a_acc, n * d * e},
+                 {a_max, n * e},
+                 {a_log_denom, n * e},
+                 {a_count, n * 8},
+                 {b_acc, n * d * e},
+                 {b_max, n * e},
+                 {b_log_denom, n * e},
+                 {b_count, n * 8},
+                 {nullptr, n * d * e},
+                 {nullptr, n * e},
+                 {nullptr, n * e},
+                 {nullptr, n * 8}},
+                dv);
+  if (rc != LAM_OK) return rc;
+  rc = lam_merge(g_stage.ctx, dtype, n, d, dv[0], dv[1], dv[2], static_cast<int64_t*>(dv[3]),
+                 dv[4], dv[5], dv[6], static_cast<int64_t*>(dv[7]), dv[8], dv[9], dv[10],
+                 static_cast<int64_t*>(dv[11]), g_stage.stream);
+  if (rc != LAM_OK) return rc;
+  auto s = g_stage.stream;
+  LAM_CUDA(cudaMemcpyAsync(o_acc, dv[8], n * d * e, cudaMemcpyDeviceToHost, s));
+  LAM_CUDA(cudaMemcpyAsync(o_max, dv[9], n * e, cudaMemcpyDeviceToHost, s));
+  LAM_CUDA(cudaMemcpyAsync(o_log_denom, dv[10], n * e, cudaMemcpyDeviceToHost, s));
+  LAM_CUDA(cudaMemcpyAsync(o_count, dv[11], n * 8, cudaMemcpyDeviceToHost, s));
+  LAM_CUDA(cudaStreamSynchronize(s));
+  return LAM_OK;
+}
+
+int lam_finalize_host(int dtype, int64_t n, int32_t d, const void* acc, const void* log_denom,
+                      const int64_t* count, void* out) {
+  int rc = g_stage.init();
+  if (rc != LAM_OK) return rc;
+  const int e = elem_bytes(dtype);
+  if (e == 0) return fail(LAM_ERR_VALIDATION, "bad dtype");
+  if (n <= 0) return LAM_OK;
+  std::vector<void*> dv;
+  rc = stage_in(0, {{acc, n * d * e}, {log_denom, n * e}, {count, n * 8}, {nullptr, n * d * e}},
+                dv);
+  if (rc != LAM_OK) return rc;
+  rc = lam_finalize(g_stage.ctx, dtype, n, d, dv[0], dv[1], static_cast<int64_t*>(dv[2]), dv[3],
+                    g_stage.stream);
+  if (rc != LAM_OK) return rc;
+  LAM_CUDA(cudaMemcpyAsync(out, dv[3], n * d * e, cudaMemcpyDeviceToHost, g_stage.stream));
+  LAM_CUDA(cudaStreamSynchronize(g_stage.stream));
+  return LAM_OK;
+}
+
+// ---------------- partitioning (host logic) ----------------
+
+int lam_head_partition(int64_t num_kv_heads, int64_t num_devices, int64_t* ranges) {
+  if (num_kv_heads < 1) return fail(LAM_ERR_VALIDATION, "num_kv_heads must be >= 1");
+  if (num_devices < 1) return fail(LAM_ERR_VALIDATION, "num_devices must be >= 1");
+  if (num_kv_heads % num_devices != 0)
+    return fail(LAM_ERR_VALIDATION,
+                "head partition requires num_kv_heads divisible by num_devices (" +
+                    std::to_string(num_kv_heads) + " % " + std::to_string(num_devices) +
+                    " != 0)");
+  const int64_t per = num_kv_heads / num_devices;
+  for (int64_t i = 0; i < num_devices; ++i) {
+    ranges[2 * i] = i * per;
+    ranges[2 * i + 1] = (i + 1) * per;
+  }
+  return LAM_OK;
+}
+
+int lam_request_partition(const double* kv_sizes, int64_t n, int64_t num_devices,
+                          int64_t* device_of, double* device_load, double* imbalance) {
+  if (num_devices < 1) return fail(LAM_ERR_VALIDATION, "num_devices must be >= 1");
+  for (int64_t i = 0; i < n; ++i) device_of[i] = 0;
+  for (int64_t d = 0; d < num_devices; ++d) device_load[d] = 0.0;
+  std::vector<int64_t> order(static_cast<size_t>(n));
+  std::iota(order.begin(), order.end(), int64_t{0});
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int64_t a, int64_t b) { return kv_sizes[a] > kv_sizes[b]; });
+  for (int64_t r : order) {
+    int64_t t = 0;
+    for (int64_t d = 1; d < num_devices; ++d)
+      if (device_load[d] < device_load[t]) t = d;
+    device_of[r] = t;
+    device_load[t] += kv_sizes[r];
+  }
+  double total = 0, peak = device_load[0];
+  for (int64_t d = 0; d < num_devices; ++d) {
+    total += device_load[d];
+    peak = std::max(peak, device_load[d]);
+  }
+  const double mean = total / static_cast<double>(num_devices);
+  *imbalance = mean > 0 ? peak / mean : 1.0;
+  return LAM_OK;
+}
+
+// ---------------- production decode path ----------------
+
+int lam_decode_plan(lam_ctx* ctx, const lam_decode_args* a, int32_t* kernel, int32_t* num_splits,
+                    int32_t* split_tokens) {
+  if (!ctx) return fail(LAM_ERR_VALIDATION, "null context");
+  LAM_CUDA(cudaSetDevice(ctx->device));
+  Plan pl;
+  int rc = plan_decode(ctx, a, &pl);
+  if (rc != LAM_OK) return rc;
+  if (kernel) *kernel = pl.kernel;
+  if (num_splits) *num_splits = pl.S;
+  if (split_tokens) *split_tokens = pl.chunk;
+  return LAM_OK;
+}
+
+int lam_decode(lam_ctx* ctx, const lam_decode_args* a, void* stream) {
+  if (!ctx) return fail(LAM_ERR_VALIDATION, "null context");
+  Plan pl;
+  int rc = plan_decode(ctx, a, &pl);
+  if (rc != LAM_OK) return rc;
+  if (a->batch == 0) return LAM_OK;
+  const int G = a->num_q_heads / a->num_kv_heads;
+  const int D = a->head_dim;
+  lam::DecodeParams p{};
+  p.q = a->q;
+  p.k_pool = a->k_pool;
+  p.v_pool = a->v_pool;
+  p.page_table = a->page_table;
+  p.seq_lens = a->seq_lens;
+  p.out = a->out;
+  p.lse = a->lse;
+  p.B = a->batch;
+  p.Hq = a->num_q_heads;
+  p.Hkv = a->num_kv_heads;
+  p.G = G;
+  p.D = D;
+  p.page_size = a->page_size;
+  p.pt_stride = a->pt_stride;
+  p.chunk = pl.chunk;
+  p.S = pl.S;
+  p.QG = pl.QG;
+  p.scale = a->scale;
+  p.scale_log2 = a->scale * 1.4426950408889634f;
+  p.out_f32 = a->out_dtype == LAM_F32;
+  if (pl.S > 1) {
+    const int64_t rows = static_cast<int64_t>(a->batch) * a->num_q_heads * pl.S;
+    const int64_t cnt = static_cast<int64_t>(a->batch) * a->num_kv_heads * pl.QG;
+    if (rows * D > ctx->ws_acc_cap || rows * 2 > ctx->ws_ml_cap || cnt > ctx->counters_cap) {
+      rc = lam_ctx_reserve(ctx, std::max<int64_t>(rows, ctx->ws_ml_cap / 2), D,
+                           std::max<int64_t>(cnt, ctx->counters_cap));
+      if (rc != LAM_OK) return rc;
+    }
+    p.ws_acc = ctx->ws_acc;
+    p.ws_ml = ctx->ws_ml;
+    p.counters = ctx->counters;
+  }
+  auto s = static_cast<cudaStream_t>(stream);
+  if (pl.kernel == LAM_KERNEL_GQA_MMA) {
+    const int64_t rows = a->page_table
+                             ? a->num_pages * a->num_kv_heads * static_cast<int64_t>(a->page_size)
+                             : static_cast<int64_t>(a->batch) * a->num_kv_heads * a->page_size;
+    if (rows >= (int64_t{1} << 31))
+      return fail(LAM_ERR_VALIDATION, "pool exceeds 2^31 rows for the tensor map");
+    CUtensorMap kmap, vmap;
+    rc = make_pool_map(&kmap, a->kv_dtype, a->k_pool, rows, D);
+    if (rc != LAM_OK) return rc;
+    rc = make_pool_map(&vmap, a->kv_dtype, a->v_pool, rows, D);
+    if (rc != LAM_OK) return rc;
+    LAM_CUDA(lam::launch_decode_mma(a->kv_dtype, p, kmap, vmap, pl.S, s));
+  } else {
+    LAM_CUDA(lam::launch_decode_simt(a->kv_dtype, D, pl.GQ, p, pl.S, s));
+  }
+  return LAM_OK;
+}
+
+int lam_kv_append(int32_t dtype, int32_t batch, int32_t num_kv_heads, int32_t head_dim,
+                  int32_t page_size, int32_t pt_stride, const int32_t* page_table,
+                  const int32_t* positions, const void* k_new, const void* v_new, void* k_pool,
+                  void* v_pool, void* stream) {
+  const int e = elem_bytes(dtype);
+  if (e == 0 || (head_dim * e) % 16 != 0)
+    return fail(LAM_ERR_VALIDATION, "kv_append needs rows that are a multiple of 16 bytes");
+  if (page_size < 1) return fail(LAM_ERR_VALIDATION, "page_size must be >= 1");
+  LAM_CUDA(lam::launch_kv_append(e, batch, num_kv_heads, head_dim, page_size, pt_stride,
+                                 page_table, positions, k_new, v_new, k_pool, v_pool,
+                                 static_cast<cudaStream_t>(stream)));
+  return LAM_OK;
+}
+
+int lam_kv_gather(int32_t dtype, int32_t batch, int32_t num_kv_heads, int32_t head_dim,
+                  int32_t page_size, int32_t pt_stride, const int32_t* page_table,
+                  const int32_t* seq_lens, int32_t l_max, const void* pool, void* dense,
+                  void* stream) {
+  const int e = elem_bytes(dtype);
+  if (e == 0 || (head_dim * e) % 16 != 0)
+    return fail(LAM_ERR_VALIDATION, "kv_gather needs rows that are a multiple of 16 bytes");
+  if (!page_table) return fail(LAM_ERR_VALIDATION, "kv_gather needs a page table");
+  LAM_CUDA(lam::launch_kv_gather(e, batch, num_kv_heads, head_dim, page_size, pt_stride,
+                                 page_table, seq_lens, l_max, pool, dense,
+                                 static_cast<cudaStream_t>(stream)));
+  return LAM_OK;
+}
+
+int lam_decode_step_host(lam_ctx* ctx, const lam_decode_args* a, const void* h_q,
+                         const void* h_k_new, const void* h_v_new, void* h_out, void* d_k_new,
+                         void* d_v_new, const int32_t* d_positions, void* stream) {
+  if (!ctx || !a) return fail(LAM_ERR_VALIDATION, "null context or args");
+  auto s = static_cast<cudaStream_t>(stream);
+  const int e = elem_bytes(a->kv_dtype);
+  const int eo = elem_bytes(a->out_dtype);
+  const int64_t qb = static_cast<int64_t>(a->batch) * a->num_q_heads * a->head_dim * e;
+  const int64_t kb = static_cast<int64_t>(a->batch) * a->num_kv_heads * a->head_dim * e;
+  const int64_t ob = static_cast<int64_t>(a->batch) * a->num_q_heads * a->head_dim * eo;
+  LAM_CUDA(cudaMemcpyAsync(const_cast<void*>(a->q), h_q, qb, cudaMemcpyHostToDevice, s));
+  LAM_CUDA(cudaMemcpyAsync(d_k_new, h_k_new, kb, cudaMemcpyHostToDevice, s));
+  LAM_CUDA(cudaMemcpyAsync(d_v_new, h_v_new, kb, cudaMemcpyHostToDevice, s));
+  int rc = lam_kv_append(a->kv_dtype, a->batch, a->num_kv_heads, a->head_dim, a->page_size,
+                         a->pt_stride, a->page_table, d_positions, d_k_new, d_v_new,
+                         const_cast<void*>(a->k_pool), const_cast<void*>(a->v_pool), stream);
+  if (rc != LAM_OK) return rc;
+  rc = lam_decode(ctx, a, stream);
+  if (rc != LAM_OK) return rc;
+  LAM_CUDA(cudaMemcpyAsync(h_out, a->out, ob, cudaMemcpyDeviceToHost, s));
+  return LAM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,231 @@
+// decode_gqa_mma.cuh — split-K GQA decode attention on tensor cores.
+//
+// With grouped-query attention (attention.hpp:75-76, attention.cpp:141-150) the G query
+// heads that share a KV head turn the per-token GEMV into a genuine small contraction:
+//   S^T[tokens x G]  = K[tokens x d] · Q^T[d x G]
+//   O^T[d x G]      += V^T[d x tokens] · P^T[tokens x G]
+// Both are mma.sync m16n8k16 with N = G = 8 (fp32 accumulate), so the KV tile is read
+// from HBM once for all G heads and no MMA lane is padding when G == 8.
+//
+// One CTA = (request, kv head, split); warp NW is the TMA producer, warps 0..NW-1 each own
+// 16 tokens of every 64-token tile.  K/V tiles arrive through 2-D tensor-map TMA with the
+// 128-byte swizzle (two 64-column boxes per 128-wide row block), so the ldmatrix fragment
+// loads are bank-conflict free.  The S^T accumulator is turned into the P^T B-operand
+// in registers (exp2 -> bf16 pack -> movmatrix.trans), never touching shared memory.
+#pragma once
+
+#include "decode_common.cuh"
+
+namespace lam {
+
+struct MmaCfg {
+  static constexpr int NW = 4;
+  static constexpr int TILE = 64;  // tokens per stage, 16 per consumer warp
+  static constexpr int STAGES = 3;
+  static constexpr int D = 128;
+  static constexpr int GQ = 8;
+  static constexpr int BOX_BYTES = TILE * 64 * 2;    // [64 rows][64 cols] 16-bit = 8 KB
+  static constexpr int MAT_BYTES = 2 * BOX_BYTES;    // one K (or V) tile, 16 KB
+  static constexpr int STAGE_BYTES = 2 * MAT_BYTES;  // K + V
+  static constexpr int RING_BYTES = STAGES * STAGE_BYTES;
+  static constexpr int RED_BYTES = NW * GQ * (D + 2) * 4;
+  static constexpr int MAIN_BYTES = RING_BYTES > RED_BYTES ? RING_BYTES : RED_BYTES;
+  static constexpr int SMEM_BYTES = MAIN_BYTES + 2 * STAGES * 8 + 16 + 1024;  // +align slack
+};
+
+// Byte offset of 16-byte chunk `c` (0..15 across the 128-wide row) of tile row `r`
+// inside one K or V tile stored as two 128B-swizzled boxes.
+__device__ __forceinline__ uint32_t swz(int r, int c) {
+  return (c >> 3) * MmaCfg::BOX_BYTES + r * 128 + (((c & 7) ^ (r & 7)) << 4);
+}
+
+template <typename T>
+__global__ void __launch_bounds__((MmaCfg::NW + 1) * 32)
+    decode_gqa_mma_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap kmap,
+                          const __grid_constant__ CUtensorMap vmap) {
+  using C = MmaCfg;
+  constexpr int NW = C::NW, TILE = C::TILE, STAGES = C::STAGES, D = C::D, GQ = C::GQ;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::MAIN_BYTES);
+  uint64_t* empty = full + STAGES;
+  int* s_flag = reinterpret_cast<int*>(empty + STAGES);
+
+  const int split = blockIdx.x;
+  const int kvh = blockIdx.y;
+  const int b = blockIdx.z;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int G = p.G;  // real q heads in the group (<= 8); the rest are zero padding
+
+  const int len = __ldg(p.seq_lens + b);
+  const int t_begin = split * p.chunk;
+  const int t_end = min(len, t_begin + p.chunk);
+  const int n_tiles = t_end > t_begin ? (t_end - t_begin + TILE - 1) / TILE : 0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    fence_barrier_init();
+  }
+  if (warp == NW && lane == 0) {
+    prefetch_tensormap(&kmap);
+    prefetch_tensormap(&vmap);
+  }
+  __syncthreads();
+
+  if (warp == NW) {
+    if (lane == 0 && n_tiles > 0) {
+      const uint64_t pol = policy_evict_first();
+      for (int i = 0; i < n_tiles; ++i) {
+        const int s = i % STAGES;
+        if (i >= STAGES) mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
+        const int tok = t_begin + i * TILE;
+        const int32_t row = static_cast<int32_t>(kv_row(p, b, kvh, tok));
+        uint8_t* st = smem + s * C::STAGE_BYTES;
+        mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
+        tma_load_2d(st, &kmap, 0, row, &full[s], pol);
+        tma_load_2d(st + C::BOX_BYTES, &kmap, 64, row, &full[s], pol);
+        tma_load_2d(st + C::MAT_BYTES, &vmap, 0, row, &full[s], pol);
+        tma_load_2d(st + C::MAT_BYTES + C::BOX_BYTES, &vmap, 64, row, &full[s], pol);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  const int gr = lane >> 2;       // fragment "group" row
+  const int gc = (lane & 3) * 2;  // fragment column pair
+  // Q^T B-fragments: b0 = Q[g=gr][ks*16 + gc .. +1], b1 = Q[g=gr][ks*16 + 8 + gc .. +1].
+  uint32_t qf[8][2];
+  {
+    const int qh = kvh * G + gr;
+    const uint32_t* qrow = reinterpret_cast<const uint32_t*>(
+        static_cast<const T*>(p.q) + (static_cast<int64_t>(b) * p.Hq + qh) * D);
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      qf[ks][0] = gr < G ? __ldg(qrow + (ks * 16 + gc) / 2) : 0u;
+      qf[ks][1] = gr < G ? __ldg(qrow + (ks * 16 + 8 + gc) / 2) : 0u;
+    }
+  }
+  const float sl2 = p.scale_log2;
+
+  float m0 = -INFINITY, m1 = -INFINITY;  // running max (log2 units) of columns gc, gc+1
+  float l0 = 0.f, l1 = 0.f;              // this lane's share of the softmax sums
+  float o[8][4];
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) o[mt][e] = 0.f;
+
+  // per-lane ldmatrix row/chunk selectors
+  const int a_row = (lane & 7) + ((lane >> 3) & 1) * 8;  // K: x4 matrices {r0-7,r8-15}x{c,c+1}
+  const int a_chk = lane >> 4;
+  const int v_row = (lane & 7) + (lane >> 4) * 8;        // V^T: {c,c+1}x{r0-7,r8-15}
+  const int v_chk = (lane >> 3) & 1;
+
+  const uint32_t base = smem_u32(smem);
+  for (int i = 0; i < n_tiles; ++i) {
+    const int s = i % STAGES;
+    mbar_wait(&full[s], (i / STAGES) & 1);
+    const int tok0 = t_begin + i * TILE + warp * 16;
+    const int nval = min(16, t_end - tok0);
+    const uint32_t kb = base + s * C::STAGE_BYTES;
+    const uint32_t vb = kb + C::MAT_BYTES;
+    if (nval > 0) {
+      if (nval < 16) {
+        // rows past the sequence end hold stale data: zero this warp's V rows so that
+        // p = 0 never meets a non-finite value in the P·V product.
+        uint8_t* vrows = smem + s * C::STAGE_BYTES + C::MAT_BYTES;
+        for (int r = nval; r < 16; ++r) {
+          const int tr = warp * 16 + r;
+          reinterpret_cast<uint2*>(vrows + (lane >> 4) * C::BOX_BYTES + tr * 128)[lane & 15] =
+              make_uint2(0u, 0u);
+        }
+        __syncwarp();
+      }
+      // S^T = K · Q^T
+      float c[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        uint32_t a0, a1, a2, a3;
+        ldmatrix_x4(kb + swz(warp * 16 + a_row, ks * 2 + a_chk), a0, a1, a2, a3);
+        Mma16816<T>::run(c, a0, a1, a2, a3, qf[ks][0], qf[ks][1]);
+      }
+      // logits (log2 units); rows gr and gr+8 of the warp's 16 tokens
+      const bool ok_lo = gr < nval, ok_hi = gr + 8 < nval;
+      const float x0 = ok_lo ? c[0] * sl2 : -INFINITY;
+      const float x1 = ok_lo ? c[1] * sl2 : -INFINITY;
+      const float x2 = ok_hi ? c[2] * sl2 : -INFINITY;
+      const float x3 = ok_hi ? c[3] * sl2 : -INFINITY;
+      float t0 = fmaxf(x0, x2), t1 = fmaxf(x1, x3);
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) {
+        t0 = fmaxf(t0, __shfl_xor_sync(0xffffffffu, t0, off));
+        t1 = fmaxf(t1, __shfl_xor_sync(0xffffffffu, t1, off));
+      }
+      const float n0 = fmaxf(m0, t0), n1 = fmaxf(m1, t1);  // finite: >= 1 valid token
+      const float al0 = m0 == -INFINITY ? 0.f : exp2f(m0 - n0);
+      const float al1 = m1 == -INFINITY ? 0.f : exp2f(m1 - n1);
+      m0 = n0;
+      m1 = n1;
+      const uint32_t plo = Elem<T>::pack2(exp2f(x0 - n0), exp2f(x1 - n1));
+      const uint32_t phi = Elem<T>::pack2(exp2f(x2 - n0), exp2f(x3 - n1));
+      // the softmax sums use the rounded weights actually fed to the MMA, so the output
+      // stays an exact convex combination of the value rows.
+      float r0, r1, r2, r3;
+      Elem<T>::unpack2(plo, r0, r1);
+      Elem<T>::unpack2(phi, r2, r3);
+      l0 = l0 * al0 + (r0 + r2);
+      l1 = l1 * al1 + (r1 + r3);
+      const uint32_t b0 = movmatrix_trans(plo);
+      const uint32_t b1 = movmatrix_trans(phi);
+      // O^T = O^T * alpha + V^T · P^T
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        o[mt][0] *= al0;
+        o[mt][1] *= al1;
+        o[mt][2] *= al0;
+        o[mt][3] *= al1;
+        uint32_t a0, a1, a2, a3;
+        ldmatrix_x4_trans(vb + swz(warp * 16 + v_row, mt * 2 + v_chk), a0, a1, a2, a3);
+        Mma16816<T>::run(o[mt], a0, a1, a2, a3, b0, b1);
+      }
+      if (nval < 16) fence_proxy_async_smem();  // generic zero-stores before the next TMA
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+
+  // reduce the softmax sums over the 8 row groups (lanes with equal lane&3).
+#pragma unroll
+  for (int off = 4; off < 32; off <<= 1) {
+    l0 += __shfl_xor_sync(0xffffffffu, l0, off);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, off);
+  }
+
+  named_bar_sync(1, NW * 32);
+  float* red_m = reinterpret_cast<float*>(smem);
+  float* red_l = red_m + NW * GQ;
+  float* red_acc = red_l + NW * GQ;
+  if (gr == 0) {
+    red_m[warp * GQ + gc] = m0;
+    red_m[warp * GQ + gc + 1] = m1;
+    red_l[warp * GQ + gc] = l0;
+    red_l[warp * GQ + gc + 1] = l1;
+  }
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt) {
+    const int d = mt * 16 + gr;
+    red_acc[(warp * GQ + gc) * D + d] = o[mt][0];
+    red_acc[(warp * GQ + gc + 1) * D + d] = o[mt][1];
+    red_acc[(warp * GQ + gc) * D + d + 8] = o[mt][2];
+    red_acc[(warp * GQ + gc + 1) * D + d + 8] = o[mt][3];
+  }
+  named_bar_sync(1, NW * 32);
+  finish_cta<T, D, GQ, NW, true>(p, b, kvh, 0, split, G, red_m, red_l, red_acc, s_flag);
+}
+
+}  // namespace lam

@@ -1,0 +1,135 @@
+"""Device-tensor API of the production decode path (torch tensors in, torch tensors out).
+
+torch provides device memory and streams only; every kernel is ours (liblamina_attn.so):
+
+  decode(q, k_pool, v_pool, seq_lens, ...)  split-K decode attention (SIMT or GQA tensor-core)
+  kv_append(...)                            bit-exact new-token write into the paged pools
+  kv_gather(...)                            paged -> dense copy (inverse of the paging)
+
+KV pools are [num_pages, Hkv, page_size, D] with a page table [B, pt_stride] (paged), or
+[B, Hkv, l_max, D] with page_table=None (dense, the reference's per-request layout).
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import _lib
+from ._lib import DecodeArgs, check
+
+_DT = {torch.float32: _lib.LAM_F32, torch.bfloat16: _lib.LAM_BF16, torch.float16: _lib.LAM_F16}
+_KERNELS = {"auto": _lib.LAM_KERNEL_AUTO, "simt": _lib.LAM_KERNEL_SIMT,
+            "gqa_mma": _lib.LAM_KERNEL_GQA_MMA}
+
+
+def _stream_ptr(stream) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _require_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise _lib.ValidationError("decode path tensors must live on a CUDA device")
+
+
+def make_args(q: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor,
+              seq_lens: torch.Tensor, *, page_table: torch.Tensor | None = None,
+              max_len: int | None = None, scale: float | None = None,
+              out: torch.Tensor | None = None, out_dtype: torch.dtype | None = None,
+              lse: torch.Tensor | None = None, kernel: str = "auto",
+              split_tokens: int = 0) -> tuple[DecodeArgs, torch.Tensor]:
+    """Fill lam_decode_args from tensors; returns (args, out)."""
+    _require_cuda(q, k_pool, v_pool, seq_lens, page_table)
+    if q.dim() != 3:
+        raise _lib.ValidationError("q must be [B, Hq, D]")
+    B, Hq, D = q.shape
+    if k_pool.dim() != 4 or k_pool.shape != v_pool.shape:
+        raise _lib.ValidationError("k_pool/v_pool must be equal-shaped 4-D pools")
+    Hkv, P = k_pool.shape[1], k_pool.shape[2]
+    if k_pool.shape[3] != D:
+        raise _lib.ValidationError("pool head_dim differs from q")
+    if k_pool.dtype != q.dtype or v_pool.dtype != q.dtype:
+        raise _lib.ValidationError("q and the KV pools must share a dtype")
+    for t in (q, k_pool, v_pool):
+        if not t.is_contiguous():
+            raise _lib.ValidationError("decode tensors must be contiguous")
+    if seq_lens.dtype != torch.int32:
+        raise _lib.ValidationError("seq_lens must be int32")
+    if page_table is not None and page_table.dtype != torch.int32:
+        raise _lib.ValidationError("page_table must be int32")
+    odt = out_dtype or (out.dtype if out is not None else q.dtype)
+    if out is None:
+        out = torch.empty((B, Hq, D), dtype=odt, device=q.device)
+    a = DecodeArgs()
+    a.kv_dtype = _DT[q.dtype]
+    a.out_dtype = _DT[odt]
+    a.batch, a.num_q_heads, a.num_kv_heads, a.head_dim = B, Hq, Hkv, D
+    a.scale = float(scale if scale is not None else 1.0 / math.sqrt(D))
+    a.page_size = P
+    a.pt_stride = page_table.shape[1] if page_table is not None else 0
+    a.max_len = int(max_len if max_len is not None else
+                    (page_table.shape[1] * P if page_table is not None else P))
+    a.split_tokens = int(split_tokens)
+    a.kernel = _KERNELS[kernel]
+    a.num_pages = k_pool.shape[0] if page_table is not None else 0
+    a.q, a.k_pool, a.v_pool = q.data_ptr(), k_pool.data_ptr(), v_pool.data_ptr()
+    a.page_table = page_table.data_ptr() if page_table is not None else None
+    a.seq_lens = seq_lens.data_ptr()
+    a.out = out.data_ptr()
+    a.lse = lse.data_ptr() if lse is not None else None
+    return a, out
+
+
+def decode(q, k_pool, v_pool, seq_lens, *, page_table=None, max_len=None, scale=None, out=None,
+           out_dtype=None, return_lse=False, kernel="auto", split_tokens=0, ctx=None,
+           stream=None):
+    """softmax(q K^T scale) V per (request, q head) over the request's first seq_lens[b]
+    tokens; q head h reads KV head h // (Hq // Hkv)."""
+    lse = None
+    if return_lse:
+        lse = torch.empty(q.shape[:2], dtype=torch.float32, device=q.device)
+    a, out = make_args(q, k_pool, v_pool, seq_lens, page_table=page_table, max_len=max_len,
+                       scale=scale, out=out, out_dtype=out_dtype, lse=lse, kernel=kernel,
+                       split_tokens=split_tokens)
+    ctx = ctx or _lib.context(q.device.index or 0)
+    check(_lib.load().lam_decode(ctx.handle, a, _stream_ptr(stream)))
+    return (out, lse) if return_lse else out
+
+
+def plan(q, k_pool, v_pool, seq_lens, **kw):
+    """(kernel family, splits, tokens per split) lam_decode would use."""
+    ctx = kw.pop("ctx", None) or _lib.context(q.device.index or 0)
+    a, _ = make_args(q, k_pool, v_pool, seq_lens, **kw)
+    import ctypes as C
+
+    k, s, t = C.c_int32(), C.c_int32(), C.c_int32()
+    check(_lib.load().lam_decode_plan(ctx.handle, a, C.byref(k), C.byref(s), C.byref(t)))
+    names = {_lib.LAM_KERNEL_SIMT: "simt", _lib.LAM_KERNEL_GQA_MMA: "gqa_mma"}
+    return names[k.value], s.value, t.value
+
+
+def kv_append(k_new, v_new, k_pool, v_pool, positions, page_table=None, stream=None):
+    """k_pool[page(b, pos)][h][pos % P] = k_new[b][h] (and V), pos = positions[b]."""
+    _require_cuda(k_new, v_new, k_pool, v_pool, positions, page_table)
+    B, Hkv, D = k_new.shape
+    P = k_pool.shape[2]
+    pts = page_table.shape[1] if page_table is not None else 0
+    check(_lib.load().lam_kv_append(
+        _DT[k_new.dtype], B, Hkv, D, P, pts,
+        page_table.data_ptr() if page_table is not None else None, positions.data_ptr(),
+        k_new.data_ptr(), v_new.data_ptr(), k_pool.data_ptr(), v_pool.data_ptr(),
+        _stream_ptr(stream)))
+
+
+def kv_gather(pool, page_table, seq_lens, l_max, stream=None):
+    """Dense [B, Hkv, l_max, D] copy of the first seq_lens[b] tokens of each request."""
+    _require_cuda(pool, page_table, seq_lens)
+    B = seq_lens.shape[0]
+    _, Hkv, P, D = pool.shape
+    dense = torch.zeros((B, Hkv, l_max, D), dtype=pool.dtype, device=pool.device)
+    check(_lib.load().lam_kv_gather(_DT[pool.dtype], B, Hkv, D, P, page_table.shape[1],
+                                    page_table.data_ptr(), seq_lens.data_ptr(), l_max,
+                                    pool.data_ptr(), dense.data_ptr(), _stream_ptr(stream)))
+    return dense

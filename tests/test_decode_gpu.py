@@ -1,0 +1,214 @@
+"""Parity of the production decode path (lam_decode, lam_kv_append, lam_kv_gather) against
+the CPU oracle on identical inputs.
+
+Tolerances (north star): fp32 KV max-abs <= 1e-5 against exact_attention<float>;
+bf16/fp16 KV max-abs <= 2e-3 against exact_attention<float> on the exactly upcast values
+(fp32 output, so the bound measures the kernel, not the final rounding).  Paging and
+appends are bit-exact.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from tests.helpers import make_dense, oracle_decode, page_table_for, to_paged
+
+pytestmark = pytest.mark.gpu
+
+TOL = {torch.float32: 1e-5, torch.bfloat16: 2e-3, torch.float16: 2e-3}
+
+
+def _decode(*a, **kw):
+    from paper_2405_01814_b200 import decode as dec
+
+    return dec.decode(*a, **kw)
+
+
+def _lens_t(lens):
+    return torch.tensor(np.asarray(lens, np.int32), device="cuda")
+
+
+def _maxabs(a, b):
+    return float(np.max(np.abs(np.asarray(a, np.float64) - np.asarray(b, np.float64))))
+
+
+def test_config1_fp32_mha_full_parity(built):
+    """BASELINE config 1: B=8, 32 heads, d=128, l=1024, fp32 — every head vs the oracle."""
+    B, H, D, L = 8, 32, 128, 1024
+    q, k, v = make_dense(B, H, H, D, L, torch.float32, seed=1)
+    lens = [L] * B
+    scale = 1 / math.sqrt(D)
+    want = oracle_decode(q, k, v, lens, scale)
+    for split in (0, 256, 96):
+        out = _decode(q, k, v, _lens_t(lens), scale=scale, split_tokens=split)
+        torch.cuda.synchronize()
+        assert _maxabs(out.cpu().numpy(), want) <= 1e-5, split
+
+
+def test_golden_fixtures(built, golden):
+    for name, dtype in (("decode_mha_f32.npz", torch.float32), ("decode_gqa_bf16.npz", torch.bfloat16)):
+        g = golden(name)
+        q = torch.tensor(g["q"], device="cuda").to(dtype)
+        k = torch.tensor(g["k"], device="cuda").to(dtype)
+        v = torch.tensor(g["v"], device="cuda").to(dtype)
+        out = _decode(q, k, v, _lens_t(g["lens"]), scale=float(g["scale"]), out_dtype=torch.float32)
+        assert _maxabs(out.cpu().numpy(), g["out_f32"]) <= TOL[dtype], name
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+@pytest.mark.parametrize("paged", [False, True])
+def test_decode_vs_oracle(built, dtype, G, paged):
+    B, Hkv, D = 3, 2, 128
+    Hq = Hkv * G
+    lens = [1, 77, 300]
+    lmax = 320
+    q, k, v = make_dense(B, Hq, Hkv, D, lmax, dtype, seed=G * 10 + int(paged))
+    for b, l in enumerate(lens):  # poison rows past the sequence end
+        k[b, :, l:] = float("nan")
+        v[b, :, l:] = float("nan")
+    scale = 1 / math.sqrt(D)
+    want, want_lse = oracle_decode(q, k, v, lens, scale, want_lse=True)
+    if paged:
+        P = 64
+        pt, npages = page_table_for(lens, P, seed=G)
+        kp, vp = to_paged(k, lens, P, pt, npages), to_paged(v, lens, P, pt, npages)
+        ptt = torch.tensor(pt, device="cuda")
+    else:
+        kp, vp, ptt = k, v, None
+    for split in (0, 64, 128):
+        out, lse = _decode(q, kp, vp, _lens_t(lens), page_table=ptt, max_len=max(lens),
+                           scale=scale, out_dtype=torch.float32, split_tokens=split,
+                           return_lse=True)
+        torch.cuda.synchronize()
+        assert _maxabs(out.cpu().numpy(), want) <= TOL[dtype], (split,)
+        assert _maxabs(lse.cpu().numpy(), want_lse) <= 1e-3, (split,)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_paged_equals_dense_bitwise(built, dtype):
+    B, Hq, Hkv, D = 4, 16, 2 if dtype == torch.bfloat16 else 16, 128
+    lens = [64, 640, 1000, 5]
+    lmax = 1024
+    q, k, v = make_dense(B, Hq, Hkv, D, lmax, dtype, seed=7)
+    pt, npages = page_table_for(lens, 64, seed=3)
+    kp, vp = to_paged(k, lens, 64, pt, npages), to_paged(v, lens, 64, pt, npages)
+    for split in (128, 0):
+        a = _decode(q, k, v, _lens_t(lens), split_tokens=split, max_len=max(lens))
+        b = _decode(q, kp, vp, _lens_t(lens), page_table=torch.tensor(pt, device="cuda"),
+                    split_tokens=split, max_len=max(lens))
+        assert torch.equal(a, b)
+        c = _decode(q, k, v, _lens_t(lens), split_tokens=split, max_len=max(lens))
+        assert torch.equal(a, c)  # deterministic
+
+
+def test_bf16_output_is_rounded_fp32_output(built):
+    q, k, v = make_dense(2, 16, 2, 128, 200, torch.bfloat16, seed=5)
+    lens = _lens_t([200, 150])
+    a = _decode(q, k, v, lens, out_dtype=torch.float32)
+    b = _decode(q, k, v, lens)
+    assert b.dtype == torch.bfloat16
+    assert torch.equal(a.to(torch.bfloat16), b)
+
+
+def test_empty_sequence_gives_zeros(built):
+    q, k, v = make_dense(2, 4, 4, 128, 64, torch.float32, seed=9)
+    out, lse = _decode(q, k, v, _lens_t([0, 64]), return_lse=True)
+    assert torch.all(out[0] == 0) and torch.all(torch.isinf(lse[0]))
+    want = oracle_decode(q[1:], k[1:], v[1:], [64], 1 / math.sqrt(128))
+    assert _maxabs(out[1:].cpu().numpy(), want) <= 1e-5
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_kv_append_and_gather_are_bit_exact(built, dtype):
+    from oracle import oracle as O
+    from paper_2405_01814_b200 import decode as dec
+
+    B, Hkv, D, P = 3, 4, 128, 32
+    lens = [70, 1, 33]
+    pt, npages = page_table_for(lens, P, seed=11)
+    ptt = torch.tensor(pt, device="cuda")
+    g = torch.Generator(device="cuda").manual_seed(0)
+    kp = torch.zeros((npages, Hkv, P, D), dtype=dtype, device="cuda")
+    vp = torch.zeros_like(kp)
+    dense_k = torch.randn((B, Hkv, max(lens), D), generator=g, device="cuda").to(dtype)
+    dense_v = torch.randn((B, Hkv, max(lens), D), generator=g, device="cuda").to(dtype)
+    for b in range(B):
+        dense_k[b, :, lens[b]:] = 0
+        dense_v[b, :, lens[b]:] = 0
+    # append token by token (all requests at once, positions per request)
+    for t in range(max(lens)):
+        active = [b for b in range(B) if t < lens[b]]
+        pos = torch.tensor([t if b in active else lens[b] - 1 for b in range(B)],
+                           dtype=torch.int32, device="cuda")
+        kn = torch.stack([dense_k[b, :, min(t, lens[b] - 1)] for b in range(B)])
+        vn = torch.stack([dense_v[b, :, min(t, lens[b] - 1)] for b in range(B)])
+        dec.kv_append(kn.contiguous(), vn.contiguous(), kp, vp, pos, ptt)
+    lens_t = _lens_t(lens)
+    gk = dec.kv_gather(kp, ptt, lens_t, max(lens))
+    gv = dec.kv_gather(vp, ptt, lens_t, max(lens))
+    assert torch.equal(gk, dense_k) and torch.equal(gv, dense_v)
+    # the oracle's byte-level paging agrees with the pool the kernel wrote
+    rb = D * kp.element_size()
+    pool_bytes = kp.view(torch.uint8).cpu().numpy().reshape(npages, Hkv, P, rb)
+    dense_bytes = O.page_gather(pool_bytes, pt, np.array(lens, np.int32), max(lens))
+    assert np.array_equal(dense_bytes, dense_k.view(torch.uint8).cpu().numpy().reshape(dense_bytes.shape))
+
+
+def test_dense_append(built):
+    from paper_2405_01814_b200 import decode as dec
+
+    k = torch.zeros((2, 3, 16, 64), dtype=torch.bfloat16, device="cuda")
+    v = torch.zeros_like(k)
+    kn = torch.randn((2, 3, 64), device="cuda").to(torch.bfloat16)
+    vn = torch.randn((2, 3, 64), device="cuda").to(torch.bfloat16)
+    dec.kv_append(kn, vn, k, v, torch.tensor([5, 15], dtype=torch.int32, device="cuda"))
+    assert torch.equal(k[0, :, 5], kn[0]) and torch.equal(k[1, :, 15], kn[1])
+    assert torch.equal(v[0, :, 5], vn[0]) and float(k.float().abs().sum() - kn.float().abs().sum()) == 0
+
+
+def test_validation_errors(built):
+    from paper_2405_01814_b200 import _lib
+    from paper_2405_01814_b200 import decode as dec
+
+    q, k, v = make_dense(1, 6, 4, 128, 64, torch.bfloat16)
+    with pytest.raises(_lib.ValidationError):
+        dec.decode(q, k, v, _lens_t([64]))  # 6 % 4 != 0
+    q, k, v = make_dense(1, 8, 8, 96, 64, torch.float32)
+    with pytest.raises(_lib.ValidationError):
+        dec.decode(q, k, v, _lens_t([64]))  # head_dim 96 unsupported on this path
+    q, k, v = make_dense(1, 8, 1, 128, 64, torch.bfloat16)
+    with pytest.raises(_lib.ValidationError):
+        dec.decode(q, k[:, :, :32].contiguous(), v[:, :, :32].contiguous(), _lens_t([64]),
+                   max_len=64)  # dense: length exceeds the row capacity
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", ["c3", "c4"])
+def test_llama2_70b_layer_subset_parity(built, cfg):
+    """BASELINE configs 3/4 at full size for one layer (paged bf16, GQA 64/8): a seeded
+    subset of (request, q head) pairs against the oracle, all heads finite and bounded."""
+    B, L = (128, 4096) if cfg == "c3" else (32, 32768)
+    Hq, Hkv, D, P = 64, 8, 128, 64
+    npages = B * L // P
+    g = torch.Generator(device="cuda").manual_seed(3)
+    kp = torch.empty((npages, Hkv, P, D), dtype=torch.bfloat16, device="cuda").uniform_(-1, 1, generator=g)
+    vp = torch.empty_like(kp).uniform_(-1, 1, generator=g)
+    q = torch.empty((B, Hq, D), dtype=torch.bfloat16, device="cuda").uniform_(-1, 1, generator=g)
+    perm = torch.randperm(npages, generator=torch.Generator().manual_seed(5)).to(torch.int32)
+    pt = perm.view(B, L // P).cuda()
+    lens = _lens_t([L] * B)
+    out = _decode(q, kp, vp, lens, page_table=pt, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out).all() and out.abs().max() <= 1.0
+    rng = np.random.default_rng(0)
+    bs = rng.choice(B, 3, replace=False)
+    scale = 1 / math.sqrt(D)
+    for b in bs:
+        kd = kp[pt[b].long()].permute(1, 0, 2, 3).reshape(1, Hkv, L, D)
+        vd = vp[pt[b].long()].permute(1, 0, 2, 3).reshape(1, Hkv, L, D)
+        heads = rng.choice(Hq, 4, replace=False)
+        want = oracle_decode(q[b:b + 1], kd, vd, [L], scale, pairs=[(0, int(h)) for h in heads])
+        for h in heads:
+            assert _maxabs(out[b, h].cpu().numpy(), want[0, h]) <= 2e-3

@@ -1,0 +1,165 @@
+"""The reference operator API, executed on the GPU, against the reference.
+
+1. The reference's own tests/test_attention.cpp (15 cases, 1571 checks), compiled unmodified
+   against our C++ drop-in (oracle/Makefile -> oracle/_ref/test_attention_dropin).
+2. The Python mirror on the reference's golden fixtures and properties.
+"""
+import subprocess
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _rel(a, b):
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-12)))
+
+
+def test_reference_test_file_passes_through_dropin(built):
+    if not O.REF_TEST_DROPIN.exists():
+        pytest.skip("oracle/_ref/test_attention_dropin not built")
+    r = subprocess.run([str(O.REF_TEST_DROPIN)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "15 passed | 0 failed" in r.stdout
+    assert "1571 passed | 0 failed" in r.stdout
+
+
+@pytest.mark.parametrize("name", ["instances_seed42.npz", "instances_seed7.npz",
+                                  "instances_seed3.npz"])
+def test_exact_and_partial_vs_reference(built, golden, name):
+    from paper_2405_01814_b200 import attention as A
+
+    g = golden(name)
+    for i in range(g["q"].shape[0]):
+        inst = A.AttnInstance(g["q"][i], g["k"][i], g["v"][i], float(g["scale"][i]))
+        assert _rel(A.exact_attention(inst), g["exact"][i]) <= 1e-12
+        p = A.partial_attention(inst, np.arange(inst.length()))
+        assert p.token_count == inst.length()
+        assert p.max_logit == g["max_logit"][i]  # max is exact
+        assert abs(p.log_denom - g["log_denom"][i]) <= 1e-12 * max(1.0, abs(g["log_denom"][i]))
+        assert _rel(A.finalize(p), g["exact"][i]) <= 1e-6
+
+
+def test_merge_trees_vs_reference(built, golden):
+    from paper_2405_01814_b200 import attention as A
+
+    g = golden("merge_trees_seed6.npz")
+    for i in range(int(g["n"])):
+        inst = A.AttnInstance(g[f"q_{i}"], g[f"k_{i}"], g[f"v_{i}"], float(g[f"scale_{i}"]))
+        part_of = g[f"part_of_{i}"]
+        parts = [np.nonzero(part_of == p)[0] for p in range(int(part_of.max()) + 1)]
+        fwd = A.PartialAttention.identity(inst.head_dim())
+        for p in parts:
+            fwd = A.merge(fwd, A.partial_attention(inst, p))
+        rev = A.PartialAttention.identity(inst.head_dim())
+        for p in reversed(parts):
+            rev = A.merge(rev, A.partial_attention(inst, p))
+        a, b = A.finalize(fwd), A.finalize(rev)
+        assert _rel(a, b) <= 1e-7
+        assert _rel(a, g[f"tree_{i}"]) <= 1e-6
+        assert _rel(a, g[f"exact_{i}"]) <= 1e-6
+        # identity law is bitwise (test_attention.cpp:86-97)
+        m = A.merge(fwd, A.PartialAttention.identity(inst.head_dim()))
+        assert np.array_equal(m.acc, fwd.acc) and m.log_denom == fwd.log_denom
+        assert m.max_logit == fwd.max_logit and m.token_count == fwd.token_count
+
+
+def test_known_answers_and_errors(built):
+    from paper_2405_01814_b200 import attention as A
+
+    rng = np.random.default_rng(1)
+    v = rng.uniform(-1, 1, (1, 8))
+    inst = A.AttnInstance(rng.uniform(-1, 1, 8), rng.uniform(-2, 2, (1, 8)), v, 0.3)
+    assert np.array_equal(A.exact_attention(inst), v[0])           # l = 1 -> value row
+    q0 = A.AttnInstance(np.zeros(4), rng.uniform(-1, 1, (5, 4)), rng.uniform(-1, 1, (5, 4)), 0.5)
+    assert np.allclose(A.exact_attention(q0), q0.values.mean(0), rtol=1e-12, atol=0)
+    with pytest.raises(A.Error):
+        A.exact_attention(A.AttnInstance(np.ones(1), np.zeros((0, 1)), np.zeros((0, 1)), 1.0))
+    with pytest.raises(A.Error):
+        A.partial_attention(q0, [0, 5])                            # index out of range
+    e = A.partial_attention(q0, [])
+    assert e.empty() and e.log_denom == -np.inf and np.all(e.acc == 0)
+    with pytest.raises(A.Error):
+        A.finalize(e)
+    single = A.partial_attention(q0, [3])
+    assert np.array_equal(A.finalize(single), q0.values[3])
+    prev, fresh = A.split_prev_new(q0, 4)
+    assert fresh.token_count == 1
+    assert _rel(A.finalize(A.merge(prev, fresh)), A.exact_attention(q0)) <= 1e-12
+    with pytest.raises(A.Error):
+        A.split_prev_new(q0, 6)
+    with pytest.raises(A.ValidationError):
+        A.merge(A.partial_attention(q0, [1]),
+                A.partial_attention(A.AttnInstance(np.ones(3), np.ones((2, 3)), np.ones((2, 3))), [0]))
+
+
+def test_float_instantiation(built):
+    from paper_2405_01814_b200 import attention as A
+
+    rng = np.random.default_rng(10)
+    inst = A.AttnInstance(rng.uniform(-1, 1, 8).astype(np.float32),
+                          rng.uniform(-1, 1, (32, 8)).astype(np.float32),
+                          rng.uniform(-1, 1, (32, 8)).astype(np.float32), np.float32(8 ** -0.5))
+    got = A.finalize(A.partial_attention(inst, np.arange(32)))
+    want = O.exact(inst.query, inst.keys, inst.values, float(inst.scale))
+    assert got.dtype == np.float32
+    assert np.allclose(got, want, rtol=1e-4, atol=1e-6)
+
+
+def test_multi_head_gqa_is_exact(built):
+    """Head-partition stitching and GQA-vs-replicated MHA are bitwise (test_attention.cpp:210-269)."""
+    from paper_2405_01814_b200 import attention as A
+
+    rng = np.random.default_rng(11)
+    hq, hkv, l, d = 8, 4, 12, 4
+    inst = A.MultiHeadInstance(rng.uniform(-1, 1, (hq, d)), rng.uniform(-1, 1, (hkv, l, d)),
+                               rng.uniform(-1, 1, (hkv, l, d)), 0.5)
+    full = A.multi_head_attention(inst)
+    g = hq // hkv
+    stitched = np.zeros_like(full)
+    for r in A.head_partition(hkv, 2):
+        shard = A.MultiHeadInstance(inst.queries[r.begin * g: r.end * g],
+                                    inst.kv_keys[r.begin: r.end], inst.kv_values[r.begin: r.end],
+                                    inst.scale)
+        stitched[r.begin * g: r.end * g] = A.multi_head_attention(shard)
+    assert np.array_equal(stitched, full)
+    rep = A.MultiHeadInstance(inst.queries, np.repeat(inst.kv_keys, g, 0),
+                              np.repeat(inst.kv_values, g, 0), inst.scale)
+    assert np.array_equal(A.multi_head_attention(rep), full)
+    for h in range(hq):
+        want = O.exact(inst.queries[h], inst.kv_keys[h // g], inst.kv_values[h // g], 0.5)
+        assert _rel(full[h], want) <= 1e-12
+
+
+def test_acceptance_criterion_3(built):
+    """acceptance.cpp:132-205 (seed 20240809): 1000 random merge trees, tree <= 1e-6 and
+    commutativity <= 1e-7 against exact, identity exact — on the reference's generators."""
+    from paper_2405_01814_b200 import attention as A
+
+    if not O.ref_available():
+        pytest.skip("needs the reference generators (oracle/_ref)")
+    rng = O.RefRng(20240809)
+    worst_tree = worst_comm = 0.0
+    for trial in range(200):
+        d = 1 + rng.next() % 64
+        l = 2 + rng.next() % 255
+        parts = 1 + rng.next() % 8
+        q, k, v, s = rng.random_instance(d, l, 80)
+        inst = A.AttnInstance(q, k, v, s)
+        exact = O.exact(q, k, v, s, lib="ref")
+        partials = [A.partial_attention(inst, p) for p in rng.random_partition(l, parts)]
+        fwd = A.PartialAttention.identity(d)
+        for p in partials:
+            fwd = A.merge(fwd, p)
+        rev = A.PartialAttention.identity(d)
+        for p in reversed(partials):
+            rev = A.merge(rev, p)
+        a, b = A.finalize(fwd), A.finalize(rev)
+        worst_tree = max(worst_tree, _rel(a, exact))
+        worst_comm = max(worst_comm, _rel(a, b))
+        m = A.merge(fwd, A.PartialAttention.identity(d))
+        assert np.array_equal(m.acc, fwd.acc) and m.log_denom == fwd.log_denom
+    assert worst_tree <= 1e-6 and worst_comm <= 1e-7
