@@ -38,7 +38,8 @@ def test_exact_and_partial_vs_reference(built, golden, name):
         assert _rel(A.exact_attention(inst), g["exact"][i]) <= 1e-12
         p = A.partial_attention(inst, np.arange(inst.length()))
         assert p.token_count == inst.length()
-        assert p.max_logit == g["max_logit"][i]  # max is exact
+        # logits are q.k*scale with FMA contraction on the GPU: equal to ~1 ulp, not bitwise
+        assert abs(p.max_logit - g["max_logit"][i]) <= 1e-12 * max(1.0, abs(g["max_logit"][i]))
         assert abs(p.log_denom - g["log_denom"][i]) <= 1e-12 * max(1.0, abs(g["log_denom"][i]))
         assert _rel(A.finalize(p), g["exact"][i]) <= 1e-6
 
