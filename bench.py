@@ -244,10 +244,22 @@ class Workload:
         self.B_local = w["B"]                 # requests whose q/k/v this rank produces
         self.B = w["B"] * world               # requests whose local heads this rank attends
         self.layers = w["layers"]
-        if w.get("mixed"):
-            self.lens = np.concatenate([mixed_lengths(w["B"], 2024 + r) for r in range(world)])
-        else:
-            self.lens = np.full(self.B, w["l"], np.int32)
+        self.mb = 2 if world > 1 else 1       # staggered micro-batches (multi-GPU only)
+        self.geo = None
+        if world > 1:
+            from paper_2405_01814_b200.dist import ShardGeometry
+
+            self.geo = ShardGeometry(rank, world, self.layers, self.B_local, self.Hq, self.Hkv,
+                                     self.D, self.mb)
+        # per-source request lengths; attention-side rows are micro-batch major
+        src_lens = [mixed_lengths(w["B"], 2024 + r) if w.get("mixed")
+                    else np.full(w["B"], w["l"], np.int32) for r in range(world)]
+        self.lens = np.zeros(self.B, np.int32)
+        for src in range(world):
+            for b in range(self.B_local):
+                row = self.geo.kv_row(src, b) if self.geo else b
+                self.lens[row] = src_lens[src][b]
+        self.B_launch = self.B // self.mb
         self.max_len = int(self.lens.max())
         esz = torch.tensor([], dtype=self.dtype).element_size()
         P = w["P"]
@@ -285,24 +297,34 @@ class Workload:
         self.positions = (self.seq_lens - 1).contiguous()
         gi = torch.Generator(device=device).manual_seed(99 + rank)
         # model-worker side inputs for this rank's B_local requests, per layer
-        self.q_in = torch.empty((self.layers, self.B_local, self.Hq, self.D), dtype=self.dtype,
-                                device=device).uniform_(-1, 1, generator=gi)
-        self.kn_in = torch.empty((self.layers, self.B_local, self.Hkv, self.D), dtype=self.dtype,
-                                 device=device).uniform_(-1, 1, generator=gi)
+        if self.geo is None:
+            qs = (self.layers, self.B_local, self.Hq, self.D)
+            ks = (self.layers, self.B_local, self.Hkv, self.D)
+        else:
+            qs, ks = self.geo.q_shape(), self.geo.kv_shape()
+        self.q_in = torch.empty(qs, dtype=self.dtype, device=device).uniform_(-1, 1, generator=gi)
+        self.kn_in = torch.empty(ks, dtype=self.dtype, device=device).uniform_(-1, 1, generator=gi)
         self.vn_in = torch.empty_like(self.kn_in).uniform_(-1, 1, generator=gi)
-        self.out = torch.empty((self.layers, self.B_local, self.Hq, self.D), dtype=self.dtype,
-                               device=device)
+        self.out = torch.empty(qs, dtype=self.dtype, device=device)
+        # reference attn_cost bytes of one step over ALL requests and heads (whole job)
         self.step_bytes = float(PF.kv_bytes_per_token(self.spec)) * float(self.lens.sum())
-        self.decode_bytes_per_launch = float(self.lens.sum()) * 2 * self.hkv_local * self.D * esz
+        # this rank's algorithmic bytes per decode launch (its KV heads, one micro-batch)
+        self.decode_bytes_per_launch = (float(self.lens.sum()) * 2 * self.hkv_local * self.D *
+                                        esz / self.mb)
         # plan once (fixed shapes): kernel family + splits; reserve the split-K workspace
         from paper_2405_01814_b200 import decode as dec
 
-        qd = torch.empty((self.B, self.hq_local, self.D), dtype=self.dtype, device=device)
-        kw = dict(page_table=self.page_table, max_len=self.max_len)
-        self.kernel, self.splits, self.chunk = dec.plan(qd, self.k_layers[0], self.v_layers[0],
-                                                        self.seq_lens, ctx=self.ctx, **kw)
-        self.ctx.reserve(self.B * self.hq_local * max(self.splits, 1), self.D,
-                         self.B * self.hkv_local)
+        qd = torch.empty((self.B_launch, self.hq_local, self.D), dtype=self.dtype, device=device)
+        kw = dict(page_table=self.page_table[: self.B_launch] if self.page_table is not None
+                  else None, max_len=self.max_len)
+        self.kernel, self.splits, self.chunk = dec.plan(
+            qd, self.k_layers[0], self.v_layers[0], self.seq_lens[: self.B_launch], ctx=self.ctx,
+            **kw)
+        self.ctx.reserve(self.B_launch * self.hq_local * max(self.splits, 1), self.D,
+                         self.B_launch * self.hkv_local)
+
+    def rows(self, m: int):
+        return slice(m * self.B_launch, (m + 1) * self.B_launch)
 
     def layer_pools(self, layer: int, step: int = 0):
         i = (step * self.layers + layer) % self.resident
@@ -332,7 +354,20 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
     if world > 1:
         from paper_2405_01814_b200.dist import HeadShardedAttention
 
-        engine = HeadShardedAttention(W, dist)
+        def append(layer, m, k, v):
+            kp, vp = W.layer_pools(layer)
+            sl = W.rows(m)
+            dec.kv_append(k, v, kp, vp, W.positions[sl],
+                          W.page_table[sl] if W.page_table is not None else None)
+
+        def attend(layer, m, q, out):
+            kp, vp = W.layer_pools(layer)
+            sl = W.rows(m)
+            dec.decode(q, kp, vp, W.seq_lens[sl],
+                       page_table=W.page_table[sl] if W.page_table is not None else None,
+                       max_len=W.max_len, out=out, ctx=W.ctx, split_tokens=W.chunk)
+
+        engine = HeadShardedAttention(W.geo, dist, append, attend, device, W.dtype)
 
     counter = [0]
 
@@ -355,7 +390,8 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
         if engine is None:
             step_local(ev)
         else:
-            engine.step(ev)
+            engine.step(W.q_in, W.kn_in, W.vn_in, W.out,
+                        [e for pair in ev for e in pair] if ev is not None else None)
 
     def barrier():
         torch.cuda.synchronize(device)
@@ -369,8 +405,8 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
     barrier()
 
     # ---- timed region (device-resident inputs)
-    ev = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(W.layers)]
-          for _ in range(args.steps)]
+    ev = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)]
+           for _ in range(W.layers * W.mb)] for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(device.index if "CUDA_VISIBLE_DEVICES" not in os.environ else
                            int(os.environ["CUDA_VISIBLE_DEVICES"].split(",")[device.index]))
@@ -385,8 +421,7 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
     barrier()
     clocks = sampler.stop() if rank == 0 else None
     ms_total = t0.elapsed_time(t1)
-    kern_ms = [ev[s][l][0].elapsed_time(ev[s][l][1]) for s in range(args.steps)
-               for l in range(W.layers)]
+    kern_ms = [e[0].elapsed_time(e[1]) for s in range(args.steps) for e in ev[s]]
     ms_step = ms_total / max(args.steps, 1)
     if dist is not None:
         t = torch.tensor([ms_step, statistics.mean(kern_ms)], device=device)
@@ -394,7 +429,7 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
         ms_step, kern_avg = float(t[0]), float(t[1])
     else:
         kern_avg = statistics.mean(kern_ms)
-    launches = args.steps * W.layers * 2
+    launches = args.steps * W.layers * W.mb * 2
 
     # ---- end-to-end through the C-ABI host-buffer entry point (pinned host buffers)
     e2e = None
@@ -407,8 +442,7 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
         return
     peaks = measured_peaks()
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    total_bytes = W.step_bytes * world
-    value = total_bytes / (ms_step / 1e3) / 1e9
+    value = W.step_bytes / (ms_step / 1e3) / 1e9
     achieved = W.decode_bytes_per_launch / (kern_avg / 1e3) / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
@@ -462,7 +496,31 @@ def run_e2e(args, W, engine, dist, device, stream):
     h_vn = W.vn_in.cpu().pin_memory()
     h_out = torch.empty(W.out.shape, dtype=W.out.dtype).pin_memory()
     if engine is not None:
-        return engine.e2e(args, h_q, h_kn, h_vn, h_out)
+        def step_mg():
+            W.q_in.copy_(h_q, non_blocking=True)
+            W.kn_in.copy_(h_kn, non_blocking=True)
+            W.vn_in.copy_(h_vn, non_blocking=True)
+            engine.step(W.q_in, W.kn_in, W.vn_in, W.out)
+            h_out.copy_(W.out, non_blocking=True)
+
+        for _ in range(max(1, args.warmup)):
+            step_mg()
+        torch.cuda.synchronize(device)
+        dist.barrier()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(args.steps):
+            step_mg()
+        t1.record(stream)
+        torch.cuda.synchronize(device)
+        t = torch.tensor([t0.elapsed_time(t1) / max(args.steps, 1)], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+        h2d = (h_q.numel() + h_kn.numel() + h_vn.numel()) * h_q.element_size()
+        d2h = h_out.numel() * h_out.element_size()
+        return {"value": W.step_bytes / (ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
+                "h2d_bytes_per_step": int(h2d) * W.world, "d2h_bytes_per_step": int(d2h) * W.world,
+                "api": "HeadShardedAttention.step (pinned host in/out, NCCL all-to-all)"}
     d_q = torch.empty_like(W.q_in[0])
     d_kn = torch.empty_like(W.kn_in[0])
     d_vn = torch.empty_like(W.vn_in[0])

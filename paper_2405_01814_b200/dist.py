@@ -1,0 +1,205 @@
+"""KV-head-sharded attention worker pool over torch.distributed (NCCL on GPUs, gloo on CPU).
+
+The paper's attention-offload step (reference SPEC/PAPER; modeled analytically in
+core/src/sim.cpp:286-346) on N GPUs of one box:
+
+* head_partition (attention.cpp:164-177): rank j owns KV heads [j*Hkv/N, (j+1)*Hkv/N) of every
+  request, and therefore q heads [j*Hq/N, (j+1)*Hq/N).  Sharding by heads needs no
+  cross-GPU reduction: outputs concatenate by head exactly (test_attention.cpp:237-256).
+* Every rank is also a model worker for B_local requests.  Per layer it scatters those
+  requests' Q, K_new, V_new to the head owners and gathers the attention outputs back —
+  the send-Q / send-KV / return-output messages of sim.cpp:310-316, (2 + 2/G) e d B per layer
+  (perf.cpp:142-148), as NCCL all-to-alls.
+* Two staggered micro-batches (the n = 2 rotational schedule, pipeline.cpp:30-33, 44-118):
+  micro-batch 1's scatter and micro-batch 0's gather run on a communication stream while the
+  other micro-batch's attention runs on the compute stream, so the step approaches
+  max(attention, communication) (sim.cpp:374-379).
+
+Layouts (all contiguous, micro-batch outermost so every collective moves one contiguous
+buffer):  inputs  q_in [L, MB, N, Bh, hq_l, D], k_in/v_in [L, MB, N, Bh, hkv_l, D] where the
+N axis is the destination head shard; outputs out [L, MB, N, Bh, hq_l, D] where N is the
+source head shard.  On the attention side request r of micro-batch m from source s is row
+m*N*Bh + s*Bh + i of the KV store, so a micro-batch is a contiguous slice of the page table.
+The local append/attend ops are injected: the GPU path passes our kernels (lam_kv_append,
+lam_decode); the CPU gloo test passes the oracle.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable
+
+import torch
+
+
+@dataclass
+class ShardGeometry:
+    rank: int
+    world: int
+    layers: int
+    B_local: int
+    Hq: int
+    Hkv: int
+    D: int
+    micro_batches: int = 2
+
+    def __post_init__(self):
+        if self.Hkv % self.world:
+            raise ValueError(
+                f"head partition requires num_kv_heads divisible by num_devices "
+                f"({self.Hkv} % {self.world} != 0)")
+        if self.B_local % self.micro_batches:
+            raise ValueError("B_local must split evenly into micro-batches")
+
+    @property
+    def hq_l(self) -> int:
+        return self.Hq // self.world
+
+    @property
+    def hkv_l(self) -> int:
+        return self.Hkv // self.world
+
+    @property
+    def Bh(self) -> int:
+        return self.B_local // self.micro_batches
+
+    @property
+    def B_mb(self) -> int:
+        """requests per micro-batch on the attention side"""
+        return self.world * self.Bh
+
+    @property
+    def B_attn(self) -> int:
+        return self.world * self.B_local
+
+    def kv_row(self, src: int, b_local: int) -> int:
+        """attention-side row of request b_local of model worker src"""
+        m, i = divmod(b_local, self.Bh)
+        return m * self.B_mb + src * self.Bh + i
+
+    def q_shape(self):
+        return (self.layers, self.micro_batches, self.world, self.Bh, self.hq_l, self.D)
+
+    def kv_shape(self):
+        return (self.layers, self.micro_batches, self.world, self.Bh, self.hkv_l, self.D)
+
+
+class HeadShardedAttention:
+    """One rank of the attention worker pool.
+
+    append(layer, mb, k[B_mb, hkv_l, D], v[...])          writes the new tokens
+    attend(layer, mb, q[B_mb, hq_l, D], out[B_mb, hq_l, D])  local decode attention
+    """
+
+    def __init__(self, geo: ShardGeometry, dist, append: Callable, attend: Callable,
+                 device: torch.device, dtype: torch.dtype):
+        self.geo, self.dist = geo, dist
+        self.append_fn, self.attend_fn = append, attend
+        self.device, self.dtype = device, dtype
+        g = geo
+        MB = g.micro_batches
+        # attention-side receive / send buffers, one per micro-batch
+        self.q_r = [torch.empty((g.world, g.Bh, g.hq_l, g.D), dtype=dtype, device=device)
+                    for _ in range(MB)]
+        self.k_r = [torch.empty((g.world, g.Bh, g.hkv_l, g.D), dtype=dtype, device=device)
+                    for _ in range(MB)]
+        self.v_r = [torch.empty_like(self.k_r[0]) for _ in range(MB)]
+        self.o_l = [torch.empty_like(self.q_r[0]) for _ in range(MB)]
+        self.cuda = device.type == "cuda"
+        if self.cuda:
+            self.comm = torch.cuda.Stream(device=device)
+            self.compute = torch.cuda.current_stream(device)
+
+    # ---- collectives ----
+    def _a2a(self, out: torch.Tensor, inp: torch.Tensor):
+        self.dist.all_to_all_single(out, inp)
+
+    def step(self, q_in, k_in, v_in, out, ev=None):
+        """One decode step over all layers; returns when the work is enqueued (CUDA) or done
+        (CPU).  `ev`, if given, is a list of (start, end) CUDA event pairs, one per local
+        attention launch, recorded on the compute stream."""
+        g = self.geo
+        MB = g.micro_batches
+        if not self.cuda:
+            for layer in range(g.layers):
+                for m in range(MB):
+                    self._scatter(layer, m, q_in, k_in, v_in)
+                    self._attend(layer, m, None)
+                    self._a2a(out[layer, m], self.o_l[m])
+            return
+        comm, comp = self.comm, self.compute
+        comm.wait_stream(comp)  # inputs produced on the compute stream are visible
+        scat = [[torch.cuda.Event() for _ in range(MB)] for _ in range(g.layers)]
+        done = [[torch.cuda.Event() for _ in range(MB)] for _ in range(g.layers)]
+        gath = [torch.cuda.Event() for _ in range(MB)]
+
+        def scatter(layer, m):
+            with torch.cuda.stream(comm):
+                if layer > 0:
+                    # micro-batch m's next layer follows its previous output gather (data
+                    # dependency through the model worker) and the reuse of its receive buffers
+                    comm.wait_event(done[layer - 1][m])
+                self._scatter(layer, m, q_in, k_in, v_in)
+                scat[layer][m].record(comm)
+
+        def gather(layer, m):
+            with torch.cuda.stream(comm):
+                comm.wait_event(done[layer][m])
+                self._a2a(out[layer, m], self.o_l[m])
+                gath[m].record(comm)
+
+        for m in range(MB):
+            scatter(0, m)
+        k = 0
+        for layer in range(g.layers):
+            for m in range(MB):
+                comp.wait_event(scat[layer][m])
+                if layer > 0:
+                    comp.wait_event(gath_prev[m])  # o_l[m] free again
+                e = ev[k] if ev is not None else None
+                k += 1
+                self._attend(layer, m, e)
+                done[layer][m].record(comp)
+                gather(layer, m)
+                if layer + 1 < g.layers:
+                    scatter(layer + 1, m)
+            gath_prev = list(gath)
+            gath = [torch.cuda.Event() for _ in range(MB)]
+        comp.wait_stream(comm)
+
+    def _scatter(self, layer, m, q_in, k_in, v_in):
+        self._a2a(self.q_r[m], q_in[layer, m])
+        self._a2a(self.k_r[m], k_in[layer, m])
+        self._a2a(self.v_r[m], v_in[layer, m])
+
+    def _attend(self, layer, m, e):
+        g = self.geo
+        kr = self.k_r[m].view(g.B_mb, g.hkv_l, g.D)
+        vr = self.v_r[m].view(g.B_mb, g.hkv_l, g.D)
+        self.append_fn(layer, m, kr, vr)
+        if e is not None:
+            e[0].record(self.compute)
+        self.attend_fn(layer, m, self.q_r[m].view(g.B_mb, g.hq_l, g.D),
+                       self.o_l[m].view(g.B_mb, g.hq_l, g.D))
+        if e is not None:
+            e[1].record(self.compute)
+
+
+def stitch_outputs(out: torch.Tensor) -> torch.Tensor:
+    """[L, MB, N(src shard), Bh, hq_l, D] -> [L, B_local, Hq, D] head-major (test helper and
+    the layout a consumer of concatenated heads expects)."""
+    L, MB, N, Bh, hq_l, D = out.shape
+    return out.permute(0, 1, 3, 2, 4, 5).reshape(L, MB * Bh, N * hq_l, D)
+
+
+def shard_inputs(q: torch.Tensor, kn: torch.Tensor, vn: torch.Tensor, world: int,
+                 micro_batches: int = 2):
+    """[L, B_local, H, D] head-major model-worker tensors -> destination-major send layout."""
+    L, B, Hq, D = q.shape
+    Hkv = kn.shape[2]
+    Bh = B // micro_batches
+
+    def f(x, H):
+        return (x.view(L, micro_batches, Bh, world, H // world, D)
+                .permute(0, 1, 3, 2, 4, 5).contiguous())
+
+    return f(q, Hq), f(kn, Hkv), f(vn, Hkv)

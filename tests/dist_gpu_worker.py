@@ -1,0 +1,98 @@
+"""torchrun worker for tests/test_dist_gpu.py: the KV-head-sharded engine with the real kernels
+(lam_kv_append + lam_decode over a paged store) over NCCL, checked against the CPU oracle."""
+import math
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+from oracle import oracle as O  # noqa: E402
+from paper_2405_01814_b200 import decode as dec  # noqa: E402
+from paper_2405_01814_b200.dist import (HeadShardedAttention, ShardGeometry, shard_inputs,  # noqa: E402
+                                        stitch_outputs)
+from paper_2405_01814_b200.kvcache import PagedKVCache  # noqa: E402
+
+L, B_LOCAL, HQ, HKV, D, MB, P = 3, 8, 64, 8, 128, 2, 64
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    dev = torch.device("cuda", int(os.environ["LOCAL_RANK"]))
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", device_id=dev)
+    geo = ShardGeometry(rank, world, L, B_LOCAL, HQ, HKV, D, MB)
+    rng = np.random.default_rng(11)
+    B = world * B_LOCAL
+    lens = rng.integers(1, 300, B).astype(np.int32)           # tokens cached before the step
+    lmax = int(lens.max()) + 1
+    bf = lambda x: torch.from_numpy(x).to(torch.bfloat16)  # noqa: E731
+    ck = bf(rng.uniform(-1, 1, (L, B, HKV, lmax, D)).astype(np.float32))
+    cv = bf(rng.uniform(-1, 1, (L, B, HKV, lmax, D)).astype(np.float32))
+    q = bf(rng.uniform(-1, 1, (L, B, HQ, D)).astype(np.float32))
+    kn = bf(rng.uniform(-1, 1, (L, B, HKV, D)).astype(np.float32))
+    vn = bf(rng.uniform(-1, 1, (L, B, HKV, D)).astype(np.float32))
+
+    h0, h1 = rank * geo.hkv_l, (rank + 1) * geo.hkv_l
+    row_req = np.zeros(geo.B_attn, np.int64)
+    for src in range(world):
+        for b in range(B_LOCAL):
+            row_req[geo.kv_row(src, b)] = src * B_LOCAL + b
+    row_lens = lens[row_req] + 1
+    cache = PagedKVCache(L, geo.hkv_l, D, P, int((-(-row_lens // P)).sum()) + 2, geo.B_attn,
+                         int(-(-row_lens.max() // P)), dtype=torch.bfloat16, device=dev,
+                         shuffle_seed=rank)
+    cache.set_lengths(row_lens)
+    cache.sync()
+    pt = cache.page_table_host
+    for layer in range(L):  # prefill the cached prefix (test infrastructure: torch indexing)
+        for r, req in enumerate(row_req):
+            for t in range(lens[req]):
+                page, off = pt[r, t // P], t % P
+                cache.k[layer, page, :, off] = ck[layer, req, h0:h1, t].to(dev)
+                cache.v[layer, page, :, off] = cv[layer, req, h0:h1, t].to(dev)
+    positions = torch.tensor(row_lens - 1, dtype=torch.int32, device=dev)
+
+    def append(layer, m, k, v):
+        sl = slice(m * geo.B_mb, (m + 1) * geo.B_mb)
+        dec.kv_append(k, v, cache.k[layer], cache.v[layer], positions[sl], cache.page_table[sl])
+
+    def attend(layer, m, qr, out):
+        sl = slice(m * geo.B_mb, (m + 1) * geo.B_mb)
+        dec.decode(qr, cache.k[layer], cache.v[layer], cache.seq_lens[sl],
+                   page_table=cache.page_table[sl], max_len=int(row_lens.max()), out=out)
+
+    eng = HeadShardedAttention(geo, dist, append, attend, dev, torch.bfloat16)
+    mine = slice(rank * B_LOCAL, (rank + 1) * B_LOCAL)
+    q_in, k_in, v_in = (t.to(dev) for t in shard_inputs(q[:, mine], kn[:, mine], vn[:, mine],
+                                                        world, MB))
+    out = torch.zeros(geo.q_shape(), dtype=torch.bfloat16, device=dev)
+    eng.step(q_in, k_in, v_in, out)
+    torch.cuda.synchronize()
+    got = stitch_outputs(out).float().cpu().numpy()
+    worst = 0.0
+    for layer in range(L):
+        for b in range(B_LOCAL):
+            req = rank * B_LOCAL + b
+            k = ck[layer, req:req + 1].float().numpy().copy()
+            v = cv[layer, req:req + 1].float().numpy().copy()
+            k[0, :, lens[req]] = kn[layer, req].float().numpy()
+            v[0, :, lens[req]] = vn[layer, req].float().numpy()
+            want = O.decode_dense(q[layer, req:req + 1].float().numpy(), k, v, [lens[req] + 1],
+                                  1 / math.sqrt(D))[0]
+            worst = max(worst, float(np.abs(got[layer, b] - want).max()))
+    # bf16 output: kernel tolerance 2e-3 plus the final bf16 rounding of |out| <= 1
+    ok = worst <= 2e-3 + 2 ** -9
+    print(f"rank {rank} worst max-abs {worst:.3e} {'OK' if ok else 'FAIL'}", flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()

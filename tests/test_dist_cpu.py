@@ -1,0 +1,119 @@
+"""The multi-GPU exchange logic (paper_2405_01814_b200/dist.py) on CPU: world_size 2 over gloo.
+
+Each rank is a model worker for B_local requests and the attention worker for half the KV
+heads.  The local append/attend ops are the CPU oracle (injected), so this test checks the
+sharding, the all-to-all layouts, the micro-batch row mapping and the output stitching; the
+GPU kernels are covered by the -m gpu tests.  Result: every request's attention output equals
+the single-process oracle over all heads, and appended tokens land where decode reads them.
+"""
+import os
+import socket
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+ROOT = Path(__file__).resolve().parent.parent
+
+L, B_LOCAL, HQ, HKV, D, WORLD, MB = 2, 4, 8, 4, 8, 2, 2
+
+
+def _global_problem(seed=7):
+    rng = np.random.default_rng(seed)
+    B = WORLD * B_LOCAL
+    lens = rng.integers(1, 20, B).astype(np.int32)       # cached tokens before this step
+    lmax = int(lens.max()) + 1
+    cache_k = rng.uniform(-1, 1, (L, B, HKV, lmax, D)).astype(np.float32)
+    cache_v = rng.uniform(-1, 1, (L, B, HKV, lmax, D)).astype(np.float32)
+    q = rng.uniform(-1, 1, (L, B, HQ, D)).astype(np.float32)
+    kn = rng.uniform(-1, 1, (L, B, HKV, D)).astype(np.float32)
+    vn = rng.uniform(-1, 1, (L, B, HKV, D)).astype(np.float32)
+    return lens, lmax, cache_k, cache_v, q, kn, vn
+
+
+def _expected(layer, req):
+    from oracle import oracle as O
+
+    lens, lmax, ck, cv, q, kn, vn = _global_problem()
+    k = ck[layer, req:req + 1].copy()
+    v = cv[layer, req:req + 1].copy()
+    k[0, :, lens[req]] = kn[layer, req]
+    v[0, :, lens[req]] = vn[layer, req]
+    return O.decode_dense(q[layer, req:req + 1], k, v, [lens[req] + 1], 1 / np.sqrt(D))[0]
+
+
+def _worker(rank, port, result_dir):
+    sys.path.insert(0, str(ROOT))
+    import torch.distributed as dist
+
+    from oracle import oracle as O
+    from paper_2405_01814_b200.dist import (HeadShardedAttention, ShardGeometry, shard_inputs,
+                                            stitch_outputs)
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    geo = ShardGeometry(rank, WORLD, L, B_LOCAL, HQ, HKV, D, MB)
+    lens, lmax, ck, cv, q, kn, vn = _global_problem()
+    h0, h1 = rank * geo.hkv_l, (rank + 1) * geo.hkv_l
+    # attention-side store: rows in micro-batch-major order, this rank's KV heads only
+    row_req = np.zeros(geo.B_attn, np.int64)
+    for src in range(WORLD):
+        for b in range(B_LOCAL):
+            row_req[geo.kv_row(src, b)] = src * B_LOCAL + b
+    store_k = ck[:, row_req, h0:h1].copy()
+    store_v = cv[:, row_req, h0:h1].copy()
+    pos = lens[row_req]                     # new token position of each row
+
+    def append(layer, m, k, v):
+        rows = range(m * geo.B_mb, (m + 1) * geo.B_mb)
+        for i, r in enumerate(rows):
+            store_k[layer, r, :, pos[r]] = k[i].numpy()
+            store_v[layer, r, :, pos[r]] = v[i].numpy()
+
+    def attend(layer, m, qr, out):
+        sl = slice(m * geo.B_mb, (m + 1) * geo.B_mb)
+        res = O.decode_dense(qr.numpy(), store_k[layer, sl], store_v[layer, sl], pos[sl] + 1,
+                             1 / np.sqrt(D))
+        out.copy_(torch.from_numpy(res))
+
+    eng = HeadShardedAttention(geo, dist, append, attend, torch.device("cpu"), torch.float32)
+    mine = slice(rank * B_LOCAL, (rank + 1) * B_LOCAL)
+    q_in, k_in, v_in = shard_inputs(torch.from_numpy(q[:, mine]), torch.from_numpy(kn[:, mine]),
+                                    torch.from_numpy(vn[:, mine]), WORLD, MB)
+    out = torch.zeros(geo.q_shape())
+    eng.step(q_in, k_in, v_in, out)
+    np.save(Path(result_dir) / f"out{rank}.npy", stitch_outputs(out).numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_head_sharded_exchange_matches_oracle(tmp_path):
+    import torch.multiprocessing as mp
+
+    os.environ["PYTHONPATH"] = str(ROOT) + os.pathsep + os.environ.get("PYTHONPATH", "")
+    mp.spawn(_worker, args=(_free_port(), str(tmp_path)), nprocs=WORLD, join=True)
+    for rank in range(WORLD):
+        got = np.load(tmp_path / f"out{rank}.npy")          # [L, B_local, Hq, D]
+        for layer in range(L):
+            for b in range(B_LOCAL):
+                want = _expected(layer, rank * B_LOCAL + b)
+                assert np.allclose(got[layer, b], want, rtol=0, atol=1e-6)
+
+
+def test_geometry_validation():
+    from paper_2405_01814_b200.dist import ShardGeometry
+
+    with pytest.raises(ValueError, match="divisible"):
+        ShardGeometry(0, 3, 1, 4, 8, 8, 128)
+    g = ShardGeometry(1, 4, 80, 128, 64, 8, 128)
+    assert (g.hq_l, g.hkv_l, g.Bh, g.B_mb, g.B_attn) == (16, 2, 64, 256, 512)
+    rows = sorted(g.kv_row(s, b) for s in range(4) for b in range(128))
+    assert rows == list(range(512))
