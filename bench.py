@@ -390,8 +390,7 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
         if engine is None:
             step_local(ev)
         else:
-            engine.step(W.q_in, W.kn_in, W.vn_in, W.out,
-                        [e for pair in ev for e in pair] if ev is not None else None)
+            engine.step(W.q_in, W.kn_in, W.vn_in, W.out, ev)
 
     def barrier():
         torch.cuda.synchronize(device)
