@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <numeric>
@@ -27,6 +28,7 @@ struct lam_ctx {
   int32_t* counters = nullptr;
   int64_t counters_cap = 0;
   int32_t* err = nullptr;  // device error word for the instance API
+  int32_t* work = nullptr; // [2] persistent-kernel work counters (self-resetting)
   void* scratch = nullptr; // instance API: logits workspace
   int64_t scratch_cap = 0; // bytes
   int64_t* offs = nullptr; // instance API: logit offsets
@@ -95,12 +97,13 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 }
 
 // 2-D view [rows][D] of a 16-bit pool, 64x64 boxes, 128-byte swizzle.
-int make_pool_map(CUtensorMap* map, int dtype, const void* base, int64_t rows, int D) {
+int make_pool_map(CUtensorMap* map, int dtype, const void* base, int64_t rows, int D,
+                  int box_rows) {
   auto enc = tensor_map_encoder();
   if (!enc) return fail(LAM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(rows)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(D) * 2};
-  const cuuint32_t box[2] = {64, 64};
+  const cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
   const cuuint32_t estr[2] = {1, 1};
   const CUtensorMapDataType dt =
       dtype == LAM_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
@@ -112,42 +115,52 @@ int make_pool_map(CUtensorMap* map, int dtype, const void* base, int64_t rows, i
   return LAM_OK;
 }
 
+// Kernel variants (decode.cu LAM_MMA_VARIANTS / LAM_SIMT_VARIANTS); variant 0 is the tuned
+// default, LAM_GQA_VARIANT / LAM_SIMT_VARIANT / LAM_ITEMS_PER_CTA override it for tuning.
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+int gqa_variant() {
+  static int v = env_int("LAM_GQA_VARIANT", 0);
+  return v;
+}
+int simt_variant() {
+  static int v = env_int("LAM_SIMT_VARIANT", 0);
+  return v;
+}
+int items_per_cta() {
+  static int v = env_int("LAM_ITEMS_PER_CTA", 4);
+  return v;
+}
+
 struct Plan {
   int kernel = 0;  // LAM_KERNEL_SIMT / LAM_KERNEL_GQA_MMA
+  int variant = 0;
   int GQ = 1;      // q heads per CTA
   int QG = 1;      // q-head groups per kv head
   int tile = 32;
+  int ctas = 0;    // persistent grid
   int chunk = 0;
   int S = 1;
 };
 
-// Pick the split count that minimises (waves x per-CTA tiles) with a fixed per-CTA cost.
-void choose_splits(Plan& pl, int64_t units, int max_len, int slots, int split_tokens) {
+// Persistent kernels claim items dynamically, so the split count only has to give every
+// resident CTA enough items to balance the tail: the smallest S with
+// units * S >= items_per_cta * ctas (each split at least one tile).
+void choose_splits(Plan& pl, int64_t units, int max_len, int ctas, int split_tokens) {
   const int tiles_total = std::max(1, (max_len + pl.tile - 1) / pl.tile);
+  int ct;
   if (split_tokens > 0) {
-    const int ct = std::max(1, (split_tokens + pl.tile - 1) / pl.tile);
-    pl.chunk = ct * pl.tile;
-    pl.S = (tiles_total + ct - 1) / ct;
-    return;
+    ct = std::max(1, (split_tokens + pl.tile - 1) / pl.tile);
+  } else {
+    const int64_t want = static_cast<int64_t>(items_per_cta()) * ctas;
+    int64_t s = units > 0 ? (want + units - 1) / units : 1;
+    s = std::max<int64_t>(1, std::min<int64_t>(s, tiles_total));
+    ct = static_cast<int>((tiles_total + s - 1) / s);
   }
-  const double kOverheadTiles = 2.0;
-  double best = 1e300;
-  int best_ct = tiles_total;
-  const int max_s = std::min(tiles_total, 256);
-  for (int s = 1; s <= max_s; ++s) {
-    const int ct = (tiles_total + s - 1) / s;
-    const int s_eff = (tiles_total + ct - 1) / ct;
-    if (s_eff != s) continue;
-    const double ctas = static_cast<double>(units) * s_eff;
-    const double waves = std::ceil(ctas / std::max(1, slots));
-    const double cost = waves * (ct + kOverheadTiles) + (s_eff > 1 ? 0.5 : 0.0);
-    if (cost < best - 1e-9) {
-      best = cost;
-      best_ct = ct;
-    }
-  }
-  pl.chunk = best_ct * pl.tile;
-  pl.S = (tiles_total + best_ct - 1) / best_ct;
+  pl.chunk = ct * pl.tile;
+  pl.S = (tiles_total + ct - 1) / ct;
 }
 
 int plan_decode(lam_ctx* ctx, const lam_decode_args* a, Plan* pl) {
@@ -170,33 +183,42 @@ int plan_decode(lam_ctx* ctx, const lam_decode_args* a, Plan* pl) {
   if (!paged && a->max_len > a->page_size)
     return fail(LAM_ERR_VALIDATION, "dense layout: max_len exceeds the row capacity page_size");
 
+  const int variant = gqa_variant();
+  const int mtile = lam::mma_variant_tile(variant);
   const bool mma_ok = (kvd == LAM_BF16 || kvd == LAM_F16) && a->head_dim == 128 && G >= 2 &&
-                      G <= 8 && (!paged || a->page_size % 64 == 0);
+                      G <= 8 && mtile > 0 && (!paged || a->page_size % mtile == 0);
   int kernel = a->kernel;
   if (kernel == LAM_KERNEL_AUTO) kernel = mma_ok ? LAM_KERNEL_GQA_MMA : LAM_KERNEL_SIMT;
   if (kernel == LAM_KERNEL_GQA_MMA) {
     if (!mma_ok)
       return fail(LAM_ERR_VALIDATION,
-                  "GQA MMA kernel needs 16-bit KV, head_dim 128, 2 <= G <= 8 and page_size % 64 == 0");
+                  "GQA MMA kernel needs 16-bit KV, head_dim 128, 2 <= G <= 8 and page_size a "
+                  "multiple of its tile (" + std::to_string(mtile) + " tokens)");
     pl->kernel = kernel;
+    pl->variant = variant;
     pl->GQ = 8;
     pl->QG = 1;
-    pl->tile = 64;
+    pl->tile = mtile;
   } else if (kernel == LAM_KERNEL_SIMT) {
-    if (paged && a->page_size % 32 != 0)
-      return fail(LAM_ERR_VALIDATION, "paged layout needs page_size % 32 == 0");
     pl->kernel = kernel;
     pl->GQ = G % 4 == 0 ? 4 : (G % 2 == 0 ? 2 : 1);
     pl->QG = G / pl->GQ;
-    pl->tile = 32;
+    pl->variant = (a->head_dim == 128 && pl->GQ == 1) ? simt_variant() : 0;
+    pl->tile = lam::simt_variant_tile(kvd, a->head_dim, pl->GQ, pl->variant);
+    if (pl->tile == 0) return fail(LAM_ERR_VALIDATION, "unsupported SIMT decode shape");
+    if (paged && a->page_size % pl->tile != 0)
+      return fail(LAM_ERR_VALIDATION, "paged layout needs page_size a multiple of " +
+                                          std::to_string(pl->tile) + " tokens");
   } else {
     return fail(LAM_ERR_VALIDATION, "unknown kernel family");
   }
-  const int occ = pl->kernel == LAM_KERNEL_GQA_MMA ? lam::occupancy_mma(kvd)
-                                                   : lam::occupancy_simt(kvd, a->head_dim, pl->GQ);
+  const int occ = pl->kernel == LAM_KERNEL_GQA_MMA
+                      ? lam::occupancy_mma(kvd, pl->variant)
+                      : lam::occupancy_simt(kvd, a->head_dim, pl->GQ, pl->variant);
   if (occ <= 0) return fail(LAM_ERR_CUDA, "decode kernel cannot be resident on this device");
+  pl->ctas = occ * ctx->num_sms;
   const int64_t units = static_cast<int64_t>(a->batch) * a->num_kv_heads * pl->QG;
-  choose_splits(*pl, units, a->max_len, occ * ctx->num_sms, a->split_tokens);
+  choose_splits(*pl, units, a->max_len, pl->ctas, a->split_tokens);
   if (pl->S > 65535) return fail(LAM_ERR_VALIDATION, "too many splits");
   return LAM_OK;
 }
@@ -307,6 +329,8 @@ int lam_ctx_create(int device, lam_ctx** out) {
   cudaError_t e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (e == cudaSuccess) e = cudaMalloc(&c->err, sizeof(int32_t));
   if (e == cudaSuccess) e = cudaMemset(c->err, 0, sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&c->work, 2 * sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMemset(c->work, 0, 2 * sizeof(int32_t));
   if (e != cudaSuccess) {
     delete c;
     return cuda_fail(e, "lam_ctx_create");
@@ -322,6 +346,7 @@ int lam_ctx_destroy(lam_ctx* c) {
   cudaFree(c->ws_ml);
   cudaFree(c->counters);
   cudaFree(c->err);
+  cudaFree(c->work);
   cudaFree(c->scratch);
   cudaFree(c->offs);
   delete c;
@@ -623,6 +648,8 @@ int lam_decode(lam_ctx* ctx, const lam_decode_args* a, void* stream) {
   p.chunk = pl.chunk;
   p.S = pl.S;
   p.QG = pl.QG;
+  p.n_items = static_cast<int32_t>(static_cast<int64_t>(a->batch) * a->num_kv_heads * pl.QG * pl.S);
+  p.work = ctx->work;
   p.scale = a->scale;
   p.scale_log2 = a->scale * 1.4426950408889634f;
   p.out_f32 = a->out_dtype == LAM_F32;
@@ -646,13 +673,13 @@ int lam_decode(lam_ctx* ctx, const lam_decode_args* a, void* stream) {
     if (rows >= (int64_t{1} << 31))
       return fail(LAM_ERR_VALIDATION, "pool exceeds 2^31 rows for the tensor map");
     CUtensorMap kmap, vmap;
-    rc = make_pool_map(&kmap, a->kv_dtype, a->k_pool, rows, D);
+    rc = make_pool_map(&kmap, a->kv_dtype, a->k_pool, rows, D, pl.tile);
     if (rc != LAM_OK) return rc;
-    rc = make_pool_map(&vmap, a->kv_dtype, a->v_pool, rows, D);
+    rc = make_pool_map(&vmap, a->kv_dtype, a->v_pool, rows, D, pl.tile);
     if (rc != LAM_OK) return rc;
-    LAM_CUDA(lam::launch_decode_mma(a->kv_dtype, p, kmap, vmap, pl.S, s));
+    LAM_CUDA(lam::launch_decode_mma(a->kv_dtype, pl.variant, p, kmap, vmap, pl.ctas, s));
   } else {
-    LAM_CUDA(lam::launch_decode_simt(a->kv_dtype, D, pl.GQ, p, pl.S, s));
+    LAM_CUDA(lam::launch_decode_simt(a->kv_dtype, D, pl.GQ, pl.variant, p, pl.ctas, s));
   }
   return LAM_OK;
 }

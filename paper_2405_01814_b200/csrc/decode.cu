@@ -22,23 +22,47 @@ cudaError_t ensure_smem_attr(K kernel, int bytes, std::atomic<uint64_t>& done_ma
   return e;
 }
 
-template <typename T, int D, int GQ>
-cudaError_t simt_launch(const DecodeParams& p, int grid_x, cudaStream_t stream) {
-  using C = SimtCfg<T, D, GQ>;
+template <typename T, int D, int GQ, int NW, int TILE, int STAGES>
+cudaError_t simt_launch(const DecodeParams& p, int ctas, cudaStream_t stream) {
+  using C = SimtCfg<T, D, GQ, NW, TILE, STAGES>;
   static std::atomic<uint64_t> done{0};
-  auto* k = decode_simt_kernel<T, D, GQ>;
+  auto* k = decode_simt_kernel<T, D, GQ, NW, TILE, STAGES>;
   cudaError_t e = ensure_smem_attr(k, C::SMEM_BYTES, done);
   if (e != cudaSuccess) return e;
-  dim3 grid(grid_x, p.Hkv * p.QG, p.B);
-  k<<<grid, (C::NW + 1) * 32, C::SMEM_BYTES, stream>>>(p);
+  k<<<ctas, (NW + 1) * 32, C::SMEM_BYTES, stream>>>(p);
   return cudaGetLastError();
 }
 
-template <typename T, int D, int GQ>
+template <typename T, int D, int GQ, int NW, int TILE, int STAGES>
 int simt_occ() {
-  using C = SimtCfg<T, D, GQ>;
+  using C = SimtCfg<T, D, GQ, NW, TILE, STAGES>;
   static std::atomic<uint64_t> done{0};
-  auto* k = decode_simt_kernel<T, D, GQ>;
+  auto* k = decode_simt_kernel<T, D, GQ, NW, TILE, STAGES>;
+  if (ensure_smem_attr(k, C::SMEM_BYTES, done) != cudaSuccess) return 0;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, (NW + 1) * 32, C::SMEM_BYTES) !=
+      cudaSuccess)
+    return 0;
+  return n;
+}
+
+template <typename T, int NW, int STAGES>
+cudaError_t mma_launch_v(const DecodeParams& p, const CUtensorMap& kmap, const CUtensorMap& vmap,
+                         int ctas, cudaStream_t stream) {
+  using C = MmaCfg<NW, STAGES>;
+  static std::atomic<uint64_t> done{0};
+  auto* k = decode_gqa_mma_kernel<T, NW, STAGES>;
+  cudaError_t e = ensure_smem_attr(k, C::SMEM_BYTES, done);
+  if (e != cudaSuccess) return e;
+  k<<<ctas, (C::NW + 1) * 32, C::SMEM_BYTES, stream>>>(p, kmap, vmap);
+  return cudaGetLastError();
+}
+
+template <typename T, int NW, int STAGES>
+int mma_occ_v() {
+  using C = MmaCfg<NW, STAGES>;
+  static std::atomic<uint64_t> done{0};
+  auto* k = decode_gqa_mma_kernel<T, NW, STAGES>;
   if (ensure_smem_attr(k, C::SMEM_BYTES, done) != cudaSuccess) return 0;
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, (C::NW + 1) * 32, C::SMEM_BYTES) !=
@@ -47,57 +71,76 @@ int simt_occ() {
   return n;
 }
 
+// GQA kernel variants (consumer warps, stages): tile = 16 tokens per consumer warp.
+#define LAM_MMA_VARIANTS(X) X(0, 4, 6) X(1, 4, 3) X(2, 8, 3) X(3, 2, 6) X(4, 2, 4)
+
 template <typename T>
-cudaError_t mma_launch(const DecodeParams& p, const CUtensorMap& kmap, const CUtensorMap& vmap,
-                       int grid_x, cudaStream_t stream) {
-  static std::atomic<uint64_t> done{0};
-  auto* k = decode_gqa_mma_kernel<T>;
-  cudaError_t e = ensure_smem_attr(k, MmaCfg::SMEM_BYTES, done);
-  if (e != cudaSuccess) return e;
-  dim3 grid(grid_x, p.Hkv, p.B);
-  k<<<grid, (MmaCfg::NW + 1) * 32, MmaCfg::SMEM_BYTES, stream>>>(p, kmap, vmap);
-  return cudaGetLastError();
+cudaError_t mma_launch(int variant, const DecodeParams& p, const CUtensorMap& kmap,
+                       const CUtensorMap& vmap, int grid_x, cudaStream_t stream) {
+#define X(id, nw, st) \
+  if (variant == id) return mma_launch_v<T, nw, st>(p, kmap, vmap, grid_x, stream);
+  LAM_MMA_VARIANTS(X)
+#undef X
+  return cudaErrorInvalidValue;
 }
 
 template <typename T>
-int mma_occ() {
-  static std::atomic<uint64_t> done{0};
-  auto* k = decode_gqa_mma_kernel<T>;
-  if (ensure_smem_attr(k, MmaCfg::SMEM_BYTES, done) != cudaSuccess) return 0;
-  int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, (MmaCfg::NW + 1) * 32,
-                                                    MmaCfg::SMEM_BYTES) != cudaSuccess)
-    return 0;
-  return n;
+int mma_occ(int variant) {
+#define X(id, nw, st) \
+  if (variant == id) return mma_occ_v<T, nw, st>();
+  LAM_MMA_VARIANTS(X)
+#undef X
+  return 0;
 }
 
-// dtype codes: 0 f32, 2 bf16, 3 f16 (lamina_attn.h)
-#define LAM_SIMT_DISPATCH(DT, Dv, GQv, EXPR)                          \
-  do {                                                                \
-    if ((DT) == 0) {                                                  \
-      using T = float;                                                \
-      constexpr int D_ = Dv, GQ_ = GQv;                               \
-      EXPR;                                                           \
-    } else if ((DT) == 2) {                                           \
-      using T = __nv_bfloat16;                                        \
-      constexpr int D_ = Dv, GQ_ = GQv;                               \
-      EXPR;                                                           \
-    } else if ((DT) == 3) {                                           \
-      using T = __half;                                               \
-      constexpr int D_ = Dv, GQ_ = GQv;                               \
-      EXPR;                                                           \
-    }                                                                 \
-  } while (0)
+// SIMT variants (consumer warps, tokens per stage for 32-bit / 16-bit KV, stages).  Variant 0
+// is the default for every (dtype, D, GQ); the others exist for D = 128, GQ = 1 (tuning).
+#define LAM_SIMT_VARIANTS(X) \
+  X(0, 8, 32, 64, 6) X(1, 16, 32, 64, 6) X(2, 8, 32, 64, 3) X(3, 4, 32, 32, 4)
 
-#define LAM_SIMT_SWITCH(DT, D, GQ, EXPR)                               \
-  do {                                                                 \
-    if ((D) == 64 && (GQ) == 1) LAM_SIMT_DISPATCH(DT, 64, 1, EXPR);    \
-    else if ((D) == 64 && (GQ) == 2) LAM_SIMT_DISPATCH(DT, 64, 2, EXPR); \
-    else if ((D) == 64 && (GQ) == 4) LAM_SIMT_DISPATCH(DT, 64, 4, EXPR); \
-    else if ((D) == 128 && (GQ) == 1) LAM_SIMT_DISPATCH(DT, 128, 1, EXPR); \
-    else if ((D) == 128 && (GQ) == 2) LAM_SIMT_DISPATCH(DT, 128, 2, EXPR); \
-    else if ((D) == 128 && (GQ) == 4) LAM_SIMT_DISPATCH(DT, 128, 4, EXPR); \
-  } while (0)
+struct SimtLaunchF {
+  const DecodeParams& p;
+  int ctas;
+  cudaStream_t s;
+  template <typename T, int DD, int GG, int NW, int TILE, int ST>
+  cudaError_t operator()() const { return simt_launch<T, DD, GG, NW, TILE, ST>(p, ctas, s); }
+};
+struct SimtOccF {
+  template <typename T, int DD, int GG, int NW, int TILE, int ST>
+  int operator()() const { return simt_occ<T, DD, GG, NW, TILE, ST>(); }
+};
+struct SimtTileF {
+  template <typename T, int DD, int GG, int NW, int TILE, int ST>
+  int operator()() const { return TILE; }
+};
+
+template <typename T, int D, int GQ, class F>
+auto simt_variant(int variant, F f) {
+  constexpr bool wide = sizeof(T) == 4;
+  if (variant == 0) return f.template operator()<T, D, GQ, 8, wide ? 32 : 64, 6>();
+  if constexpr (D == 128 && GQ == 1) {
+#define X(id, nw, t32, t16, st) \
+    if (variant == id) return f.template operator()<T, D, GQ, nw, wide ? t32 : t16, st>();
+    LAM_SIMT_VARIANTS(X)
+#undef X
+  }
+  return decltype(f.template operator()<T, D, GQ, 8, wide ? 32 : 64, 6>())();
+}
+
+template <class F>
+auto simt_dispatch(int dt, int D, int GQ, int variant, F f) {
+  using R = decltype(f.template operator()<float, 128, 1, 8, 32, 6>());
+#define LAM_ONE(TT, DD, GG) \
+  if (D == DD && GQ == GG) return simt_variant<TT, DD, GG>(variant, f);
+#define LAM_ALL(TT) LAM_ONE(TT, 64, 1) LAM_ONE(TT, 64, 2) LAM_ONE(TT, 64, 4) \
+                    LAM_ONE(TT, 128, 1) LAM_ONE(TT, 128, 2) LAM_ONE(TT, 128, 4)
+  if (dt == 0) { LAM_ALL(float) }
+  if (dt == 2) { LAM_ALL(__nv_bfloat16) }
+  if (dt == 3) { LAM_ALL(__half) }
+#undef LAM_ALL
+#undef LAM_ONE
+  return R();
+}
 
 }  // namespace
 
@@ -106,29 +149,41 @@ bool simt_supported(int kv_dtype, int D, int GQ) {
          (GQ == 1 || GQ == 2 || GQ == 4);
 }
 
-cudaError_t launch_decode_simt(int kv_dtype, int D, int GQ, const DecodeParams& p, int grid_x,
-                               cudaStream_t stream) {
-  cudaError_t r = cudaErrorInvalidValue;
-  LAM_SIMT_SWITCH(kv_dtype, D, GQ, (r = simt_launch<T, D_, GQ_>(p, grid_x, stream)));
-  return r;
+int simt_variant_tile(int kv_dtype, int D, int GQ, int variant);
+
+cudaError_t launch_decode_simt(int kv_dtype, int D, int GQ, int variant, const DecodeParams& p,
+                               int ctas, cudaStream_t stream) {
+  if (simt_variant_tile(kv_dtype, D, GQ, variant) == 0) return cudaErrorInvalidValue;
+  return simt_dispatch(kv_dtype, D, GQ, variant, SimtLaunchF{p, ctas, stream});
 }
 
-int occupancy_simt(int kv_dtype, int D, int GQ) {
-  int r = 0;
-  LAM_SIMT_SWITCH(kv_dtype, D, GQ, (r = simt_occ<T, D_, GQ_>()));
-  return r;
+int occupancy_simt(int kv_dtype, int D, int GQ, int variant) {
+  return simt_dispatch(kv_dtype, D, GQ, variant, SimtOccF{});
 }
 
-cudaError_t launch_decode_mma(int kv_dtype, const DecodeParams& p, const CUtensorMap& kmap,
-                              const CUtensorMap& vmap, int grid_x, cudaStream_t stream) {
-  if (kv_dtype == 2) return mma_launch<__nv_bfloat16>(p, kmap, vmap, grid_x, stream);
-  if (kv_dtype == 3) return mma_launch<__half>(p, kmap, vmap, grid_x, stream);
+int simt_variant_tile(int kv_dtype, int D, int GQ, int variant) {
+  return simt_dispatch(kv_dtype, D, GQ, variant, SimtTileF{});
+}
+
+int mma_variant_tile(int variant) {
+#define X(id, nw, st) \
+  if (variant == id) return 16 * nw;
+  LAM_MMA_VARIANTS(X)
+#undef X
+  return 0;
+}
+
+cudaError_t launch_decode_mma(int kv_dtype, int variant, const DecodeParams& p,
+                              const CUtensorMap& kmap, const CUtensorMap& vmap, int grid_x,
+                              cudaStream_t stream) {
+  if (kv_dtype == 2) return mma_launch<__nv_bfloat16>(variant, p, kmap, vmap, grid_x, stream);
+  if (kv_dtype == 3) return mma_launch<__half>(variant, p, kmap, vmap, grid_x, stream);
   return cudaErrorInvalidValue;
 }
 
-int occupancy_mma(int kv_dtype) {
-  if (kv_dtype == 2) return mma_occ<__nv_bfloat16>();
-  if (kv_dtype == 3) return mma_occ<__half>();
+int occupancy_mma(int kv_dtype, int variant) {
+  if (kv_dtype == 2) return mma_occ<__nv_bfloat16>(variant);
+  if (kv_dtype == 3) return mma_occ<__half>(variant);
   return 0;
 }
 

@@ -7,8 +7,8 @@
 // Both are mma.sync m16n8k16 with N = G = 8 (fp32 accumulate), so the KV tile is read
 // from HBM once for all G heads and no MMA lane is padding when G == 8.
 //
-// One CTA = (request, kv head, split); warp NW is the TMA producer, warps 0..NW-1 each own
-// 16 tokens of every 64-token tile.  K/V tiles arrive through 2-D tensor-map TMA with the
+// Persistent: a work item is (request, kv head, split); warp NW is the TMA producer
+// (decode_common.cuh:producer_loop), warps 0..NW-1 each own 16 tokens of every tile.  K/V tiles arrive through 2-D tensor-map TMA with the
 // 128-byte swizzle (two 64-column boxes per 128-wide row block), so the ldmatrix fragment
 // loads are bank-conflict free.  The S^T accumulator is turned into the P^T B-operand
 // in registers (exp2 -> bf16 pack -> movmatrix.trans), never touching shared memory.
@@ -18,50 +18,48 @@
 
 namespace lam {
 
+template <int NW_, int STAGES_>
 struct MmaCfg {
-  static constexpr int NW = 4;
-  static constexpr int TILE = 64;  // tokens per stage, 16 per consumer warp
-  static constexpr int STAGES = 3;
+  static constexpr int NW = NW_;
+  static constexpr int TILE = 16 * NW;  // tokens per stage, 16 per consumer warp
+  static constexpr int STAGES = STAGES_;
   static constexpr int D = 128;
   static constexpr int GQ = 8;
-  static constexpr int BOX_BYTES = TILE * 64 * 2;    // [64 rows][64 cols] 16-bit = 8 KB
-  static constexpr int MAT_BYTES = 2 * BOX_BYTES;    // one K (or V) tile, 16 KB
+  static constexpr int BOX_BYTES = TILE * 64 * 2;    // [TILE rows][64 cols] 16-bit
+  static constexpr int MAT_BYTES = 2 * BOX_BYTES;    // one K (or V) tile
   static constexpr int STAGE_BYTES = 2 * MAT_BYTES;  // K + V
   static constexpr int RING_BYTES = STAGES * STAGE_BYTES;
-  static constexpr int RED_BYTES = NW * GQ * (D + 2) * 4;
-  static constexpr int MAIN_BYTES = RING_BYTES > RED_BYTES ? RING_BYTES : RED_BYTES;
-  static constexpr int SMEM_BYTES = MAIN_BYTES + 2 * STAGES * 8 + 16 + 1024;  // +align slack
+  static constexpr int RED_FLOATS = NW * GQ * (D + 2);
+  static constexpr int SMEM_BYTES =
+      RING_BYTES + RED_FLOATS * 4 + STAGES * 16 + 2 * STAGES * 8 + 16 + 1024;  // +align slack
 };
 
 // Byte offset of 16-byte chunk `c` (0..15 across the 128-wide row) of tile row `r`
-// inside one K or V tile stored as two 128B-swizzled boxes.
+// inside one K or V tile stored as two 128B-swizzled boxes of BOX_BYTES each.
+template <int BOX_BYTES>
 __device__ __forceinline__ uint32_t swz(int r, int c) {
-  return (c >> 3) * MmaCfg::BOX_BYTES + r * 128 + (((c & 7) ^ (r & 7)) << 4);
+  return (c >> 3) * BOX_BYTES + r * 128 + (((c & 7) ^ (r & 7)) << 4);
 }
 
-template <typename T>
-__global__ void __launch_bounds__((MmaCfg::NW + 1) * 32)
+template <typename T, int NW_, int STAGES_>
+__global__ void __launch_bounds__((NW_ + 1) * 32)
     decode_gqa_mma_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap kmap,
                           const __grid_constant__ CUtensorMap vmap) {
-  using C = MmaCfg;
+  using C = MmaCfg<NW_, STAGES_>;
   constexpr int NW = C::NW, TILE = C::TILE, STAGES = C::STAGES, D = C::D, GQ = C::GQ;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::MAIN_BYTES);
+  float* red_m = reinterpret_cast<float*>(smem + C::RING_BYTES);
+  float* red_l = red_m + NW * GQ;
+  float* red_acc = red_l + NW * GQ;
+  int4* meta = reinterpret_cast<int4*>(red_m + C::RED_FLOATS);
+  uint64_t* full = reinterpret_cast<uint64_t*>(meta + STAGES);
   uint64_t* empty = full + STAGES;
   int* s_flag = reinterpret_cast<int*>(empty + STAGES);
 
-  const int split = blockIdx.x;
-  const int kvh = blockIdx.y;
-  const int b = blockIdx.z;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int G = p.G;  // real q heads in the group (<= 8); the rest are zero padding
-
-  const int len = __ldg(p.seq_lens + b);
-  const int t_begin = split * p.chunk;
-  const int t_end = min(len, t_begin + p.chunk);
-  const int n_tiles = t_end > t_begin ? (t_end - t_begin + TILE - 1) / TILE : 0;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -77,20 +75,18 @@ __global__ void __launch_bounds__((MmaCfg::NW + 1) * 32)
   __syncthreads();
 
   if (warp == NW) {
-    if (lane == 0 && n_tiles > 0) {
+    if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      for (int i = 0; i < n_tiles; ++i) {
-        const int s = i % STAGES;
-        if (i >= STAGES) mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
-        const int tok = t_begin + i * TILE;
-        const int32_t row = static_cast<int32_t>(kv_row(p, b, kvh, tok));
+      producer_loop<STAGES, TILE>(p, full, empty, meta, [&](int s, const Item& it, int j) {
+        const int tok = it.t_begin + j * TILE;
+        const int32_t row = static_cast<int32_t>(kv_row(p, it.b, it.kvh, tok));
         uint8_t* st = smem + s * C::STAGE_BYTES;
         mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
         tma_load_2d(st, &kmap, 0, row, &full[s], pol);
         tma_load_2d(st + C::BOX_BYTES, &kmap, 64, row, &full[s], pol);
         tma_load_2d(st + C::MAT_BYTES, &vmap, 0, row, &full[s], pol);
         tma_load_2d(st + C::MAT_BYTES + C::BOX_BYTES, &vmap, 64, row, &full[s], pol);
-      }
+      });
     }
     return;
   }
@@ -98,40 +94,42 @@ __global__ void __launch_bounds__((MmaCfg::NW + 1) * 32)
   // ---------------- consumers ----------------
   const int gr = lane >> 2;       // fragment "group" row
   const int gc = (lane & 3) * 2;  // fragment column pair
-  // Q^T B-fragments: b0 = Q[g=gr][ks*16 + gc .. +1], b1 = Q[g=gr][ks*16 + 8 + gc .. +1].
-  uint32_t qf[8][2];
-  {
-    const int qh = kvh * G + gr;
-    const uint32_t* qrow = reinterpret_cast<const uint32_t*>(
-        static_cast<const T*>(p.q) + (static_cast<int64_t>(b) * p.Hq + qh) * D);
-#pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
-      qf[ks][0] = gr < G ? __ldg(qrow + (ks * 16 + gc) / 2) : 0u;
-      qf[ks][1] = gr < G ? __ldg(qrow + (ks * 16 + 8 + gc) / 2) : 0u;
-    }
-  }
   const float sl2 = p.scale_log2;
-
-  float m0 = -INFINITY, m1 = -INFINITY;  // running max (log2 units) of columns gc, gc+1
-  float l0 = 0.f, l1 = 0.f;              // this lane's share of the softmax sums
-  float o[8][4];
-#pragma unroll
-  for (int mt = 0; mt < 8; ++mt)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) o[mt][e] = 0.f;
-
   // per-lane ldmatrix row/chunk selectors
   const int a_row = (lane & 7) + ((lane >> 3) & 1) * 8;  // K: x4 matrices {r0-7,r8-15}x{c,c+1}
   const int a_chk = lane >> 4;
   const int v_row = (lane & 7) + (lane >> 4) * 8;        // V^T: {c,c+1}x{r0-7,r8-15}
   const int v_chk = (lane >> 3) & 1;
-
   const uint32_t base = smem_u32(smem);
-  for (int i = 0; i < n_tiles; ++i) {
+
+  uint32_t qf[8][2];    // Q^T B-fragments: Q[g=gr][ks*16 + gc (+8) .. +1]
+  float m0, m1;         // running max (log2 units) of columns gc, gc+1
+  float l0, l1;         // this lane's share of the softmax sums
+  float o[8][4];        // O^T accumulators: (d = mt*16 + gr (+8), g = gc, gc+1)
+  Item it{};
+  for (int i = 0;; ++i) {
     const int s = i % STAGES;
     mbar_wait(&full[s], (i / STAGES) & 1);
-    const int tok0 = t_begin + i * TILE + warp * 16;
-    const int nval = min(16, t_end - tok0);
+    const int4 mt = meta[s];
+    if (mt.x < 0) break;
+    if (mt.y == 0) {
+      it = make_item(p, mt.x, TILE);
+      const uint32_t* qrow = reinterpret_cast<const uint32_t*>(
+          static_cast<const T*>(p.q) + (static_cast<int64_t>(it.b) * p.Hq + it.kvh * G + gr) * D);
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        qf[ks][0] = gr < G ? __ldg(qrow + (ks * 16 + gc) / 2) : 0u;
+        qf[ks][1] = gr < G ? __ldg(qrow + (ks * 16 + 8 + gc) / 2) : 0u;
+      }
+      m0 = m1 = -INFINITY;
+      l0 = l1 = 0.f;
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) o[t][e] = 0.f;
+    }
+    const int tok0 = it.t_begin + mt.y * TILE + warp * 16;
+    const int nval = mt.z > 0 ? min(16, it.t_end - tok0) : 0;
     const uint32_t kb = base + s * C::STAGE_BYTES;
     const uint32_t vb = kb + C::MAT_BYTES;
     if (nval > 0) {
@@ -151,7 +149,7 @@ __global__ void __launch_bounds__((MmaCfg::NW + 1) * 32)
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
         uint32_t a0, a1, a2, a3;
-        ldmatrix_x4(kb + swz(warp * 16 + a_row, ks * 2 + a_chk), a0, a1, a2, a3);
+        ldmatrix_x4(kb + swz<C::BOX_BYTES>(warp * 16 + a_row, ks * 2 + a_chk), a0, a1, a2, a3);
         Mma16816<T>::run(c, a0, a1, a2, a3, qf[ks][0], qf[ks][1]);
       }
       // logits (log2 units); rows gr and gr+8 of the warp's 16 tokens
@@ -184,48 +182,48 @@ __global__ void __launch_bounds__((MmaCfg::NW + 1) * 32)
       const uint32_t b1 = movmatrix_trans(phi);
       // O^T = O^T * alpha + V^T · P^T
 #pragma unroll
-      for (int mt = 0; mt < 8; ++mt) {
-        o[mt][0] *= al0;
-        o[mt][1] *= al1;
-        o[mt][2] *= al0;
-        o[mt][3] *= al1;
+      for (int t = 0; t < 8; ++t) {
+        o[t][0] *= al0;
+        o[t][1] *= al1;
+        o[t][2] *= al0;
+        o[t][3] *= al1;
         uint32_t a0, a1, a2, a3;
-        ldmatrix_x4_trans(vb + swz(warp * 16 + v_row, mt * 2 + v_chk), a0, a1, a2, a3);
-        Mma16816<T>::run(o[mt], a0, a1, a2, a3, b0, b1);
+        ldmatrix_x4_trans(vb + swz<C::BOX_BYTES>(warp * 16 + v_row, t * 2 + v_chk), a0, a1, a2, a3);
+        Mma16816<T>::run(o[t], a0, a1, a2, a3, b0, b1);
       }
       if (nval < 16) fence_proxy_async_smem();  // generic zero-stores before the next TMA
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
-  }
 
-  // reduce the softmax sums over the 8 row groups (lanes with equal lane&3).
+    if (mt.y == max(mt.z, 1) - 1) {
+      // end of the item: reduce the softmax sums over the 8 row groups (lanes with equal
+      // lane&3), then merge the warps and the splits.
+      float s0 = l0, s1 = l1;
 #pragma unroll
-  for (int off = 4; off < 32; off <<= 1) {
-    l0 += __shfl_xor_sync(0xffffffffu, l0, off);
-    l1 += __shfl_xor_sync(0xffffffffu, l1, off);
-  }
-
-  named_bar_sync(1, NW * 32);
-  float* red_m = reinterpret_cast<float*>(smem);
-  float* red_l = red_m + NW * GQ;
-  float* red_acc = red_l + NW * GQ;
-  if (gr == 0) {
-    red_m[warp * GQ + gc] = m0;
-    red_m[warp * GQ + gc + 1] = m1;
-    red_l[warp * GQ + gc] = l0;
-    red_l[warp * GQ + gc + 1] = l1;
-  }
+      for (int off = 4; off < 32; off <<= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, off);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, off);
+      }
+      named_bar_sync(1, NW * 32);  // the previous item's epilogue is done with red_*
+      if (gr == 0) {
+        red_m[warp * GQ + gc] = m0;
+        red_m[warp * GQ + gc + 1] = m1;
+        red_l[warp * GQ + gc] = s0;
+        red_l[warp * GQ + gc + 1] = s1;
+      }
 #pragma unroll
-  for (int mt = 0; mt < 8; ++mt) {
-    const int d = mt * 16 + gr;
-    red_acc[(warp * GQ + gc) * D + d] = o[mt][0];
-    red_acc[(warp * GQ + gc + 1) * D + d] = o[mt][1];
-    red_acc[(warp * GQ + gc) * D + d + 8] = o[mt][2];
-    red_acc[(warp * GQ + gc + 1) * D + d + 8] = o[mt][3];
+      for (int t = 0; t < 8; ++t) {
+        const int d = t * 16 + gr;
+        red_acc[(warp * GQ + gc) * D + d] = o[t][0];
+        red_acc[(warp * GQ + gc + 1) * D + d] = o[t][1];
+        red_acc[(warp * GQ + gc) * D + d + 8] = o[t][2];
+        red_acc[(warp * GQ + gc + 1) * D + d + 8] = o[t][3];
+      }
+      named_bar_sync(1, NW * 32);
+      finish_item<T, D, GQ, NW, true>(p, it, G, red_m, red_l, red_acc, s_flag);
+    }
   }
-  named_bar_sync(1, NW * 32);
-  finish_cta<T, D, GQ, NW, true>(p, b, kvh, 0, split, G, red_m, red_l, red_acc, s_flag);
 }
 
 }  // namespace lam

@@ -10,13 +10,17 @@ namespace lam {
 struct DecodeParams;
 
 // decode.cu
-cudaError_t launch_decode_simt(int kv_dtype, int D, int GQ, const DecodeParams& p, int grid_x,
-                               cudaStream_t stream);
-cudaError_t launch_decode_mma(int kv_dtype, const DecodeParams& p, const CUtensorMap& kmap,
-                              const CUtensorMap& vmap, int grid_x, cudaStream_t stream);
+// persistent launches: `ctas` resident CTAs (num_SMs x occupancy)
+cudaError_t launch_decode_simt(int kv_dtype, int D, int GQ, int variant, const DecodeParams& p,
+                               int ctas, cudaStream_t stream);
+int simt_variant_tile(int kv_dtype, int D, int GQ, int variant);  // 0 = invalid
+cudaError_t launch_decode_mma(int kv_dtype, int variant, const DecodeParams& p,
+                              const CUtensorMap& kmap, const CUtensorMap& vmap, int grid_x,
+                              cudaStream_t stream);
+int mma_variant_tile(int variant);  // tokens per stage of a GQA kernel variant (0 = invalid)
 // resident CTAs per SM for an instantiation (0 if unsupported)
-int occupancy_simt(int kv_dtype, int D, int GQ);
-int occupancy_mma(int kv_dtype);
+int occupancy_simt(int kv_dtype, int D, int GQ, int variant);
+int occupancy_mma(int kv_dtype, int variant);
 bool simt_supported(int kv_dtype, int D, int GQ);
 
 // instance.cu
