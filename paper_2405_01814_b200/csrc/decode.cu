@@ -29,7 +29,7 @@ cudaError_t simt_launch(const DecodeParams& p, int ctas, cudaStream_t stream) {
   auto* k = decode_simt_kernel<T, D, GQ, NW, TILE, STAGES>;
   cudaError_t e = ensure_smem_attr(k, C::SMEM_BYTES, done);
   if (e != cudaSuccess) return e;
-  k<<<ctas, (NW + 1) * 32, C::SMEM_BYTES, stream>>>(p);
+  k<<<ctas, C::THREADS, C::SMEM_BYTES, stream>>>(p);
   return cudaGetLastError();
 }
 
@@ -40,7 +40,7 @@ int simt_occ() {
   auto* k = decode_simt_kernel<T, D, GQ, NW, TILE, STAGES>;
   if (ensure_smem_attr(k, C::SMEM_BYTES, done) != cudaSuccess) return 0;
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, (NW + 1) * 32, C::SMEM_BYTES) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, C::THREADS, C::SMEM_BYTES) !=
       cudaSuccess)
     return 0;
   return n;
@@ -54,7 +54,7 @@ cudaError_t mma_launch_v(const DecodeParams& p, const CUtensorMap& kmap, const C
   auto* k = decode_gqa_mma_kernel<T, NW, STAGES>;
   cudaError_t e = ensure_smem_attr(k, C::SMEM_BYTES, done);
   if (e != cudaSuccess) return e;
-  k<<<ctas, (C::NW + 1) * 32, C::SMEM_BYTES, stream>>>(p, kmap, vmap);
+  k<<<ctas, C::THREADS, C::SMEM_BYTES, stream>>>(p, kmap, vmap);
   return cudaGetLastError();
 }
 
@@ -65,7 +65,7 @@ int mma_occ_v() {
   auto* k = decode_gqa_mma_kernel<T, NW, STAGES>;
   if (ensure_smem_attr(k, C::SMEM_BYTES, done) != cudaSuccess) return 0;
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, (C::NW + 1) * 32, C::SMEM_BYTES) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, C::THREADS, C::SMEM_BYTES) !=
       cudaSuccess)
     return 0;
   return n;

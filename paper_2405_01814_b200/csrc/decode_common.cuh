@@ -130,22 +130,21 @@ __device__ __forceinline__ void store_out(const DecodeParams& p, int64_t idx, fl
     static_cast<T*>(p.out)[idx] = Elem<T>::from_float(v);
 }
 
-// End of one work item, run by all NW*32 consumer threads after a consumer barrier.
-// red_m/red_l/red_acc hold the NW per-warp partials for GQ q heads: red_m[w*GQ+g] (log2 units
-// if kLog2, else natural), red_l[w*GQ+g], red_acc[(w*GQ+g)*D + d].  `nvalid` q heads of the
-// group are real (the MMA kernel pads to 8).
+// Split-K epilogue of one work item, run by the CTA's dedicated epilogue warp while the
+// consumer warps already stream the next item.  red_m/red_l/red_acc hold the NW per-warp
+// partials for GQ q heads: red_m[w*GQ+g] (log2 units if kLog2, else natural), red_l[w*GQ+g],
+// red_acc[(w*GQ+g)*D + d].  `nvalid` q heads of the group are real (the MMA kernel pads to 8).
 template <typename T, int D, int GQ, int NW, bool kLog2>
-__device__ __forceinline__ void finish_item(const DecodeParams& p, const Item& it, int nvalid,
-                                            const float* red_m, const float* red_l,
-                                            const float* red_acc, int* s_flag) {
-  constexpr int kThreads = NW * 32;
+__device__ __forceinline__ void finish_item_warp(const DecodeParams& p, const Item& it,
+                                                 int nvalid, const float* red_m,
+                                                 const float* red_l, const float* red_acc) {
   constexpr float kLn2 = 0.6931471805599453f;
-  const int tid = threadIdx.x;
+  const int lane = threadIdx.x % 32;
   const int b = it.b;
   const int qh0 = it.kvh * p.G + it.qg * GQ;
 
-  // 1. merge the NW warp partials (fixed warp order => deterministic).
-  float cta_m[GQ], cta_l[GQ];
+  // 1. merge weights of the NW warp partials (fixed warp order => deterministic).
+  float wsc[GQ][NW], cta_m[GQ], cta_l[GQ];
 #pragma unroll
   for (int g = 0; g < GQ; ++g) {
     float M = -INFINITY;
@@ -155,84 +154,113 @@ __device__ __forceinline__ void finish_item(const DecodeParams& p, const Item& i
 #pragma unroll
     for (int w = 0; w < NW; ++w) {
       const float mw = red_m[w * GQ + g];
-      if (mw != -INFINITY) L += (kLog2 ? exp2f(mw - M) : expf(mw - M)) * red_l[w * GQ + g];
+      wsc[g][w] = mw == -INFINITY ? 0.f : (kLog2 ? exp2f(mw - M) : expf(mw - M));
+      L += wsc[g][w] * red_l[w * GQ + g];
     }
     cta_m[g] = (M == -INFINITY) ? -INFINITY : (kLog2 ? M * kLn2 : M);  // natural units
     cta_l[g] = L;
   }
   auto merged_acc = [&](int g, int d) {
-    float M = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) M = fmaxf(M, red_m[w * GQ + g]);
     float A = 0.f;
 #pragma unroll
-    for (int w = 0; w < NW; ++w) {
-      const float mw = red_m[w * GQ + g];
-      if (mw != -INFINITY)
-        A += (kLog2 ? exp2f(mw - M) : expf(mw - M)) * red_acc[(w * GQ + g) * D + d];
-    }
+    for (int w = 0; w < NW; ++w) A = fmaf(wsc[g][w], red_acc[(w * GQ + g) * D + d], A);
     return A;
   };
 
-  if (live_splits(p, it.len) == 1) {
-    for (int e = tid; e < GQ * D; e += kThreads) {
-      const int g = e / D, d = e % D;
-      if (g >= nvalid) continue;
-      const float A = merged_acc(g, d), L = cta_l[g];
-      const int64_t o = (static_cast<int64_t>(b) * p.Hq + qh0 + g) * D + d;
-      store_out<T>(p, o, L > 0.f ? A / L : 0.f);
+  const int S_live = live_splits(p, it.len);
+  if (S_live == 1) {
+#pragma unroll
+    for (int g = 0; g < GQ; ++g) {
+      if (g >= nvalid) break;
+      const int64_t o = (static_cast<int64_t>(b) * p.Hq + qh0 + g) * D;
+      for (int d = lane; d < D; d += 32) {
+        const float L = cta_l[g];
+        store_out<T>(p, o + d, L > 0.f ? merged_acc(g, d) / L : 0.f);
+      }
+      if (lane == 0 && p.lse != nullptr)
+        p.lse[static_cast<int64_t>(b) * p.Hq + qh0 + g] =
+            cta_l[g] > 0.f ? cta_m[g] + logf(cta_l[g]) : -INFINITY;
     }
-    if (p.lse != nullptr && tid < GQ && tid < nvalid)
-      p.lse[static_cast<int64_t>(b) * p.Hq + qh0 + tid] =
-          cta_l[tid] > 0.f ? cta_m[tid] + logf(cta_l[tid]) : -INFINITY;
     return;
   }
 
-  // 2. write this split's partial.
-  for (int e = tid; e < GQ * D; e += kThreads) {
-    const int g = e / D, d = e % D;
-    if (g >= nvalid) continue;
+  // 2. write this split's partial, then count it in.
+#pragma unroll
+  for (int g = 0; g < GQ; ++g) {
+    if (g >= nvalid) break;
     const int64_t row = (static_cast<int64_t>(b) * p.Hq + qh0 + g) * p.S + it.split;
-    p.ws_acc[row * D + d] = merged_acc(g, d);
-  }
-  if (tid < GQ && tid < nvalid) {
-    const int64_t row = (static_cast<int64_t>(b) * p.Hq + qh0 + tid) * p.S + it.split;
-    p.ws_ml[row * 2 + 0] = cta_m[tid];
-    p.ws_ml[row * 2 + 1] = cta_l[tid];
+    for (int d = lane; d < D; d += 32) p.ws_acc[row * D + d] = merged_acc(g, d);
+    if (lane == 0) {
+      p.ws_ml[row * 2 + 0] = cta_m[g];
+      p.ws_ml[row * 2 + 1] = cta_l[g];
+    }
   }
   __threadfence();
-  named_bar_sync(1, kThreads);
+  __syncwarp();
   int32_t* counter = p.counters + (static_cast<int64_t>(b) * p.Hkv + it.kvh) * p.QG + it.qg;
-  if (tid == 0) {
-    const int prev = atomicAdd(counter, 1);
-    *s_flag = (prev == live_splits(p, it.len) - 1);
-  }
-  named_bar_sync(1, kThreads);
-  if (!*s_flag) return;
+  int last = 0;
+  if (lane == 0) last = (atomicAdd(counter, 1) == S_live - 1);
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return;
   __threadfence();
 
   // 3. last split of this unit: merge the live partials in split order and finalize.
-  const int S_live = live_splits(p, it.len);
-  for (int e = tid; e < GQ * D; e += kThreads) {
-    const int g = e / D, d = e % D;
-    if (g >= nvalid) continue;
+  for (int g = 0; g < nvalid && g < GQ; ++g) {
     const int64_t row0 = (static_cast<int64_t>(b) * p.Hq + qh0 + g) * p.S;
     float M = -INFINITY;
     for (int s = 0; s < S_live; ++s) M = fmaxf(M, __ldcg(p.ws_ml + (row0 + s) * 2));
-    float A = 0.f, L = 0.f;
+    float L = 0.f;
     for (int s = 0; s < S_live; ++s) {
       const float ms = __ldcg(p.ws_ml + (row0 + s) * 2);
-      if (ms == -INFINITY) continue;
-      const float w = expf(ms - M);
-      L += w * __ldcg(p.ws_ml + (row0 + s) * 2 + 1);
-      A += w * __ldcg(p.ws_acc + (row0 + s) * D + d);
+      if (ms != -INFINITY) L += expf(ms - M) * __ldcg(p.ws_ml + (row0 + s) * 2 + 1);
     }
-    const int64_t o = (static_cast<int64_t>(b) * p.Hq + qh0 + g) * D + d;
-    store_out<T>(p, o, L > 0.f ? A / L : 0.f);
-    if (d == 0 && p.lse != nullptr)
+    const int64_t o = (static_cast<int64_t>(b) * p.Hq + qh0 + g) * D;
+    for (int d = lane; d < D; d += 32) {
+      float A = 0.f;
+      for (int s = 0; s < S_live; ++s) {
+        const float ms = __ldcg(p.ws_ml + (row0 + s) * 2);
+        if (ms != -INFINITY) A += expf(ms - M) * __ldcg(p.ws_acc + (row0 + s) * D + d);
+      }
+      store_out<T>(p, o + d, L > 0.f ? A / L : 0.f);
+    }
+    if (lane == 0 && p.lse != nullptr)
       p.lse[static_cast<int64_t>(b) * p.Hq + qh0 + g] = L > 0.f ? M + logf(L) : -INFINITY;
   }
-  if (tid == 0) *counter = 0;  // ready for the next launch
+  if (lane == 0) *counter = 0;  // ready for the next launch
+}
+
+// Hand-off of per-warp partials from the consumer warps to the epilogue warp.  Single
+// red buffer: red_full (count NW) fills it, red_empty (count 1) frees it.  Item index k
+// counts hand-offs; the sentinel hand-off carries item -1.
+struct RedPipe {
+  uint64_t* full;
+  uint64_t* empty;
+  int* item;  // smem: item index of the buffered partials
+};
+
+// Consumer side, per warp: wait until the epilogue warp released the buffer (k > 0).
+__device__ __forceinline__ void red_acquire(const RedPipe& r, int k) {
+  if (k > 0) mbar_wait(r.empty, (k - 1) & 1);
+}
+__device__ __forceinline__ void red_commit(const RedPipe& r) {
+  __syncwarp();
+  if (threadIdx.x % 32 == 0) mbar_arrive(r.full);
+}
+
+// Epilogue warp main loop.
+template <typename T, int D, int GQ, int NW, bool kLog2, int TILE>
+__device__ __forceinline__ void epilogue_loop(const DecodeParams& p, const RedPipe& r,
+                                              int nvalid, const float* red_m,
+                                              const float* red_l, const float* red_acc) {
+  for (int k = 0;; ++k) {
+    mbar_wait(r.full, k & 1);
+    const int idx = *r.item;
+    if (idx < 0) break;
+    const Item it = make_item(p, idx, TILE);
+    finish_item_warp<T, D, GQ, NW, kLog2>(p, it, nvalid, red_m, red_l, red_acc);
+    __syncwarp();
+    if (threadIdx.x % 32 == 0) mbar_arrive(r.empty);
+  }
 }
 
 }  // namespace lam

@@ -29,9 +29,11 @@ struct MmaCfg {
   static constexpr int MAT_BYTES = 2 * BOX_BYTES;    // one K (or V) tile
   static constexpr int STAGE_BYTES = 2 * MAT_BYTES;  // K + V
   static constexpr int RING_BYTES = STAGES * STAGE_BYTES;
+  static constexpr int Q_BYTES = GQ * D * 2;        // one item's (padded) q rows
   static constexpr int RED_FLOATS = NW * GQ * (D + 2);
-  static constexpr int SMEM_BYTES =
-      RING_BYTES + RED_FLOATS * 4 + STAGES * 16 + 2 * STAGES * 8 + 16 + 1024;  // +align slack
+  static constexpr int SMEM_BYTES = RING_BYTES + STAGES * Q_BYTES + RED_FLOATS * 4 + STAGES * 16 +
+                                    (2 * STAGES + 2) * 8 + 16 + 1024;  // +align slack
+  static constexpr int THREADS = (NW + 2) * 32;    // + producer warp + epilogue warp
 };
 
 // Byte offset of 16-byte chunk `c` (0..15 across the 128-wide row) of tile row `r`
@@ -42,7 +44,7 @@ __device__ __forceinline__ uint32_t swz(int r, int c) {
 }
 
 template <typename T, int NW_, int STAGES_>
-__global__ void __launch_bounds__((NW_ + 1) * 32)
+__global__ void __launch_bounds__((NW_ + 2) * 32)
     decode_gqa_mma_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap kmap,
                           const __grid_constant__ CUtensorMap vmap) {
   using C = MmaCfg<NW_, STAGES_>;
@@ -50,13 +52,14 @@ __global__ void __launch_bounds__((NW_ + 1) * 32)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  float* red_m = reinterpret_cast<float*>(smem + C::RING_BYTES);
+  uint8_t* qslot = smem + C::RING_BYTES;  // [STAGES][8][D]
+  float* red_m = reinterpret_cast<float*>(qslot + STAGES * C::Q_BYTES);
   float* red_l = red_m + NW * GQ;
   float* red_acc = red_l + NW * GQ;
   int4* meta = reinterpret_cast<int4*>(red_m + C::RED_FLOATS);
   uint64_t* full = reinterpret_cast<uint64_t*>(meta + STAGES);
   uint64_t* empty = full + STAGES;
-  int* s_flag = reinterpret_cast<int*>(empty + STAGES);
+  RedPipe red{empty + STAGES, empty + STAGES + 1, reinterpret_cast<int*>(empty + STAGES + 2)};
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int G = p.G;  // real q heads in the group (<= 8); the rest are zero padding
@@ -66,6 +69,8 @@ __global__ void __launch_bounds__((NW_ + 1) * 32)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NW);
     }
+    mbar_init(red.full, NW);
+    mbar_init(red.empty, 1);
     fence_barrier_init();
   }
   if (warp == NW && lane == 0) {
@@ -81,13 +86,22 @@ __global__ void __launch_bounds__((NW_ + 1) * 32)
         const int tok = it.t_begin + j * TILE;
         const int32_t row = static_cast<int32_t>(kv_row(p, it.b, it.kvh, tok));
         uint8_t* st = smem + s * C::STAGE_BYTES;
-        mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
+        const uint32_t qb = static_cast<uint32_t>(G) * D * 2;
+        mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES + (j == 0 ? qb : 0));
+        if (j == 0)
+          tma_load_1d(qslot + s * C::Q_BYTES,
+                      static_cast<const T*>(p.q) + (static_cast<int64_t>(it.b) * p.Hq + it.kvh * G) * D,
+                      qb, &full[s], pol);
         tma_load_2d(st, &kmap, 0, row, &full[s], pol);
         tma_load_2d(st + C::BOX_BYTES, &kmap, 64, row, &full[s], pol);
         tma_load_2d(st + C::MAT_BYTES, &vmap, 0, row, &full[s], pol);
         tma_load_2d(st + C::MAT_BYTES + C::BOX_BYTES, &vmap, 64, row, &full[s], pol);
       });
     }
+    return;
+  }
+  if (warp == NW + 1) {
+    epilogue_loop<T, D, GQ, NW, true, TILE>(p, red, G, red_m, red_l, red_acc);
     return;
   }
 
@@ -107,19 +121,30 @@ __global__ void __launch_bounds__((NW_ + 1) * 32)
   float l0, l1;         // this lane's share of the softmax sums
   float o[8][4];        // O^T accumulators: (d = mt*16 + gr (+8), g = gc, gc+1)
   Item it{};
+  int k_item = 0;  // hand-offs to the epilogue warp
+  const uint32_t q_addr = smem_u32(qslot);
   for (int i = 0;; ++i) {
     const int s = i % STAGES;
     mbar_wait(&full[s], (i / STAGES) & 1);
     const int4 mt = meta[s];
-    if (mt.x < 0) break;
-    if (mt.y == 0) {
+    if (mt.x < 0) {
+      red_acquire(red, k_item);
+      if (warp == 0 && lane == 0) *red.item = -1;
+      red_commit(red);
+      break;
+    }
+    if (mt.y == 0) {  // first tile of a new item: its q rows arrived with this stage
       it = make_item(p, mt.x, TILE);
-      const uint32_t* qrow = reinterpret_cast<const uint32_t*>(
-          static_cast<const T*>(p.q) + (static_cast<int64_t>(it.b) * p.Hq + it.kvh * G + gr) * D);
+      const uint32_t qrow = q_addr + s * C::Q_BYTES + gr * D * 2;
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
-        qf[ks][0] = gr < G ? __ldg(qrow + (ks * 16 + gc) / 2) : 0u;
-        qf[ks][1] = gr < G ? __ldg(qrow + (ks * 16 + 8 + gc) / 2) : 0u;
+        uint32_t v0 = 0u, v1 = 0u;
+        if (gr < G && mt.z > 0) {
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v0) : "r"(qrow + (ks * 16 + gc) * 2));
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v1) : "r"(qrow + (ks * 16 + 8 + gc) * 2));
+        }
+        qf[ks][0] = v0;
+        qf[ks][1] = v1;
       }
       m0 = m1 = -INFINITY;
       l0 = l1 = 0.f;
@@ -205,7 +230,7 @@ __global__ void __launch_bounds__((NW_ + 1) * 32)
         s0 += __shfl_xor_sync(0xffffffffu, s0, off);
         s1 += __shfl_xor_sync(0xffffffffu, s1, off);
       }
-      named_bar_sync(1, NW * 32);  // the previous item's epilogue is done with red_*
+      red_acquire(red, k_item);
       if (gr == 0) {
         red_m[warp * GQ + gc] = m0;
         red_m[warp * GQ + gc + 1] = m1;
@@ -220,8 +245,9 @@ __global__ void __launch_bounds__((NW_ + 1) * 32)
         red_acc[(warp * GQ + gc) * D + d + 8] = o[t][2];
         red_acc[(warp * GQ + gc + 1) * D + d + 8] = o[t][3];
       }
-      named_bar_sync(1, NW * 32);
-      finish_item<T, D, GQ, NW, true>(p, it, G, red_m, red_l, red_acc, s_flag);
+      if (warp == 0 && lane == 0) *red.item = mt.x;
+      red_commit(red);
+      ++k_item;
     }
   }
 }

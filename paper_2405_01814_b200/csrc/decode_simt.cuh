@@ -8,7 +8,9 @@
 // own TILE/NW tokens of every tile and run an independent online softmax over them: q·k by
 // 16-byte vector FMAs reduced with warp shuffles, running max / rescale, p·v accumulated in fp32
 // registers.  At the end of an item the NW warp partials, and then the split partials, are
-// merged in fixed order (finish_item).
+// merged in fixed order by a dedicated epilogue warp (finish_item_warp) while the consumers
+// already stream the next item; the producer also prefetches each item's q rows by TMA, so an
+// item boundary costs the consumers nothing.
 //
 // Reference semantics: exact_attention / partial_attention
 // (/root/reference/proj/core/src/attention.cpp:48-98), logits = (q·k)·scale, fp32
@@ -33,27 +35,31 @@ struct SimtCfg {
   static constexpr int ITER = TPW / RPI;
   static constexpr int TILE_BYTES = TILE * D * sizeof(T);
   static constexpr int RING_BYTES = STAGES * 2 * TILE_BYTES;
+  static constexpr int Q_BYTES = GQ * D * sizeof(T);  // one item's q rows
   static constexpr int RED_FLOATS = NW * GQ * (D + 2);
-  static constexpr int SMEM_BYTES = RING_BYTES + RED_FLOATS * 4 + STAGES * 16 + 2 * STAGES * 8 + 16;
+  static constexpr int SMEM_BYTES = RING_BYTES + STAGES * Q_BYTES + RED_FLOATS * 4 + STAGES * 16 +
+                                    (2 * STAGES + 2) * 8 + 16;
+  static constexpr int THREADS = (NW + 2) * 32;      // + producer warp + epilogue warp
   static constexpr bool kLog2 = sizeof(T) < 4;
   static_assert(LPR >= 1 && LPR <= 32 && 32 % LPR == 0, "row must map onto a warp");
   static_assert(TPW % RPI == 0 && ITER >= 1, "warp slice must be whole instructions");
 };
 
 template <typename T, int D, int GQ, int NW, int TILE, int STAGES>
-__global__ void __launch_bounds__((NW + 1) * 32)
+__global__ void __launch_bounds__((NW + 2) * 32)
     decode_simt_kernel(const DecodeParams p) {
   using C = SimtCfg<T, D, GQ, NW, TILE, STAGES>;
   constexpr int VEC = C::VEC, LPR = C::LPR, RPI = C::RPI, TPW = C::TPW, ITER = C::ITER;
   extern __shared__ __align__(128) uint8_t smem[];
   T* ring = reinterpret_cast<T*>(smem);  // [STAGES][2][TILE][D]
-  float* red_m = reinterpret_cast<float*>(smem + C::RING_BYTES);
+  uint8_t* qslot = smem + C::RING_BYTES;  // [STAGES][GQ][D]
+  float* red_m = reinterpret_cast<float*>(qslot + STAGES * C::Q_BYTES);
   float* red_l = red_m + NW * GQ;
   float* red_acc = red_l + NW * GQ;
   int4* meta = reinterpret_cast<int4*>(red_m + C::RED_FLOATS);
   uint64_t* full = reinterpret_cast<uint64_t*>(meta + STAGES);
   uint64_t* empty = full + STAGES;
-  int* s_flag = reinterpret_cast<int*>(empty + STAGES);
+  RedPipe red{empty + STAGES, empty + STAGES + 1, reinterpret_cast<int*>(empty + STAGES + 2)};
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
@@ -61,6 +67,8 @@ __global__ void __launch_bounds__((NW + 1) * 32)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NW);
     }
+    mbar_init(red.full, NW);
+    mbar_init(red.empty, 1);
     fence_barrier_init();
   }
   __syncthreads();
@@ -77,11 +85,20 @@ __global__ void __launch_bounds__((NW + 1) * 32)
         const uint32_t bytes = static_cast<uint32_t>(rows) * D * sizeof(T);
         const int64_t row = kv_row(p, it.b, it.kvh, tok);
         T* ks = ring + static_cast<size_t>(s) * 2 * TILE * D;
-        mbar_arrive_expect_tx(&full[s], 2 * bytes);
+        mbar_arrive_expect_tx(&full[s], 2 * bytes + (j == 0 ? C::Q_BYTES : 0));
+        if (j == 0) {
+          const T* qsrc = static_cast<const T*>(p.q) +
+                          (static_cast<int64_t>(it.b) * p.Hq + it.kvh * p.G + it.qg * GQ) * D;
+          tma_load_1d(qslot + s * C::Q_BYTES, qsrc, C::Q_BYTES, &full[s], pol);
+        }
         tma_load_1d(ks, kp + row * D, bytes, &full[s], pol);
         tma_load_1d(ks + TILE * D, vp + row * D, bytes, &full[s], pol);
       });
     }
+    return;
+  }
+  if (warp == NW + 1) {
+    epilogue_loop<T, D, GQ, NW, C::kLog2, TILE>(p, red, GQ, red_m, red_l, red_acc);
     return;
   }
 
@@ -90,22 +107,27 @@ __global__ void __launch_bounds__((NW + 1) * 32)
   const int rg = lane / LPR;   // row group within one instruction
   const float sc = C::kLog2 ? p.scale_log2 : p.scale;
   const uint32_t ring_addr = smem_u32(ring);
+  const uint32_t q_addr = smem_u32(qslot);
 
   float q[GQ][VEC], m[GQ], l[GQ], acc[GQ][VEC];
   Item it{};
+  int k_item = 0;  // hand-offs to the epilogue warp
   for (int i = 0;; ++i) {
     const int s = i % STAGES;
     mbar_wait(&full[s], (i / STAGES) & 1);
     const int4 mt = meta[s];
-    if (mt.x < 0) break;
-    if (mt.y == 0) {  // first tile of a new item: load its q, reset the softmax state
+    if (mt.x < 0) {
+      red_acquire(red, k_item);
+      if (warp == 0 && lane == 0) *red.item = -1;
+      red_commit(red);
+      break;
+    }
+    if (mt.y == 0) {  // first tile of a new item: its q rows arrived with this stage
       it = make_item(p, mt.x, TILE);
-      const int qh0 = it.kvh * p.G + it.qg * GQ;
 #pragma unroll
       for (int g = 0; g < GQ; ++g) {
-        const T* qp = static_cast<const T*>(p.q) +
-                      (static_cast<int64_t>(it.b) * p.Hq + qh0 + g) * D + sub * VEC;
-        Elem<T>::unpack(*reinterpret_cast<const uint4*>(qp), q[g]);
+        if (mt.z > 0)
+          Elem<T>::unpack(lds128(q_addr + s * C::Q_BYTES + (g * D + sub * VEC) * sizeof(T)), q[g]);
         m[g] = -INFINITY;
         l[g] = 0.f;
 #pragma unroll
@@ -186,38 +208,32 @@ __global__ void __launch_bounds__((NW + 1) * 32)
     if (lane == 0) mbar_arrive(&empty[s]);
 
     if (mt.y == max(mt.z, 1) - 1) {
-      // end of the item: reduce the RPI row groups of each warp (they share m), then the
-      // warps, then the splits.
-      float lr[GQ], ar[GQ][VEC];
-#pragma unroll
-      for (int g = 0; g < GQ; ++g) {
-        lr[g] = l[g];
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) ar[g][e] = acc[g][e];
-      }
+      // end of the item: reduce the RPI row groups of each warp (they share m) and hand the
+      // warp partial to the epilogue warp.
 #pragma unroll
       for (int off = LPR; off < 32; off <<= 1) {
 #pragma unroll
         for (int g = 0; g < GQ; ++g) {
-          lr[g] += __shfl_xor_sync(0xffffffffu, lr[g], off);
+          l[g] += __shfl_xor_sync(0xffffffffu, l[g], off);
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) ar[g][e] += __shfl_xor_sync(0xffffffffu, ar[g][e], off);
+          for (int e = 0; e < VEC; ++e) acc[g][e] += __shfl_xor_sync(0xffffffffu, acc[g][e], off);
         }
       }
-      named_bar_sync(1, NW * 32);  // the previous item's epilogue is done with red_*
+      red_acquire(red, k_item);
       if (rg == 0) {
 #pragma unroll
         for (int g = 0; g < GQ; ++g) {
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) red_acc[(warp * GQ + g) * D + sub * VEC + e] = ar[g][e];
+          for (int e = 0; e < VEC; ++e) red_acc[(warp * GQ + g) * D + sub * VEC + e] = acc[g][e];
           if (sub == 0) {
             red_m[warp * GQ + g] = m[g];
-            red_l[warp * GQ + g] = lr[g];
+            red_l[warp * GQ + g] = l[g];
           }
         }
       }
-      named_bar_sync(1, NW * 32);
-      finish_item<T, D, GQ, NW, C::kLog2>(p, it, GQ, red_m, red_l, red_acc, s_flag);
+      if (warp == 0 && lane == 0) *red.item = mt.x;
+      red_commit(red);
+      ++k_item;
     }
   }
 }
