@@ -81,6 +81,11 @@ cudaError_t grow(T** ptr, int64_t* cap, int64_t need, bool zero) {
   return cudaSuccess;
 }
 
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+
 // ---- driver entry point for tensor maps (no -lcuda link dependency) ----
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -107,9 +112,15 @@ int make_pool_map(CUtensorMap* map, int dtype, const void* base, int64_t rows, i
   const cuuint32_t estr[2] = {1, 1};
   const CUtensorMapDataType dt =
       dtype == LAM_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  static const int promo = env_int("LAM_TMAP_PROMOTION", 3);  // 0 none, 1 64B, 2 128B, 3 256B
+  const CUtensorMapL2promotion pr =
+      promo == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                 : promo == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                              : promo == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                           : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   CUresult r = enc(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, pr,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(LAM_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
   return LAM_OK;
@@ -117,10 +128,6 @@ int make_pool_map(CUtensorMap* map, int dtype, const void* base, int64_t rows, i
 
 // Kernel variants (decode.cu LAM_MMA_VARIANTS / LAM_SIMT_VARIANTS); variant 0 is the tuned
 // default, LAM_GQA_VARIANT / LAM_SIMT_VARIANT / LAM_ITEMS_PER_CTA override it for tuning.
-int env_int(const char* name, int dflt) {
-  const char* e = std::getenv(name);
-  return e ? std::atoi(e) : dflt;
-}
 int gqa_variant() {
   static int v = env_int("LAM_GQA_VARIANT", 0);
   return v;

@@ -96,7 +96,7 @@ int mma_occ(int variant) {
 // SIMT variants (consumer warps, tokens per stage for 32-bit / 16-bit KV, stages).  Variant 0
 // is the default for every (dtype, D, GQ); the others exist for D = 128, GQ = 1 (tuning).
 #define LAM_SIMT_VARIANTS(X) \
-  X(0, 8, 32, 64, 6) X(1, 16, 32, 64, 6) X(2, 8, 32, 64, 3) X(3, 4, 32, 32, 4)
+  X(1, 8, 32, 64, 6) X(2, 8, 32, 64, 3) X(3, 4, 32, 32, 4) X(4, 16, 32, 64, 4)
 
 struct SimtLaunchF {
   const DecodeParams& p;
@@ -117,7 +117,8 @@ struct SimtTileF {
 template <typename T, int D, int GQ, class F>
 auto simt_variant(int variant, F f) {
   constexpr bool wide = sizeof(T) == 4;
-  if (variant == 0) return f.template operator()<T, D, GQ, 8, wide ? 32 : 64, 6>();
+  // default: 16 consumer warps (measured best on B200 for MHA), 8 when GQ = 4 (smem)
+  if (variant == 0) return f.template operator()<T, D, GQ, GQ <= 2 ? 16 : 8, wide ? 32 : 64, 6>();
   if constexpr (D == 128 && GQ == 1) {
 #define X(id, nw, t32, t16, st) \
     if (variant == id) return f.template operator()<T, D, GQ, nw, wide ? t32 : t16, st>();

@@ -205,24 +205,41 @@ __device__ __forceinline__ void finish_item_warp(const DecodeParams& p, const It
   __threadfence();
 
   // 3. last split of this unit: merge the live partials in split order and finalize.
+  //    Split statistics are loaded once per q head (lane s holds split s, s < 32 per pass)
+  //    and the accumulator rows of all splits are streamed with independent loads.
+  constexpr int DPL = D / 32;  // output dims per lane
   for (int g = 0; g < nvalid && g < GQ; ++g) {
     const int64_t row0 = (static_cast<int64_t>(b) * p.Hq + qh0 + g) * p.S;
     float M = -INFINITY;
-    for (int s = 0; s < S_live; ++s) M = fmaxf(M, __ldcg(p.ws_ml + (row0 + s) * 2));
-    float L = 0.f;
-    for (int s = 0; s < S_live; ++s) {
-      const float ms = __ldcg(p.ws_ml + (row0 + s) * 2);
-      if (ms != -INFINITY) L += expf(ms - M) * __ldcg(p.ws_ml + (row0 + s) * 2 + 1);
-    }
-    const int64_t o = (static_cast<int64_t>(b) * p.Hq + qh0 + g) * D;
-    for (int d = lane; d < D; d += 32) {
-      float A = 0.f;
-      for (int s = 0; s < S_live; ++s) {
-        const float ms = __ldcg(p.ws_ml + (row0 + s) * 2);
-        if (ms != -INFINITY) A += expf(ms - M) * __ldcg(p.ws_acc + (row0 + s) * D + d);
+    for (int s = lane; s < S_live; s += 32) M = fmaxf(M, __ldcg(p.ws_ml + (row0 + s) * 2));
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+    float L = 0.f, A[DPL];
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) A[e] = 0.f;
+    for (int s0 = 0; s0 < S_live; s0 += 32) {
+      float w = 0.f;
+      if (s0 + lane < S_live) {
+        const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + (row0 + s0 + lane) * 2));
+        w = ml.x == -INFINITY ? 0.f : expf(ml.x - M);
+        L += w * ml.y;
       }
-      store_out<T>(p, o + d, L > 0.f ? A / L : 0.f);
+      const int n = min(32, S_live - s0);
+      for (int j = 0; j < n; ++j) {
+        const float wj = __shfl_sync(0xffffffffu, w, j);
+        const float* src = p.ws_acc + (row0 + s0 + j) * D + lane;
+        float v[DPL];
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) v[e] = __ldcg(src + e * 32);
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) A[e] = fmaf(wj, v[e], A[e]);
+      }
     }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
+    const int64_t o = (static_cast<int64_t>(b) * p.Hq + qh0 + g) * D;
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) store_out<T>(p, o + lane + e * 32, L > 0.f ? A[e] / L : 0.f);
     if (lane == 0 && p.lse != nullptr)
       p.lse[static_cast<int64_t>(b) * p.Hq + qh0 + g] = L > 0.f ? M + logf(L) : -INFINITY;
   }
