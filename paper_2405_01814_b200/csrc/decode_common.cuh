@@ -85,7 +85,10 @@ __device__ __forceinline__ int live_splits(const DecodeParams& p, int len) {
 
 // ---- persistent producer ---------------------------------------------------------------
 // meta[s] = {item, tile index, tiles of the item, 0}; item < 0 is the end-of-work sentinel.
-// `issue(s, it, j)` must arrive on full[s] with expect_tx and start the stage's TMA copies.
+// `issue(s, it, j, row)` must arrive on full[s] with expect_tx and start the stage's TMA
+// copies of tile j, whose first KV row is `row`.  Global-memory latencies are kept off the
+// stream: the next tile's page-table entry is loaded one tile ahead, and the next item is
+// claimed (atomicAdd) and its length loaded while the current item streams.
 template <int STAGES, int TILE, class Issue>
 __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* full,
                                               uint64_t* empty, int4* meta, Issue issue) {
@@ -95,22 +98,37 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
     if (k >= STAGES) mbar_wait(&empty[s], ((k / STAGES) - 1) & 1);
     return s;
   };
-  for (;;) {
-    const int idx = atomicAdd(p.work, 1);
-    if (idx >= p.n_items) break;
-    const Item it = make_item(p, idx, TILE);
+  int idx = atomicAdd(p.work, 1);
+  Item it = make_item(p, idx < p.n_items ? idx : 0, TILE);
+  while (idx < p.n_items) {
+    const int next_idx = atomicAdd(p.work, 1);
+    const int next_safe = next_idx < p.n_items ? next_idx : 0;
+    Item nit;
+    bool have_next = false;
     if (it.ntiles == 0) {
-      if (it.split != 0 || it.len > 0) continue;  // empty split: nothing to merge
-      const int s = acquire(i++);                 // empty request: zero-output marker
-      meta[s] = make_int4(idx, 0, 0, 0);
-      mbar_arrive(&full[s]);
-      continue;
+      if (it.split == 0 && it.len == 0) {  // empty request: zero-output marker
+        const int s = acquire(i++);
+        meta[s] = make_int4(idx, 0, 0, 0);
+        mbar_arrive(&full[s]);
+      }                                    // (an empty split has nothing to merge)
+    } else {
+      int64_t row = kv_row(p, it.b, it.kvh, it.t_begin);
+      for (int j = 0; j < it.ntiles; ++j) {
+        const int64_t row_next =
+            j + 1 < it.ntiles ? kv_row(p, it.b, it.kvh, it.t_begin + (j + 1) * TILE) : 0;
+        const int s = acquire(i++);
+        meta[s] = make_int4(idx, j, it.ntiles, 0);
+        issue(s, it, j, row);
+        row = row_next;
+        if (j == 0) {
+          nit = make_item(p, next_safe, TILE);
+          have_next = true;
+        }
+      }
     }
-    for (int j = 0; j < it.ntiles; ++j) {
-      const int s = acquire(i++);
-      meta[s] = make_int4(idx, j, it.ntiles, 0);
-      issue(s, it, j);
-    }
+    if (!have_next) nit = make_item(p, next_safe, TILE);
+    idx = next_idx;
+    it = nit;
   }
   const int s = acquire(i);
   meta[s] = make_int4(-1, 0, 0, 0);

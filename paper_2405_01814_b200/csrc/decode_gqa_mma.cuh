@@ -82,9 +82,7 @@ __global__ void __launch_bounds__((NW_ + 2) * 32)
   if (warp == NW) {
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      producer_loop<STAGES, TILE>(p, full, empty, meta, [&](int s, const Item& it, int j) {
-        const int tok = it.t_begin + j * TILE;
-        const int32_t row = static_cast<int32_t>(kv_row(p, it.b, it.kvh, tok));
+      producer_loop<STAGES, TILE>(p, full, empty, meta, [&](int s, const Item& it, int j, int64_t row) {
         uint8_t* st = smem + s * C::STAGE_BYTES;
         const uint32_t qb = static_cast<uint32_t>(G) * D * 2;
         mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES + (j == 0 ? qb : 0));
@@ -92,10 +90,11 @@ __global__ void __launch_bounds__((NW_ + 2) * 32)
           tma_load_1d(qslot + s * C::Q_BYTES,
                       static_cast<const T*>(p.q) + (static_cast<int64_t>(it.b) * p.Hq + it.kvh * G) * D,
                       qb, &full[s], pol);
-        tma_load_2d(st, &kmap, 0, row, &full[s], pol);
-        tma_load_2d(st + C::BOX_BYTES, &kmap, 64, row, &full[s], pol);
-        tma_load_2d(st + C::MAT_BYTES, &vmap, 0, row, &full[s], pol);
-        tma_load_2d(st + C::MAT_BYTES + C::BOX_BYTES, &vmap, 64, row, &full[s], pol);
+        const int32_t r32 = static_cast<int32_t>(row);
+        tma_load_2d(st, &kmap, 0, r32, &full[s], pol);
+        tma_load_2d(st + C::BOX_BYTES, &kmap, 64, r32, &full[s], pol);
+        tma_load_2d(st + C::MAT_BYTES, &vmap, 0, r32, &full[s], pol);
+        tma_load_2d(st + C::MAT_BYTES + C::BOX_BYTES, &vmap, 64, r32, &full[s], pol);
       });
     }
     return;

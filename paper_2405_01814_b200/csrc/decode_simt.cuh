@@ -79,11 +79,10 @@ __global__ void __launch_bounds__((NW + 2) * 32)
       const uint64_t pol = policy_evict_first();
       const T* kp = static_cast<const T*>(p.k_pool);
       const T* vp = static_cast<const T*>(p.v_pool);
-      producer_loop<STAGES, TILE>(p, full, empty, meta, [&](int s, const Item& it, int j) {
+      producer_loop<STAGES, TILE>(p, full, empty, meta, [&](int s, const Item& it, int j, int64_t row) {
         const int tok = it.t_begin + j * TILE;
         const int rows = min(TILE, it.t_end - tok);
         const uint32_t bytes = static_cast<uint32_t>(rows) * D * sizeof(T);
-        const int64_t row = kv_row(p, it.b, it.kvh, tok);
         T* ks = ring + static_cast<size_t>(s) * 2 * TILE * D;
         mbar_arrive_expect_tx(&full[s], 2 * bytes + (j == 0 ? C::Q_BYTES : 0));
         if (j == 0) {
