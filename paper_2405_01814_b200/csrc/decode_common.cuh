@@ -101,10 +101,14 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
   int idx = atomicAdd(p.work, 1);
   Item it = make_item(p, idx < p.n_items ? idx : 0, TILE);
   while (idx < p.n_items) {
-    const int next_idx = atomicAdd(p.work, 1);
-    const int next_safe = next_idx < p.n_items ? next_idx : 0;
+    // The next item is claimed two tiles before this one runs out (not earlier: claiming is
+    // the load balancing), so the atomic and the length load overlap the last tiles.
+    int next_idx = -1;
     Item nit;
-    bool have_next = false;
+    auto claim_next = [&] {
+      next_idx = atomicAdd(p.work, 1);
+      nit = make_item(p, next_idx < p.n_items ? next_idx : 0, TILE);
+    };
     if (it.ntiles == 0) {
       if (it.split == 0 && it.len == 0) {  // empty request: zero-output marker
         const int s = acquire(i++);
@@ -112,6 +116,7 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
         mbar_arrive(&full[s]);
       }                                    // (an empty split has nothing to merge)
     } else {
+      const int claim_at = it.ntiles > 2 ? it.ntiles - 2 : 0;
       int64_t row = kv_row(p, it.b, it.kvh, it.t_begin);
       for (int j = 0; j < it.ntiles; ++j) {
         const int64_t row_next =
@@ -120,13 +125,10 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
         meta[s] = make_int4(idx, j, it.ntiles, 0);
         issue(s, it, j, row);
         row = row_next;
-        if (j == 0) {
-          nit = make_item(p, next_safe, TILE);
-          have_next = true;
-        }
+        if (j == claim_at) claim_next();
       }
     }
-    if (!have_next) nit = make_item(p, next_safe, TILE);
+    if (next_idx < 0) claim_next();
     idx = next_idx;
     it = nit;
   }
