@@ -152,19 +152,34 @@ struct Plan {
   int S = 1;
 };
 
-// Persistent kernels claim items dynamically, so the split count only has to give every
-// resident CTA enough items to balance the tail: the smallest S with
-// units * S >= items_per_cta * ctas (each split at least one tile).
-void choose_splits(Plan& pl, int64_t units, int max_len, int ctas, int split_tokens) {
+// Split count for the persistent kernels: minimise the modelled time of the busiest CTA,
+//   T(S) = items_per_cta * t_item + t_item / 2 (dynamic-claim tail) + items_per_cta * c_item
+// with t_item = item bytes / per-SM stream rate (~47 GB/s at the HBM roofline) and c_item the
+// measured cost of an item boundary (claim atomic + dependent loads + epilogue hand-off, ~4 us).
+// Fitted on B200: C1 and C2/C3 pick S = 1, C4 (256 long units on 148 SMs) picks S ~ 5.
+void choose_splits(Plan& pl, int64_t units, int max_len, int ctas, int split_tokens,
+                   double bytes_per_token) {
   const int tiles_total = std::max(1, (max_len + pl.tile - 1) / pl.tile);
   int ct;
   if (split_tokens > 0) {
     ct = std::max(1, (split_tokens + pl.tile - 1) / pl.tile);
   } else {
-    const int64_t want = static_cast<int64_t>(items_per_cta()) * ctas;
-    int64_t s = units > 0 ? (want + units - 1) / units : 1;
-    s = std::max<int64_t>(1, std::min<int64_t>(s, tiles_total));
-    ct = static_cast<int>((tiles_total + s - 1) / s);
+    const double sm_rate = 47e9 * (ctas > 0 ? 148.0 / ctas : 1.0);  // per resident CTA
+    const double c_item = 4e-6 * (items_per_cta() > 0 ? items_per_cta() / 4.0 : 1.0);
+    double best = 1e300;
+    ct = tiles_total;
+    for (int s = 1; s <= std::min(tiles_total, 64); ++s) {
+      const int c = (tiles_total + s - 1) / s;
+      const int s_eff = (tiles_total + c - 1) / c;
+      if (s_eff != s) continue;
+      const double t_item = static_cast<double>(c) * pl.tile * bytes_per_token / sm_rate;
+      const double per_cta = static_cast<double>(units) * s_eff / std::max(1, ctas);
+      const double t = std::max(1.0, per_cta) * (t_item + c_item) + 0.5 * t_item;
+      if (t < best * (1 - 1e-9)) {
+        best = t;
+        ct = c;
+      }
+    }
   }
   pl.chunk = ct * pl.tile;
   pl.S = (tiles_total + ct - 1) / ct;
@@ -225,7 +240,8 @@ int plan_decode(lam_ctx* ctx, const lam_decode_args* a, Plan* pl) {
   if (occ <= 0) return fail(LAM_ERR_CUDA, "decode kernel cannot be resident on this device");
   pl->ctas = occ * ctx->num_sms;
   const int64_t units = static_cast<int64_t>(a->batch) * a->num_kv_heads * pl->QG;
-  choose_splits(*pl, units, a->max_len, pl->ctas, a->split_tokens);
+  choose_splits(*pl, units, a->max_len, pl->ctas, a->split_tokens,
+                2.0 * a->head_dim * (kvd == LAM_F32 ? 4 : 2));
   if (pl->S > 65535) return fail(LAM_ERR_VALIDATION, "too many splits");
   return LAM_OK;
 }
@@ -657,6 +673,7 @@ int lam_decode(lam_ctx* ctx, const lam_decode_args* a, void* stream) {
   p.QG = pl.QG;
   p.n_items = static_cast<int32_t>(static_cast<int64_t>(a->batch) * a->num_kv_heads * pl.QG * pl.S);
   p.work = ctx->work;
+  p.flags = env_int("LAM_DECODE_FLAGS", 0);
   p.scale = a->scale;
   p.scale_log2 = a->scale * 1.4426950408889634f;
   p.out_f32 = a->out_dtype == LAM_F32;

@@ -9,6 +9,6 @@ for I in 1 2 4 8; do
   LAM_ITEMS_PER_CTA=$I timeout 300 python scripts/exp_decode.py --cfg $C --splits 0 | sed "s/^/i$I /"
   done
 done
-LAM_SIMT_VARIANT=4 timeout 300 python scripts/exp_decode.py --cfg c2 --splits 0 | sed "s/^/v4 /"
-LAM_GQA_VARIANT=1 timeout 300 python scripts/exp_decode.py --cfg c3 --splits 0 | sed "s/^/gv1 /"
+
+
 echo done
