@@ -44,7 +44,7 @@ struct DecodeParams {
   float scale;              // softmax scale (natural units)
   float scale_log2;         // scale * log2(e)
   int32_t out_f32;
-  int32_t flags;            // bit1: static round-robin items (default dynamic claiming)
+  int32_t flags;            // reserved (tuning experiments)
 };
 
 // Physical row of token t of (request b, kv head h) in a pool viewed as [rows][D].
@@ -84,76 +84,106 @@ __device__ __forceinline__ int live_splits(const DecodeParams& p, int len) {
   return len > 0 ? min(p.S, (len + p.chunk - 1) / p.chunk) : 1;
 }
 
-// ---- persistent producer ---------------------------------------------------------------
+// ---- persistent work pipeline ------------------------------------------------------------
+// Three agents per CTA:
+//  * scheduler warp (one lane): claims items from a global counter (dynamic scheduling absorbs
+//    the 2-3 % per-SM rate differences of the two-die part), loads the request length and the
+//    first page-table entry, and posts the item in a one-slot mailbox — one item ahead of the
+//    producer, so no global round trip ever sits between two tiles;
+//  * producer warp (one lane): streams the posted item's tiles into the stage ring;
+//  * consumer warps: follow the ring (meta[s] tags every stage with its item).
+struct SchedSlot {
+  int idx, b, kvh, qg, split, len, t_begin, t_end, ntiles, pad0;
+  long long row0;
+};
+
+struct SchedPipe {
+  uint64_t* full;   // count 1: scheduler posted an item
+  uint64_t* empty;  // count 1: producer took it
+  SchedSlot* slot;
+};
+
+template <int TILE>
+__device__ __forceinline__ void scheduler_loop(const DecodeParams& p, const SchedPipe& q) {
+  for (int k = 0;; ++k) {
+    // claim only once the producer has taken the previous item: exactly one item of lookahead
+    if (k > 0) mbar_wait(q.empty, (k - 1) & 1);
+    int idx;
+    Item it;
+    for (;;) {  // skip splits with nothing to merge
+      idx = atomicAdd(p.work, 1);
+      if (idx >= p.n_items) break;
+      it = make_item(p, idx, TILE);
+      if (it.ntiles > 0 || (it.split == 0 && it.len == 0)) break;
+    }
+    SchedSlot& s = *q.slot;
+    if (idx >= p.n_items) {
+      s.idx = -1;
+      mbar_arrive(q.full);
+      break;
+    }
+    s.idx = idx;
+    s.b = it.b;
+    s.kvh = it.kvh;
+    s.qg = it.qg;
+    s.split = it.split;
+    s.len = it.len;
+    s.t_begin = it.t_begin;
+    s.t_end = it.t_end;
+    s.ntiles = it.ntiles;
+    s.row0 = it.ntiles > 0 ? kv_row(p, it.b, it.kvh, it.t_begin) : 0;
+    mbar_arrive(q.full);
+  }
+  // the last scheduler to leave resets the counters for the next launch
+  if (atomicAdd(p.work + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+    p.work[0] = 0;
+    p.work[1] = 0;
+  }
+}
+
 // meta[s] = {item, tile index, tiles of the item, 0}; item < 0 is the end-of-work sentinel.
 // `issue(s, it, j, row)` must arrive on full[s] with expect_tx and start the stage's TMA
 // copies of tile j, whose first KV row is `row`.
-//
-// Two schedules (DecodeParams::flags bit 1 selects static):
-//  * dynamic (default): items are claimed from a global counter after the current one is
-//    issued.  Measured on B200 this beats a static split by 2-3 %: per-SM streaming rates differ
-//    (two dies, L2 distance) and dynamic claiming absorbs that.  Cost: one atomic plus two
-//    dependent loads at every item boundary (~2-4 us of one SM's stream, see choose_splits).
-//  * static: CTA c owns items c, c + gridDim.x, ...; the next item's length and first
-//    page-table entry are prefetched while the current item streams.
 template <int STAGES, int TILE, class Issue>
-__device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* full,
-                                              uint64_t* empty, int4* meta, Issue issue) {
+__device__ __forceinline__ void producer_loop(const DecodeParams& p, const SchedPipe& q,
+                                              uint64_t* full, uint64_t* empty, int4* meta,
+                                              Issue issue) {
   int i = 0;
   auto acquire = [&](int k) {
     const int s = k % STAGES;
     if (k >= STAGES) mbar_wait(&empty[s], ((k / STAGES) - 1) & 1);
     return s;
   };
-  auto run_item = [&](int idx, const Item& it, int64_t row0, auto&& during_first_tile) {
-    if (it.ntiles == 0) {
-      if (it.split == 0 && it.len == 0) {  // empty request: zero-output marker
-        const int s = acquire(i++);
-        meta[s] = make_int4(idx, 0, 0, 0);
-        mbar_arrive(&full[s]);
-      }                                    // (an empty split has nothing to merge)
-      during_first_tile();
-      return;
+  for (int k = 0;; ++k) {
+    mbar_wait(q.full, k & 1);
+    const SchedSlot ss = *q.slot;
+    mbar_arrive(q.empty);
+    if (ss.idx < 0) break;
+    Item it;
+    it.b = ss.b;
+    it.kvh = ss.kvh;
+    it.qg = ss.qg;
+    it.split = ss.split;
+    it.len = ss.len;
+    it.t_begin = ss.t_begin;
+    it.t_end = ss.t_end;
+    it.ntiles = ss.ntiles;
+    if (it.ntiles == 0) {  // empty request: zero-output marker
+      const int s = acquire(i++);
+      meta[s] = make_int4(ss.idx, 0, 0, 0);
+      mbar_arrive(&full[s]);
+      continue;
     }
     for (int j = 0; j < it.ntiles; ++j) {
       const int s = acquire(i++);
-      meta[s] = make_int4(idx, j, it.ntiles, 0);
-      issue(s, it, j, j == 0 ? row0 : kv_row(p, it.b, it.kvh, it.t_begin + j * TILE));
-      if (j == 0) during_first_tile();
-    }
-  };
-  const bool dynamic = (p.flags & 2) == 0;
-  if (!dynamic) {
-    int idx = blockIdx.x;
-    Item it = make_item(p, idx < p.n_items ? idx : 0, TILE);
-    int64_t row = it.ntiles ? kv_row(p, it.b, it.kvh, it.t_begin) : 0;
-    while (idx < p.n_items) {
-      const int nidx = idx + static_cast<int>(gridDim.x);
-      Item nit;
-      int64_t nrow = 0;
-      run_item(idx, it, row, [&] {  // prefetch the next item while this one streams
-        nit = make_item(p, nidx < p.n_items ? nidx : 0, TILE);
-        nrow = kv_row(p, nit.b, nit.kvh, nit.t_begin < nit.len ? nit.t_begin : 0);
-      });
-      idx = nidx;
-      it = nit;
-      row = nrow;
-    }
-  } else {
-    for (;;) {
-      const int idx = atomicAdd(p.work, 1);
-      if (idx >= p.n_items) break;
-      const Item it = make_item(p, idx, TILE);
-      run_item(idx, it, it.ntiles ? kv_row(p, it.b, it.kvh, it.t_begin) : 0, [] {});
+      meta[s] = make_int4(ss.idx, j, it.ntiles, 0);
+      issue(s, it, j, j == 0 ? static_cast<int64_t>(ss.row0)
+                              : kv_row(p, it.b, it.kvh, it.t_begin + j * TILE));
     }
   }
   const int s = acquire(i);
   meta[s] = make_int4(-1, 0, 0, 0);
   mbar_arrive(&full[s]);
-  if (dynamic && atomicAdd(p.work + 1, 1) == static_cast<int>(gridDim.x) - 1) {
-    p.work[0] = 0;  // the last producer to leave resets the counters for the next launch
-    p.work[1] = 0;
-  }
 }
 
 template <typename T>
