@@ -78,6 +78,24 @@ __device__ __forceinline__ Item make_item(const DecodeParams& p, int idx, int ti
   return it;
 }
 
+// Item fields from a stage tag {idx, tile, len, t_end} without touching global memory
+// (consumers must never stall on a load at an item boundary).
+template <int TILE>
+__device__ __forceinline__ Item item_from_tag(const DecodeParams& p, int4 tag) {
+  Item it;
+  it.split = tag.x % p.S;
+  int unit = tag.x / p.S;
+  it.qg = unit % p.QG;
+  unit /= p.QG;
+  it.kvh = unit % p.Hkv;
+  it.b = unit / p.Hkv;
+  it.len = tag.z;
+  it.t_begin = it.split * p.chunk;
+  it.t_end = tag.w;
+  it.ntiles = it.t_end > it.t_begin ? (it.t_end - it.t_begin + TILE - 1) / TILE : 0;
+  return it;
+}
+
 // Splits of a (request, kv head, q group) unit that carry tokens (>= 1: an empty request
 // still produces its zero output through split 0).
 __device__ __forceinline__ int live_splits(const DecodeParams& p, int len) {
@@ -141,7 +159,7 @@ __device__ __forceinline__ void scheduler_loop(const DecodeParams& p, const Sche
   }
 }
 
-// meta[s] = {item, tile index, tiles of the item, 0}; item < 0 is the end-of-work sentinel.
+// meta[s] = {item, tile index, request length, item end token}; item < 0 ends the work.
 // `issue(s, it, j, row)` must arrive on full[s] with expect_tx and start the stage's TMA
 // copies of tile j, whose first KV row is `row`.
 template <int STAGES, int TILE, class Issue>
@@ -170,13 +188,13 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, const Sched
     it.ntiles = ss.ntiles;
     if (it.ntiles == 0) {  // empty request: zero-output marker
       const int s = acquire(i++);
-      meta[s] = make_int4(ss.idx, 0, 0, 0);
+      meta[s] = make_int4(ss.idx, 0, 0, 0);  // len 0, t_end 0
       mbar_arrive(&full[s]);
       continue;
     }
     for (int j = 0; j < it.ntiles; ++j) {
       const int s = acquire(i++);
-      meta[s] = make_int4(ss.idx, j, it.ntiles, 0);
+      meta[s] = make_int4(ss.idx, j, it.len, it.t_end);
       issue(s, it, j, j == 0 ? static_cast<int64_t>(ss.row0)
                               : kv_row(p, it.b, it.kvh, it.t_begin + j * TILE));
     }
@@ -316,7 +334,7 @@ __device__ __forceinline__ void finish_item_warp(const DecodeParams& p, const It
 struct RedPipe {
   uint64_t* full;
   uint64_t* empty;
-  int* item;  // smem: item index of the buffered partials
+  int* item;  // smem: {item index, request length, item end token} of the buffered partials
 };
 
 // Consumer side, per warp: wait until the epilogue warp released the buffer (k > 0).
@@ -335,9 +353,9 @@ __device__ __forceinline__ void epilogue_loop(const DecodeParams& p, const RedPi
                                               const float* red_l, const float* red_acc) {
   for (int k = 0;; ++k) {
     mbar_wait(r.full, k & 1);
-    const int idx = *r.item;
+    const int idx = r.item[0];
     if (idx < 0) break;
-    const Item it = make_item(p, idx, TILE);
+    const Item it = item_from_tag<TILE>(p, make_int4(idx, 0, r.item[1], r.item[2]));
     finish_item_warp<T, D, GQ, NW, kLog2>(p, it, nvalid, red_m, red_l, red_acc);
     __syncwarp();
     if (threadIdx.x % 32 == 0) mbar_arrive(r.empty);

@@ -60,7 +60,7 @@ __global__ void __launch_bounds__((NW_ + 3) * 32)
   uint64_t* full = reinterpret_cast<uint64_t*>(meta + STAGES);
   uint64_t* empty = full + STAGES;
   RedPipe red{empty + STAGES, empty + STAGES + 1, reinterpret_cast<int*>(empty + STAGES + 2)};
-  SchedPipe sched{empty + STAGES + 3, empty + STAGES + 4,
+  SchedPipe sched{empty + STAGES + 4, empty + STAGES + 5,
                   reinterpret_cast<SchedSlot*>(empty + STAGES + 6)};
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -136,17 +136,17 @@ __global__ void __launch_bounds__((NW_ + 3) * 32)
     const int4 mt = meta[s];
     if (mt.x < 0) {
       red_acquire(red, k_item);
-      if (warp == 0 && lane == 0) *red.item = -1;
+      if (warp == 0 && lane == 0) red.item[0] = -1;
       red_commit(red);
       break;
     }
     if (mt.y == 0) {  // first tile of a new item: its q rows arrived with this stage
-      it = make_item(p, mt.x, TILE);
+      it = item_from_tag<TILE>(p, mt);
       const uint32_t qrow = q_addr + s * C::Q_BYTES + gr * D * 2;
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
         uint32_t v0 = 0u, v1 = 0u;
-        if (gr < G && mt.z > 0) {
+        if (gr < G && it.ntiles > 0) {
           asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v0) : "r"(qrow + (ks * 16 + gc) * 2));
           asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v1) : "r"(qrow + (ks * 16 + 8 + gc) * 2));
         }
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__((NW_ + 3) * 32)
         for (int e = 0; e < 4; ++e) o[t][e] = 0.f;
     }
     const int tok0 = it.t_begin + mt.y * TILE + warp * 16;
-    const int nval = mt.z > 0 ? min(16, it.t_end - tok0) : 0;
+    const int nval = it.ntiles > 0 ? min(16, it.t_end - tok0) : 0;
     const uint32_t kb = base + s * C::STAGE_BYTES;
     const uint32_t vb = kb + C::MAT_BYTES;
     if (nval > 0) {
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__((NW_ + 3) * 32)
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
 
-    if (mt.y == max(mt.z, 1) - 1) {
+    if (mt.y == max(it.ntiles, 1) - 1) {
       // end of the item: reduce the softmax sums over the 8 row groups (lanes with equal
       // lane&3), then merge the warps and the splits.
       float s0 = l0, s1 = l1;
@@ -252,7 +252,11 @@ __global__ void __launch_bounds__((NW_ + 3) * 32)
         red_acc[(warp * GQ + gc) * D + d + 8] = o[t][2];
         red_acc[(warp * GQ + gc + 1) * D + d + 8] = o[t][3];
       }
-      if (warp == 0 && lane == 0) *red.item = mt.x;
+      if (warp == 0 && lane == 0) {
+        red.item[0] = mt.x;
+        red.item[1] = mt.z;
+        red.item[2] = mt.w;
+      }
       red_commit(red);
       ++k_item;
     }

@@ -60,7 +60,7 @@ __global__ void __launch_bounds__((NW + 3) * 32)
   uint64_t* full = reinterpret_cast<uint64_t*>(meta + STAGES);
   uint64_t* empty = full + STAGES;
   RedPipe red{empty + STAGES, empty + STAGES + 1, reinterpret_cast<int*>(empty + STAGES + 2)};
-  SchedPipe sched{empty + STAGES + 3, empty + STAGES + 4,
+  SchedPipe sched{empty + STAGES + 4, empty + STAGES + 5,
                   reinterpret_cast<SchedSlot*>(empty + STAGES + 6)};
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -125,15 +125,15 @@ __global__ void __launch_bounds__((NW + 3) * 32)
     const int4 mt = meta[s];
     if (mt.x < 0) {
       red_acquire(red, k_item);
-      if (warp == 0 && lane == 0) *red.item = -1;
+      if (warp == 0 && lane == 0) red.item[0] = -1;
       red_commit(red);
       break;
     }
     if (mt.y == 0) {  // first tile of a new item: its q rows arrived with this stage
-      it = make_item(p, mt.x, TILE);
+      it = item_from_tag<TILE>(p, mt);
 #pragma unroll
       for (int g = 0; g < GQ; ++g) {
-        if (mt.z > 0)
+        if (it.ntiles > 0)
           Elem<T>::unpack(lds128(q_addr + s * C::Q_BYTES + (g * D + sub * VEC) * sizeof(T)), q[g]);
         m[g] = -INFINITY;
         l[g] = 0.f;
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__((NW + 3) * 32)
         for (int e = 0; e < VEC; ++e) acc[g][e] = 0.f;
       }
     }
-    if (mt.z > 0) {
+    if (it.ntiles > 0) {
       const int tile_tok = it.t_begin + mt.y * TILE;
       const uint32_t k_addr = ring_addr + s * 2 * C::TILE_BYTES;
       const uint32_t v_addr = k_addr + C::TILE_BYTES;
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__((NW + 3) * 32)
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
 
-    if (mt.y == max(mt.z, 1) - 1) {
+    if (mt.y == max(it.ntiles, 1) - 1) {
       // end of the item: reduce the RPI row groups of each warp (they share m) and hand the
       // warp partial to the epilogue warp.
 #pragma unroll
@@ -238,7 +238,11 @@ __global__ void __launch_bounds__((NW + 3) * 32)
           }
         }
       }
-      if (warp == 0 && lane == 0) *red.item = mt.x;
+      if (warp == 0 && lane == 0) {
+        red.item[0] = mt.x;
+        red.item[1] = mt.z;
+        red.item[2] = mt.w;
+      }
       red_commit(red);
       ++k_item;
     }
