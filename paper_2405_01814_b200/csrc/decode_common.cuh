@@ -216,10 +216,11 @@ __device__ __forceinline__ void store_out(const DecodeParams& p, int64_t idx, fl
 // consumer warps already stream the next item.  red_m/red_l/red_acc hold the NW per-warp
 // partials for GQ q heads: red_m[w*GQ+g] (log2 units if kLog2, else natural), red_l[w*GQ+g],
 // red_acc[(w*GQ+g)*D + d].  `nvalid` q heads of the group are real (the MMA kernel pads to 8).
-template <typename T, int D, int GQ, int NW, bool kLog2>
+template <typename T, int D, int GQ, int NW, bool kLog2, class Release>
 __device__ __forceinline__ void finish_item_warp(const DecodeParams& p, const Item& it,
                                                  int nvalid, const float* red_m,
-                                                 const float* red_l, const float* red_acc) {
+                                                 const float* red_l, const float* red_acc,
+                                                 Release release) {
   constexpr float kLn2 = 0.6931471805599453f;
   const int lane = threadIdx.x % 32;
   const int b = it.b;
@@ -263,6 +264,7 @@ __device__ __forceinline__ void finish_item_warp(const DecodeParams& p, const It
         p.lse[static_cast<int64_t>(b) * p.Hq + qh0 + g] =
             cta_l[g] > 0.f ? cta_m[g] + logf(cta_l[g]) : -INFINITY;
     }
+    release();
     return;
   }
 
@@ -277,6 +279,7 @@ __device__ __forceinline__ void finish_item_warp(const DecodeParams& p, const It
       p.ws_ml[row * 2 + 1] = cta_l[g];
     }
   }
+  release();  // the consumers may refill red_* while this warp counts and merges splits
   __threadfence();
   __syncwarp();
   int32_t* counter = p.counters + (static_cast<int64_t>(b) * p.Hkv + it.kvh) * p.QG + it.qg;
@@ -287,34 +290,56 @@ __device__ __forceinline__ void finish_item_warp(const DecodeParams& p, const It
   __threadfence();
 
   // 3. last split of this unit: merge the live partials in split order and finalize.
-  //    Split statistics are loaded once per q head (lane s holds split s, s < 32 per pass)
-  //    and the accumulator rows of all splits are streamed with independent loads.
+  //    The split statistics of every q head are loaded together (lane s holds split s), so a
+  //    merge costs a couple of L2 round trips, not one chain per head.
   constexpr int DPL = D / 32;  // output dims per lane
-  for (int g = 0; g < nvalid && g < GQ; ++g) {
+  float ms[GQ], ls[GQ];
+#pragma unroll
+  for (int g = 0; g < GQ; ++g) {
+    ms[g] = -INFINITY;
+    ls[g] = 0.f;
+    if (g < nvalid && lane < S_live) {
+      const float2 ml = __ldcg(reinterpret_cast<const float2*>(
+          p.ws_ml + ((static_cast<int64_t>(b) * p.Hq + qh0 + g) * p.S + lane) * 2));
+      ms[g] = ml.x;
+      ls[g] = ml.y;
+    }
+  }
+#pragma unroll
+  for (int g = 0; g < GQ; ++g) {
+    if (g >= nvalid) break;
     const int64_t row0 = (static_cast<int64_t>(b) * p.Hq + qh0 + g) * p.S;
-    float M = -INFINITY;
-    for (int s = lane; s < S_live; s += 32) M = fmaxf(M, __ldcg(p.ws_ml + (row0 + s) * 2));
+    float M = ms[g];
+    for (int s0 = 32 + lane; s0 < S_live; s0 += 32) M = fmaxf(M, __ldcg(p.ws_ml + (row0 + s0) * 2));
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-    float L = 0.f, A[DPL];
+    // lanes >= S_live hold -inf and weigh nothing; splits beyond 32 take a slow path
+    const float w = ms[g] == -INFINITY ? 0.f : expf(ms[g] - M);
+    float L = w * ls[g];
+    float A[DPL];
 #pragma unroll
     for (int e = 0; e < DPL; ++e) A[e] = 0.f;
-    for (int s0 = 0; s0 < S_live; s0 += 32) {
-      float w = 0.f;
+    const int n = min(32, S_live);
+    for (int j = 0; j < n; ++j) {
+      const float wj = __shfl_sync(0xffffffffu, w, j);
+      const float* src = p.ws_acc + (row0 + j) * D + lane;
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) A[e] = fmaf(wj, __ldcg(src + e * 32), A[e]);
+    }
+    for (int s0 = 32; s0 < S_live; s0 += 32) {  // more than 32 splits (rare)
+      float w2 = 0.f, m2 = -INFINITY;
       if (s0 + lane < S_live) {
         const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + (row0 + s0 + lane) * 2));
-        w = ml.x == -INFINITY ? 0.f : expf(ml.x - M);
-        L += w * ml.y;
+        m2 = ml.x;
+        w2 = ml.x == -INFINITY ? 0.f : expf(ml.x - M);
+        L += w2 * ml.y;
       }
-      const int n = min(32, S_live - s0);
-      for (int j = 0; j < n; ++j) {
-        const float wj = __shfl_sync(0xffffffffu, w, j);
+      (void)m2;
+      for (int j = 0; j < min(32, S_live - s0); ++j) {
+        const float wj = __shfl_sync(0xffffffffu, w2, j);
         const float* src = p.ws_acc + (row0 + s0 + j) * D + lane;
-        float v[DPL];
 #pragma unroll
-        for (int e = 0; e < DPL; ++e) v[e] = __ldcg(src + e * 32);
-#pragma unroll
-        for (int e = 0; e < DPL; ++e) A[e] = fmaf(wj, v[e], A[e]);
+        for (int e = 0; e < DPL; ++e) A[e] = fmaf(wj, __ldcg(src + e * 32), A[e]);
       }
     }
 #pragma unroll
@@ -356,9 +381,10 @@ __device__ __forceinline__ void epilogue_loop(const DecodeParams& p, const RedPi
     const int idx = r.item[0];
     if (idx < 0) break;
     const Item it = item_from_tag<TILE>(p, make_int4(idx, 0, r.item[1], r.item[2]));
-    finish_item_warp<T, D, GQ, NW, kLog2>(p, it, nvalid, red_m, red_l, red_acc);
-    __syncwarp();
-    if (threadIdx.x % 32 == 0) mbar_arrive(r.empty);
+    finish_item_warp<T, D, GQ, NW, kLog2>(p, it, nvalid, red_m, red_l, red_acc, [&] {
+      __syncwarp();
+      if (threadIdx.x % 32 == 0) mbar_arrive(r.empty);
+    });
   }
 }
 

@@ -212,3 +212,16 @@ def test_llama2_70b_layer_subset_parity(built, cfg):
         want = oracle_decode(q[b:b + 1], kd, vd, [L], scale, pairs=[(0, int(h)) for h in heads])
         for h in heads:
             assert _maxabs(out[b, h].cpu().numpy(), want[0, h]) <= 2e-3
+
+
+@pytest.mark.parametrize("dtype,G", [(torch.bfloat16, 8), (torch.bfloat16, 1), (torch.float32, 1)])
+def test_many_splits_combine(built, dtype, G):
+    """More than 32 live splits per head exercises the long combine path."""
+    B, Hkv, D, L = 2, 2, 128, 4000
+    q, k, v = make_dense(B, Hkv * G, Hkv, D, L, dtype, seed=21)
+    lens = [L, 2100]
+    scale = 1 / math.sqrt(D)
+    want = oracle_decode(q, k, v, lens, scale)
+    out = _decode(q, k, v, _lens_t(lens), scale=scale, out_dtype=torch.float32, split_tokens=64)
+    torch.cuda.synchronize()
+    assert _maxabs(out.cpu().numpy(), want) <= TOL[dtype]
