@@ -102,106 +102,50 @@ __device__ __forceinline__ int live_splits(const DecodeParams& p, int len) {
   return len > 0 ? min(p.S, (len + p.chunk - 1) / p.chunk) : 1;
 }
 
-// ---- persistent work pipeline ------------------------------------------------------------
-// Three agents per CTA:
-//  * scheduler warp (one lane): claims items from a global counter (dynamic scheduling absorbs
-//    the 2-3 % per-SM rate differences of the two-die part), loads the request length and the
-//    first page-table entry, and posts the item in a one-slot mailbox — one item ahead of the
-//    producer, so no global round trip ever sits between two tiles;
-//  * producer warp (one lane): streams the posted item's tiles into the stage ring;
-//  * consumer warps: follow the ring (meta[s] tags every stage with its item).
-struct SchedSlot {
-  int idx, b, kvh, qg, split, len, t_begin, t_end, ntiles, pad0;
-  long long row0;
-};
-
-struct SchedPipe {
-  uint64_t* full;   // count 1: scheduler posted an item
-  uint64_t* empty;  // count 1: producer took it
-  SchedSlot* slot;
-};
-
-template <int TILE>
-__device__ __forceinline__ void scheduler_loop(const DecodeParams& p, const SchedPipe& q) {
-  for (int k = 0;; ++k) {
-    // claim only once the producer has taken the previous item: exactly one item of lookahead
-    if (k > 0) mbar_wait(q.empty, (k - 1) & 1);
-    int idx;
-    Item it;
-    for (;;) {  // skip splits with nothing to merge
-      idx = atomicAdd(p.work, 1);
-      if (idx >= p.n_items) break;
-      it = make_item(p, idx, TILE);
-      if (it.ntiles > 0 || (it.split == 0 && it.len == 0)) break;
-    }
-    SchedSlot& s = *q.slot;
-    if (idx >= p.n_items) {
-      s.idx = -1;
-      mbar_arrive(q.full);
-      break;
-    }
-    s.idx = idx;
-    s.b = it.b;
-    s.kvh = it.kvh;
-    s.qg = it.qg;
-    s.split = it.split;
-    s.len = it.len;
-    s.t_begin = it.t_begin;
-    s.t_end = it.t_end;
-    s.ntiles = it.ntiles;
-    s.row0 = it.ntiles > 0 ? kv_row(p, it.b, it.kvh, it.t_begin) : 0;
-    mbar_arrive(q.full);
-  }
-  // the last scheduler to leave resets the counters for the next launch
-  if (atomicAdd(p.work + 1, 1) == static_cast<int>(gridDim.x) - 1) {
-    p.work[0] = 0;
-    p.work[1] = 0;
-  }
-}
-
+// ---- persistent producer ---------------------------------------------------------------
 // meta[s] = {item, tile index, request length, item end token}; item < 0 ends the work.
 // `issue(s, it, j, row)` must arrive on full[s] with expect_tx and start the stage's TMA
 // copies of tile j, whose first KV row is `row`.
+//
+// Items are claimed from a global counter right after the previous item's tiles are issued.
+// Measured on B200 this dynamic schedule beats a static round-robin split by 2-3 % (per-SM
+// streaming rates differ across the two dies) and beats claiming one item ahead (that costs up
+// to one item of tail imbalance); the stage ring covers the claim's round trips.
 template <int STAGES, int TILE, class Issue>
-__device__ __forceinline__ void producer_loop(const DecodeParams& p, const SchedPipe& q,
-                                              uint64_t* full, uint64_t* empty, int4* meta,
-                                              Issue issue) {
+__device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* full,
+                                              uint64_t* empty, int4* meta, Issue issue) {
   int i = 0;
   auto acquire = [&](int k) {
     const int s = k % STAGES;
     if (k >= STAGES) mbar_wait(&empty[s], ((k / STAGES) - 1) & 1);
     return s;
   };
-  for (int k = 0;; ++k) {
-    mbar_wait(q.full, k & 1);
-    const SchedSlot ss = *q.slot;
-    mbar_arrive(q.empty);
-    if (ss.idx < 0) break;
-    Item it;
-    it.b = ss.b;
-    it.kvh = ss.kvh;
-    it.qg = ss.qg;
-    it.split = ss.split;
-    it.len = ss.len;
-    it.t_begin = ss.t_begin;
-    it.t_end = ss.t_end;
-    it.ntiles = ss.ntiles;
-    if (it.ntiles == 0) {  // empty request: zero-output marker
-      const int s = acquire(i++);
-      meta[s] = make_int4(ss.idx, 0, 0, 0);  // len 0, t_end 0
-      mbar_arrive(&full[s]);
+  for (;;) {
+    const int idx = atomicAdd(p.work, 1);
+    if (idx >= p.n_items) break;
+    const Item it = make_item(p, idx, TILE);
+    if (it.ntiles == 0) {
+      if (it.split == 0 && it.len == 0) {  // empty request: zero-output marker
+        const int s = acquire(i++);
+        meta[s] = make_int4(idx, 0, 0, 0);
+        mbar_arrive(&full[s]);
+      }                                    // (an empty split has nothing to merge)
       continue;
     }
     for (int j = 0; j < it.ntiles; ++j) {
       const int s = acquire(i++);
-      meta[s] = make_int4(ss.idx, j, it.len, it.t_end);
-      issue(s, it, j, j == 0 ? static_cast<int64_t>(ss.row0)
-                              : kv_row(p, it.b, it.kvh, it.t_begin + j * TILE));
+      meta[s] = make_int4(idx, j, it.len, it.t_end);
+      issue(s, it, j, kv_row(p, it.b, it.kvh, it.t_begin + j * TILE));
     }
   }
   const int s = acquire(i);
   meta[s] = make_int4(-1, 0, 0, 0);
   mbar_arrive(&full[s]);
+  // the last producer to leave resets the counters for the next launch
+  if (atomicAdd(p.work + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+    p.work[0] = 0;
+    p.work[1] = 0;
+  }
 }
 
 template <typename T>

@@ -33,7 +33,7 @@ struct MmaCfg {
   static constexpr int RED_FLOATS = NW * GQ * (D + 2);
   static constexpr int SMEM_BYTES = RING_BYTES + STAGES * Q_BYTES + RED_FLOATS * 4 + STAGES * 16 +
                                     (2 * STAGES + 4) * 8 + 16 + 64 + 1024;  // +align slack
-  static constexpr int THREADS = (NW + 3) * 32;  // + producer, epilogue, scheduler warps
+  static constexpr int THREADS = (NW + 2) * 32;  // + producer warp + epilogue warp
 };
 
 // Byte offset of 16-byte chunk `c` (0..15 across the 128-wide row) of tile row `r`
@@ -44,7 +44,7 @@ __device__ __forceinline__ uint32_t swz(int r, int c) {
 }
 
 template <typename T, int NW_, int STAGES_>
-__global__ void __launch_bounds__((NW_ + 3) * 32)
+__global__ void __launch_bounds__((NW_ + 2) * 32)
     decode_gqa_mma_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap kmap,
                           const __grid_constant__ CUtensorMap vmap) {
   using C = MmaCfg<NW_, STAGES_>;
@@ -60,8 +60,6 @@ __global__ void __launch_bounds__((NW_ + 3) * 32)
   uint64_t* full = reinterpret_cast<uint64_t*>(meta + STAGES);
   uint64_t* empty = full + STAGES;
   RedPipe red{empty + STAGES, empty + STAGES + 1, reinterpret_cast<int*>(empty + STAGES + 2)};
-  SchedPipe sched{empty + STAGES + 4, empty + STAGES + 5,
-                  reinterpret_cast<SchedSlot*>(empty + STAGES + 6)};
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int G = p.G;  // real q heads in the group (<= 8); the rest are zero padding
@@ -73,8 +71,6 @@ __global__ void __launch_bounds__((NW_ + 3) * 32)
     }
     mbar_init(red.full, NW);
     mbar_init(red.empty, 1);
-    mbar_init(sched.full, 1);
-    mbar_init(sched.empty, 1);
     fence_barrier_init();
   }
   if (warp == NW && lane == 0) {
@@ -86,7 +82,7 @@ __global__ void __launch_bounds__((NW_ + 3) * 32)
   if (warp == NW) {
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      producer_loop<STAGES, TILE>(p, sched, full, empty, meta, [&](int s, const Item& it, int j, int64_t row) {
+      producer_loop<STAGES, TILE>(p, full, empty, meta, [&](int s, const Item& it, int j, int64_t row) {
         uint8_t* st = smem + s * C::STAGE_BYTES;
         const uint32_t qb = static_cast<uint32_t>(G) * D * 2;
         mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES + (j == 0 ? qb : 0));
@@ -101,10 +97,6 @@ __global__ void __launch_bounds__((NW_ + 3) * 32)
         tma_load_2d(st + C::MAT_BYTES + C::BOX_BYTES, &vmap, 64, r32, &full[s], pol);
       });
     }
-    return;
-  }
-  if (warp == NW + 2) {
-    if (lane == 0) scheduler_loop<TILE>(p, sched);
     return;
   }
   if (warp == NW + 1) {

@@ -39,14 +39,14 @@ struct SimtCfg {
   static constexpr int RED_FLOATS = NW * GQ * (D + 2);
   static constexpr int SMEM_BYTES = RING_BYTES + STAGES * Q_BYTES + RED_FLOATS * 4 + STAGES * 16 +
                                     (2 * STAGES + 4) * 8 + 16 + 64;
-  static constexpr int THREADS = (NW + 3) * 32;  // + producer, epilogue, scheduler warps
+  static constexpr int THREADS = (NW + 2) * 32;  // + producer warp + epilogue warp
   static constexpr bool kLog2 = sizeof(T) < 4;
   static_assert(LPR >= 1 && LPR <= 32 && 32 % LPR == 0, "row must map onto a warp");
   static_assert(TPW % RPI == 0 && ITER >= 1, "warp slice must be whole instructions");
 };
 
 template <typename T, int D, int GQ, int NW, int TILE, int STAGES>
-__global__ void __launch_bounds__((NW + 3) * 32)
+__global__ void __launch_bounds__((NW + 2) * 32)
     decode_simt_kernel(const DecodeParams p) {
   using C = SimtCfg<T, D, GQ, NW, TILE, STAGES>;
   constexpr int VEC = C::VEC, LPR = C::LPR, RPI = C::RPI, TPW = C::TPW, ITER = C::ITER;
@@ -60,8 +60,6 @@ __global__ void __launch_bounds__((NW + 3) * 32)
   uint64_t* full = reinterpret_cast<uint64_t*>(meta + STAGES);
   uint64_t* empty = full + STAGES;
   RedPipe red{empty + STAGES, empty + STAGES + 1, reinterpret_cast<int*>(empty + STAGES + 2)};
-  SchedPipe sched{empty + STAGES + 4, empty + STAGES + 5,
-                  reinterpret_cast<SchedSlot*>(empty + STAGES + 6)};
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
@@ -71,8 +69,6 @@ __global__ void __launch_bounds__((NW + 3) * 32)
     }
     mbar_init(red.full, NW);
     mbar_init(red.empty, 1);
-    mbar_init(sched.full, 1);
-    mbar_init(sched.empty, 1);
     fence_barrier_init();
   }
   __syncthreads();
@@ -83,7 +79,7 @@ __global__ void __launch_bounds__((NW + 3) * 32)
       const uint64_t pol = policy_evict_first();
       const T* kp = static_cast<const T*>(p.k_pool);
       const T* vp = static_cast<const T*>(p.v_pool);
-      producer_loop<STAGES, TILE>(p, sched, full, empty, meta, [&](int s, const Item& it, int j, int64_t row) {
+      producer_loop<STAGES, TILE>(p, full, empty, meta, [&](int s, const Item& it, int j, int64_t row) {
         const int tok = it.t_begin + j * TILE;
         const int rows = min(TILE, it.t_end - tok);
         const uint32_t bytes = static_cast<uint32_t>(rows) * D * sizeof(T);
@@ -98,10 +94,6 @@ __global__ void __launch_bounds__((NW + 3) * 32)
         tma_load_1d(ks + TILE * D, vp + row * D, bytes, &full[s], pol);
       });
     }
-    return;
-  }
-  if (warp == NW + 2) {
-    if (lane == 0) scheduler_loop<TILE>(p, sched);
     return;
   }
   if (warp == NW + 1) {
