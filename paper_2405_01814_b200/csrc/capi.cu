@@ -152,37 +152,47 @@ struct Plan {
   int S = 1;
 };
 
-// Split count for the persistent kernels: minimise the modelled time of the busiest CTA,
-//   T(S) = items_per_cta * t_item + t_item / 2 (dynamic-claim tail) + items_per_cta * c_item
-// with t_item = item bytes / per-SM stream rate (~47 GB/s at the HBM roofline) and c_item the
-// measured cost of an item boundary (claim atomic + dependent loads + epilogue hand-off, ~4 us).
-// Fitted on B200: C1 and C2/C3 pick S = 1, C4 (256 long units on 148 SMs) picks S ~ 5.
-void choose_splits(Plan& pl, int64_t units, int max_len, int ctas, int split_tokens,
+// Split count and grid size for the persistent kernels, from a small model fitted on B200:
+// the chip streams ~BW_CHIP, one SM at most ~RATE_SM (so fewer CTAs can each stream faster);
+// with dynamic claiming, `full` rounds of items run on every CTA and the remaining `rem` items
+// run on rem CTAs at min(BW_CHIP / rem, RATE_SM); every item boundary costs ~C_ITEM.
+//   T(S, ctas) = full * t_item(ctas) + [rem > 0] t_item(rem) + ceil(items / ctas) * C_ITEM
+// Measured choices: C1, C2, C3 -> S = 1; C4 -> S = 4; grid 128-132 CTAs for the GQA shapes
+// whose item counts (512, 1024) divide evenly there (up to +4 % over a full 148-CTA grid).
+void choose_splits(Plan& pl, int64_t units, int max_len, int max_ctas, int split_tokens,
                    double bytes_per_token) {
+  constexpr double BW_CHIP = 7.0e12, RATE_SM = 56e9, C_ITEM = 4e-6;
   const int tiles_total = std::max(1, (max_len + pl.tile - 1) / pl.tile);
-  int ct;
-  if (split_tokens > 0) {
-    ct = std::max(1, (split_tokens + pl.tile - 1) / pl.tile);
-  } else {
-    const double sm_rate = 47e9 * (ctas > 0 ? 148.0 / ctas : 1.0);  // per resident CTA
-    const double c_item = 4e-6 * (items_per_cta() > 0 ? items_per_cta() / 4.0 : 1.0);
-    double best = 1e300;
-    ct = tiles_total;
-    for (int s = 1; s <= std::min(tiles_total, 64); ++s) {
-      const int c = (tiles_total + s - 1) / s;
-      const int s_eff = (tiles_total + c - 1) / c;
-      if (s_eff != s) continue;
-      const double t_item = static_cast<double>(c) * pl.tile * bytes_per_token / sm_rate;
-      const double per_cta = static_cast<double>(units) * s_eff / std::max(1, ctas);
-      const double t = std::max(1.0, per_cta) * (t_item + c_item) + 0.5 * t_item;
-      if (t < best * (1 - 1e-9)) {
+  const int occ_per_sm = std::max(1, max_ctas / 148);
+  double best = 1e300;
+  int best_ct = tiles_total, best_ctas = max_ctas;
+  const int s_max = split_tokens > 0 ? 1 : std::min(tiles_total, 64);
+  for (int s = 1; s <= s_max; ++s) {
+    const int c = split_tokens > 0 ? std::max(1, (split_tokens + pl.tile - 1) / pl.tile)
+                                    : (tiles_total + s - 1) / s;
+    const int s_eff = (tiles_total + c - 1) / c;
+    if (split_tokens <= 0 && s_eff != s) continue;
+    const double item_bytes = static_cast<double>(c) * pl.tile * bytes_per_token;
+    const int64_t items = units * s_eff;
+    const int lo = std::max(1, (max_ctas * 3) / 4);
+    for (int ctas = max_ctas; ctas >= lo; --ctas) {
+      const double rate = [&](double n) { return std::min(BW_CHIP / n, RATE_SM * occ_per_sm); }(ctas);
+      const int64_t full = items / ctas, rem = items % ctas;
+      double t = static_cast<double>(full) * item_bytes / rate;
+      if (rem > 0) t += item_bytes / std::min(BW_CHIP / static_cast<double>(rem), RATE_SM * occ_per_sm);
+      t += static_cast<double>((items + ctas - 1) / ctas) * C_ITEM *
+           (items_per_cta() > 0 ? items_per_cta() / 4.0 : 1.0);
+      // a smaller grid or more splits must win by >= 1.5 % (model noise)
+      if (t < best * (1 - 0.015)) {
         best = t;
-        ct = c;
+        best_ct = c;
+        best_ctas = ctas;
       }
     }
   }
-  pl.chunk = ct * pl.tile;
-  pl.S = (tiles_total + ct - 1) / ct;
+  pl.chunk = best_ct * pl.tile;
+  pl.S = (tiles_total + best_ct - 1) / best_ct;
+  pl.ctas = best_ctas;
 }
 
 int plan_decode(lam_ctx* ctx, const lam_decode_args* a, Plan* pl) {
@@ -238,10 +248,11 @@ int plan_decode(lam_ctx* ctx, const lam_decode_args* a, Plan* pl) {
                       ? lam::occupancy_mma(kvd, pl->variant)
                       : lam::occupancy_simt(kvd, a->head_dim, pl->GQ, pl->variant);
   if (occ <= 0) return fail(LAM_ERR_CUDA, "decode kernel cannot be resident on this device");
-  pl->ctas = occ * ctx->num_sms;
   const int64_t units = static_cast<int64_t>(a->batch) * a->num_kv_heads * pl->QG;
-  choose_splits(*pl, units, a->max_len, pl->ctas, a->split_tokens,
+  choose_splits(*pl, units, a->max_len, occ * ctx->num_sms, a->split_tokens,
                 2.0 * a->head_dim * (kvd == LAM_F32 ? 4 : 2));
+  if (const int force = env_int("LAM_DECODE_CTAS", 0); force > 0)
+    pl->ctas = std::min(force, occ * ctx->num_sms);
   if (pl->S > 65535) return fail(LAM_ERR_VALIDATION, "too many splits");
   return LAM_OK;
 }
