@@ -300,11 +300,14 @@ class Workload:
         if self.geo is None:
             qs = (self.layers, self.B_local, self.Hq, self.D)
             ks = (self.layers, self.B_local, self.Hkv, self.D)
+            self.q_in = torch.empty(qs, dtype=self.dtype, device=device).uniform_(-1, 1, generator=gi)
+            self.kn_in = torch.empty(ks, dtype=self.dtype, device=device).uniform_(-1, 1, generator=gi)
+            self.vn_in = torch.empty_like(self.kn_in).uniform_(-1, 1, generator=gi)
         else:
-            qs, ks = self.geo.q_shape(), self.geo.kv_shape()
-        self.q_in = torch.empty(qs, dtype=self.dtype, device=device).uniform_(-1, 1, generator=gi)
-        self.kn_in = torch.empty(ks, dtype=self.dtype, device=device).uniform_(-1, 1, generator=gi)
-        self.vn_in = torch.empty_like(self.kn_in).uniform_(-1, 1, generator=gi)
+            qs = self.geo.q_shape()
+            # packed QKV projection rows per destination shard (one all-to-all per micro-batch)
+            self.qkv_in = torch.empty(self.geo.qkv_shape(), dtype=self.dtype,
+                                      device=device).uniform_(-1, 1, generator=gi)
         self.out = torch.empty(qs, dtype=self.dtype, device=device)
         # reference attn_cost bytes of one step over ALL requests and heads (whole job)
         self.step_bytes = float(PF.kv_bytes_per_token(self.spec)) * float(self.lens.sum())
@@ -390,7 +393,7 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
         if engine is None:
             step_local(ev)
         else:
-            engine.step(W.q_in, W.kn_in, W.vn_in, W.out, ev)
+            engine.step(W.qkv_in, W.out, ev)
 
     def barrier():
         torch.cuda.synchronize(device)
@@ -490,16 +493,13 @@ def run_e2e(args, W, engine, dist, device, stream):
 
     lib = _lib.load()
     L = W.layers
-    h_q = W.q_in.cpu().pin_memory()
-    h_kn = W.kn_in.cpu().pin_memory()
-    h_vn = W.vn_in.cpu().pin_memory()
     h_out = torch.empty(W.out.shape, dtype=W.out.dtype).pin_memory()
     if engine is not None:
+        h_qkv = W.qkv_in.cpu().pin_memory()
+
         def step_mg():
-            W.q_in.copy_(h_q, non_blocking=True)
-            W.kn_in.copy_(h_kn, non_blocking=True)
-            W.vn_in.copy_(h_vn, non_blocking=True)
-            engine.step(W.q_in, W.kn_in, W.vn_in, W.out)
+            W.qkv_in.copy_(h_qkv, non_blocking=True)
+            engine.step(W.qkv_in, W.out)
             h_out.copy_(W.out, non_blocking=True)
 
         for _ in range(max(1, args.warmup)):
@@ -515,11 +515,14 @@ def run_e2e(args, W, engine, dist, device, stream):
         t = torch.tensor([t0.elapsed_time(t1) / max(args.steps, 1)], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t[0])
-        h2d = (h_q.numel() + h_kn.numel() + h_vn.numel()) * h_q.element_size()
+        h2d = h_qkv.numel() * h_qkv.element_size()
         d2h = h_out.numel() * h_out.element_size()
         return {"value": W.step_bytes / (ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
                 "h2d_bytes_per_step": int(h2d) * W.world, "d2h_bytes_per_step": int(d2h) * W.world,
                 "api": "HeadShardedAttention.step (pinned host in/out, NCCL all-to-all)"}
+    h_q = W.q_in.cpu().pin_memory()
+    h_kn = W.kn_in.cpu().pin_memory()
+    h_vn = W.vn_in.cpu().pin_memory()
     d_q = torch.empty_like(W.q_in[0])
     d_kn = torch.empty_like(W.kn_in[0])
     d_vn = torch.empty_like(W.vn_in[0])

@@ -161,6 +161,9 @@ typedef struct lam_decode_args {
   const int32_t* seq_lens;
   void* out;
   float* lse;
+  /* elements between consecutive requests' q blocks; 0 = num_q_heads * head_dim.  A packed QKV
+   * projection output [B][Hq + 2 Hkv][D] is decoded in place with (Hq + 2 Hkv) * head_dim. */
+  int64_t q_batch_stride;
 } lam_decode_args;
 
 int lam_decode(lam_ctx* ctx, const lam_decode_args* args, void* stream);
@@ -169,12 +172,13 @@ int lam_decode_plan(lam_ctx* ctx, const lam_decode_args* args, int32_t* kernel,
                     int32_t* num_splits, int32_t* split_tokens);
 
 /* Write the new token of every request into the paged pools (bit-exact copy):
- *   k_pool[page_table[b][pos/P]][h][pos%P][:] = k_new[b][h][:], same for V,
- *   pos = positions[b].  Dense layout when page_table == NULL (pos < page_size). */
+ *   k_pool[page_table[b][pos/P]][h][pos%P][:] = k_new[b*new_batch_stride + h*D ...], same for V,
+ *   pos = positions[b].  Dense layout when page_table == NULL (pos < page_size).
+ *   new_batch_stride = 0 means num_kv_heads * head_dim (dense [B][Hkv][D] inputs). */
 int lam_kv_append(int32_t dtype, int32_t batch, int32_t num_kv_heads, int32_t head_dim,
                   int32_t page_size, int32_t pt_stride, const int32_t* page_table,
                   const int32_t* positions, const void* k_new, const void* v_new,
-                  void* k_pool, void* v_pool, void* stream);
+                  int64_t new_batch_stride, void* k_pool, void* v_pool, void* stream);
 
 /* Gather tokens [0, len_b) of every request from the paged pool into a dense
  * [B][Hkv][l_max][D] buffer (inverse of the paging; used to prove bit-exactness). */

@@ -54,6 +54,7 @@ class DecodeArgs(C.Structure):
         ("seq_lens", C.c_void_p),
         ("out", C.c_void_p),
         ("lse", C.c_void_p),
+        ("q_batch_stride", C.c_int64),
     ]
 
 
@@ -81,7 +82,8 @@ SIGNATURES = {
     "lam_request_partition": (C.c_int, [_P, _I64, _I64, _P, _P, _P]),
     "lam_decode": (C.c_int, [_P, C.POINTER(DecodeArgs), _P]),
     "lam_decode_plan": (C.c_int, [_P, C.POINTER(DecodeArgs), _P, _P, _P]),
-    "lam_kv_append": (C.c_int, [_I32, _I32, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P]),
+    "lam_kv_append": (C.c_int, [_I32, _I32, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _I64, _P, _P,
+                                _P]),
     "lam_kv_gather": (C.c_int, [_I32, _I32, _I32, _I32, _I32, _I32, _P, _P, _I32, _P, _P, _P]),
     "lam_decode_step_host": (C.c_int, [_P, C.POINTER(DecodeArgs), _P, _P, _P, _P, _P, _P, _P,
                                        _P]),

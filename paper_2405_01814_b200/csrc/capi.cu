@@ -210,6 +210,10 @@ int plan_decode(lam_ctx* ctx, const lam_decode_args* a, Plan* pl) {
     return fail(LAM_ERR_VALIDATION, "head_dim must be 64 or 128 on the decode path");
   if (a->page_size < 1) return fail(LAM_ERR_VALIDATION, "page_size must be >= 1");
   if (a->max_len < 0) return fail(LAM_ERR_VALIDATION, "max_len must be >= 0");
+  if (a->q_batch_stride != 0 &&
+      (a->q_batch_stride < static_cast<int64_t>(a->num_q_heads) * a->head_dim ||
+       (a->q_batch_stride * (kvd == LAM_F32 ? 4 : 2)) % 16 != 0))
+    return fail(LAM_ERR_VALIDATION, "q_batch_stride must cover Hq*D and keep 16-byte rows");
   const int G = a->num_q_heads / a->num_kv_heads;
   const bool paged = a->page_table != nullptr;
   if (!paged && a->max_len > a->page_size)
@@ -666,6 +670,8 @@ int lam_decode(lam_ctx* ctx, const lam_decode_args* a, void* stream) {
   const int D = a->head_dim;
   lam::DecodeParams p{};
   p.q = a->q;
+  p.q_stride = a->q_batch_stride > 0 ? a->q_batch_stride
+                                     : static_cast<int64_t>(a->num_q_heads) * a->head_dim;
   p.k_pool = a->k_pool;
   p.v_pool = a->v_pool;
   p.page_table = a->page_table;
@@ -721,14 +727,18 @@ int lam_decode(lam_ctx* ctx, const lam_decode_args* a, void* stream) {
 
 int lam_kv_append(int32_t dtype, int32_t batch, int32_t num_kv_heads, int32_t head_dim,
                   int32_t page_size, int32_t pt_stride, const int32_t* page_table,
-                  const int32_t* positions, const void* k_new, const void* v_new, void* k_pool,
-                  void* v_pool, void* stream) {
+                  const int32_t* positions, const void* k_new, const void* v_new,
+                  int64_t new_batch_stride, void* k_pool, void* v_pool, void* stream) {
   const int e = elem_bytes(dtype);
   if (e == 0 || (head_dim * e) % 16 != 0)
     return fail(LAM_ERR_VALIDATION, "kv_append needs rows that are a multiple of 16 bytes");
   if (page_size < 1) return fail(LAM_ERR_VALIDATION, "page_size must be >= 1");
+  const int64_t stride = new_batch_stride > 0 ? new_batch_stride
+                                              : static_cast<int64_t>(num_kv_heads) * head_dim;
+  if ((stride * e) % 16 != 0)
+    return fail(LAM_ERR_VALIDATION, "kv_append batch stride must keep rows 16-byte aligned");
   LAM_CUDA(lam::launch_kv_append(e, batch, num_kv_heads, head_dim, page_size, pt_stride,
-                                 page_table, positions, k_new, v_new, k_pool, v_pool,
+                                 page_table, positions, k_new, v_new, stride, k_pool, v_pool,
                                  static_cast<cudaStream_t>(stream)));
   return LAM_OK;
 }
@@ -761,7 +771,7 @@ int lam_decode_step_host(lam_ctx* ctx, const lam_decode_args* a, const void* h_q
   LAM_CUDA(cudaMemcpyAsync(d_k_new, h_k_new, kb, cudaMemcpyHostToDevice, s));
   LAM_CUDA(cudaMemcpyAsync(d_v_new, h_v_new, kb, cudaMemcpyHostToDevice, s));
   int rc = lam_kv_append(a->kv_dtype, a->batch, a->num_kv_heads, a->head_dim, a->page_size,
-                         a->pt_stride, a->page_table, d_positions, d_k_new, d_v_new,
+                         a->pt_stride, a->page_table, d_positions, d_k_new, d_v_new, 0,
                          const_cast<void*>(a->k_pool), const_cast<void*>(a->v_pool), stream);
   if (rc != LAM_OK) return rc;
   rc = lam_decode(ctx, a, stream);

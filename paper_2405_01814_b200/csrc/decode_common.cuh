@@ -24,7 +24,8 @@
 namespace lam {
 
 struct DecodeParams {
-  const void* q;            // [B][Hq][D]
+  const void* q;            // request b, q head h at q + b * q_stride + h * D
+  int64_t q_stride;
   const void* k_pool;       // see lamina_attn.h for the layouts
   const void* v_pool;
   const int32_t* page_table;  // nullptr => dense [B][Hkv][P][D]

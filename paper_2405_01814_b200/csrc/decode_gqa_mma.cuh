@@ -88,7 +88,8 @@ __global__ void __launch_bounds__((NW_ + 2) * 32)
         mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES + (j == 0 ? qb : 0));
         if (j == 0)
           tma_load_1d(qslot + s * C::Q_BYTES,
-                      static_cast<const T*>(p.q) + (static_cast<int64_t>(it.b) * p.Hq + it.kvh * G) * D,
+                      static_cast<const T*>(p.q) + static_cast<int64_t>(it.b) * p.q_stride +
+                          static_cast<int64_t>(it.kvh) * G * D,
                       qb, &full[s], pol);
         const int32_t r32 = static_cast<int32_t>(row);
         tma_load_2d(st, &kmap, 0, r32, &full[s], pol);

@@ -86,8 +86,8 @@ __global__ void __launch_bounds__((NW + 2) * 32)
         T* ks = ring + static_cast<size_t>(s) * 2 * TILE * D;
         mbar_arrive_expect_tx(&full[s], 2 * bytes + (j == 0 ? C::Q_BYTES : 0));
         if (j == 0) {
-          const T* qsrc = static_cast<const T*>(p.q) +
-                          (static_cast<int64_t>(it.b) * p.Hq + it.kvh * p.G + it.qg * GQ) * D;
+          const T* qsrc = static_cast<const T*>(p.q) + static_cast<int64_t>(it.b) * p.q_stride +
+                          static_cast<int64_t>(it.kvh * p.G + it.qg * GQ) * D;
           tma_load_1d(qslot + s * C::Q_BYTES, qsrc, C::Q_BYTES, &full[s], pol);
         }
         tma_load_1d(ks, kp + row * D, bytes, &full[s], pol);

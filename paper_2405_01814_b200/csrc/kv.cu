@@ -17,7 +17,8 @@ __global__ void kv_append_kernel(int32_t B, int32_t Hkv, int32_t row_vecs, int32
                                  int32_t pt_stride, const int32_t* __restrict__ page_table,
                                  const int32_t* __restrict__ positions,
                                  const uint4* __restrict__ k_new, const uint4* __restrict__ v_new,
-                                 uint4* __restrict__ k_pool, uint4* __restrict__ v_pool) {
+                                 int64_t src_batch_vecs, uint4* __restrict__ k_pool,
+                                 uint4* __restrict__ v_pool) {
   const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
   const int lane = threadIdx.x % 32;
   if (wid >= static_cast<int64_t>(B) * Hkv) return;
@@ -26,7 +27,7 @@ __global__ void kv_append_kernel(int32_t B, int32_t Hkv, int32_t row_vecs, int32
   const int64_t blk = page_table ? page_table[static_cast<int64_t>(b) * pt_stride + pos / page_size]
                                  : static_cast<int64_t>(b);
   const int64_t dst = ((blk * Hkv + h) * page_size + pos % page_size) * row_vecs;
-  const int64_t src = wid * row_vecs;
+  const int64_t src = b * src_batch_vecs + static_cast<int64_t>(h) * row_vecs;
   for (int e = lane; e < row_vecs; e += 32) {
     k_pool[dst + e] = k_new[src + e];
     v_pool[dst + e] = v_new[src + e];
@@ -56,7 +57,7 @@ __global__ void kv_gather_kernel(int32_t Hkv, int32_t row_vecs, int32_t page_siz
 cudaError_t launch_kv_append(int32_t elem_bytes, int32_t B, int32_t Hkv, int32_t D,
                              int32_t page_size, int32_t pt_stride, const int32_t* page_table,
                              const int32_t* positions, const void* k_new, const void* v_new,
-                             void* k_pool, void* v_pool, cudaStream_t stream) {
+                             int64_t new_stride, void* k_pool, void* v_pool, cudaStream_t stream) {
   const int32_t row_vecs = D * elem_bytes / 16;
   const int64_t warps = static_cast<int64_t>(B) * Hkv;
   if (warps == 0) return cudaSuccess;
@@ -65,7 +66,7 @@ cudaError_t launch_kv_append(int32_t elem_bytes, int32_t B, int32_t Hkv, int32_t
   kv_append_kernel<<<static_cast<unsigned>(blocks), threads, 0, stream>>>(
       B, Hkv, row_vecs, page_size, pt_stride, page_table, positions,
       static_cast<const uint4*>(k_new), static_cast<const uint4*>(v_new),
-      static_cast<uint4*>(k_pool), static_cast<uint4*>(v_pool));
+      new_stride * elem_bytes / 16, static_cast<uint4*>(k_pool), static_cast<uint4*>(v_pool));
   return cudaGetLastError();
 }
 

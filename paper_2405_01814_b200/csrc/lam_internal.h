@@ -44,7 +44,7 @@ cudaError_t launch_finalize(int dtype, int64_t n, int32_t d, const void* acc, co
 cudaError_t launch_kv_append(int32_t elem_bytes, int32_t B, int32_t Hkv, int32_t D,
                              int32_t page_size, int32_t pt_stride, const int32_t* page_table,
                              const int32_t* positions, const void* k_new, const void* v_new,
-                             void* k_pool, void* v_pool, cudaStream_t stream);
+                             int64_t new_stride, void* k_pool, void* v_pool, cudaStream_t stream);
 cudaError_t launch_kv_gather(int32_t elem_bytes, int32_t B, int32_t Hkv, int32_t D,
                              int32_t page_size, int32_t pt_stride, const int32_t* page_table,
                              const int32_t* seq_lens, int32_t l_max, const void* pool,

@@ -52,9 +52,11 @@ def make_args(q: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor,
         raise _lib.ValidationError("pool head_dim differs from q")
     if k_pool.dtype != q.dtype or v_pool.dtype != q.dtype:
         raise _lib.ValidationError("q and the KV pools must share a dtype")
-    for t in (q, k_pool, v_pool):
+    for t in (k_pool, v_pool):
         if not t.is_contiguous():
-            raise _lib.ValidationError("decode tensors must be contiguous")
+            raise _lib.ValidationError("KV pools must be contiguous")
+    if q.stride(2) != 1 or q.stride(1) != D:
+        raise _lib.ValidationError("q rows must be contiguous [B, Hq, D] (a batch stride is allowed)")
     if seq_lens.dtype != torch.int32:
         raise _lib.ValidationError("seq_lens must be int32")
     if page_table is not None and page_table.dtype != torch.int32:
@@ -79,6 +81,7 @@ def make_args(q: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor,
     a.seq_lens = seq_lens.data_ptr()
     a.out = out.data_ptr()
     a.lse = lse.data_ptr() if lse is not None else None
+    a.q_batch_stride = q.stride(0) if B > 1 and q.stride(0) != Hq * D else 0
     return a, out
 
 
@@ -111,16 +114,20 @@ def plan(q, k_pool, v_pool, seq_lens, **kw):
 
 
 def kv_append(k_new, v_new, k_pool, v_pool, positions, page_table=None, stream=None):
-    """k_pool[page(b, pos)][h][pos % P] = k_new[b][h] (and V), pos = positions[b]."""
+    """k_pool[page(b, pos)][h][pos % P] = k_new[b][h] (and V), pos = positions[b].
+    k_new / v_new are [B, Hkv, D] with contiguous heads; a batch stride (e.g. slices of a packed
+    QKV projection output [B, Hq + 2 Hkv, D]) is allowed if both share it."""
     _require_cuda(k_new, v_new, k_pool, v_pool, positions, page_table)
     B, Hkv, D = k_new.shape
+    if (k_new.stride(2) != 1 or k_new.stride(1) != D or v_new.stride() != k_new.stride()):
+        raise _lib.ValidationError("k_new/v_new must be [B, Hkv, D] rows with one shared batch stride")
     P = k_pool.shape[2]
     pts = page_table.shape[1] if page_table is not None else 0
     check(_lib.load().lam_kv_append(
         _DT[k_new.dtype], B, Hkv, D, P, pts,
         page_table.data_ptr() if page_table is not None else None, positions.data_ptr(),
-        k_new.data_ptr(), v_new.data_ptr(), k_pool.data_ptr(), v_pool.data_ptr(),
-        _stream_ptr(stream)))
+        k_new.data_ptr(), v_new.data_ptr(), k_new.stride(0) if B > 1 else 0, k_pool.data_ptr(),
+        v_pool.data_ptr(), _stream_ptr(stream)))
 
 
 def kv_gather(pool, page_table, seq_lens, l_max, stream=None):

@@ -16,9 +16,11 @@ core/src/sim.cpp:286-346) on N GPUs of one box:
   max(attention, communication) (sim.cpp:374-379).
 
 Layouts (all contiguous, micro-batch outermost so every collective moves one contiguous
-buffer):  inputs  q_in [L, MB, N, Bh, hq_l, D], k_in/v_in [L, MB, N, Bh, hkv_l, D] where the
-N axis is the destination head shard; outputs out [L, MB, N, Bh, hq_l, D] where N is the
-source head shard.  On the attention side request r of micro-batch m from source s is row
+buffer): inputs qkv_in [L, MB, N, Bh, W, D] with W = hq_l + 2 hkv_l — per destination head shard
+(the N axis) each request's packed QKV-projection rows [q heads | k heads | v heads], the layout a
+QKV GEMM produces — so one all-to-all per (layer, micro-batch) carries Q, K_new and V_new;
+outputs out [L, MB, N, Bh, hq_l, D] where N is the source head shard.  The receiving side
+decodes q and appends k/v straight out of the packed buffer (batch strides, no repacking).  On the attention side request r of micro-batch m from source s is row
 m*N*Bh + s*Bh + i of the KV store, so a micro-batch is a contiguous slice of the page table.
 The local append/attend ops are injected: the GPU path passes our kernels (lam_kv_append,
 lam_decode); the CPU gloo test passes the oracle.
@@ -76,11 +78,16 @@ class ShardGeometry:
         m, i = divmod(b_local, self.Bh)
         return m * self.B_mb + src * self.Bh + i
 
+    @property
+    def W(self) -> int:
+        """packed rows per request and shard: q heads, k heads, v heads"""
+        return self.hq_l + 2 * self.hkv_l
+
     def q_shape(self):
         return (self.layers, self.micro_batches, self.world, self.Bh, self.hq_l, self.D)
 
-    def kv_shape(self):
-        return (self.layers, self.micro_batches, self.world, self.Bh, self.hkv_l, self.D)
+    def qkv_shape(self):
+        return (self.layers, self.micro_batches, self.world, self.Bh, self.W, self.D)
 
 
 class HeadShardedAttention:
@@ -98,12 +105,10 @@ class HeadShardedAttention:
         g = geo
         MB = g.micro_batches
         # attention-side receive / send buffers, one per micro-batch
-        self.q_r = [torch.empty((g.world, g.Bh, g.hq_l, g.D), dtype=dtype, device=device)
+        self.qkv_r = [torch.empty((g.world, g.Bh, g.W, g.D), dtype=dtype, device=device)
+                      for _ in range(MB)]
+        self.o_l = [torch.empty((g.world, g.Bh, g.hq_l, g.D), dtype=dtype, device=device)
                     for _ in range(MB)]
-        self.k_r = [torch.empty((g.world, g.Bh, g.hkv_l, g.D), dtype=dtype, device=device)
-                    for _ in range(MB)]
-        self.v_r = [torch.empty_like(self.k_r[0]) for _ in range(MB)]
-        self.o_l = [torch.empty_like(self.q_r[0]) for _ in range(MB)]
         self.cuda = device.type == "cuda"
         if self.cuda:
             self.comm = torch.cuda.Stream(device=device)
@@ -113,7 +118,7 @@ class HeadShardedAttention:
     def _a2a(self, out: torch.Tensor, inp: torch.Tensor):
         self.dist.all_to_all_single(out, inp)
 
-    def step(self, q_in, k_in, v_in, out, ev=None):
+    def step(self, qkv_in, out, ev=None):
         """One decode step over all layers; returns when the work is enqueued (CUDA) or done
         (CPU).  `ev`, if given, is a list of (start, end) CUDA event pairs, one per local
         attention launch, recorded on the compute stream."""
@@ -122,7 +127,7 @@ class HeadShardedAttention:
         if not self.cuda:
             for layer in range(g.layers):
                 for m in range(MB):
-                    self._scatter(layer, m, q_in, k_in, v_in)
+                    self._scatter(layer, m, qkv_in)
                     self._attend(layer, m, None)
                     self._a2a(out[layer, m], self.o_l[m])
             return
@@ -138,7 +143,7 @@ class HeadShardedAttention:
                     # micro-batch m's next layer follows its previous output gather (data
                     # dependency through the model worker) and the reuse of its receive buffers
                     comm.wait_event(done[layer - 1][m])
-                self._scatter(layer, m, q_in, k_in, v_in)
+                self._scatter(layer, m, qkv_in)
                 scat[layer][m].record(comm)
 
         def gather(layer, m):
@@ -166,20 +171,19 @@ class HeadShardedAttention:
             gath = [torch.cuda.Event() for _ in range(MB)]
         comp.wait_stream(comm)
 
-    def _scatter(self, layer, m, q_in, k_in, v_in):
-        self._a2a(self.q_r[m], q_in[layer, m])
-        self._a2a(self.k_r[m], k_in[layer, m])
-        self._a2a(self.v_r[m], v_in[layer, m])
+    def _scatter(self, layer, m, qkv_in):
+        self._a2a(self.qkv_r[m], qkv_in[layer, m])
 
     def _attend(self, layer, m, e):
         g = self.geo
-        kr = self.k_r[m].view(g.B_mb, g.hkv_l, g.D)
-        vr = self.v_r[m].view(g.B_mb, g.hkv_l, g.D)
-        self.append_fn(layer, m, kr, vr)
+        packed = self.qkv_r[m].view(g.B_mb, g.W, g.D)
+        q = packed[:, : g.hq_l]
+        k = packed[:, g.hq_l: g.hq_l + g.hkv_l]
+        v = packed[:, g.hq_l + g.hkv_l:]
+        self.append_fn(layer, m, k, v)
         if e is not None:
             e[0].record(self.compute)
-        self.attend_fn(layer, m, self.q_r[m].view(g.B_mb, g.hq_l, g.D),
-                       self.o_l[m].view(g.B_mb, g.hq_l, g.D))
+        self.attend_fn(layer, m, q, self.o_l[m].view(g.B_mb, g.hq_l, g.D))
         if e is not None:
             e[1].record(self.compute)
 
@@ -192,14 +196,14 @@ def stitch_outputs(out: torch.Tensor) -> torch.Tensor:
 
 
 def shard_inputs(q: torch.Tensor, kn: torch.Tensor, vn: torch.Tensor, world: int,
-                 micro_batches: int = 2):
-    """[L, B_local, H, D] head-major model-worker tensors -> destination-major send layout."""
+                 micro_batches: int = 2) -> torch.Tensor:
+    """[L, B_local, H, D] head-major model-worker tensors -> packed destination-major send
+    layout [L, MB, N, Bh, hq_l + 2 hkv_l, D]."""
     L, B, Hq, D = q.shape
     Hkv = kn.shape[2]
     Bh = B // micro_batches
 
     def f(x, H):
-        return (x.view(L, micro_batches, Bh, world, H // world, D)
-                .permute(0, 1, 3, 2, 4, 5).contiguous())
+        return x.view(L, micro_batches, Bh, world, H // world, D).permute(0, 1, 3, 2, 4, 5)
 
-    return f(q, Hq), f(kn, Hkv), f(vn, Hkv)
+    return torch.cat([f(q, Hq), f(kn, Hkv), f(vn, Hkv)], dim=4).contiguous()

@@ -69,10 +69,9 @@ def main():
 
     eng = HeadShardedAttention(geo, dist, append, attend, dev, torch.bfloat16)
     mine = slice(rank * B_LOCAL, (rank + 1) * B_LOCAL)
-    q_in, k_in, v_in = (t.to(dev) for t in shard_inputs(q[:, mine], kn[:, mine], vn[:, mine],
-                                                        world, MB))
+    qkv_in = shard_inputs(q[:, mine], kn[:, mine], vn[:, mine], world, MB).to(dev)
     out = torch.zeros(geo.q_shape(), dtype=torch.bfloat16, device=dev)
-    eng.step(q_in, k_in, v_in, out)
+    eng.step(qkv_in, out)
     torch.cuda.synchronize()
     got = stitch_outputs(out).float().cpu().numpy()
     worst = 0.0

@@ -225,3 +225,28 @@ def test_many_splits_combine(built, dtype, G):
     out = _decode(q, k, v, _lens_t(lens), scale=scale, out_dtype=torch.float32, split_tokens=64)
     torch.cuda.synchronize()
     assert _maxabs(out.cpu().numpy(), want) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("G", [1, 8])
+def test_packed_qkv_strides(built, G):
+    """q / k_new / v_new taken straight out of a packed QKV projection output
+    [B, Hq + 2 Hkv, D] (batch strides) give exactly the contiguous results."""
+    from paper_2405_01814_b200 import decode as dec
+
+    B, Hkv, D, P, L = 3, 2, 128, 64, 200
+    Hq = Hkv * G
+    q, k, v = make_dense(B, Hq, Hkv, D, L, torch.bfloat16, seed=31)
+    lens = [200, 64, 129]
+    pt, npages = page_table_for(lens, P, seed=5)
+    ptt = torch.tensor(pt, device="cuda")
+    kp, vp = to_paged(k, lens, P, pt, npages, fill=0.0), to_paged(v, lens, P, pt, npages, fill=0.0)
+    kp2, vp2 = kp.clone(), vp.clone()
+    packed = torch.randn((B, Hq + 2 * Hkv, D), device="cuda").to(torch.bfloat16)
+    qv, kv_, vv = packed[:, :Hq], packed[:, Hq:Hq + Hkv], packed[:, Hq + Hkv:]
+    pos = torch.tensor([l - 1 for l in lens], dtype=torch.int32, device="cuda")
+    dec.kv_append(kv_, vv, kp, vp, pos, ptt)
+    dec.kv_append(kv_.contiguous(), vv.contiguous(), kp2, vp2, pos, ptt)
+    assert torch.equal(kp, kp2) and torch.equal(vp, vp2)
+    a = dec.decode(qv, kp, vp, _lens_t(lens), page_table=ptt, max_len=max(lens))
+    b = dec.decode(qv.contiguous(), kp, vp, _lens_t(lens), page_table=ptt, max_len=max(lens))
+    assert torch.equal(a, b)

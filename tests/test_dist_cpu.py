@@ -69,21 +69,21 @@ def _worker(rank, port, result_dir):
     def append(layer, m, k, v):
         rows = range(m * geo.B_mb, (m + 1) * geo.B_mb)
         for i, r in enumerate(rows):
-            store_k[layer, r, :, pos[r]] = k[i].numpy()
-            store_v[layer, r, :, pos[r]] = v[i].numpy()
+            store_k[layer, r, :, pos[r]] = k[i].contiguous().numpy()
+            store_v[layer, r, :, pos[r]] = v[i].contiguous().numpy()
 
     def attend(layer, m, qr, out):
         sl = slice(m * geo.B_mb, (m + 1) * geo.B_mb)
-        res = O.decode_dense(qr.numpy(), store_k[layer, sl], store_v[layer, sl], pos[sl] + 1,
+        res = O.decode_dense(qr.contiguous().numpy(), store_k[layer, sl], store_v[layer, sl], pos[sl] + 1,
                              1 / np.sqrt(D))
         out.copy_(torch.from_numpy(res))
 
     eng = HeadShardedAttention(geo, dist, append, attend, torch.device("cpu"), torch.float32)
     mine = slice(rank * B_LOCAL, (rank + 1) * B_LOCAL)
-    q_in, k_in, v_in = shard_inputs(torch.from_numpy(q[:, mine]), torch.from_numpy(kn[:, mine]),
-                                    torch.from_numpy(vn[:, mine]), WORLD, MB)
+    qkv_in = shard_inputs(torch.from_numpy(q[:, mine]), torch.from_numpy(kn[:, mine]),
+                          torch.from_numpy(vn[:, mine]), WORLD, MB)
     out = torch.zeros(geo.q_shape())
-    eng.step(q_in, k_in, v_in, out)
+    eng.step(qkv_in, out)
     np.save(Path(result_dir) / f"out{rank}.npy", stitch_outputs(out).numpy())
     dist.barrier()
     dist.destroy_process_group()
