@@ -196,6 +196,20 @@ int lam_decode_step_host(lam_ctx* ctx, const lam_decode_args* args, const void* 
                          const void* h_k_new, const void* h_v_new, void* h_out, void* d_k_new,
                          void* d_v_new, const int32_t* d_positions, void* stream);
 
+/* One decode step over n_layers layers from host buffers — the attention worker's end-to-end
+ * step.  Layer l's q / k_new / v_new are copied H2D on `copy_stream` into one of two device
+ * staging sets while layer l-1 appends + decodes on `stream`, and each layer's output returns
+ * D2H on `copy_stream` as soon as it is ready, so the host copies hide under the HBM-bound
+ * attention.  layer_args[l] describes layer l's pools (its q/out fields are ignored: the staging
+ * set is used).  d_stage must hold 2 * (q + k_new + v_new + out) bytes of one layer, each part
+ * 256-byte aligned (lam_decode_layers_host_stage_bytes).  Returns after enqueueing; the caller
+ * synchronises `stream`. */
+int lam_decode_layers_host(lam_ctx* ctx, const lam_decode_args* layer_args, int32_t n_layers,
+                           const void* const* h_q, const void* const* h_k_new,
+                           const void* const* h_v_new, void* const* h_out, void* d_stage,
+                           const int32_t* d_positions, void* stream, void* copy_stream);
+int64_t lam_decode_layers_host_stage_bytes(const lam_decode_args* layer_args);
+
 #ifdef __cplusplus
 }
 #endif

@@ -87,6 +87,9 @@ SIGNATURES = {
     "lam_kv_gather": (C.c_int, [_I32, _I32, _I32, _I32, _I32, _I32, _P, _P, _I32, _P, _P, _P]),
     "lam_decode_step_host": (C.c_int, [_P, C.POINTER(DecodeArgs), _P, _P, _P, _P, _P, _P, _P,
                                        _P]),
+    "lam_decode_layers_host": (C.c_int, [_P, C.POINTER(DecodeArgs), _I32, _P, _P, _P, _P, _P, _P,
+                                         _P, _P]),
+    "lam_decode_layers_host_stage_bytes": (C.c_int64, [C.POINTER(DecodeArgs)]),
 }
 
 _lib = None

@@ -780,4 +780,95 @@ int lam_decode_step_host(lam_ctx* ctx, const lam_decode_args* a, const void* h_q
   return LAM_OK;
 }
 
+namespace {
+struct StageLayout {
+  int64_t q, kv, out, set;  // bytes of each part (256-aligned) and of one staging set
+};
+StageLayout stage_layout(const lam_decode_args* a) {
+  auto al = [](int64_t x) { return (x + 255) / 256 * 256; };
+  const int64_t e = elem_bytes(a->kv_dtype), eo = elem_bytes(a->out_dtype);
+  StageLayout s;
+  s.q = al(static_cast<int64_t>(a->batch) * a->num_q_heads * a->head_dim * e);
+  s.kv = al(static_cast<int64_t>(a->batch) * a->num_kv_heads * a->head_dim * e);
+  s.out = al(static_cast<int64_t>(a->batch) * a->num_q_heads * a->head_dim * eo);
+  s.set = s.q + 2 * s.kv + s.out;
+  return s;
+}
+}  // namespace
+
+int64_t lam_decode_layers_host_stage_bytes(const lam_decode_args* a) {
+  return a ? 2 * stage_layout(a).set : 0;
+}
+
+int lam_decode_layers_host(lam_ctx* ctx, const lam_decode_args* layer_args, int32_t n_layers,
+                           const void* const* h_q, const void* const* h_k_new,
+                           const void* const* h_v_new, void* const* h_out, void* d_stage,
+                           const int32_t* d_positions, void* stream, void* copy_stream) {
+  if (!ctx || !layer_args || n_layers < 0) return fail(LAM_ERR_VALIDATION, "bad arguments");
+  if (n_layers == 0) return LAM_OK;
+  LAM_CUDA(cudaSetDevice(ctx->device));
+  auto cs = static_cast<cudaStream_t>(stream);
+  auto xs = static_cast<cudaStream_t>(copy_stream);
+  const StageLayout L = stage_layout(&layer_args[0]);
+  auto base = [&](int set) { return static_cast<uint8_t*>(d_stage) + set * L.set; };
+  // in_ready[s]: H2D of staging set s landed; consumed[s]: compute done reading set s inputs;
+  // out_ready[s]: output of set s written; out_free[s]: D2H of set s finished.
+  cudaEvent_t in_ready[2], consumed[2], out_ready[2], out_free[2];
+  for (int s = 0; s < 2; ++s) {
+    LAM_CUDA(cudaEventCreateWithFlags(&in_ready[s], cudaEventDisableTiming));
+    LAM_CUDA(cudaEventCreateWithFlags(&consumed[s], cudaEventDisableTiming));
+    LAM_CUDA(cudaEventCreateWithFlags(&out_ready[s], cudaEventDisableTiming));
+    LAM_CUDA(cudaEventCreateWithFlags(&out_free[s], cudaEventDisableTiming));
+  }
+  auto h2d = [&](int l) -> int {
+    const int s = l & 1;
+    if (l >= 2) LAM_CUDA(cudaStreamWaitEvent(xs, consumed[s], 0));
+    uint8_t* b = base(s);
+    const int64_t qb = static_cast<int64_t>(layer_args[l].batch) * layer_args[l].num_q_heads *
+                       layer_args[l].head_dim * elem_bytes(layer_args[l].kv_dtype);
+    const int64_t kb = static_cast<int64_t>(layer_args[l].batch) * layer_args[l].num_kv_heads *
+                       layer_args[l].head_dim * elem_bytes(layer_args[l].kv_dtype);
+    LAM_CUDA(cudaMemcpyAsync(b, h_q[l], qb, cudaMemcpyHostToDevice, xs));
+    LAM_CUDA(cudaMemcpyAsync(b + L.q, h_k_new[l], kb, cudaMemcpyHostToDevice, xs));
+    LAM_CUDA(cudaMemcpyAsync(b + L.q + L.kv, h_v_new[l], kb, cudaMemcpyHostToDevice, xs));
+    LAM_CUDA(cudaEventRecord(in_ready[s], xs));
+    return LAM_OK;
+  };
+  int rc = LAM_OK;
+  LAM_CUDA(cudaEventRecord(consumed[0], cs));  // copy stream starts after prior compute work
+  LAM_CUDA(cudaStreamWaitEvent(xs, consumed[0], 0));
+  if ((rc = h2d(0)) != LAM_OK) return rc;
+  for (int l = 0; l < n_layers; ++l) {
+    const int s = l & 1;
+    if (l + 1 < n_layers && (rc = h2d(l + 1)) != LAM_OK) return rc;
+    uint8_t* b = base(s);
+    lam_decode_args a = layer_args[l];
+    a.q = b;
+    a.out = b + L.q + 2 * L.kv;
+    LAM_CUDA(cudaStreamWaitEvent(cs, in_ready[s], 0));
+    if (l >= 2) LAM_CUDA(cudaStreamWaitEvent(cs, out_free[s], 0));
+    rc = lam_kv_append(a.kv_dtype, a.batch, a.num_kv_heads, a.head_dim, a.page_size, a.pt_stride,
+                       a.page_table, d_positions, b + L.q, b + L.q + L.kv, 0,
+                       const_cast<void*>(a.k_pool), const_cast<void*>(a.v_pool), stream);
+    if (rc != LAM_OK) return rc;
+    if ((rc = lam_decode(ctx, &a, stream)) != LAM_OK) return rc;
+    LAM_CUDA(cudaEventRecord(consumed[s], cs));
+    LAM_CUDA(cudaEventRecord(out_ready[s], cs));
+    LAM_CUDA(cudaStreamWaitEvent(xs, out_ready[s], 0));
+    const int64_t ob = static_cast<int64_t>(a.batch) * a.num_q_heads * a.head_dim *
+                       elem_bytes(a.out_dtype);
+    LAM_CUDA(cudaMemcpyAsync(h_out[l], a.out, ob, cudaMemcpyDeviceToHost, xs));
+    LAM_CUDA(cudaEventRecord(out_free[s], xs));
+  }
+  LAM_CUDA(cudaEventRecord(out_free[0], xs));
+  LAM_CUDA(cudaStreamWaitEvent(cs, out_free[0], 0));  // `stream` completes after the last D2H
+  for (int s = 0; s < 2; ++s) {
+    cudaEventDestroy(in_ready[s]);
+    cudaEventDestroy(consumed[s]);
+    cudaEventDestroy(out_ready[s]);
+    cudaEventDestroy(out_free[s]);
+  }
+  return LAM_OK;
+}
+
 }  // extern "C"

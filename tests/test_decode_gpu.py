@@ -250,3 +250,49 @@ def test_packed_qkv_strides(built, G):
     a = dec.decode(qv, kp, vp, _lens_t(lens), page_table=ptt, max_len=max(lens))
     b = dec.decode(qv.contiguous(), kp, vp, _lens_t(lens), page_table=ptt, max_len=max(lens))
     assert torch.equal(a, b)
+
+
+def test_decode_layers_host_matches_device_path(built):
+    """lam_decode_layers_host (host buffers, overlapped copies) == append + decode per layer."""
+    import ctypes as C
+
+    from paper_2405_01814_b200 import _lib
+    from paper_2405_01814_b200 import decode as dec
+
+    L, B, Hq, Hkv, D, P = 3, 4, 16, 2, 128, 64
+    lens = [130, 64, 300, 1]
+    pt, npages = page_table_for(lens, P, seed=2)
+    ptt = torch.tensor(pt, device="cuda")
+    lens_t = _lens_t(lens)
+    pos = (lens_t - 1).contiguous()
+    g = torch.Generator(device="cuda").manual_seed(4)
+    pools = [[torch.empty((npages, Hkv, P, D), device="cuda").uniform_(-1, 1, generator=g)
+              .to(torch.bfloat16) for _ in range(2)] for _ in range(L)]
+    ref_pools = [[t.clone() for t in pl] for pl in pools]
+    hq = torch.empty((L, B, Hq, D)).uniform_(-1, 1).to(torch.bfloat16).pin_memory()
+    hk = torch.empty((L, B, Hkv, D)).uniform_(-1, 1).to(torch.bfloat16).pin_memory()
+    hv = torch.empty((L, B, Hkv, D)).uniform_(-1, 1).to(torch.bfloat16).pin_memory()
+    ho = torch.zeros((L, B, Hq, D), dtype=torch.bfloat16).pin_memory()
+    dq = torch.empty((B, Hq, D), dtype=torch.bfloat16, device="cuda")
+    arr = (dec.DecodeArgs * L)()
+    for l in range(L):
+        a, _ = dec.make_args(dq, pools[l][0], pools[l][1], lens_t, page_table=ptt, max_len=max(lens),
+                             out=torch.empty_like(dq))
+        arr[l] = a
+    lib = _lib.load()
+    stage = torch.empty(int(lib.lam_decode_layers_host_stage_bytes(arr)), dtype=torch.uint8,
+                        device="cuda")
+    Pt = C.c_void_p * L
+    s, xs = torch.cuda.current_stream(), torch.cuda.Stream()
+    _lib.check(lib.lam_decode_layers_host(
+        _lib.context(0).handle, arr, L, Pt(*[hq[l].data_ptr() for l in range(L)]),
+        Pt(*[hk[l].data_ptr() for l in range(L)]), Pt(*[hv[l].data_ptr() for l in range(L)]),
+        Pt(*[ho[l].data_ptr() for l in range(L)]), stage.data_ptr(), pos.data_ptr(),
+        s.cuda_stream, xs.cuda_stream))
+    torch.cuda.synchronize()
+    for l in range(L):
+        kp, vp = ref_pools[l]
+        dec.kv_append(hk[l].cuda(), hv[l].cuda(), kp, vp, pos, ptt)
+        want = dec.decode(hq[l].cuda(), kp, vp, lens_t, page_table=ptt, max_len=max(lens))
+        assert torch.equal(ho[l], want.cpu()), l
+        assert torch.equal(pools[l][0], kp) and torch.equal(pools[l][1], vp)
