@@ -153,7 +153,7 @@ def cpu_baseline(w: dict, target_s: float, seed: int = 1) -> dict:
                                  1.0 / math.sqrt(D), units)
         lib.ref_bench_run(h, threads, None)  # warm
         runs, secs = 0, 0.0
-        while secs < target_s:
+        while runs == 0 or secs < target_s:
             secs += lib.ref_bench_run(h, threads, None)
             runs += 1
         lib.ref_bench_destroy(h)
@@ -161,7 +161,7 @@ def cpu_baseline(w: dict, target_s: float, seed: int = 1) -> dict:
     else:
         threads = 1
         runs, secs = 0, 0.0
-        while secs < target_s:
+        while runs == 0 or secs < target_s:
             t0 = time.perf_counter()
             O.decode_dense(q, k, v, lens, 1.0 / math.sqrt(D))
             secs += time.perf_counter() - t0
