@@ -111,6 +111,17 @@ class ClockSampler:
                 "reasons": sorted(reasons)}
 
 
+def ncu_traffic(workload: str, world: int):
+    """DRAM bytes per decode launch from the committed ncu capture of this workload's kernel
+    (profiles/ncu_traffic.json), or None when no capture of this launch shape exists."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    try:
+        d = json.loads(p.read_text()).get(workload)
+    except Exception:
+        return None
+    return d["traffic"] if d and world == 1 else None
+
+
 def measured_peaks() -> dict:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -466,7 +477,7 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
                      "frac": achieved / peak,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650",
                      "kernel": f"decode_{W.kernel}", "bytes_per_launch": W.decode_bytes_per_launch,
-                     "avg_launch_ms": kern_avg, "traffic": None},
+                     "avg_launch_ms": kern_avg, "traffic": ncu_traffic(args.workload, world)},
         "gpu_launches": launches,
         "clocks": clocks,
     }

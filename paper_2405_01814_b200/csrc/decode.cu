@@ -72,7 +72,7 @@ int mma_occ_v() {
 }
 
 // GQA kernel variants (consumer warps, stages): tile = 16 tokens per consumer warp.
-#define LAM_MMA_VARIANTS(X) X(0, 4, 6) X(1, 4, 3) X(2, 8, 3) X(3, 2, 6) X(4, 2, 4)
+#define LAM_MMA_VARIANTS(X) X(0, 4, 6) X(1, 4, 3) X(2, 8, 2) X(3, 2, 6) X(4, 2, 4) X(5, 4, 2) X(6, 2, 3)
 
 template <typename T>
 cudaError_t mma_launch(int variant, const DecodeParams& p, const CUtensorMap& kmap,
