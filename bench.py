@@ -192,7 +192,8 @@ def cpu_baseline(w: dict, target_s: float, seed: int = 1) -> dict:
             "sample": (f"{units} (request, kv head) units x {G} q heads x l={l}, d={D} of one "
                        f"layer, exact_attention<float> on fp32 upcasts, {runs} runs, "
                        f"{threads} threads; bytes = attn_cost with e={e}"),
-            "cpu_model": cpu_model, "tokens_per_s_equiv": gbs * 1e9 / PF.kv_bytes_per_token(spec)}
+            "cpu_model": cpu_model,
+            "attn_tokens_per_s_equiv": gbs * 1e9 / (PF.kv_bytes_per_token(spec) * l)}
 
 
 def run_reference(args, w: dict, rank: int, world: int) -> None:
@@ -218,7 +219,7 @@ def run_reference(args, w: dict, rank: int, world: int) -> None:
             "config": {"workload": f"{args.workload}: {w['desc']}", "global_batch": w["B"],
                        "seq_len": w["l"], "layers": w["layers"],
                        "parallelism": "host threads"},
-            "attn_tokens_per_s": value * 1e9 / PF.kv_bytes_per_token(spec),
+            "attn_tokens_per_s": value * 1e9 / (PF.kv_bytes_per_token(spec) * w["l"]),
             "cpu_baseline": {"value": value, "unit": "GB/s", "cores": r["cores"],
                              "kind": r["kind"], "sample": r["sample"], "cpu_model": r["cpu_model"]},
             "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0,
