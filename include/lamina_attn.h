@@ -164,6 +164,14 @@ typedef struct lam_decode_args {
   /* elements between consecutive requests' q blocks; 0 = num_q_heads * head_dim.  A packed QKV
    * projection output [B][Hq + 2 Hkv][D] is decoded in place with (Hq + 2 Hkv) * head_dim. */
   int64_t q_batch_stride;
+  /* Fused append (optional, both or neither): k_new/v_new hold each request's new token,
+   * request b / kv head h at + b * new_batch_stride + h * head_dim (0 = Hkv * head_dim).  The
+   * token is position seq_lens[b] - 1: the kernel attends over it from these buffers and writes
+   * it into k_pool/v_pool (which must then be writable) — lam_kv_append + lam_decode in one
+   * launch. */
+  const void* k_new;
+  const void* v_new;
+  int64_t new_batch_stride;
 } lam_decode_args;
 
 int lam_decode(lam_ctx* ctx, const lam_decode_args* args, void* stream);

@@ -55,6 +55,9 @@ class DecodeArgs(C.Structure):
         ("out", C.c_void_p),
         ("lse", C.c_void_p),
         ("q_batch_stride", C.c_int64),
+        ("k_new", C.c_void_p),
+        ("v_new", C.c_void_p),
+        ("new_batch_stride", C.c_int64),
     ]
 
 

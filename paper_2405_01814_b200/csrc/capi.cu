@@ -690,6 +690,15 @@ int lam_decode(lam_ctx* ctx, const lam_decode_args* a, void* stream) {
   p.QG = pl.QG;
   p.n_items = static_cast<int32_t>(static_cast<int64_t>(a->batch) * a->num_kv_heads * pl.QG * pl.S);
   p.work = ctx->work;
+  if (a->k_new != nullptr) {  // fused append
+    if (a->v_new == nullptr) return fail(LAM_ERR_VALIDATION, "fused append needs both k_new and v_new");
+    p.k_new = a->k_new;
+    p.v_new = a->v_new;
+    p.new_stride = a->new_batch_stride > 0 ? a->new_batch_stride
+                                           : static_cast<int64_t>(a->num_kv_heads) * D;
+    p.k_pool_w = const_cast<void*>(a->k_pool);
+    p.v_pool_w = const_cast<void*>(a->v_pool);
+  }
   p.flags = env_int("LAM_DECODE_FLAGS", 0);
   p.scale = a->scale;
   p.scale_log2 = a->scale * 1.4426950408889634f;

@@ -46,6 +46,14 @@ struct DecodeParams {
   float scale_log2;         // scale * log2(e)
   int32_t out_f32;
   int32_t flags;            // reserved (tuning experiments)
+  // fused append (optional): the new token of request b (position seq_lens[b] - 1) comes from
+  // k_new/v_new (request b, kv head h at + b * new_stride + h * D); the kernel attends over it
+  // from shared memory and writes it into the pools for later steps.
+  const void* k_new;
+  const void* v_new;
+  int64_t new_stride;
+  void* k_pool_w;
+  void* v_pool_w;
 };
 
 // Physical row of token t of (request b, kv head h) in a pool viewed as [rows][D].
@@ -97,6 +105,12 @@ __device__ __forceinline__ Item item_from_tag(const DecodeParams& p, int4 tag) {
   return it;
 }
 
+// Does tile j of this item hold the request's new token (fused append)?
+template <int TILE>
+__device__ __forceinline__ bool tile_has_new(const DecodeParams& p, const Item& it, int j) {
+  return p.k_new != nullptr && it.t_end == it.len && it.len > 0 && j == it.ntiles - 1;
+}
+
 // Splits of a (request, kv head, q group) unit that carry tokens (>= 1: an empty request
 // still produces its zero output through split 0).
 __device__ __forceinline__ int live_splits(const DecodeParams& p, int len) {
@@ -105,6 +119,7 @@ __device__ __forceinline__ int live_splits(const DecodeParams& p, int len) {
 
 // ---- persistent producer ---------------------------------------------------------------
 // meta[s] = {item, tile index, request length, item end token}; item < 0 ends the work.
+// meta_row[s] = first pool row of the stage's tile (consumers write the fused new token there).
 // `issue(s, it, j, row)` must arrive on full[s] with expect_tx and start the stage's TMA
 // copies of tile j, whose first KV row is `row`.
 //
@@ -114,7 +129,8 @@ __device__ __forceinline__ int live_splits(const DecodeParams& p, int len) {
 // to one item of tail imbalance); the stage ring covers the claim's round trips.
 template <int STAGES, int TILE, class Issue>
 __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* full,
-                                              uint64_t* empty, int4* meta, Issue issue) {
+                                              uint64_t* empty, int4* meta, long long* meta_row,
+                                              Issue issue) {
   int i = 0;
   auto acquire = [&](int k) {
     const int s = k % STAGES;
@@ -135,8 +151,10 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
     }
     for (int j = 0; j < it.ntiles; ++j) {
       const int s = acquire(i++);
+      const int64_t row = kv_row(p, it.b, it.kvh, it.t_begin + j * TILE);
       meta[s] = make_int4(idx, j, it.len, it.t_end);
-      issue(s, it, j, kv_row(p, it.b, it.kvh, it.t_begin + j * TILE));
+      meta_row[s] = row;
+      issue(s, it, j, row);
     }
   }
   const int s = acquire(i);

@@ -30,9 +30,12 @@ struct MmaCfg {
   static constexpr int STAGE_BYTES = 2 * MAT_BYTES;  // K + V
   static constexpr int RING_BYTES = STAGES * STAGE_BYTES;
   static constexpr int Q_BYTES = GQ * D * 2;        // one item's (padded) q rows
+  static constexpr int ROW_BYTES = D * 2;
+  static constexpr int SLOT_BYTES = Q_BYTES + 2 * ROW_BYTES;  // q rows + fused new k, v rows
   static constexpr int RED_FLOATS = NW * GQ * (D + 2);
-  static constexpr int SMEM_BYTES = RING_BYTES + STAGES * Q_BYTES + RED_FLOATS * 4 + STAGES * 16 +
-                                    (2 * STAGES + 4) * 8 + 16 + 64 + 1024;  // +align slack
+  static constexpr int SMEM_BYTES = RING_BYTES + STAGES * SLOT_BYTES + RED_FLOATS * 4 +
+                                    STAGES * 16 + STAGES * 8 + (2 * STAGES + 4) * 8 + 16 + 64 +
+                                    1024;  // +align slack
   static constexpr int THREADS = (NW + 2) * 32;  // + producer warp + epilogue warp
 };
 
@@ -52,12 +55,13 @@ __global__ void __launch_bounds__((NW_ + 2) * 32)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint8_t* qslot = smem + C::RING_BYTES;  // [STAGES][8][D]
-  float* red_m = reinterpret_cast<float*>(qslot + STAGES * C::Q_BYTES);
+  uint8_t* qslot = smem + C::RING_BYTES;  // [STAGES][q rows 8 | new k | new v][D]
+  float* red_m = reinterpret_cast<float*>(qslot + STAGES * C::SLOT_BYTES);
   float* red_l = red_m + NW * GQ;
   float* red_acc = red_l + NW * GQ;
   int4* meta = reinterpret_cast<int4*>(red_m + C::RED_FLOATS);
-  uint64_t* full = reinterpret_cast<uint64_t*>(meta + STAGES);
+  long long* meta_row = reinterpret_cast<long long*>(meta + STAGES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(meta_row + STAGES);
   uint64_t* empty = full + STAGES;
   RedPipe red{empty + STAGES, empty + STAGES + 1, reinterpret_cast<int*>(empty + STAGES + 2)};
 
@@ -82,12 +86,22 @@ __global__ void __launch_bounds__((NW_ + 2) * 32)
   if (warp == NW) {
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      producer_loop<STAGES, TILE>(p, full, empty, meta, [&](int s, const Item& it, int j, int64_t row) {
+      producer_loop<STAGES, TILE>(p, full, empty, meta, meta_row,
+                                  [&](int s, const Item& it, int j, int64_t row) {
         uint8_t* st = smem + s * C::STAGE_BYTES;
         const uint32_t qb = static_cast<uint32_t>(G) * D * 2;
-        mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES + (j == 0 ? qb : 0));
+        const bool fused = tile_has_new<TILE>(p, it, j);
+        mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES + (j == 0 ? qb : 0) +
+                                            (fused ? 2 * C::ROW_BYTES : 0));
+        if (fused) {
+          const int64_t off = static_cast<int64_t>(it.b) * p.new_stride + static_cast<int64_t>(it.kvh) * D;
+          uint8_t* kn = qslot + s * C::SLOT_BYTES + C::Q_BYTES;
+          tma_load_1d(kn, static_cast<const T*>(p.k_new) + off, C::ROW_BYTES, &full[s], pol);
+          tma_load_1d(kn + C::ROW_BYTES, static_cast<const T*>(p.v_new) + off, C::ROW_BYTES,
+                      &full[s], pol);
+        }
         if (j == 0)
-          tma_load_1d(qslot + s * C::Q_BYTES,
+          tma_load_1d(qslot + s * C::SLOT_BYTES,
                       static_cast<const T*>(p.q) + static_cast<int64_t>(it.b) * p.q_stride +
                           static_cast<int64_t>(it.kvh) * G * D,
                       qb, &full[s], pol);
@@ -135,7 +149,7 @@ __global__ void __launch_bounds__((NW_ + 2) * 32)
     }
     if (mt.y == 0) {  // first tile of a new item: its q rows arrived with this stage
       it = item_from_tag<TILE>(p, mt);
-      const uint32_t qrow = q_addr + s * C::Q_BYTES + gr * D * 2;
+      const uint32_t qrow = q_addr + s * C::SLOT_BYTES + gr * D * 2;
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
         uint32_t v0 = 0u, v1 = 0u;
@@ -157,7 +171,23 @@ __global__ void __launch_bounds__((NW_ + 2) * 32)
     const int nval = it.ntiles > 0 ? min(16, it.t_end - tok0) : 0;
     const uint32_t kb = base + s * C::STAGE_BYTES;
     const uint32_t vb = kb + C::MAT_BYTES;
+    // fused append: the warp holding the new token copies it from the slot into its K/V tile
+    // rows (swizzled) and into the pools for later steps
+    const int new_r = tile_has_new<TILE>(p, it, mt.y) ? it.len - 1 - (it.t_begin + mt.y * TILE)
+                                                      : -1;
+    const bool my_new = new_r >= warp * 16 && new_r < warp * 16 + 16;
     if (nval > 0) {
+      if (my_new) {
+        const uint8_t* kn = qslot + s * C::SLOT_BYTES + C::Q_BYTES;
+        const int c = lane & 15;
+        const int is_v = lane >> 4;
+        const uint4 val = *reinterpret_cast<const uint4*>(kn + is_v * C::ROW_BYTES + c * 16);
+        *reinterpret_cast<uint4*>(smem + s * C::STAGE_BYTES + is_v * C::MAT_BYTES +
+                                  swz<C::BOX_BYTES>(new_r, c)) = val;
+        T* pool = static_cast<T*>(is_v ? p.v_pool_w : p.k_pool_w);
+        *reinterpret_cast<uint4*>(pool + (meta_row[s] + new_r) * D + c * 8) = val;
+        __syncwarp();
+      }
       if (nval < 16) {
         // rows past the sequence end hold stale data: zero this warp's V rows so that
         // p = 0 never meets a non-finite value in the P·V product.
@@ -216,7 +246,7 @@ __global__ void __launch_bounds__((NW_ + 2) * 32)
         ldmatrix_x4_trans(vb + swz<C::BOX_BYTES>(warp * 16 + v_row, t * 2 + v_chk), a0, a1, a2, a3);
         Mma16816<T>::run(o[t], a0, a1, a2, a3, b0, b1);
       }
-      if (nval < 16) fence_proxy_async_smem();  // generic zero-stores before the next TMA
+      if (nval < 16 || my_new) fence_proxy_async_smem();  // generic stores before the next TMA
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);

@@ -36,9 +36,11 @@ struct SimtCfg {
   static constexpr int TILE_BYTES = TILE * D * sizeof(T);
   static constexpr int RING_BYTES = STAGES * 2 * TILE_BYTES;
   static constexpr int Q_BYTES = GQ * D * sizeof(T);  // one item's q rows
+  static constexpr int ROW_BYTES = D * sizeof(T);
+  static constexpr int SLOT_BYTES = Q_BYTES + 2 * ROW_BYTES;  // q rows + fused new k, v rows
   static constexpr int RED_FLOATS = NW * GQ * (D + 2);
-  static constexpr int SMEM_BYTES = RING_BYTES + STAGES * Q_BYTES + RED_FLOATS * 4 + STAGES * 16 +
-                                    (2 * STAGES + 4) * 8 + 16 + 64;
+  static constexpr int SMEM_BYTES = RING_BYTES + STAGES * SLOT_BYTES + RED_FLOATS * 4 +
+                                    STAGES * 16 + STAGES * 8 + (2 * STAGES + 4) * 8 + 16 + 64;
   static constexpr int THREADS = (NW + 2) * 32;  // + producer warp + epilogue warp
   static constexpr bool kLog2 = sizeof(T) < 4;
   static_assert(LPR >= 1 && LPR <= 32 && 32 % LPR == 0, "row must map onto a warp");
@@ -52,12 +54,13 @@ __global__ void __launch_bounds__((NW + 2) * 32)
   constexpr int VEC = C::VEC, LPR = C::LPR, RPI = C::RPI, TPW = C::TPW, ITER = C::ITER;
   extern __shared__ __align__(128) uint8_t smem[];
   T* ring = reinterpret_cast<T*>(smem);  // [STAGES][2][TILE][D]
-  uint8_t* qslot = smem + C::RING_BYTES;  // [STAGES][GQ][D]
-  float* red_m = reinterpret_cast<float*>(qslot + STAGES * C::Q_BYTES);
+  uint8_t* qslot = smem + C::RING_BYTES;  // [STAGES][q rows GQ | new k | new v][D]
+  float* red_m = reinterpret_cast<float*>(qslot + STAGES * C::SLOT_BYTES);
   float* red_l = red_m + NW * GQ;
   float* red_acc = red_l + NW * GQ;
   int4* meta = reinterpret_cast<int4*>(red_m + C::RED_FLOATS);
-  uint64_t* full = reinterpret_cast<uint64_t*>(meta + STAGES);
+  long long* meta_row = reinterpret_cast<long long*>(meta + STAGES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(meta_row + STAGES);
   uint64_t* empty = full + STAGES;
   RedPipe red{empty + STAGES, empty + STAGES + 1, reinterpret_cast<int*>(empty + STAGES + 2)};
 
@@ -79,16 +82,27 @@ __global__ void __launch_bounds__((NW + 2) * 32)
       const uint64_t pol = policy_evict_first();
       const T* kp = static_cast<const T*>(p.k_pool);
       const T* vp = static_cast<const T*>(p.v_pool);
-      producer_loop<STAGES, TILE>(p, full, empty, meta, [&](int s, const Item& it, int j, int64_t row) {
+      producer_loop<STAGES, TILE>(p, full, empty, meta, meta_row,
+                                  [&](int s, const Item& it, int j, int64_t row) {
         const int tok = it.t_begin + j * TILE;
         const int rows = min(TILE, it.t_end - tok);
         const uint32_t bytes = static_cast<uint32_t>(rows) * D * sizeof(T);
         T* ks = ring + static_cast<size_t>(s) * 2 * TILE * D;
-        mbar_arrive_expect_tx(&full[s], 2 * bytes + (j == 0 ? C::Q_BYTES : 0));
+        const bool fused = tile_has_new<TILE>(p, it, j);
+        mbar_arrive_expect_tx(&full[s], 2 * bytes + (j == 0 ? C::Q_BYTES : 0) +
+                                            (fused ? 2 * C::ROW_BYTES : 0));
+        uint8_t* slot = qslot + s * C::SLOT_BYTES;
         if (j == 0) {
           const T* qsrc = static_cast<const T*>(p.q) + static_cast<int64_t>(it.b) * p.q_stride +
                           static_cast<int64_t>(it.kvh * p.G + it.qg * GQ) * D;
-          tma_load_1d(qslot + s * C::Q_BYTES, qsrc, C::Q_BYTES, &full[s], pol);
+          tma_load_1d(slot, qsrc, C::Q_BYTES, &full[s], pol);
+        }
+        if (fused) {
+          const int64_t off = static_cast<int64_t>(it.b) * p.new_stride + static_cast<int64_t>(it.kvh) * D;
+          tma_load_1d(slot + C::Q_BYTES, static_cast<const T*>(p.k_new) + off, C::ROW_BYTES,
+                      &full[s], pol);
+          tma_load_1d(slot + C::Q_BYTES + C::ROW_BYTES, static_cast<const T*>(p.v_new) + off,
+                      C::ROW_BYTES, &full[s], pol);
         }
         tma_load_1d(ks, kp + row * D, bytes, &full[s], pol);
         tma_load_1d(ks + TILE * D, vp + row * D, bytes, &full[s], pol);
@@ -126,7 +140,7 @@ __global__ void __launch_bounds__((NW + 2) * 32)
 #pragma unroll
       for (int g = 0; g < GQ; ++g) {
         if (it.ntiles > 0)
-          Elem<T>::unpack(lds128(q_addr + s * C::Q_BYTES + (g * D + sub * VEC) * sizeof(T)), q[g]);
+          Elem<T>::unpack(lds128(q_addr + s * C::SLOT_BYTES + (g * D + sub * VEC) * sizeof(T)), q[g]);
         m[g] = -INFINITY;
         l[g] = 0.f;
 #pragma unroll
@@ -137,6 +151,9 @@ __global__ void __launch_bounds__((NW + 2) * 32)
       const int tile_tok = it.t_begin + mt.y * TILE;
       const uint32_t k_addr = ring_addr + s * 2 * C::TILE_BYTES;
       const uint32_t v_addr = k_addr + C::TILE_BYTES;
+      // fused append: the request's new token is read from the slot, not from the pool
+      const int new_r = tile_has_new<TILE>(p, it, mt.y) ? it.len - 1 - tile_tok : -1;
+      const uint32_t kn_addr = q_addr + s * C::SLOT_BYTES + C::Q_BYTES + sub * VEC * sizeof(T);
 
       // q·k for this warp's TPW tokens.
       float logit[ITER][GQ];
@@ -146,7 +163,14 @@ __global__ void __launch_bounds__((NW + 2) * 32)
         const int r = warp * TPW + r8 * RPI + rg;  // row within the tile
         valid[r8] = tile_tok + r < it.t_end;
         float kf[VEC];
-        Elem<T>::unpack(lds128(k_addr + (r * D + sub * VEC) * sizeof(T)), kf);
+        const uint4 kraw = lds128(r == new_r ? kn_addr : k_addr + (r * D + sub * VEC) * sizeof(T));
+        if (r == new_r) {  // write the new token into the pool for later steps
+          const uint4 vraw = lds128(kn_addr + C::ROW_BYTES);
+          const int64_t dst = (meta_row[s] + r) * D + sub * VEC;
+          *reinterpret_cast<uint4*>(static_cast<T*>(p.k_pool_w) + dst) = kraw;
+          *reinterpret_cast<uint4*>(static_cast<T*>(p.v_pool_w) + dst) = vraw;
+        }
+        Elem<T>::unpack(kraw, kf);
 #pragma unroll
         for (int g = 0; g < GQ; ++g) {
           float d0 = 0.f;
@@ -193,7 +217,8 @@ __global__ void __launch_bounds__((NW + 2) * 32)
         if (!valid[r8]) continue;
         const int r = warp * TPW + r8 * RPI + rg;
         float vf[VEC];
-        Elem<T>::unpack(lds128(v_addr + (r * D + sub * VEC) * sizeof(T)), vf);
+        Elem<T>::unpack(lds128(r == new_r ? kn_addr + C::ROW_BYTES
+                                          : v_addr + (r * D + sub * VEC) * sizeof(T)), vf);
 #pragma unroll
         for (int g = 0; g < GQ; ++g) {
           const float pr = C::kLog2 ? exp2f(logit[r8][g] - m[g]) : expf(logit[r8][g] - m[g]);

@@ -39,8 +39,11 @@ def make_args(q: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor,
               max_len: int | None = None, scale: float | None = None,
               out: torch.Tensor | None = None, out_dtype: torch.dtype | None = None,
               lse: torch.Tensor | None = None, kernel: str = "auto",
-              split_tokens: int = 0) -> tuple[DecodeArgs, torch.Tensor]:
-    """Fill lam_decode_args from tensors; returns (args, out)."""
+              split_tokens: int = 0, k_new: torch.Tensor | None = None,
+              v_new: torch.Tensor | None = None) -> tuple[DecodeArgs, torch.Tensor]:
+    """Fill lam_decode_args from tensors; returns (args, out).  With k_new/v_new ([B, Hkv, D],
+    a shared batch stride allowed) the launch also appends each request's new token at
+    position seq_lens[b] - 1 (fused lam_kv_append)."""
     _require_cuda(q, k_pool, v_pool, seq_lens, page_table)
     if q.dim() != 3:
         raise _lib.ValidationError("q must be [B, Hq, D]")
@@ -82,20 +85,32 @@ def make_args(q: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor,
     a.out = out.data_ptr()
     a.lse = lse.data_ptr() if lse is not None else None
     a.q_batch_stride = q.stride(0) if B > 1 and q.stride(0) != Hq * D else 0
+    if (k_new is None) != (v_new is None):
+        raise _lib.ValidationError("fused append needs both k_new and v_new")
+    if k_new is not None:
+        _require_cuda(k_new, v_new)
+        if (k_new.shape != (B, Hkv, D) or k_new.dtype != q.dtype or k_new.stride(2) != 1
+                or k_new.stride(1) != D or v_new.stride() != k_new.stride()
+                or v_new.shape != k_new.shape):
+            raise _lib.ValidationError("k_new/v_new must be [B, Hkv, D] rows sharing a batch stride")
+        a.k_new, a.v_new = k_new.data_ptr(), v_new.data_ptr()
+        a.new_batch_stride = k_new.stride(0) if B > 1 else 0
     return a, out
 
 
 def decode(q, k_pool, v_pool, seq_lens, *, page_table=None, max_len=None, scale=None, out=None,
            out_dtype=None, return_lse=False, kernel="auto", split_tokens=0, ctx=None,
-           stream=None):
+           stream=None, k_new=None, v_new=None):
     """softmax(q K^T scale) V per (request, q head) over the request's first seq_lens[b]
-    tokens; q head h reads KV head h // (Hq // Hkv)."""
+    tokens; q head h reads KV head h // (Hq // Hkv).  With k_new / v_new the request's new
+    token (position seq_lens[b] - 1) is taken from them and appended to the pools in the same
+    launch."""
     lse = None
     if return_lse:
         lse = torch.empty(q.shape[:2], dtype=torch.float32, device=q.device)
     a, out = make_args(q, k_pool, v_pool, seq_lens, page_table=page_table, max_len=max_len,
                        scale=scale, out=out, out_dtype=out_dtype, lse=lse, kernel=kernel,
-                       split_tokens=split_tokens)
+                       split_tokens=split_tokens, k_new=k_new, v_new=v_new)
     ctx = ctx or _lib.context(q.device.index or 0)
     check(_lib.load().lam_decode(ctx.handle, a, _stream_ptr(stream)))
     return (out, lse) if return_lse else out

@@ -296,3 +296,36 @@ def test_decode_layers_host_matches_device_path(built):
         want = dec.decode(hq[l].cuda(), kp, vp, lens_t, page_table=ptt, max_len=max(lens))
         assert torch.equal(ho[l], want.cpu()), l
         assert torch.equal(pools[l][0], kp) and torch.equal(pools[l][1], vp)
+
+
+@pytest.mark.parametrize("dtype,G,paged", [(torch.bfloat16, 8, True), (torch.bfloat16, 1, True),
+                                           (torch.float32, 1, False), (torch.float16, 4, True),
+                                           (torch.float32, 4, True)])
+def test_fused_append_equals_append_then_decode(built, dtype, G, paged):
+    """decode(..., k_new, v_new) == kv_append + decode: bitwise outputs and pools, for the
+    last tile, split boundaries and single-token requests (new token at seq_lens - 1)."""
+    from paper_2405_01814_b200 import decode as dec
+
+    B, Hkv, D = 5, 2, 128
+    lens = [1, 64, 65, 300, 129]
+    lmax = 320
+    q, k, v = make_dense(B, Hkv * G, Hkv, D, lmax, dtype, seed=41 + G)
+    kn = torch.randn((B, Hkv, D), device="cuda").to(dtype)
+    vn = torch.randn((B, Hkv, D), device="cuda").to(dtype)
+    if paged:
+        pt, npages = page_table_for(lens, 64, seed=9)
+        ptt = torch.tensor(pt, device="cuda")
+        kp, vp = to_paged(k, lens, 64, pt, npages, fill=7.0), to_paged(v, lens, 64, pt, npages, fill=7.0)
+    else:
+        ptt, kp, vp = None, k.clone(), v.clone()
+    kp2, vp2 = kp.clone(), vp.clone()
+    lt = _lens_t(lens)
+    for split in (0, 64):
+        a = dec.decode(q, kp, vp, lt, page_table=ptt, max_len=max(lens), split_tokens=split,
+                       k_new=kn, v_new=vn, out_dtype=torch.float32)
+        dec.kv_append(kn, vn, kp2, vp2, (lt - 1).contiguous(), ptt)
+        b = dec.decode(q, kp2, vp2, lt, page_table=ptt, max_len=max(lens), split_tokens=split,
+                       out_dtype=torch.float32)
+        torch.cuda.synchronize()
+        assert torch.equal(a, b), split
+        assert torch.equal(kp, kp2) and torch.equal(vp, vp2), split
