@@ -4,8 +4,9 @@ HBM roofline, attention tokens/s).
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--impl ours|reference]
 
 A step is one decode iteration of the workload over every layer: per layer, append each
-request's new-token K/V into the paged HBM store (lam_kv_append) and run decode attention
-over the full context (lam_decode).  KV bytes are the reference's algorithmic bytes
+request's new-token K/V into the paged HBM store and run decode attention over the full
+context — one fused lam_decode launch (k_new/v_new), or lam_kv_append + lam_decode with
+--separate-append.  KV bytes are the reference's algorithmic bytes
 (attn_cost, reference core/src/perf.cpp:77-88): 2 e (d/G) L l B per step.
 
 Default workload (N=1): BASELINE config 2, LLaMA-2-7B all 32 layers, bf16, B=64, l=4096 —
@@ -369,20 +370,15 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
     if world > 1:
         from paper_2405_01814_b200.dist import HeadShardedAttention
 
-        def append(layer, m, k, v):
-            kp, vp = W.layer_pools(layer)
-            sl = W.rows(m)
-            dec.kv_append(k, v, kp, vp, W.positions[sl],
-                          W.page_table[sl] if W.page_table is not None else None)
-
-        def attend(layer, m, q, out):
-            kp, vp = W.layer_pools(layer)
+        def attend(layer, m, q, k, v, out):  # fused append + decode, straight from the
+            kp, vp = W.layer_pools(layer)      # packed receive buffer
             sl = W.rows(m)
             dec.decode(q, kp, vp, W.seq_lens[sl],
                        page_table=W.page_table[sl] if W.page_table is not None else None,
-                       max_len=W.max_len, out=out, ctx=W.ctx, split_tokens=W.chunk)
+                       max_len=W.max_len, out=out, ctx=W.ctx, split_tokens=W.chunk,
+                       k_new=k, v_new=v)
 
-        engine = HeadShardedAttention(W.geo, dist, append, attend, device, W.dtype)
+        engine = HeadShardedAttention(W.geo, dist, None, attend, device, W.dtype)
 
     counter = [0]
 
@@ -392,12 +388,16 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
         counter[0] += 1
         for layer in range(W.layers):
             kp, vp = W.layer_pools(layer, s)
-            dec.kv_append(W.kn_in[layer], W.vn_in[layer], kp, vp, W.positions, W.page_table)
             if ev is not None:
                 ev[layer][0].record(stream)
-            dec.decode(W.q_in[layer], kp, vp, W.seq_lens, page_table=W.page_table,
-                       max_len=W.max_len, out=W.out[layer], ctx=W.ctx,
-                       split_tokens=W.chunk)
+            if args.separate_append:
+                dec.kv_append(W.kn_in[layer], W.vn_in[layer], kp, vp, W.positions, W.page_table)
+                dec.decode(W.q_in[layer], kp, vp, W.seq_lens, page_table=W.page_table,
+                           max_len=W.max_len, out=W.out[layer], ctx=W.ctx, split_tokens=W.chunk)
+            else:  # one launch: append the new token and attend (fused lam_kv_append)
+                dec.decode(W.q_in[layer], kp, vp, W.seq_lens, page_table=W.page_table,
+                           max_len=W.max_len, out=W.out[layer], ctx=W.ctx, split_tokens=W.chunk,
+                           k_new=W.kn_in[layer], v_new=W.vn_in[layer])
             if ev is not None:
                 ev[layer][1].record(stream)
 
@@ -443,7 +443,7 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
         ms_step, kern_avg = float(t[0]), float(t[1])
     else:
         kern_avg = statistics.mean(kern_ms)
-    launches = args.steps * W.layers * W.mb * 2
+    launches = args.steps * W.layers * W.mb * (2 if args.separate_append else 1)
 
     # ---- end-to-end through the C-ABI host-buffer entry point (pinned host buffers)
     e2e = None
@@ -593,6 +593,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=3.0)
+    ap.add_argument("--separate-append", action="store_true",
+                    help="lam_kv_append + lam_decode per layer instead of the fused launch")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))

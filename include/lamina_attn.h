@@ -206,7 +206,8 @@ int lam_decode_step_host(lam_ctx* ctx, const lam_decode_args* args, const void* 
 
 /* One decode step over n_layers layers from host buffers — the attention worker's end-to-end
  * step.  Layer l's q / k_new / v_new are copied H2D on `copy_stream` into one of two device
- * staging sets while layer l-1 appends + decodes on `stream`, and each layer's output returns
+ * staging sets while layer l-1 appends + decodes (one fused launch, the new token at
+ * seq_lens[b] - 1; d_positions is unused and may be NULL) on `stream`, and each layer's output returns
  * D2H on `copy_stream` as soon as it is ready, so the host copies hide under the HBM-bound
  * attention.  layer_args[l] describes layer l's pools (its q/out fields are ignored: the staging
  * set is used).  d_stage must hold 2 * (q + k_new + v_new + out) bytes of one layer, each part

@@ -856,10 +856,11 @@ int lam_decode_layers_host(lam_ctx* ctx, const lam_decode_args* layer_args, int3
     a.out = b + L.q + 2 * L.kv;
     LAM_CUDA(cudaStreamWaitEvent(cs, in_ready[s], 0));
     if (l >= 2) LAM_CUDA(cudaStreamWaitEvent(cs, out_free[s], 0));
-    rc = lam_kv_append(a.kv_dtype, a.batch, a.num_kv_heads, a.head_dim, a.page_size, a.pt_stride,
-                       a.page_table, d_positions, b + L.q, b + L.q + L.kv, 0,
-                       const_cast<void*>(a.k_pool), const_cast<void*>(a.v_pool), stream);
-    if (rc != LAM_OK) return rc;
+    // fused append: the new token (position seq_lens[b] - 1) comes from the staging set
+    (void)d_positions;
+    a.k_new = b + L.q;
+    a.v_new = b + L.q + L.kv;
+    a.new_batch_stride = 0;
     if ((rc = lam_decode(ctx, &a, stream)) != LAM_OK) return rc;
     LAM_CUDA(cudaEventRecord(consumed[s], cs));
     LAM_CUDA(cudaEventRecord(out_ready[s], cs));

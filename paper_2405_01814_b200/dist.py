@@ -95,6 +95,7 @@ class HeadShardedAttention:
 
     append(layer, mb, k[B_mb, hkv_l, D], v[...])          writes the new tokens
     attend(layer, mb, q[B_mb, hq_l, D], out[B_mb, hq_l, D])  local decode attention
+    With append=None, attend(layer, mb, q, k, v, out) does both (the fused decode launch).
     """
 
     def __init__(self, geo: ShardGeometry, dist, append: Callable, attend: Callable,
@@ -180,10 +181,15 @@ class HeadShardedAttention:
         q = packed[:, : g.hq_l]
         k = packed[:, g.hq_l: g.hq_l + g.hkv_l]
         v = packed[:, g.hq_l + g.hkv_l:]
-        self.append_fn(layer, m, k, v)
+        out = self.o_l[m].view(g.B_mb, g.hq_l, g.D)
+        if self.append_fn is not None:
+            self.append_fn(layer, m, k, v)
         if e is not None:
             e[0].record(self.compute)
-        self.attend_fn(layer, m, q, self.o_l[m].view(g.B_mb, g.hq_l, g.D))
+        if self.append_fn is None:
+            self.attend_fn(layer, m, q, k, v, out)
+        else:
+            self.attend_fn(layer, m, q, out)
         if e is not None:
             e[1].record(self.compute)
 

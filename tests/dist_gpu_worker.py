@@ -58,6 +58,8 @@ def main():
                 cache.v[layer, page, :, off] = cv[layer, req, h0:h1, t].to(dev)
     positions = torch.tensor(row_lens - 1, dtype=torch.int32, device=dev)
 
+    fused = os.environ.get("LAM_TEST_FUSED", "1") == "1"
+
     def append(layer, m, k, v):
         sl = slice(m * geo.B_mb, (m + 1) * geo.B_mb)
         dec.kv_append(k, v, cache.k[layer], cache.v[layer], positions[sl], cache.page_table[sl])
@@ -67,7 +69,14 @@ def main():
         dec.decode(qr, cache.k[layer], cache.v[layer], cache.seq_lens[sl],
                    page_table=cache.page_table[sl], max_len=int(row_lens.max()), out=out)
 
-    eng = HeadShardedAttention(geo, dist, append, attend, dev, torch.bfloat16)
+    def attend_fused(layer, m, qr, k, v, out):
+        sl = slice(m * geo.B_mb, (m + 1) * geo.B_mb)
+        dec.decode(qr, cache.k[layer], cache.v[layer], cache.seq_lens[sl],
+                   page_table=cache.page_table[sl], max_len=int(row_lens.max()), out=out,
+                   k_new=k, v_new=v)
+
+    eng = (HeadShardedAttention(geo, dist, None, attend_fused, dev, torch.bfloat16) if fused
+           else HeadShardedAttention(geo, dist, append, attend, dev, torch.bfloat16))
     mine = slice(rank * B_LOCAL, (rank + 1) * B_LOCAL)
     qkv_in = shard_inputs(q[:, mine], kn[:, mine], vn[:, mine], world, MB).to(dev)
     out = torch.zeros(geo.q_shape(), dtype=torch.bfloat16, device=dev)
