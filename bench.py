@@ -308,6 +308,11 @@ class Workload:
             self.page_table = None
         self.seq_lens = torch.tensor(self.lens, dtype=torch.int32, device=device)
         self.positions = (self.seq_lens - 1).contiguous()
+        # mixed lengths: claim work longest-first (LPT), per launch
+        from paper_2405_01814_b200.decode import longest_first
+
+        self.orders = ([longest_first(self.seq_lens[m * self.B // self.mb:(m + 1) * self.B // self.mb])
+                        for m in range(self.mb)] if w.get("mixed") else [None] * self.mb)
         gi = torch.Generator(device=device).manual_seed(99 + rank)
         # model-worker side inputs for this rank's B_local requests, per layer
         if self.geo is None:
@@ -376,7 +381,7 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
             dec.decode(q, kp, vp, W.seq_lens[sl],
                        page_table=W.page_table[sl] if W.page_table is not None else None,
                        max_len=W.max_len, out=out, ctx=W.ctx, split_tokens=W.chunk,
-                       k_new=k, v_new=v)
+                       k_new=k, v_new=v, request_order=W.orders[m])
 
         engine = HeadShardedAttention(W.geo, dist, None, attend, device, W.dtype)
 
@@ -397,7 +402,8 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
             else:  # one launch: append the new token and attend (fused lam_kv_append)
                 dec.decode(W.q_in[layer], kp, vp, W.seq_lens, page_table=W.page_table,
                            max_len=W.max_len, out=W.out[layer], ctx=W.ctx, split_tokens=W.chunk,
-                           k_new=W.kn_in[layer], v_new=W.vn_in[layer])
+                           k_new=W.kn_in[layer], v_new=W.vn_in[layer],
+                           request_order=W.orders[0])
             if ev is not None:
                 ev[layer][1].record(stream)
 
@@ -546,7 +552,8 @@ def run_e2e(args, W, engine, dist, device, stream):
         for layer in range(L):
             kp, vp = W.layer_pools(layer, s)
             a, _ = dec.make_args(d_q, kp, vp, W.seq_lens, page_table=W.page_table,
-                                 max_len=W.max_len, out=d_out, split_tokens=W.chunk)
+                                 max_len=W.max_len, out=d_out, split_tokens=W.chunk,
+                                 request_order=W.orders[0])
             arr[layer] = a
         args_sets.append(arr)
     stage = torch.empty(int(lib.lam_decode_layers_host_stage_bytes(args_sets[0])),

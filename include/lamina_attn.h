@@ -172,6 +172,10 @@ typedef struct lam_decode_args {
   const void* k_new;
   const void* v_new;
   int64_t new_batch_stride;
+  /* Optional [B] int32 device permutation of the requests, longest first: work items are claimed
+   * in this order (longest-processing-time-first keeps mixed-length batches balanced, in the
+   * spirit of request_partition, attention.cpp:185-196).  NULL = request order. */
+  const int32_t* request_order;
 } lam_decode_args;
 
 int lam_decode(lam_ctx* ctx, const lam_decode_args* args, void* stream);

@@ -58,6 +58,7 @@ class DecodeArgs(C.Structure):
         ("k_new", C.c_void_p),
         ("v_new", C.c_void_p),
         ("new_batch_stride", C.c_int64),
+        ("request_order", C.c_void_p),
     ]
 
 

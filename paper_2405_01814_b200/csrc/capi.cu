@@ -690,6 +690,7 @@ int lam_decode(lam_ctx* ctx, const lam_decode_args* a, void* stream) {
   p.QG = pl.QG;
   p.n_items = static_cast<int32_t>(static_cast<int64_t>(a->batch) * a->num_kv_heads * pl.QG * pl.S);
   p.work = ctx->work;
+  p.order = a->request_order;
   if (a->k_new != nullptr) {  // fused append
     if (a->v_new == nullptr) return fail(LAM_ERR_VALIDATION, "fused append needs both k_new and v_new");
     p.k_new = a->k_new;

@@ -54,6 +54,7 @@ struct DecodeParams {
   int64_t new_stride;
   void* k_pool_w;
   void* v_pool_w;
+  const int32_t* order;     // optional request permutation for item enumeration (LPT)
 };
 
 // Physical row of token t of (request b, kv head h) in a pool viewed as [rows][D].
@@ -80,6 +81,7 @@ __device__ __forceinline__ Item make_item(const DecodeParams& p, int idx, int ti
   unit /= p.QG;
   it.kvh = unit % p.Hkv;
   it.b = unit / p.Hkv;
+  if (p.order != nullptr) it.b = __ldg(p.order + it.b);
   it.len = __ldg(p.seq_lens + it.b);
   it.t_begin = it.split * p.chunk;
   it.t_end = min(it.len, it.t_begin + p.chunk);
@@ -98,6 +100,7 @@ __device__ __forceinline__ Item item_from_tag(const DecodeParams& p, int4 tag) {
   unit /= p.QG;
   it.kvh = unit % p.Hkv;
   it.b = unit / p.Hkv;
+  if (p.order != nullptr) it.b = __ldg(p.order + it.b);
   it.len = tag.z;
   it.t_begin = it.split * p.chunk;
   it.t_end = tag.w;

@@ -40,7 +40,8 @@ def make_args(q: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor,
               out: torch.Tensor | None = None, out_dtype: torch.dtype | None = None,
               lse: torch.Tensor | None = None, kernel: str = "auto",
               split_tokens: int = 0, k_new: torch.Tensor | None = None,
-              v_new: torch.Tensor | None = None) -> tuple[DecodeArgs, torch.Tensor]:
+              v_new: torch.Tensor | None = None,
+              request_order: torch.Tensor | None = None) -> tuple[DecodeArgs, torch.Tensor]:
     """Fill lam_decode_args from tensors; returns (args, out).  With k_new/v_new ([B, Hkv, D],
     a shared batch stride allowed) the launch also appends each request's new token at
     position seq_lens[b] - 1 (fused lam_kv_append)."""
@@ -95,12 +96,17 @@ def make_args(q: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor,
             raise _lib.ValidationError("k_new/v_new must be [B, Hkv, D] rows sharing a batch stride")
         a.k_new, a.v_new = k_new.data_ptr(), v_new.data_ptr()
         a.new_batch_stride = k_new.stride(0) if B > 1 else 0
+    if request_order is not None:
+        _require_cuda(request_order)
+        if request_order.dtype != torch.int32 or request_order.shape != (B,):
+            raise _lib.ValidationError("request_order must be int32 [B]")
+        a.request_order = request_order.data_ptr()
     return a, out
 
 
 def decode(q, k_pool, v_pool, seq_lens, *, page_table=None, max_len=None, scale=None, out=None,
            out_dtype=None, return_lse=False, kernel="auto", split_tokens=0, ctx=None,
-           stream=None, k_new=None, v_new=None):
+           stream=None, k_new=None, v_new=None, request_order=None):
     """softmax(q K^T scale) V per (request, q head) over the request's first seq_lens[b]
     tokens; q head h reads KV head h // (Hq // Hkv).  With k_new / v_new the request's new
     token (position seq_lens[b] - 1) is taken from them and appended to the pools in the same
@@ -110,10 +116,16 @@ def decode(q, k_pool, v_pool, seq_lens, *, page_table=None, max_len=None, scale=
         lse = torch.empty(q.shape[:2], dtype=torch.float32, device=q.device)
     a, out = make_args(q, k_pool, v_pool, seq_lens, page_table=page_table, max_len=max_len,
                        scale=scale, out=out, out_dtype=out_dtype, lse=lse, kernel=kernel,
-                       split_tokens=split_tokens, k_new=k_new, v_new=v_new)
+                       split_tokens=split_tokens, k_new=k_new, v_new=v_new,
+                       request_order=request_order)
     ctx = ctx or _lib.context(q.device.index or 0)
     check(_lib.load().lam_decode(ctx.handle, a, _stream_ptr(stream)))
     return (out, lse) if return_lse else out
+
+
+def longest_first(seq_lens: torch.Tensor) -> torch.Tensor:
+    """Request permutation for `request_order`: longest sequence first (LPT)."""
+    return torch.argsort(seq_lens, descending=True, stable=True).to(torch.int32)
 
 
 def plan(q, k_pool, v_pool, seq_lens, **kw):

@@ -329,3 +329,26 @@ def test_fused_append_equals_append_then_decode(built, dtype, G, paged):
         torch.cuda.synchronize()
         assert torch.equal(a, b), split
         assert torch.equal(kp, kp2) and torch.equal(vp, vp2), split
+
+
+def test_request_order_is_transparent(built):
+    """Longest-first item ordering changes only the schedule, never the result."""
+    from paper_2405_01814_b200 import decode as dec
+
+    rng = np.random.default_rng(3)
+    lens = rng.integers(1, 2000, 24).tolist()
+    B, Hkv, G, D = len(lens), 2, 8, 128
+    q, k, v = make_dense(B, Hkv * G, Hkv, D, 2048, torch.bfloat16, seed=13)
+    pt, npages = page_table_for(lens, 64, seed=4)
+    ptt = torch.tensor(pt, device="cuda")
+    kp, vp = to_paged(k, lens, 64, pt, npages), to_paged(v, lens, 64, pt, npages)
+    lt = _lens_t(lens)
+    for split in (0, 256):
+        a = dec.decode(q, kp, vp, lt, page_table=ptt, max_len=max(lens), split_tokens=split)
+        b = dec.decode(q, kp, vp, lt, page_table=ptt, max_len=max(lens), split_tokens=split,
+                       request_order=dec.longest_first(lt))
+        assert torch.equal(a, b)
+    want = oracle_decode(q, k, v, lens, 1 / math.sqrt(D))
+    out = dec.decode(q, kp, vp, lt, page_table=ptt, max_len=max(lens), out_dtype=torch.float32,
+                     request_order=dec.longest_first(lt))
+    assert _maxabs(out.cpu().numpy(), want) <= 2e-3
