@@ -517,9 +517,7 @@ def run_e2e(args, W, engine, dist, device, stream):
         h_qkv = W.qkv_in.cpu().pin_memory()
 
         def step_mg():
-            W.qkv_in.copy_(h_qkv, non_blocking=True)
-            engine.step(W.qkv_in, W.out)
-            h_out.copy_(W.out, non_blocking=True)
+            engine.step(W.qkv_in, W.out, host_in=h_qkv, host_out=h_out)
 
         for _ in range(max(1, args.warmup)):
             step_mg()
@@ -538,7 +536,7 @@ def run_e2e(args, W, engine, dist, device, stream):
         d2h = h_out.numel() * h_out.element_size()
         return {"value": W.step_bytes / (ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
                 "h2d_bytes_per_step": int(h2d) * W.world, "d2h_bytes_per_step": int(d2h) * W.world,
-                "api": "HeadShardedAttention.step (pinned host in/out, NCCL all-to-all)"}
+                "api": "HeadShardedAttention.step (pinned host in/out overlapped on copy streams, NCCL all-to-all)"}
     h_q = W.q_in.cpu().pin_memory()
     h_kn = W.kn_in.cpu().pin_memory()
     h_vn = W.vn_in.cpu().pin_memory()

@@ -114,15 +114,20 @@ class HeadShardedAttention:
         if self.cuda:
             self.comm = torch.cuda.Stream(device=device)
             self.compute = torch.cuda.current_stream(device)
+            self.h2d = torch.cuda.Stream(device=device)  # copy engines: host inputs in ...
+            self.d2h = torch.cuda.Stream(device=device)  # ... and outputs back out
 
     # ---- collectives ----
     def _a2a(self, out: torch.Tensor, inp: torch.Tensor):
         self.dist.all_to_all_single(out, inp)
 
-    def step(self, qkv_in, out, ev=None):
+    def step(self, qkv_in, out, ev=None, host_in=None, host_out=None):
         """One decode step over all layers; returns when the work is enqueued (CUDA) or done
         (CPU).  `ev`, if given, is a list of (start, end) CUDA event pairs, one per local
-        attention launch, recorded on the compute stream."""
+        attention launch, recorded on the compute stream.  With pinned `host_in` / `host_out`
+        (shapes of qkv_in / out) the step starts from host memory: every layer's inputs are copied
+        in on a copy stream ahead of their scatter and every layer's outputs copied back as soon
+        as they are gathered, both hidden under the attention of other layers."""
         g = self.geo
         MB = g.micro_batches
         if not self.cuda:
@@ -137,6 +142,16 @@ class HeadShardedAttention:
         scat = [[torch.cuda.Event() for _ in range(MB)] for _ in range(g.layers)]
         done = [[torch.cuda.Event() for _ in range(MB)] for _ in range(g.layers)]
         gath = [torch.cuda.Event() for _ in range(MB)]
+        arrived = None
+        if host_in is not None:  # every layer has its own input slot: copy them all ahead
+            self.h2d.wait_stream(comp)
+            arrived = [torch.cuda.Event() for _ in range(g.layers)]
+            with torch.cuda.stream(self.h2d):
+                for layer in range(g.layers):
+                    qkv_in[layer].copy_(host_in[layer], non_blocking=True)
+                    arrived[layer].record(self.h2d)
+        if host_out is not None:
+            self.d2h.wait_stream(comp)
 
         def scatter(layer, m):
             with torch.cuda.stream(comm):
@@ -144,6 +159,8 @@ class HeadShardedAttention:
                     # micro-batch m's next layer follows its previous output gather (data
                     # dependency through the model worker) and the reuse of its receive buffers
                     comm.wait_event(done[layer - 1][m])
+                if arrived is not None and m == 0:
+                    comm.wait_event(arrived[layer])
                 self._scatter(layer, m, qkv_in)
                 scat[layer][m].record(comm)
 
@@ -152,6 +169,10 @@ class HeadShardedAttention:
                 comm.wait_event(done[layer][m])
                 self._a2a(out[layer, m], self.o_l[m])
                 gath[m].record(comm)
+            if host_out is not None:
+                self.d2h.wait_event(gath[m])
+                with torch.cuda.stream(self.d2h):
+                    host_out[layer, m].copy_(out[layer, m], non_blocking=True)
 
         for m in range(MB):
             scatter(0, m)
@@ -171,6 +192,8 @@ class HeadShardedAttention:
             gath_prev = list(gath)
             gath = [torch.cuda.Event() for _ in range(MB)]
         comp.wait_stream(comm)
+        if host_out is not None:
+            comp.wait_stream(self.d2h)
 
     def _scatter(self, layer, m, qkv_in):
         self._a2a(self.qkv_r[m], qkv_in[layer, m])
