@@ -450,6 +450,25 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
     else:
         kern_avg = statistics.mean(kern_ms)
     launches = args.steps * W.layers * W.mb * (2 if args.separate_append else 1)
+    alone_ms = None
+    if engine is not None:
+        # the same decode launch with no collective in flight (diagnoses comm interference)
+        g = W.geo
+        packed = engine.qkv_r[0].view(g.B_mb, g.W, g.D)
+        sl = W.rows(0)
+        kp, vp = W.layer_pools(0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 10
+        torch.cuda.synchronize(device)
+        e0.record(stream)
+        for _ in range(reps):
+            dec.decode(packed[:, : g.hq_l], kp, vp, W.seq_lens[sl],
+                       page_table=W.page_table[sl] if W.page_table is not None else None,
+                       max_len=W.max_len, out=engine.o_l[0].view(g.B_mb, g.hq_l, g.D), ctx=W.ctx,
+                       split_tokens=W.chunk, request_order=W.orders[0])
+        e1.record(stream)
+        torch.cuda.synchronize(device)
+        alone_ms = e0.elapsed_time(e1) / reps
 
     # ---- end-to-end through the C-ABI host-buffer entry point (pinned host buffers)
     e2e = None
@@ -484,7 +503,8 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
                      "frac": achieved / peak,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650",
                      "kernel": f"decode_{W.kernel}", "bytes_per_launch": W.decode_bytes_per_launch,
-                     "avg_launch_ms": kern_avg, "traffic": ncu_traffic(args.workload, world)},
+                     "avg_launch_ms": kern_avg, "traffic": ncu_traffic(args.workload, world),
+                     "alone_launch_ms": alone_ms},
         "gpu_launches": launches,
         "clocks": clocks,
     }
