@@ -45,7 +45,7 @@ struct DecodeParams {
   float scale;              // softmax scale (natural units)
   float scale_log2;         // scale * log2(e)
   int32_t out_f32;
-  int32_t flags;            // reserved (tuning experiments)
+  int32_t flags;            // tuning: bit2 = all-dynamic schedule (no static rounds)
   // fused append (optional): the new token of request b (position seq_lens[b] - 1) comes from
   // k_new/v_new (request b, kv head h at + b * new_stride + h * D); the kernel attends over it
   // from shared memory and writes it into the pools for later steps.
@@ -126,10 +126,14 @@ __device__ __forceinline__ int live_splits(const DecodeParams& p, int len) {
 // `issue(s, it, j, row)` must arrive on full[s] with expect_tx and start the stage's TMA
 // copies of tile j, whose first KV row is `row`.
 //
-// Items are claimed from a global counter right after the previous item's tiles are issued.
-// Measured on B200 this dynamic schedule beats a static round-robin split by 2-3 % (per-SM
-// streaming rates differ across the two dies) and beats claiming one item ahead (that costs up
-// to one item of tail imbalance); the stage ring covers the claim's round trips.
+// Schedule: hybrid static-then-dynamic.
+//  * Static rounds: CTA c runs items c, c + G, c + 2G, ... for all but the last ~2 rounds.  Its
+//    next item is known, so the item's length and first page-table entry are loaded while the
+//    current item streams: an item boundary costs the HBM stream nothing.  (With claiming at
+//    every boundary, the claim atomic -> length -> page-entry round trips idled each SM for
+//    ~3 us per item, ~7 % of C2/C3.)
+//  * Dynamic tail: the remaining items are claimed from a global counter, which absorbs the
+//    2-3 % per-SM streaming-rate differences of the two-die part and the tail.
 template <int STAGES, int TILE, class Issue>
 __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* full,
                                               uint64_t* empty, int4* meta, long long* meta_row,
@@ -140,31 +144,65 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
     if (k >= STAGES) mbar_wait(&empty[s], ((k / STAGES) - 1) & 1);
     return s;
   };
-  for (;;) {
-    const int idx = atomicAdd(p.work, 1);
-    if (idx >= p.n_items) break;
-    const Item it = make_item(p, idx, TILE);
+  // stream one item; `during` runs once, right after the first stage is issued
+  auto run_item = [&](int idx, const Item& it, int64_t row0, auto&& during) {
     if (it.ntiles == 0) {
       if (it.split == 0 && it.len == 0) {  // empty request: zero-output marker
         const int s = acquire(i++);
         meta[s] = make_int4(idx, 0, 0, 0);
         mbar_arrive(&full[s]);
       }                                    // (an empty split has nothing to merge)
-      continue;
+      during();
+      return;
     }
     for (int j = 0; j < it.ntiles; ++j) {
       const int s = acquire(i++);
-      const int64_t row = kv_row(p, it.b, it.kvh, it.t_begin + j * TILE);
+      const int64_t row = j == 0 ? row0 : kv_row(p, it.b, it.kvh, it.t_begin + j * TILE);
       meta[s] = make_int4(idx, j, it.len, it.t_end);
       meta_row[s] = row;
       issue(s, it, j, row);
+      if (j == 0) during();
     }
+  };
+  auto first_row = [&](const Item& it) {
+    return it.ntiles > 0 ? kv_row(p, it.b, it.kvh, it.t_begin) : int64_t{0};
+  };
+  const int G = static_cast<int>(gridDim.x);
+  const int static_rounds = (p.flags & 4) ? 0 : max(0, p.n_items / G - 2);
+  const int n_static = static_rounds * G;
+  // static rounds, next item prefetched
+  int idx = blockIdx.x;
+  if (idx < n_static) {
+    Item it = make_item(p, idx, TILE);
+    int64_t row = first_row(it);
+    while (idx < n_static) {
+      const int nidx = idx + G;
+      Item nit{};
+      int64_t nrow = 0;
+      run_item(idx, it, row, [&] {
+        if (nidx < n_static) {
+          nit = make_item(p, nidx, TILE);
+          nrow = first_row(nit);
+        }
+      });
+      idx = nidx;
+      it = nit;
+      row = nrow;
+    }
+  }
+  // dynamic tail
+  for (;;) {
+    const int k = atomicAdd(p.work, 1);
+    const int didx = n_static + k;
+    if (didx >= p.n_items) break;
+    const Item it = make_item(p, didx, TILE);
+    run_item(didx, it, first_row(it), [] {});
   }
   const int s = acquire(i);
   meta[s] = make_int4(-1, 0, 0, 0);
   mbar_arrive(&full[s]);
   // the last producer to leave resets the counters for the next launch
-  if (atomicAdd(p.work + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+  if (atomicAdd(p.work + 1, 1) == G - 1) {
     p.work[0] = 0;
     p.work[1] = 0;
   }
