@@ -161,7 +161,7 @@ struct Plan {
 // whose item counts (512, 1024) divide evenly there (up to +4 % over a full 148-CTA grid).
 void choose_splits(Plan& pl, int64_t units, int max_len, int max_ctas, int split_tokens,
                    double bytes_per_token) {
-  constexpr double BW_CHIP = 7.0e12, RATE_SM = 56e9, C_ITEM = 4e-6;
+  constexpr double BW_CHIP = 7.0e12, RATE_SM = 50e9, C_ITEM = 1e-6;
   const int tiles_total = std::max(1, (max_len + pl.tile - 1) / pl.tile);
   const int occ_per_sm = std::max(1, max_ctas / 148);
   double best = 1e300;

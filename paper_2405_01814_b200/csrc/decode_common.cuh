@@ -144,8 +144,9 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
     if (k >= STAGES) mbar_wait(&empty[s], ((k / STAGES) - 1) & 1);
     return s;
   };
-  // stream one item; `during` runs once, right after the first stage is issued
-  auto run_item = [&](int idx, const Item& it, int64_t row0, auto&& during) {
+  // stream one item; `during` runs once, right after the stage of tile `at` is issued
+  // (at < 0: after the last tile)
+  auto run_item = [&](int idx, const Item& it, int64_t row0, int at, auto&& during) {
     if (it.ntiles == 0) {
       if (it.split == 0 && it.len == 0) {  // empty request: zero-output marker
         const int s = acquire(i++);
@@ -155,13 +156,14 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
       during();
       return;
     }
+    const int when = at < 0 ? it.ntiles - 1 : min(at, it.ntiles - 1);
     for (int j = 0; j < it.ntiles; ++j) {
       const int s = acquire(i++);
       const int64_t row = j == 0 ? row0 : kv_row(p, it.b, it.kvh, it.t_begin + j * TILE);
       meta[s] = make_int4(idx, j, it.len, it.t_end);
       meta_row[s] = row;
       issue(s, it, j, row);
-      if (j == 0) during();
+      if (j == when) during();
     }
   };
   auto first_row = [&](const Item& it) {
@@ -179,7 +181,7 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
       const int nidx = idx + G;
       Item nit{};
       int64_t nrow = 0;
-      run_item(idx, it, row, [&] {
+      run_item(idx, it, row, 0, [&] {
         if (nidx < n_static) {
           nit = make_item(p, nidx, TILE);
           nrow = first_row(nit);
@@ -190,13 +192,27 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
       row = nrow;
     }
   }
-  // dynamic tail
-  for (;;) {
-    const int k = atomicAdd(p.work, 1);
-    const int didx = n_static + k;
-    if (didx >= p.n_items) break;
-    const Item it = make_item(p, didx, TILE);
-    run_item(didx, it, first_row(it), [] {});
+  // dynamic tail: the next item is claimed right after the current item's last tile is
+  // issued, so the claim's round trips overlap the tiles still in the ring
+  auto claim = [&](int& didx, Item& it, int64_t& row) {
+    didx = n_static + atomicAdd(p.work, 1);
+    if (didx < p.n_items) {
+      it = make_item(p, didx, TILE);
+      row = first_row(it);
+    }
+  };
+  int didx;
+  Item dit{};
+  int64_t drow = 0;
+  claim(didx, dit, drow);
+  while (didx < p.n_items) {
+    int nidx;
+    Item nit{};
+    int64_t nrow = 0;
+    run_item(didx, dit, drow, -1, [&] { claim(nidx, nit, nrow); });
+    didx = nidx;
+    dit = nit;
+    drow = nrow;
   }
   const int s = acquire(i);
   meta[s] = make_int4(-1, 0, 0, 0);
