@@ -300,11 +300,17 @@ __device__ __forceinline__ void finish_item_warp(const DecodeParams& p, const It
     }
   }
   release();  // the consumers may refill red_* while this warp counts and merges splits
-  __threadfence();
   __syncwarp();
   int32_t* counter = p.counters + (static_cast<int64_t>(b) * p.Hkv + it.kvh) * p.QG + it.qg;
   int last = 0;
-  if (lane == 0) last = (atomicAdd(counter, 1) == S_live - 1);
+  if (lane == 0) {
+    // release: this warp's partial stores are visible before the count; acquire: the last
+    // arriver sees every other split's partial
+    int prev;
+    asm volatile("fence.acq_rel.gpu;\n\tatom.add.acq_rel.gpu.global.s32 %0, [%1], 1;"
+                 : "=r"(prev) : "l"(counter) : "memory");
+    last = (prev == S_live - 1);
+  }
   last = __shfl_sync(0xffffffffu, last, 0);
   if (!last) return;
   __threadfence();
@@ -339,22 +345,33 @@ __device__ __forceinline__ void finish_item_warp(const DecodeParams& p, const It
     float A[DPL];
 #pragma unroll
     for (int e = 0; e < DPL; ++e) A[e] = 0.f;
+    // all of a batch's split rows are loaded before any is used: one L2 round trip per batch
+    constexpr int SB = 8;
     const int n = min(32, S_live);
-    for (int j = 0; j < n; ++j) {
-      const float wj = __shfl_sync(0xffffffffu, w, j);
-      const float* src = p.ws_acc + (row0 + j) * D + lane;
+    for (int s0 = 0; s0 < n; s0 += SB) {
+      float v[SB][DPL];
 #pragma unroll
-      for (int e = 0; e < DPL; ++e) A[e] = fmaf(wj, __ldcg(src + e * 32), A[e]);
+      for (int j = 0; j < SB; ++j) {
+        const float* src = p.ws_acc + (row0 + s0 + j) * D + lane;
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) v[j][e] = s0 + j < n ? __ldcg(src + e * 32) : 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < SB; ++j) {
+        const float wj = __shfl_sync(0xffffffffu, w, (s0 + j) & 31);
+        if (s0 + j < n) {
+#pragma unroll
+          for (int e = 0; e < DPL; ++e) A[e] = fmaf(wj, v[j][e], A[e]);
+        }
+      }
     }
     for (int s0 = 32; s0 < S_live; s0 += 32) {  // more than 32 splits (rare)
-      float w2 = 0.f, m2 = -INFINITY;
+      float w2 = 0.f;
       if (s0 + lane < S_live) {
         const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + (row0 + s0 + lane) * 2));
-        m2 = ml.x;
         w2 = ml.x == -INFINITY ? 0.f : expf(ml.x - M);
         L += w2 * ml.y;
       }
-      (void)m2;
       for (int j = 0; j < min(32, S_live - s0); ++j) {
         const float wj = __shfl_sync(0xffffffffu, w2, j);
         const float* src = p.ws_acc + (row0 + s0 + j) * D + lane;
@@ -401,10 +418,15 @@ __device__ __forceinline__ void epilogue_loop(const DecodeParams& p, const RedPi
     const int idx = r.item[0];
     if (idx < 0) break;
     const Item it = item_from_tag<TILE>(p, make_int4(idx, 0, r.item[1], r.item[2]));
-    finish_item_warp<T, D, GQ, NW, kLog2>(p, it, nvalid, red_m, red_l, red_acc, [&] {
+    auto release = [&] {
       __syncwarp();
       if (threadIdx.x % 32 == 0) mbar_arrive(r.empty);
-    });
+    };
+    if (p.flags & 8) {  // diagnostic only: skip the epilogue work (outputs are not written)
+      release();
+      continue;
+    }
+    finish_item_warp<T, D, GQ, NW, kLog2>(p, it, nvalid, red_m, red_l, red_acc, release);
   }
 }
 
