@@ -236,8 +236,10 @@ __device__ __forceinline__ void store_out(const DecodeParams& p, int64_t idx, fl
 // consumer warps already stream the next item.  red_m/red_l/red_acc hold the NW per-warp
 // partials for GQ q heads: red_m[w*GQ+g] (log2 units if kLog2, else natural), red_l[w*GQ+g],
 // red_acc[(w*GQ+g)*D + d].  `nvalid` q heads of the group are real (the MMA kernel pads to 8).
+// Returns true when this item was the last live split of its unit: the caller then has the
+// unit's splits merged by combine_unit_warp (on the CTA's combine warp).
 template <typename T, int D, int GQ, int NW, bool kLog2, class Release>
-__device__ __forceinline__ void finish_item_warp(const DecodeParams& p, const Item& it,
+__device__ __forceinline__ bool finish_item_warp(const DecodeParams& p, const Item& it,
                                                  int nvalid, const float* red_m,
                                                  const float* red_l, const float* red_acc,
                                                  Release release) {
@@ -285,7 +287,7 @@ __device__ __forceinline__ void finish_item_warp(const DecodeParams& p, const It
             cta_l[g] > 0.f ? cta_m[g] + logf(cta_l[g]) : -INFINITY;
     }
     release();
-    return;
+    return false;
   }
 
   // 2. write this split's partial, then count it in.
@@ -311,8 +313,19 @@ __device__ __forceinline__ void finish_item_warp(const DecodeParams& p, const It
                  : "=r"(prev) : "l"(counter) : "memory");
     last = (prev == S_live - 1);
   }
-  last = __shfl_sync(0xffffffffu, last, 0);
-  if (!last) return;
+  return __shfl_sync(0xffffffffu, last, 0) != 0;
+}
+
+// Merge all live split partials of a unit in split order and finalize (one warp; runs on the
+// CTA's combine warp so the epilogue warp can take the next hand-off meanwhile).
+template <typename T, int D, int GQ>
+__device__ __forceinline__ void combine_unit_warp(const DecodeParams& p, const Item& it,
+                                                  int nvalid) {
+  const int lane = threadIdx.x % 32;
+  const int b = it.b;
+  const int qh0 = it.kvh * p.G + it.qg * GQ;
+  const int S_live = live_splits(p, it.len);
+  int32_t* counter = p.counters + (static_cast<int64_t>(b) * p.Hkv + it.kvh) * p.QG + it.qg;
   __threadfence();
 
   // 3. last split of this unit: merge the live partials in split order and finalize.
@@ -408,16 +421,38 @@ __device__ __forceinline__ void red_commit(const RedPipe& r) {
   if (threadIdx.x % 32 == 0) mbar_arrive(r.full);
 }
 
+// Mailbox from the epilogue warp to the combine warp: units whose last split just finished.
+struct CombPipe {
+  uint64_t* full;   // count 1
+  uint64_t* empty;  // count 1
+  int* item;        // {item index, request length, item end token}
+};
+
 // Epilogue warp main loop.
 template <typename T, int D, int GQ, int NW, bool kLog2, int TILE>
 __device__ __forceinline__ void epilogue_loop(const DecodeParams& p, const RedPipe& r,
-                                              int nvalid, const float* red_m,
+                                              const CombPipe& cq, int nvalid, const float* red_m,
                                               const float* red_l, const float* red_acc) {
+  int kc = 0;  // posts to the combine warp
+  auto post = [&](int idx, int len, int t_end) {
+    if (kc > 0) mbar_wait(cq.empty, (kc - 1) & 1);
+    if (threadIdx.x % 32 == 0) {
+      cq.item[0] = idx;
+      cq.item[1] = len;
+      cq.item[2] = t_end;
+      mbar_arrive(cq.full);
+    }
+    __syncwarp();
+    ++kc;
+  };
   for (int k = 0;; ++k) {
     mbar_wait(r.full, k & 1);
-    const int idx = r.item[0];
-    if (idx < 0) break;
-    const Item it = item_from_tag<TILE>(p, make_int4(idx, 0, r.item[1], r.item[2]));
+    const int idx = r.item[0], len = r.item[1], t_end = r.item[2];
+    if (idx < 0) {
+      post(-1, 0, 0);
+      break;
+    }
+    const Item it = item_from_tag<TILE>(p, make_int4(idx, 0, len, t_end));
     auto release = [&] {
       __syncwarp();
       if (threadIdx.x % 32 == 0) mbar_arrive(r.empty);
@@ -426,7 +461,22 @@ __device__ __forceinline__ void epilogue_loop(const DecodeParams& p, const RedPi
       release();
       continue;
     }
-    finish_item_warp<T, D, GQ, NW, kLog2>(p, it, nvalid, red_m, red_l, red_acc, release);
+    if (finish_item_warp<T, D, GQ, NW, kLog2>(p, it, nvalid, red_m, red_l, red_acc, release))
+      post(idx, len, t_end);
+  }
+}
+
+// Combine warp main loop.
+template <typename T, int D, int GQ, int TILE>
+__device__ __forceinline__ void combine_loop(const DecodeParams& p, const CombPipe& cq,
+                                             int nvalid) {
+  for (int k = 0;; ++k) {
+    mbar_wait(cq.full, k & 1);
+    const int idx = cq.item[0], len = cq.item[1], t_end = cq.item[2];
+    __syncwarp();
+    if (threadIdx.x % 32 == 0) mbar_arrive(cq.empty);
+    if (idx < 0) break;
+    combine_unit_warp<T, D, GQ>(p, item_from_tag<TILE>(p, make_int4(idx, 0, len, t_end)), nvalid);
   }
 }
 
