@@ -161,7 +161,7 @@ struct Plan {
 // whose item counts (512, 1024) divide evenly there (up to +4 % over a full 148-CTA grid).
 void choose_splits(Plan& pl, int64_t units, int max_len, int max_ctas, int split_tokens,
                    double bytes_per_token) {
-  constexpr double BW_CHIP = 7.0e12, RATE_SM = 50e9, C_ITEM = 1e-6;
+  constexpr double BW_CHIP = 7.0e12, RATE_SM = 50e9, C_ITEM = 1e-6, C_COMBINE = 5e-6;
   const int tiles_total = std::max(1, (max_len + pl.tile - 1) / pl.tile);
   const int occ_per_sm = std::max(1, max_ctas / 148);
   double best = 1e300;
@@ -182,6 +182,7 @@ void choose_splits(Plan& pl, int64_t units, int max_len, int max_ctas, int split
       if (rem > 0) t += item_bytes / std::min(BW_CHIP / static_cast<double>(rem), RATE_SM * occ_per_sm);
       t += static_cast<double>((items + ctas - 1) / ctas) * C_ITEM *
            (items_per_cta() > 0 ? items_per_cta() / 4.0 : 1.0);
+      if (s_eff > 1) t += C_COMBINE;  // the separate split-merge launch
       // a smaller grid or more splits must win by >= 1.5 % (model noise)
       if (t < best * (1 - 0.015)) {
         best = t;
@@ -714,7 +715,6 @@ int lam_decode(lam_ctx* ctx, const lam_decode_args* a, void* stream) {
     }
     p.ws_acc = ctx->ws_acc;
     p.ws_ml = ctx->ws_ml;
-    p.counters = ctx->counters;
   }
   auto s = static_cast<cudaStream_t>(stream);
   if (pl.kernel == LAM_KERNEL_GQA_MMA) {
@@ -732,6 +732,7 @@ int lam_decode(lam_ctx* ctx, const lam_decode_args* a, void* stream) {
   } else {
     LAM_CUDA(lam::launch_decode_simt(a->kv_dtype, D, pl.GQ, pl.variant, p, pl.ctas, s));
   }
+  if (pl.S > 1) LAM_CUDA(lam::launch_combine(a->kv_dtype, p, s));
   return LAM_OK;
 }
 

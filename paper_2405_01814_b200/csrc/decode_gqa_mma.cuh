@@ -36,7 +36,7 @@ struct MmaCfg {
   static constexpr int SMEM_BYTES = RING_BYTES + STAGES * SLOT_BYTES + RED_FLOATS * 4 +
                                     STAGES * 16 + STAGES * 8 + (2 * STAGES + 4) * 8 + 16 + 64 +
                                     1024;  // +align slack
-  static constexpr int THREADS = (NW + 3) * 32;  // + producer, epilogue, combine warps
+  static constexpr int THREADS = (NW + 2) * 32;  // + producer warp + epilogue warp
 };
 
 // Byte offset of 16-byte chunk `c` (0..15 across the 128-wide row) of tile row `r`
@@ -47,7 +47,7 @@ __device__ __forceinline__ uint32_t swz(int r, int c) {
 }
 
 template <typename T, int NW_, int STAGES_>
-__global__ void __launch_bounds__((NW_ + 3) * 32)
+__global__ void __launch_bounds__((NW_ + 2) * 32)
     decode_gqa_mma_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap kmap,
                           const __grid_constant__ CUtensorMap vmap) {
   using C = MmaCfg<NW_, STAGES_>;
@@ -64,7 +64,6 @@ __global__ void __launch_bounds__((NW_ + 3) * 32)
   uint64_t* full = reinterpret_cast<uint64_t*>(meta_row + STAGES);
   uint64_t* empty = full + STAGES;
   RedPipe red{empty + STAGES, empty + STAGES + 1, reinterpret_cast<int*>(empty + STAGES + 2)};
-  CombPipe comb{empty + STAGES + 4, empty + STAGES + 5, reinterpret_cast<int*>(empty + STAGES + 6)};
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int G = p.G;  // real q heads in the group (<= 8); the rest are zero padding
@@ -76,8 +75,6 @@ __global__ void __launch_bounds__((NW_ + 3) * 32)
     }
     mbar_init(red.full, NW);
     mbar_init(red.empty, 1);
-    mbar_init(comb.full, 1);
-    mbar_init(comb.empty, 1);
     fence_barrier_init();
   }
   if (warp == NW && lane == 0) {
@@ -117,12 +114,8 @@ __global__ void __launch_bounds__((NW_ + 3) * 32)
     }
     return;
   }
-  if (warp == NW + 2) {
-    combine_loop<T, D, GQ, TILE>(p, comb, G);
-    return;
-  }
   if (warp == NW + 1) {
-    epilogue_loop<T, D, GQ, NW, true, TILE>(p, red, comb, G, red_m, red_l, red_acc);
+    epilogue_loop<T, D, GQ, NW, true, TILE>(p, red, G, red_m, red_l, red_acc);
     return;
   }
 

@@ -41,14 +41,14 @@ struct SimtCfg {
   static constexpr int RED_FLOATS = NW * GQ * (D + 2);
   static constexpr int SMEM_BYTES = RING_BYTES + STAGES * SLOT_BYTES + RED_FLOATS * 4 +
                                     STAGES * 16 + STAGES * 8 + (2 * STAGES + 4) * 8 + 16 + 64;
-  static constexpr int THREADS = (NW + 3) * 32;  // + producer, epilogue, combine warps
+  static constexpr int THREADS = (NW + 2) * 32;  // + producer warp + epilogue warp
   static constexpr bool kLog2 = sizeof(T) < 4;
   static_assert(LPR >= 1 && LPR <= 32 && 32 % LPR == 0, "row must map onto a warp");
   static_assert(TPW % RPI == 0 && ITER >= 1, "warp slice must be whole instructions");
 };
 
 template <typename T, int D, int GQ, int NW, int TILE, int STAGES>
-__global__ void __launch_bounds__((NW + 3) * 32)
+__global__ void __launch_bounds__((NW + 2) * 32)
     decode_simt_kernel(const DecodeParams p) {
   using C = SimtCfg<T, D, GQ, NW, TILE, STAGES>;
   constexpr int VEC = C::VEC, LPR = C::LPR, RPI = C::RPI, TPW = C::TPW, ITER = C::ITER;
@@ -63,7 +63,6 @@ __global__ void __launch_bounds__((NW + 3) * 32)
   uint64_t* full = reinterpret_cast<uint64_t*>(meta_row + STAGES);
   uint64_t* empty = full + STAGES;
   RedPipe red{empty + STAGES, empty + STAGES + 1, reinterpret_cast<int*>(empty + STAGES + 2)};
-  CombPipe comb{empty + STAGES + 4, empty + STAGES + 5, reinterpret_cast<int*>(empty + STAGES + 6)};
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
@@ -73,8 +72,6 @@ __global__ void __launch_bounds__((NW + 3) * 32)
     }
     mbar_init(red.full, NW);
     mbar_init(red.empty, 1);
-    mbar_init(comb.full, 1);
-    mbar_init(comb.empty, 1);
     fence_barrier_init();
   }
   __syncthreads();
@@ -113,12 +110,8 @@ __global__ void __launch_bounds__((NW + 3) * 32)
     }
     return;
   }
-  if (warp == NW + 2) {
-    combine_loop<T, D, GQ, TILE>(p, comb, GQ);
-    return;
-  }
   if (warp == NW + 1) {
-    epilogue_loop<T, D, GQ, NW, C::kLog2, TILE>(p, red, comb, GQ, red_m, red_l, red_acc);
+    epilogue_loop<T, D, GQ, NW, C::kLog2, TILE>(p, red, GQ, red_m, red_l, red_acc);
     return;
   }
 
