@@ -73,7 +73,16 @@ def build(verbose: bool = False) -> dict:
               "-o", str(dropin), "-L", str(LIB), "-llamina_attn", "-Wl,-rpath,$ORIGIN"])
         if verbose:
             print("linked", dropin)
-    return {"core": str(core), "dropin": str(dropin)}
+    bench_src = ROOT / "benchmarks" / "bench_attention_b200.cpp"
+    bench_bin = ROOT / "benchmarks" / "bench_attention_b200"
+    if bench_src.exists() and (not bench_bin.exists() or bench_bin.stat().st_mtime < max(
+            _newest([bench_src, core, dropin]), _newest(list(INCLUDE.rglob("*.h*"))))):
+        _run([NVCC, "-std=c++20", "-O2", *ARCH, "-I", str(INCLUDE), str(bench_src), "-o",
+              str(bench_bin), "-L", str(LIB), "-ldisagg_attention", "-llamina_attn",
+              "-Xlinker", "-rpath,$ORIGIN/../paper_2405_01814_b200/lib"])
+        if verbose:
+            print("linked", bench_bin)
+    return {"core": str(core), "dropin": str(dropin), "bench": str(bench_bin)}
 
 
 if __name__ == "__main__":
