@@ -22,6 +22,7 @@ CFG = {
     "c3n8": dict(B=512, Hq=8, Hkv=1, L=4096, dtype=torch.bfloat16, paged=True),
     "c4": dict(B=32, Hq=64, Hkv=8, L=32768, dtype=torch.bfloat16, paged=True),
     "c4n8": dict(B=128, Hq=8, Hkv=1, L=32768, dtype=torch.bfloat16, paged=True),
+    "c5": dict(B=256, Hq=64, Hkv=8, L=16384, dtype=torch.bfloat16, paged=True, mixed=True),
 }
 
 
@@ -32,11 +33,19 @@ def main():
     ap.add_argument("--kernels", default="auto")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--P", type=int, default=64)
+    ap.add_argument("--no-order", action="store_true")
     a = ap.parse_args()
     c = CFG[a.cfg]
     B, Hq, Hkv, L, dt, D, P = c["B"], c["Hq"], c["Hkv"], c["L"], c["dtype"], 128, a.P
     esz = torch.tensor([], dtype=dt).element_size()
-    layer_bytes = 2 * B * Hkv * L * D * esz
+    import numpy as np
+
+    if c.get("mixed"):
+        r = np.random.default_rng(2024)
+        lens_np = np.exp(r.uniform(np.log(128), np.log(L), B)).astype(np.int32)
+    else:
+        lens_np = np.full(B, L, np.int32)
+    layer_bytes = 2 * int(lens_np.sum()) * Hkv * D * esz
     nbuf = max(2, math.ceil(2 * 2**30 / layer_bytes))
     g = torch.Generator(device="cuda").manual_seed(0)
     bufs = []
@@ -52,7 +61,8 @@ def main():
             pt = None
         bufs.append((kp, vp, pt))
     q = torch.empty((B, Hq, D), dtype=dt, device="cuda").uniform_(-1, 1, generator=g)
-    lens = torch.full((B,), L, dtype=torch.int32, device="cuda")
+    lens = torch.tensor(lens_np, dtype=torch.int32, device="cuda")
+    order = None if (a.no_order or not c.get("mixed")) else dec.longest_first(lens)
     out = torch.empty_like(q)
     for kern in a.kernels.split(","):
         for st in [int(x) for x in a.splits.split(",")]:
@@ -65,7 +75,7 @@ def main():
             def run(i):
                 kp, vp, pt = bufs[i % nbuf]
                 dec.decode(q, kp, vp, lens, page_table=pt, max_len=L, out=out, kernel=kern,
-                           split_tokens=st)
+                           split_tokens=st, request_order=order)
             for i in range(5):
                 run(i)
             torch.cuda.synchronize()
