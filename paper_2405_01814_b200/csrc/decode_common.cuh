@@ -171,21 +171,27 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
   const int G = static_cast<int>(gridDim.x);
   const int static_rounds = (p.flags & 4) ? 0 : max(0, p.n_items / G - 2);
   const int n_static = static_rounds * G;
-  // static rounds, next item prefetched
-  int idx = blockIdx.x;
-  if (idx < n_static) {
+  // static rounds, next item prefetched.  Round r deals items r*G .. r*G+G-1 in snake order
+  // (CTA c takes c on even rounds, G-1-c on odd ones), so with longest-first item order no CTA
+  // collects the longest item of every round.
+  const int c = blockIdx.x;
+  auto static_item = [&](int r) { return r * G + ((r & 1) ? G - 1 - c : c); };
+  int r = 0;
+  int idx = static_item(0);
+  if (static_rounds > 0) {
     Item it = make_item(p, idx, TILE);
     int64_t row = first_row(it);
-    while (idx < n_static) {
-      const int nidx = idx + G;
+    while (r < static_rounds) {
+      const int nidx = static_item(r + 1);
       Item nit{};
       int64_t nrow = 0;
       run_item(idx, it, row, 0, [&] {
-        if (nidx < n_static) {
+        if (r + 1 < static_rounds) {
           nit = make_item(p, nidx, TILE);
           nrow = first_row(nit);
         }
       });
+      ++r;
       idx = nidx;
       it = nit;
       row = nrow;
