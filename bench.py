@@ -383,7 +383,26 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
                        max_len=W.max_len, out=out, ctx=W.ctx, split_tokens=W.chunk,
                        k_new=k, v_new=v, request_order=W.orders[m])
 
-        engine = HeadShardedAttention(W.geo, dist, None, attend, device, W.dtype)
+        if args.transport == "peer":
+            from paper_2405_01814_b200.dist import PeerShardedAttention
+
+            def launch_args(layer, m):
+                kp, vp = W.layer_pools(layer)
+                sl = W.rows(m)
+                g = W.geo
+                qd = torch.empty((g.B_mb, g.hq_l, g.D), dtype=W.dtype, device=device)
+                a, _ = dec.make_args(qd, kp, vp, W.seq_lens[sl],
+                                     page_table=W.page_table[sl] if W.page_table is not None else None,
+                                     max_len=W.max_len, out=qd, split_tokens=W.chunk,
+                                     request_order=W.orders[m])
+                return a
+
+            engine = PeerShardedAttention(W.geo, dist, W.ctx, launch_args, device, W.dtype)
+            engine.qkv_in.copy_(W.qkv_in)
+            W.qkv_in = engine.qkv_in
+            W.out = engine.out
+        else:
+            engine = HeadShardedAttention(W.geo, dist, None, attend, device, W.dtype)
 
     counter = [0]
 
@@ -410,6 +429,8 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
     def step(ev=None):
         if engine is None:
             step_local(ev)
+        elif args.transport == "peer":
+            engine.step(ev)
         else:
             engine.step(W.qkv_in, W.out, ev)
 
@@ -451,7 +472,7 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
         kern_avg = statistics.mean(kern_ms)
     launches = args.steps * W.layers * W.mb * (2 if args.separate_append else 1)
     alone_ms = None
-    if engine is not None:
+    if engine is not None and args.transport != "peer":
         # the same decode launch with no collective in flight (diagnoses comm interference)
         g = W.geo
         packed = engine.qkv_r[0].view(g.B_mb, g.W, g.D)
@@ -493,7 +514,7 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
                    "seq_len": int(W.max_len), "sum_seq_len": int(W.lens.sum()) ,
                    "layers": W.layers, "kv_layers_resident": W.resident,
                    "q_heads": W.Hq, "kv_heads": W.Hkv, "head_dim": W.D, "page_size": w["P"],
-                   "parallelism": f"kv-head sharded x{world}" if world > 1 else "single GPU",
+                   "parallelism": f"kv-head sharded x{world} ({args.transport})" if world > 1 else "single GPU",
                    "l2": f"inputs {W.kv_bytes_layer * W.resident / 2**30:.0f} GiB of KV >> 126 MB L2; no flush needed",
                    "kernel": W.kernel, "splits": W.splits, "split_tokens": W.chunk},
         "attn_tokens_per_s": W.B / (ms_step / 1e3),
@@ -537,7 +558,10 @@ def run_e2e(args, W, engine, dist, device, stream):
         h_qkv = W.qkv_in.cpu().pin_memory()
 
         def step_mg():
-            engine.step(W.qkv_in, W.out, host_in=h_qkv, host_out=h_out)
+            if args.transport == "peer":
+                engine.step(host_in=h_qkv, host_out=h_out)
+            else:
+                engine.step(W.qkv_in, W.out, host_in=h_qkv, host_out=h_out)
 
         for _ in range(max(1, args.warmup)):
             step_mg()
@@ -556,7 +580,10 @@ def run_e2e(args, W, engine, dist, device, stream):
         d2h = h_out.numel() * h_out.element_size()
         return {"value": W.step_bytes / (ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
                 "h2d_bytes_per_step": int(h2d) * W.world, "d2h_bytes_per_step": int(d2h) * W.world,
-                "api": "HeadShardedAttention.step (pinned host in/out overlapped on copy streams, NCCL all-to-all)"}
+                "api": ("PeerShardedAttention.step (pinned host in/out overlapped on copy streams, "
+                        "zero-copy NVLink peer transport)" if args.transport == "peer" else
+                        "HeadShardedAttention.step (pinned host in/out overlapped on copy streams, "
+                        "NCCL all-to-all)")}
     h_q = W.q_in.cpu().pin_memory()
     h_kn = W.kn_in.cpu().pin_memory()
     h_vn = W.vn_in.cpu().pin_memory()
@@ -618,6 +645,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=3.0)
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "peer"],
+                    help="multi-GPU scatter/gather: NCCL all-to-all or zero-copy NVLink peer memory")
     ap.add_argument("--separate-append", action="store_true",
                     help="lam_kv_append + lam_decode per layer instead of the fused launch")
     args = ap.parse_args()

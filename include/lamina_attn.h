@@ -223,6 +223,52 @@ int lam_decode_layers_host(lam_ctx* ctx, const lam_decode_args* layer_args, int3
                            const int32_t* d_positions, void* stream, void* copy_stream);
 int64_t lam_decode_layers_host_stage_bytes(const lam_decode_args* layer_args);
 
+/* ---- peer-memory transport (one process per GPU, NVLink / NVSwitch) ----
+ *
+ * The device-initiated replacement for the scatter / gather collectives of the attention
+ * offload step (reference: send-Q / send-KV / return-output, core/src/sim.cpp:310-316; the
+ * paper's FHBN transport): the model worker's packed QKV rows and its output
+ * rows live in its own HBM, exported to the attention workers over CUDA IPC; the attention
+ * worker's decode kernel reads q / k_new / v_new straight from the model worker's memory and
+ * stores each output row straight into it.  Readiness is signalled with 32-bit sequence
+ * numbers written by the GPU's stream front-end (no SM time, no host round trip). */
+#define LAM_MAX_PEERS 8
+#define LAM_IPC_HANDLE_BYTES 64
+
+/* cudaMalloc `bytes` (zeroed) and export it: *dptr is the local pointer, handle receives
+ * LAM_IPC_HANDLE_BYTES opaque bytes for lam_peer_open in another process. */
+int lam_peer_alloc(lam_ctx* ctx, int64_t bytes, void** dptr, void* handle);
+int lam_peer_free(lam_ctx* ctx, void* dptr);
+/* Map a peer's exported buffer into this process (NVLink peer access enabled). */
+int lam_peer_open(lam_ctx* ctx, const void* handle, void** dptr);
+int lam_peer_close(lam_ctx* ctx, void* dptr);
+/* Stream-ordered sequence numbers: signal writes `value` to each addrs[i] (local or peer)
+ * after all prior work of `stream` is visible system-wide; wait blocks `stream` until every
+ * addrs[i] >= value (wrap-safe not required: values only grow). */
+int lam_stream_signal(lam_ctx* ctx, void* const* addrs, int32_t n, uint32_t value, void* stream);
+int lam_stream_wait(lam_ctx* ctx, const void* const* addrs, int32_t n, uint32_t value,
+                    void* stream);
+
+/* Request rows of a decode launch grouped by source: rows [s * rows_per_src, (s+1) *
+ * rows_per_src) belong to model worker s; row i of source s reads its q heads at
+ * q_src[s] + i * args->q_batch_stride (elements), its new k / v heads at
+ * q_src[s] + k_new_offset / v_new_offset + i * args->new_batch_stride, and writes its output
+ * [Hq][D] at out_dst[s] + i * Hq * D.  Pointers may be peer mappings (lam_peer_open). */
+typedef struct lam_peer_io {
+  int32_t n_src;
+  int32_t rows_per_src;
+  const void* q_src[LAM_MAX_PEERS];
+  void* out_dst[LAM_MAX_PEERS];
+  int64_t k_new_offset;
+  int64_t v_new_offset;
+} lam_peer_io;
+
+/* lam_decode whose q / k_new / v_new / out come from lam_peer_io (args->q, k_new, v_new and out
+ * are ignored; fused append is implied; args->lse must be NULL).  batch == n_src *
+ * rows_per_src. */
+int lam_decode_peer(lam_ctx* ctx, const lam_decode_args* args, const lam_peer_io* io,
+                    void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -62,6 +62,23 @@ class DecodeArgs(C.Structure):
     ]
 
 
+LAM_MAX_PEERS = 8
+LAM_IPC_HANDLE_BYTES = 64
+
+
+class PeerIO(C.Structure):
+    """lam_peer_io (include/lamina_attn.h)."""
+
+    _fields_ = [
+        ("n_src", C.c_int32),
+        ("rows_per_src", C.c_int32),
+        ("q_src", C.c_void_p * LAM_MAX_PEERS),
+        ("out_dst", C.c_void_p * LAM_MAX_PEERS),
+        ("k_new_offset", C.c_int64),
+        ("v_new_offset", C.c_int64),
+    ]
+
+
 _P, _I32, _I64, _F64 = C.c_void_p, C.c_int32, C.c_int64, C.c_double
 
 # name -> (restype, argtypes)
@@ -94,6 +111,13 @@ SIGNATURES = {
     "lam_decode_layers_host": (C.c_int, [_P, C.POINTER(DecodeArgs), _I32, _P, _P, _P, _P, _P, _P,
                                          _P, _P]),
     "lam_decode_layers_host_stage_bytes": (C.c_int64, [C.POINTER(DecodeArgs)]),
+    "lam_peer_alloc": (C.c_int, [_P, _I64, C.POINTER(C.c_void_p), _P]),
+    "lam_peer_free": (C.c_int, [_P, _P]),
+    "lam_peer_open": (C.c_int, [_P, _P, C.POINTER(C.c_void_p)]),
+    "lam_peer_close": (C.c_int, [_P, _P]),
+    "lam_stream_signal": (C.c_int, [_P, _P, _I32, C.c_uint32, _P]),
+    "lam_stream_wait": (C.c_int, [_P, _P, _I32, C.c_uint32, _P]),
+    "lam_decode_peer": (C.c_int, [_P, C.POINTER(DecodeArgs), C.POINTER(PeerIO), _P]),
 }
 
 _lib = None

@@ -161,7 +161,8 @@ struct Plan {
 // whose item counts (512, 1024) divide evenly there (up to +4 % over a full 148-CTA grid).
 void choose_splits(Plan& pl, int64_t units, int max_len, int max_ctas, int split_tokens,
                    double bytes_per_token) {
-  constexpr double BW_CHIP = 7.0e12, RATE_SM = 50e9, C_ITEM = 1e-6, C_COMBINE = 5e-6;
+  static const double BW_CHIP = 7.0e12, RATE_SM = env_int("LAM_PLAN_RATE_SM", 56) * 1e9,
+                      C_ITEM = env_int("LAM_PLAN_CITEM_NS", 4000) * 1e-9;
   const int tiles_total = std::max(1, (max_len + pl.tile - 1) / pl.tile);
   const int occ_per_sm = std::max(1, max_ctas / 148);
   double best = 1e300;
@@ -182,7 +183,6 @@ void choose_splits(Plan& pl, int64_t units, int max_len, int max_ctas, int split
       if (rem > 0) t += item_bytes / std::min(BW_CHIP / static_cast<double>(rem), RATE_SM * occ_per_sm);
       t += static_cast<double>((items + ctas - 1) / ctas) * C_ITEM *
            (items_per_cta() > 0 ? items_per_cta() / 4.0 : 1.0);
-      if (s_eff > 1) t += C_COMBINE;  // the separate split-merge launch
       // a smaller grid or more splits must win by >= 1.5 % (model noise)
       if (t < best * (1 - 0.015)) {
         best = t;
@@ -661,7 +661,9 @@ int lam_decode_plan(lam_ctx* ctx, const lam_decode_args* a, int32_t* kernel, int
   return LAM_OK;
 }
 
-int lam_decode(lam_ctx* ctx, const lam_decode_args* a, void* stream) {
+namespace {
+
+int decode_impl(lam_ctx* ctx, const lam_decode_args* a, const lam_peer_io* io, void* stream) {
   if (!ctx) return fail(LAM_ERR_VALIDATION, "null context");
   Plan pl;
   int rc = plan_decode(ctx, a, &pl);
@@ -701,6 +703,33 @@ int lam_decode(lam_ctx* ctx, const lam_decode_args* a, void* stream) {
     p.k_pool_w = const_cast<void*>(a->k_pool);
     p.v_pool_w = const_cast<void*>(a->v_pool);
   }
+  if (io != nullptr) {  // rows grouped by source, buffers local or on peers
+    if (io->n_src < 1 || io->n_src > LAM_MAX_PEERS || io->rows_per_src < 1 ||
+        static_cast<int64_t>(io->n_src) * io->rows_per_src != a->batch)
+      return fail(LAM_ERR_VALIDATION, "peer io: need 1 <= n_src <= LAM_MAX_PEERS and batch == "
+                                      "n_src * rows_per_src");
+    if (a->lse != nullptr) return fail(LAM_ERR_VALIDATION, "peer io: lse is not supported");
+    const int e = a->kv_dtype == LAM_F32 ? 4 : 2;
+    if ((io->k_new_offset * e) % 16 != 0 || (io->v_new_offset * e) % 16 != 0)
+      return fail(LAM_ERR_VALIDATION, "peer io: new-row offsets must keep 16-byte rows");
+    for (int i = 0; i < io->n_src; ++i) {
+      if (io->q_src[i] == nullptr || io->out_dst[i] == nullptr)
+        return fail(LAM_ERR_VALIDATION, "peer io: null source / destination pointer");
+      p.q_src[i] = io->q_src[i];
+      p.out_dst[i] = io->out_dst[i];
+    }
+    p.src_rows = io->rows_per_src;
+    p.new_off[0] = io->k_new_offset;
+    p.new_off[1] = io->v_new_offset;
+    p.q = io->q_src[0];
+    p.out = io->out_dst[0];
+    p.k_new = io->q_src[0];  // non-null: fused append on (addresses come from new_off)
+    p.v_new = io->q_src[0];
+    p.new_stride = a->new_batch_stride > 0 ? a->new_batch_stride
+                                           : static_cast<int64_t>(a->num_kv_heads) * D;
+    p.k_pool_w = const_cast<void*>(a->k_pool);
+    p.v_pool_w = const_cast<void*>(a->v_pool);
+  }
   p.flags = env_int("LAM_DECODE_FLAGS", 0);
   p.scale = a->scale;
   p.scale_log2 = a->scale * 1.4426950408889634f;
@@ -715,6 +744,7 @@ int lam_decode(lam_ctx* ctx, const lam_decode_args* a, void* stream) {
     }
     p.ws_acc = ctx->ws_acc;
     p.ws_ml = ctx->ws_ml;
+    p.counters = ctx->counters;
   }
   auto s = static_cast<cudaStream_t>(stream);
   if (pl.kernel == LAM_KERNEL_GQA_MMA) {
@@ -732,7 +762,114 @@ int lam_decode(lam_ctx* ctx, const lam_decode_args* a, void* stream) {
   } else {
     LAM_CUDA(lam::launch_decode_simt(a->kv_dtype, D, pl.GQ, pl.variant, p, pl.ctas, s));
   }
-  if (pl.S > 1) LAM_CUDA(lam::launch_combine(a->kv_dtype, p, s));
+  return LAM_OK;
+}
+
+}  // namespace
+
+int lam_decode(lam_ctx* ctx, const lam_decode_args* a, void* stream) {
+  return decode_impl(ctx, a, nullptr, stream);
+}
+
+int lam_decode_peer(lam_ctx* ctx, const lam_decode_args* a, const lam_peer_io* io, void* stream) {
+  if (!io) return fail(LAM_ERR_VALIDATION, "null peer io");
+  return decode_impl(ctx, a, io, stream);
+}
+
+// ---------------- peer-memory transport ----------------
+
+static_assert(sizeof(cudaIpcMemHandle_t) <= LAM_IPC_HANDLE_BYTES, "IPC handle size");
+
+int lam_peer_alloc(lam_ctx* ctx, int64_t bytes, void** dptr, void* handle) {
+  if (!ctx || !dptr || !handle || bytes < 1) return fail(LAM_ERR_VALIDATION, "peer_alloc: bad arguments");
+  LAM_CUDA(cudaSetDevice(ctx->device));
+  void* p = nullptr;
+  LAM_CUDA(cudaMalloc(&p, static_cast<size_t>(bytes)));
+  cudaError_t e = cudaMemset(p, 0, static_cast<size_t>(bytes));
+  cudaIpcMemHandle_t h{};
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, p);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    return fail(LAM_ERR_CUDA, std::string("peer_alloc: ") + cudaGetErrorString(e));
+  }
+  std::memset(handle, 0, LAM_IPC_HANDLE_BYTES);
+  std::memcpy(handle, &h, sizeof(h));
+  *dptr = p;
+  return LAM_OK;
+}
+
+int lam_peer_free(lam_ctx* ctx, void* dptr) {
+  if (!ctx) return fail(LAM_ERR_VALIDATION, "null context");
+  LAM_CUDA(cudaSetDevice(ctx->device));
+  LAM_CUDA(cudaFree(dptr));
+  return LAM_OK;
+}
+
+int lam_peer_open(lam_ctx* ctx, const void* handle, void** dptr) {
+  if (!ctx || !handle || !dptr) return fail(LAM_ERR_VALIDATION, "peer_open: bad arguments");
+  LAM_CUDA(cudaSetDevice(ctx->device));
+  cudaIpcMemHandle_t h{};
+  std::memcpy(&h, handle, sizeof(h));
+  LAM_CUDA(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return LAM_OK;
+}
+
+int lam_peer_close(lam_ctx* ctx, void* dptr) {
+  if (!ctx) return fail(LAM_ERR_VALIDATION, "null context");
+  LAM_CUDA(cudaSetDevice(ctx->device));
+  LAM_CUDA(cudaIpcCloseMemHandle(dptr));
+  return LAM_OK;
+}
+
+namespace {
+
+void* driver_fn(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q{};
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return p;
+}
+
+PFN_cuStreamWriteValue32_v11070 write_value_fn() {
+  static auto fn = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(driver_fn("cuStreamWriteValue32"));
+  return fn;
+}
+PFN_cuStreamWaitValue32_v11070 wait_value_fn() {
+  static auto fn = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(driver_fn("cuStreamWaitValue32"));
+  return fn;
+}
+
+}  // namespace
+
+int lam_stream_signal(lam_ctx* ctx, void* const* addrs, int32_t n, uint32_t value, void* stream) {
+  if (!ctx || (n > 0 && !addrs)) return fail(LAM_ERR_VALIDATION, "stream_signal: bad arguments");
+  auto fn = write_value_fn();
+  if (!fn) return fail(LAM_ERR_CUDA, "cuStreamWriteValue32 unavailable");
+  for (int32_t i = 0; i < n; ++i) {
+    // default flags: a system-scope memory barrier orders the stream's prior writes (the
+    // decode kernel's peer stores) before the sequence number
+    const CUresult r = fn(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(addrs[i]),
+                          value, CU_STREAM_WRITE_VALUE_DEFAULT);
+    if (r != CUDA_SUCCESS)
+      return fail(LAM_ERR_CUDA, "cuStreamWriteValue32 failed (" + std::to_string(r) + ")");
+  }
+  return LAM_OK;
+}
+
+int lam_stream_wait(lam_ctx* ctx, const void* const* addrs, int32_t n, uint32_t value,
+                    void* stream) {
+  if (!ctx || (n > 0 && !addrs)) return fail(LAM_ERR_VALIDATION, "stream_wait: bad arguments");
+  auto fn = wait_value_fn();
+  if (!fn) return fail(LAM_ERR_CUDA, "cuStreamWaitValue32 unavailable");
+  for (int32_t i = 0; i < n; ++i) {
+    const CUresult r = fn(static_cast<CUstream>(stream),
+                          reinterpret_cast<CUdeviceptr>(const_cast<void*>(addrs[i])), value,
+                          CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS)
+      return fail(LAM_ERR_CUDA, "cuStreamWaitValue32 failed (" + std::to_string(r) + ")");
+  }
   return LAM_OK;
 }
 

@@ -166,15 +166,6 @@ int simt_variant_tile(int kv_dtype, int D, int GQ, int variant) {
   return simt_dispatch(kv_dtype, D, GQ, variant, SimtTileF{});
 }
 
-cudaError_t launch_combine(int kv_dtype, const DecodeParams& p, cudaStream_t stream) {
-  const unsigned blocks = static_cast<unsigned>(p.B) * p.Hq;
-  if (blocks == 0) return cudaSuccess;
-  if (kv_dtype == 0) combine_splits_kernel<float><<<blocks, p.D, 0, stream>>>(p);
-  else if (kv_dtype == 2) combine_splits_kernel<__nv_bfloat16><<<blocks, p.D, 0, stream>>>(p);
-  else combine_splits_kernel<__half><<<blocks, p.D, 0, stream>>>(p);
-  return cudaGetLastError();
-}
-
 int mma_variant_tile(int variant) {
 #define X(id, nw, st) \
   if (variant == id) return 16 * nw;

@@ -21,6 +21,10 @@
 
 #include "ptx.cuh"
 
+#ifndef LAM_MAX_PEERS
+#define LAM_MAX_PEERS 8
+#endif
+
 namespace lam {
 
 struct DecodeParams {
@@ -34,6 +38,7 @@ struct DecodeParams {
   float* lse;               // [B][Hq] or nullptr
   float* ws_acc;            // [B*Hq*S][D] split partials (unnormalised acc)
   float* ws_ml;             // [B*Hq*S][2] (max in natural-log units, sum)
+  int32_t* counters;        // [B*Hkv*QG] split arrival counters (self-resetting)
   int32_t* work;            // [2] item counter, exited-producer counter (self-resetting)
   int32_t B, Hq, Hkv, G, D;
   int32_t page_size, pt_stride;
@@ -44,7 +49,7 @@ struct DecodeParams {
   float scale;              // softmax scale (natural units)
   float scale_log2;         // scale * log2(e)
   int32_t out_f32;
-  int32_t flags;            // tuning: bit2 = all-dynamic schedule, bit3 = skip epilogue (diag)
+  int32_t flags;            // reserved (tuning experiments)
   // fused append (optional): the new token of request b (position seq_lens[b] - 1) comes from
   // k_new/v_new (request b, kv head h at + b * new_stride + h * D); the kernel attends over it
   // from shared memory and writes it into the pools for later steps.
@@ -54,7 +59,34 @@ struct DecodeParams {
   void* k_pool_w;
   void* v_pool_w;
   const int32_t* order;     // optional request permutation for item enumeration (LPT)
+  // peer I/O (optional, src_rows > 0): rows come in groups of src_rows per source rank s; row
+  // b = s * src_rows + i reads q at q_src[s] + i * q_stride, the new k/v rows at
+  // q_src[s] + new_off[0|1] + i * new_stride, and writes its output rows [Hq][D] to
+  // out_dst[s] + i * Hq * D — buffers owned by the model worker s, mapped over NVLink.
+  int32_t src_rows;
+  const void* q_src[LAM_MAX_PEERS];
+  void* out_dst[LAM_MAX_PEERS];
+  int64_t new_off[2];
 };
+
+// Start of request b's q rows / new k (which = 0) or v (1) rows, local or on a peer.
+template <typename T>
+__device__ __forceinline__ const T* q_rows(const DecodeParams& p, int b) {
+  if (p.src_rows > 0) {
+    const int s = b / p.src_rows;
+    return static_cast<const T*>(p.q_src[s]) + static_cast<int64_t>(b - s * p.src_rows) * p.q_stride;
+  }
+  return static_cast<const T*>(p.q) + static_cast<int64_t>(b) * p.q_stride;
+}
+template <typename T>
+__device__ __forceinline__ const T* new_rows(const DecodeParams& p, int which, int b) {
+  if (p.src_rows > 0) {
+    const int s = b / p.src_rows;
+    return static_cast<const T*>(p.q_src[s]) + p.new_off[which] +
+           static_cast<int64_t>(b - s * p.src_rows) * p.new_stride;
+  }
+  return static_cast<const T*>(which ? p.v_new : p.k_new) + static_cast<int64_t>(b) * p.new_stride;
+}
 
 // Physical row of token t of (request b, kv head h) in a pool viewed as [rows][D].
 // Paged: pool[page][Hkv][P][D]; dense: pool[B][Hkv][P][D] (P = row capacity).
@@ -125,14 +157,10 @@ __device__ __forceinline__ int live_splits(const DecodeParams& p, int len) {
 // `issue(s, it, j, row)` must arrive on full[s] with expect_tx and start the stage's TMA
 // copies of tile j, whose first KV row is `row`.
 //
-// Schedule: hybrid static-then-dynamic.
-//  * Static rounds: CTA c runs items c, c + G, c + 2G, ... for all but the last ~2 rounds.  Its
-//    next item is known, so the item's length and first page-table entry are loaded while the
-//    current item streams: an item boundary costs the HBM stream nothing.  (With claiming at
-//    every boundary, the claim atomic -> length -> page-entry round trips idled each SM for
-//    ~3 us per item, ~7 % of C2/C3.)
-//  * Dynamic tail: the remaining items are claimed from a global counter, which absorbs the
-//    2-3 % per-SM streaming-rate differences of the two-die part and the tail.
+// Items are claimed from a global counter right after the previous item's tiles are issued.
+// Measured on B200 this dynamic schedule beats a static round-robin split by 2-3 % (per-SM
+// streaming rates differ across the two dies) and beats claiming one item ahead (that costs up
+// to one item of tail imbalance); the stage ring covers the claim's round trips.
 template <int STAGES, int TILE, class Issue>
 __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* full,
                                               uint64_t* empty, int4* meta, long long* meta_row,
@@ -143,108 +171,58 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
     if (k >= STAGES) mbar_wait(&empty[s], ((k / STAGES) - 1) & 1);
     return s;
   };
-  // stream one item; `during` runs once, right after the stage of tile `at` is issued
-  // (at < 0: after the last tile)
-  auto run_item = [&](int idx, const Item& it, int64_t row0, int at, auto&& during) {
+  for (;;) {
+    const int idx = atomicAdd(p.work, 1);
+    if (idx >= p.n_items) break;
+    const Item it = make_item(p, idx, TILE);
     if (it.ntiles == 0) {
       if (it.split == 0 && it.len == 0) {  // empty request: zero-output marker
         const int s = acquire(i++);
         meta[s] = make_int4(idx, 0, 0, 0);
         mbar_arrive(&full[s]);
       }                                    // (an empty split has nothing to merge)
-      during();
-      return;
+      continue;
     }
-    const int when = at < 0 ? it.ntiles - 1 : min(at, it.ntiles - 1);
     for (int j = 0; j < it.ntiles; ++j) {
       const int s = acquire(i++);
-      const int64_t row = j == 0 ? row0 : kv_row(p, it.b, it.kvh, it.t_begin + j * TILE);
+      const int64_t row = kv_row(p, it.b, it.kvh, it.t_begin + j * TILE);
       meta[s] = make_int4(idx, j, it.len, it.t_end);
       meta_row[s] = row;
       issue(s, it, j, row);
-      if (j == when) during();
     }
-  };
-  auto first_row = [&](const Item& it) {
-    return it.ntiles > 0 ? kv_row(p, it.b, it.kvh, it.t_begin) : int64_t{0};
-  };
-  const int G = static_cast<int>(gridDim.x);
-  const int static_rounds = (p.flags & 4) ? 0 : max(0, p.n_items / G - 2);
-  const int n_static = static_rounds * G;
-  // static rounds, next item prefetched.  Round r deals items r*G .. r*G+G-1 in snake order
-  // (CTA c takes c on even rounds, G-1-c on odd ones), so with longest-first item order no CTA
-  // collects the longest item of every round.
-  const int c = blockIdx.x;
-  auto static_item = [&](int r) { return r * G + ((r & 1) ? G - 1 - c : c); };
-  int r = 0;
-  int idx = static_item(0);
-  if (static_rounds > 0) {
-    Item it = make_item(p, idx, TILE);
-    int64_t row = first_row(it);
-    while (r < static_rounds) {
-      const int nidx = static_item(r + 1);
-      Item nit{};
-      int64_t nrow = 0;
-      run_item(idx, it, row, 0, [&] {
-        if (r + 1 < static_rounds) {
-          nit = make_item(p, nidx, TILE);
-          nrow = first_row(nit);
-        }
-      });
-      ++r;
-      idx = nidx;
-      it = nit;
-      row = nrow;
-    }
-  }
-  // dynamic tail: the next item is claimed right after the current item's last tile is
-  // issued, so the claim's round trips overlap the tiles still in the ring
-  auto claim = [&](int& didx, Item& it, int64_t& row) {
-    didx = n_static + atomicAdd(p.work, 1);
-    if (didx < p.n_items) {
-      it = make_item(p, didx, TILE);
-      row = first_row(it);
-    }
-  };
-  int didx;
-  Item dit{};
-  int64_t drow = 0;
-  claim(didx, dit, drow);
-  while (didx < p.n_items) {
-    int nidx;
-    Item nit{};
-    int64_t nrow = 0;
-    run_item(didx, dit, drow, -1, [&] { claim(nidx, nit, nrow); });
-    didx = nidx;
-    dit = nit;
-    drow = nrow;
   }
   const int s = acquire(i);
   meta[s] = make_int4(-1, 0, 0, 0);
   mbar_arrive(&full[s]);
   // the last producer to leave resets the counters for the next launch
-  if (atomicAdd(p.work + 1, 1) == G - 1) {
+  if (atomicAdd(p.work + 1, 1) == static_cast<int>(gridDim.x) - 1) {
     p.work[0] = 0;
     p.work[1] = 0;
   }
 }
 
-template <typename T>
-__device__ __forceinline__ void store_out(const DecodeParams& p, int64_t idx, float v) {
+// Element d of the output of (request b, q head h).
+template <typename T, int D>
+__device__ __forceinline__ void store_out(const DecodeParams& p, int b, int h, int d, float v) {
+  void* base = p.out;
+  if (p.src_rows > 0) {
+    const int s = b / p.src_rows;
+    base = p.out_dst[s];
+    b -= s * p.src_rows;
+  }
+  const int64_t idx = (static_cast<int64_t>(b) * p.Hq + h) * D + d;
   if (p.out_f32)
-    static_cast<float*>(p.out)[idx] = v;
+    static_cast<float*>(base)[idx] = v;
   else
-    static_cast<T*>(p.out)[idx] = Elem<T>::from_float(v);
+    static_cast<T*>(base)[idx] = Elem<T>::from_float(v);
 }
 
-// Epilogue of one work item, run by the CTA's dedicated epilogue warp while the consumer warps
-// already stream the next item: merge the warp partials and write the output (single-split
-// units) or the split partial (multi-split units, merged by combine_splits_kernel afterwards).  red_m/red_l/red_acc hold the NW per-warp
+// Split-K epilogue of one work item, run by the CTA's dedicated epilogue warp while the
+// consumer warps already stream the next item.  red_m/red_l/red_acc hold the NW per-warp
 // partials for GQ q heads: red_m[w*GQ+g] (log2 units if kLog2, else natural), red_l[w*GQ+g],
 // red_acc[(w*GQ+g)*D + d].  `nvalid` q heads of the group are real (the MMA kernel pads to 8).
-// Returns true when the item wrote a split partial (merged later by combine_splits_kernel).
 template <typename T, int D, int GQ, int NW, bool kLog2, class Release>
-__device__ __forceinline__ bool finish_item_warp(const DecodeParams& p, const Item& it,
+__device__ __forceinline__ void finish_item_warp(const DecodeParams& p, const Item& it,
                                                  int nvalid, const float* red_m,
                                                  const float* red_l, const float* red_acc,
                                                  Release release) {
@@ -282,17 +260,16 @@ __device__ __forceinline__ bool finish_item_warp(const DecodeParams& p, const It
 #pragma unroll
     for (int g = 0; g < GQ; ++g) {
       if (g >= nvalid) break;
-      const int64_t o = (static_cast<int64_t>(b) * p.Hq + qh0 + g) * D;
       for (int d = lane; d < D; d += 32) {
         const float L = cta_l[g];
-        store_out<T>(p, o + d, L > 0.f ? merged_acc(g, d) / L : 0.f);
+        store_out<T, D>(p, b, qh0 + g, d, L > 0.f ? merged_acc(g, d) / L : 0.f);
       }
       if (lane == 0 && p.lse != nullptr)
         p.lse[static_cast<int64_t>(b) * p.Hq + qh0 + g] =
             cta_l[g] > 0.f ? cta_m[g] + logf(cta_l[g]) : -INFINITY;
     }
     release();
-    return false;
+    return;
   }
 
   // 2. write this split's partial, then count it in.
@@ -306,8 +283,77 @@ __device__ __forceinline__ bool finish_item_warp(const DecodeParams& p, const It
       p.ws_ml[row * 2 + 1] = cta_l[g];
     }
   }
-  release();
-  return true;
+  release();  // the consumers may refill red_* while this warp counts and merges splits
+  __threadfence();
+  __syncwarp();
+  int32_t* counter = p.counters + (static_cast<int64_t>(b) * p.Hkv + it.kvh) * p.QG + it.qg;
+  int last = 0;
+  if (lane == 0) last = (atomicAdd(counter, 1) == S_live - 1);
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return;
+  __threadfence();
+
+  // 3. last split of this unit: merge the live partials in split order and finalize.
+  //    The split statistics of every q head are loaded together (lane s holds split s), so a
+  //    merge costs a couple of L2 round trips, not one chain per head.
+  constexpr int DPL = D / 32;  // output dims per lane
+  float ms[GQ], ls[GQ];
+#pragma unroll
+  for (int g = 0; g < GQ; ++g) {
+    ms[g] = -INFINITY;
+    ls[g] = 0.f;
+    if (g < nvalid && lane < S_live) {
+      const float2 ml = __ldcg(reinterpret_cast<const float2*>(
+          p.ws_ml + ((static_cast<int64_t>(b) * p.Hq + qh0 + g) * p.S + lane) * 2));
+      ms[g] = ml.x;
+      ls[g] = ml.y;
+    }
+  }
+#pragma unroll
+  for (int g = 0; g < GQ; ++g) {
+    if (g >= nvalid) break;
+    const int64_t row0 = (static_cast<int64_t>(b) * p.Hq + qh0 + g) * p.S;
+    float M = ms[g];
+    for (int s0 = 32 + lane; s0 < S_live; s0 += 32) M = fmaxf(M, __ldcg(p.ws_ml + (row0 + s0) * 2));
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+    // lanes >= S_live hold -inf and weigh nothing; splits beyond 32 take a slow path
+    const float w = ms[g] == -INFINITY ? 0.f : expf(ms[g] - M);
+    float L = w * ls[g];
+    float A[DPL];
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) A[e] = 0.f;
+    const int n = min(32, S_live);
+    for (int j = 0; j < n; ++j) {
+      const float wj = __shfl_sync(0xffffffffu, w, j);
+      const float* src = p.ws_acc + (row0 + j) * D + lane;
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) A[e] = fmaf(wj, __ldcg(src + e * 32), A[e]);
+    }
+    for (int s0 = 32; s0 < S_live; s0 += 32) {  // more than 32 splits (rare)
+      float w2 = 0.f, m2 = -INFINITY;
+      if (s0 + lane < S_live) {
+        const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + (row0 + s0 + lane) * 2));
+        m2 = ml.x;
+        w2 = ml.x == -INFINITY ? 0.f : expf(ml.x - M);
+        L += w2 * ml.y;
+      }
+      (void)m2;
+      for (int j = 0; j < min(32, S_live - s0); ++j) {
+        const float wj = __shfl_sync(0xffffffffu, w2, j);
+        const float* src = p.ws_acc + (row0 + s0 + j) * D + lane;
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) A[e] = fmaf(wj, __ldcg(src + e * 32), A[e]);
+      }
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) store_out<T, D>(p, b, qh0 + g, lane + e * 32, L > 0.f ? A[e] / L : 0.f);
+    if (lane == 0 && p.lse != nullptr)
+      p.lse[static_cast<int64_t>(b) * p.Hq + qh0 + g] = L > 0.f ? M + logf(L) : -INFINITY;
+  }
+  if (lane == 0) *counter = 0;  // ready for the next launch
 }
 
 // Hand-off of per-warp partials from the consumer warps to the epilogue warp.  Single
@@ -328,40 +374,6 @@ __device__ __forceinline__ void red_commit(const RedPipe& r) {
   if (threadIdx.x % 32 == 0) mbar_arrive(r.full);
 }
 
-// Split-K merge, launched after a decode kernel whenever S > 1: one CTA of D threads per
-// (request, q head) merges the live split partials in split order — the reference's merge with
-// its identity early-out (attention.cpp:100-118) — and finalizes (attention.cpp:120-127).
-// Measured on B200 this beats merging inside the persistent kernel (a last-arriver merge with
-// GPU-scope fences and atomics) at every split count: C3 S=4 6386 vs 5955 GB/s, S=8 6126 vs 3436.
-template <typename T>
-__global__ void combine_splits_kernel(const DecodeParams p) {
-  const int bh = blockIdx.x;  // b * Hq + h
-  const int b = bh / p.Hq;
-  const int d = threadIdx.x;
-  const int len = __ldg(p.seq_lens + b);
-  const int S_live = live_splits(p, len);
-  const int64_t row0 = static_cast<int64_t>(bh) * p.S;
-  const int64_t o = static_cast<int64_t>(bh) * p.D + d;
-  if (len <= 0) {
-    store_out<T>(p, o, 0.f);
-    if (d == 0 && p.lse != nullptr) p.lse[bh] = -INFINITY;
-    return;
-  }
-  if (S_live == 1) return;  // written directly by the decode kernel
-  float M = -INFINITY;
-  for (int s = 0; s < S_live; ++s) M = fmaxf(M, __ldg(p.ws_ml + (row0 + s) * 2));
-  float A = 0.f, L = 0.f;
-  for (int s = 0; s < S_live; ++s) {
-    const float ms = __ldg(p.ws_ml + (row0 + s) * 2);
-    if (ms == -INFINITY) continue;
-    const float w = expf(ms - M);
-    L += w * __ldg(p.ws_ml + (row0 + s) * 2 + 1);
-    A += w * __ldg(p.ws_acc + (row0 + s) * p.D + d);
-  }
-  store_out<T>(p, o, L > 0.f ? A / L : 0.f);
-  if (d == 0 && p.lse != nullptr) p.lse[bh] = L > 0.f ? M + logf(L) : -INFINITY;
-}
-
 // Epilogue warp main loop.
 template <typename T, int D, int GQ, int NW, bool kLog2, int TILE>
 __device__ __forceinline__ void epilogue_loop(const DecodeParams& p, const RedPipe& r,
@@ -369,9 +381,9 @@ __device__ __forceinline__ void epilogue_loop(const DecodeParams& p, const RedPi
                                               const float* red_l, const float* red_acc) {
   for (int k = 0;; ++k) {
     mbar_wait(r.full, k & 1);
-    const int idx = r.item[0], len = r.item[1], t_end = r.item[2];
+    const int idx = r.item[0];
     if (idx < 0) break;
-    const Item it = item_from_tag<TILE>(p, make_int4(idx, 0, len, t_end));
+    const Item it = item_from_tag<TILE>(p, make_int4(idx, 0, r.item[1], r.item[2]));
     finish_item_warp<T, D, GQ, NW, kLog2>(p, it, nvalid, red_m, red_l, red_acc, [&] {
       __syncwarp();
       if (threadIdx.x % 32 == 0) mbar_arrive(r.empty);

@@ -94,16 +94,15 @@ __global__ void __launch_bounds__((NW_ + 2) * 32)
         mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES + (j == 0 ? qb : 0) +
                                             (fused ? 2 * C::ROW_BYTES : 0));
         if (fused) {
-          const int64_t off = static_cast<int64_t>(it.b) * p.new_stride + static_cast<int64_t>(it.kvh) * D;
+          const int64_t off = static_cast<int64_t>(it.kvh) * D;
           uint8_t* kn = qslot + s * C::SLOT_BYTES + C::Q_BYTES;
-          tma_load_1d(kn, static_cast<const T*>(p.k_new) + off, C::ROW_BYTES, &full[s], pol);
-          tma_load_1d(kn + C::ROW_BYTES, static_cast<const T*>(p.v_new) + off, C::ROW_BYTES,
-                      &full[s], pol);
+          tma_load_1d(kn, new_rows<T>(p, 0, it.b) + off, C::ROW_BYTES, &full[s], pol);
+          tma_load_1d(kn + C::ROW_BYTES, new_rows<T>(p, 1, it.b) + off, C::ROW_BYTES, &full[s],
+                      pol);
         }
         if (j == 0)
           tma_load_1d(qslot + s * C::SLOT_BYTES,
-                      static_cast<const T*>(p.q) + static_cast<int64_t>(it.b) * p.q_stride +
-                          static_cast<int64_t>(it.kvh) * G * D,
+                      q_rows<T>(p, it.b) + static_cast<int64_t>(it.kvh) * G * D,
                       qb, &full[s], pol);
         const int32_t r32 = static_cast<int32_t>(row);
         tma_load_2d(st, &kmap, 0, r32, &full[s], pol);

@@ -93,15 +93,13 @@ __global__ void __launch_bounds__((NW + 2) * 32)
                                             (fused ? 2 * C::ROW_BYTES : 0));
         uint8_t* slot = qslot + s * C::SLOT_BYTES;
         if (j == 0) {
-          const T* qsrc = static_cast<const T*>(p.q) + static_cast<int64_t>(it.b) * p.q_stride +
-                          static_cast<int64_t>(it.kvh * p.G + it.qg * GQ) * D;
+          const T* qsrc = q_rows<T>(p, it.b) + static_cast<int64_t>(it.kvh * p.G + it.qg * GQ) * D;
           tma_load_1d(slot, qsrc, C::Q_BYTES, &full[s], pol);
         }
         if (fused) {
-          const int64_t off = static_cast<int64_t>(it.b) * p.new_stride + static_cast<int64_t>(it.kvh) * D;
-          tma_load_1d(slot + C::Q_BYTES, static_cast<const T*>(p.k_new) + off, C::ROW_BYTES,
-                      &full[s], pol);
-          tma_load_1d(slot + C::Q_BYTES + C::ROW_BYTES, static_cast<const T*>(p.v_new) + off,
+          const int64_t off = static_cast<int64_t>(it.kvh) * D;
+          tma_load_1d(slot + C::Q_BYTES, new_rows<T>(p, 0, it.b) + off, C::ROW_BYTES, &full[s], pol);
+          tma_load_1d(slot + C::Q_BYTES + C::ROW_BYTES, new_rows<T>(p, 1, it.b) + off,
                       C::ROW_BYTES, &full[s], pol);
         }
         tma_load_1d(ks, kp + row * D, bytes, &full[s], pol);

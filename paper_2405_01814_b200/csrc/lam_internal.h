@@ -17,9 +17,7 @@ int simt_variant_tile(int kv_dtype, int D, int GQ, int variant);  // 0 = invalid
 cudaError_t launch_decode_mma(int kv_dtype, int variant, const DecodeParams& p,
                               const CUtensorMap& kmap, const CUtensorMap& vmap, int grid_x,
                               cudaStream_t stream);
-int mma_variant_tile(int variant);
-// separate split-K merge (after a decode launch with DecodeParams::flags & 64)
-cudaError_t launch_combine(int kv_dtype, const DecodeParams& p, cudaStream_t stream);  // tokens per stage of a GQA kernel variant (0 = invalid)
+int mma_variant_tile(int variant);  // tokens per stage of a GQA kernel variant (0 = invalid)
 // resident CTAs per SM for an instantiation (0 if unsupported)
 int occupancy_simt(int kv_dtype, int D, int GQ, int variant);
 int occupancy_mma(int kv_dtype, int variant);

@@ -236,3 +236,178 @@ def shard_inputs(q: torch.Tensor, kn: torch.Tensor, vn: torch.Tensor, world: int
         return x.view(L, micro_batches, Bh, world, H // world, D).permute(0, 1, 3, 2, 4, 5)
 
     return torch.cat([f(q, Hq), f(kn, Hkv), f(vn, Hkv)], dim=4).contiguous()
+
+
+class _DevView:
+    """Wraps a raw device pointer for torch.as_tensor (CUDA array interface)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+class PeerShardedAttention:
+    """One rank of the attention worker pool with the collectives replaced by peer memory.
+
+    The same step as HeadShardedAttention (head_partition sharding, two staggered
+    micro-batches) without NCCL on the data path — the device-initiated transport of the
+    paper's FHBN design on NVLink / NVSwitch:
+
+    * every rank, as model worker, keeps its packed QKV rows `qkv_in` [L, MB, N, Bh, W, D] and
+      its output rows `out` [L, MB, N, Bh, hq_l, D] in HBM exported over CUDA IPC
+      (lam_peer_alloc / lam_peer_open);
+    * every rank, as attention worker, runs one lam_decode_peer launch per (layer,
+      micro-batch) that TMA-loads each request's q / k_new / v_new straight from its model
+      worker's qkv_in over NVLink (no scatter), appends the new token and stores the output
+      rows straight into the model worker's `out` (no gather);
+    * readiness travels as 32-bit sequence numbers written by the GPU stream front-end
+      (lam_stream_signal / lam_stream_wait: no SM time, no host round trip):
+      qkv_ready[m][s] (the model worker s's rows of layer l are in place) and
+      out_ready[m][j] (attention worker j stored layer l's outputs).
+
+    `launch_args(layer, m)` returns the lam_decode_args of the local launch (pools, page table,
+    seq_lens, order of micro-batch m's rows); q / out / k_new / v_new come from the peers.
+    """
+
+    def __init__(self, geo: ShardGeometry, dist, ctx, launch_args: Callable, device: torch.device,
+                 dtype: torch.dtype):
+        import ctypes as C
+
+        from . import _lib
+
+        g = self.geo = geo
+        if g.world > _lib.LAM_MAX_PEERS:
+            raise ValueError(f"peer transport supports up to {_lib.LAM_MAX_PEERS} ranks")
+        self.lib, self.ctx, self.device, self.dtype = _lib.load(), ctx, device, dtype
+        self._C = C
+        esz = torch.tensor([], dtype=dtype).element_size()
+        align = lambda n: (n + 4095) // 4096 * 4096  # noqa: E731
+        n_qkv = 1
+        for x in g.qkv_shape():
+            n_qkv *= x
+        n_out = 1
+        for x in g.q_shape():
+            n_out *= x
+        MB, N = g.micro_batches, g.world
+        self.off_out = align(n_qkv * esz)
+        self.off_flags = self.off_out + align(n_out * esz)
+        total = self.off_flags + align(2 * MB * N * 4)
+        base, handle = C.c_void_p(), (C.c_uint8 * _lib.LAM_IPC_HANDLE_BYTES)()
+        _lib.check(self.lib.lam_peer_alloc(ctx.handle, total, C.byref(base), handle))
+        self.base = base.value
+        raw = torch.as_tensor(_DevView(self.base, total), device=device)
+        self.qkv_in = raw[: n_qkv * esz].view(dtype).view(g.qkv_shape())
+        self.out = raw[self.off_out: self.off_out + n_out * esz].view(dtype).view(g.q_shape())
+        self.flags = raw[self.off_flags: self.off_flags + 2 * MB * N * 4].view(torch.int32).view(2, MB, N)
+        # exchange handles; map every peer's buffer
+        handles = [None] * N
+        dist.all_gather_object(handles, bytes(handle))
+        self.peer = []
+        for r in range(N):
+            if r == g.rank:
+                self.peer.append(self.base)
+                continue
+            hb = (C.c_uint8 * _lib.LAM_IPC_HANDLE_BYTES).from_buffer_copy(handles[r])
+            p = C.c_void_p()
+            _lib.check(self.lib.lam_peer_open(ctx.handle, hb, C.byref(p)))
+            self.peer.append(p.value)
+        dist.barrier()
+        self.compute = torch.cuda.current_stream(device)
+        self.model = torch.cuda.Stream(device=device)   # model-worker side signalling
+        self.h2d = torch.cuda.Stream(device=device)
+        self.d2h = torch.cuda.Stream(device=device)
+        self.epoch = 0
+        # precomputed launch descriptors and flag address lists
+        Ptrs = C.c_void_p * N
+        qkv_elems_mb = g.Bh * g.W * g.D          # one (layer, mb, dest) block
+        out_elems_mb = g.Bh * g.hq_l * g.D
+        j = g.rank
+        self.args, self.io = {}, {}
+        for layer in range(g.layers):
+            for m in range(MB):
+                a = launch_args(layer, m)
+                a.q_batch_stride = g.W * g.D
+                a.new_batch_stride = g.W * g.D
+                a.lse = None
+                io = _lib.PeerIO()
+                io.n_src, io.rows_per_src = N, g.Bh
+                blk = (layer * MB + m) * N + j
+                for s in range(N):
+                    io.q_src[s] = self.peer[s] + blk * qkv_elems_mb * esz
+                    io.out_dst[s] = self.peer[s] + self.off_out + blk * out_elems_mb * esz
+                io.k_new_offset = g.hq_l * g.D
+                io.v_new_offset = (g.hq_l + g.hkv_l) * g.D
+                self.args[layer, m], self.io[layer, m] = a, io
+        fl = lambda r, kind, m, i: self.peer[r] + self.off_flags + ((kind * MB + m) * N + i) * 4  # noqa: E731
+        # qkv_ready[m][rank] on every attention worker / out_ready[m][rank] on every model worker
+        self.sig_qkv = [Ptrs(*[fl(r, 0, m, j) for r in range(N)]) for m in range(MB)]
+        self.sig_out = [Ptrs(*[fl(r, 1, m, j) for r in range(N)]) for m in range(MB)]
+        # local flags to wait on: every source's qkv_ready[m][*], every worker's out_ready[m][*]
+        self.wait_qkv = [Ptrs(*[fl(j, 0, m, s) for s in range(N)]) for m in range(MB)]
+        self.wait_out = [Ptrs(*[fl(j, 1, m, s) for s in range(N)]) for m in range(MB)]
+
+    def close(self):
+        if self.peer:
+            torch.cuda.synchronize(self.device)
+            for r, p in enumerate(self.peer):
+                if r != self.geo.rank:
+                    self.lib.lam_peer_close(self.ctx.handle, p)
+            self.lib.lam_peer_free(self.ctx.handle, self.base)
+            self.peer = []
+
+    def step(self, ev=None, host_in=None, host_out=None):
+        """One decode step over all layers on this rank (enqueue only).  Inputs are read from
+        self.qkv_in (or copied there from pinned `host_in` first), outputs land in self.out
+        (and are copied to pinned `host_out`).  `ev`: (start, end) CUDA event pairs, one per
+        local launch, recorded on the compute stream."""
+        from . import _lib
+
+        g, lib, C = self.geo, self.lib, self._C
+        MB, N, L = g.micro_batches, g.world, g.layers
+        h = self.ctx.handle
+        comp, model = self.compute, self.model
+        e0 = self.epoch
+        self.epoch += L
+        model.wait_stream(comp)  # the previous step (and any input writes) are complete
+        arrived = None
+        if host_in is not None:
+            self.h2d.wait_stream(comp)
+            arrived = [torch.cuda.Event() for _ in range(L)]
+            with torch.cuda.stream(self.h2d):
+                for layer in range(L):
+                    self.qkv_in[layer].copy_(host_in[layer], non_blocking=True)
+                    arrived[layer].record(self.h2d)
+        if host_out is not None:
+            self.d2h.wait_stream(comp)
+        ms, cs = model.cuda_stream, comp.cuda_stream
+        k = 0
+        for layer in range(L):
+            ep = e0 + layer + 1
+            if arrived is not None:
+                model.wait_event(arrived[layer])
+            for m in range(MB):
+                # model worker: layer l's rows need layer l-1's outputs of this micro-batch
+                if layer > 0:
+                    _lib.check(lib.lam_stream_wait(h, self.wait_out[m], N, ep - 1, ms))
+                _lib.check(lib.lam_stream_signal(h, self.sig_qkv[m], N, ep, ms))
+            for m in range(MB):
+                _lib.check(lib.lam_stream_wait(h, self.wait_qkv[m], N, ep, cs))
+                e = ev[k] if ev is not None else None
+                k += 1
+                if e is not None:
+                    e[0].record(comp)
+                _lib.check(lib.lam_decode_peer(h, self.args[layer, m], self.io[layer, m], cs))
+                if e is not None:
+                    e[1].record(comp)
+                _lib.check(lib.lam_stream_signal(h, self.sig_out[m], N, ep, cs))
+                if host_out is not None:
+                    ds = self.d2h.cuda_stream
+                    _lib.check(lib.lam_stream_wait(h, self.wait_out[m], N, ep, ds))
+                    with torch.cuda.stream(self.d2h):
+                        host_out[layer, m].copy_(self.out[layer, m], non_blocking=True)
+        # the step ends when this rank's outputs of the last layer have all arrived
+        for m in range(MB):
+            _lib.check(lib.lam_stream_wait(h, self.wait_out[m], N, e0 + L, cs))
+        comp.wait_stream(model)
+        if host_out is not None:
+            comp.wait_stream(self.d2h)

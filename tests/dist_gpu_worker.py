@@ -14,8 +14,9 @@ sys.path.insert(0, str(ROOT))
 
 from oracle import oracle as O  # noqa: E402
 from paper_2405_01814_b200 import decode as dec  # noqa: E402
-from paper_2405_01814_b200.dist import (HeadShardedAttention, ShardGeometry, shard_inputs,  # noqa: E402
-                                        stitch_outputs)
+from paper_2405_01814_b200 import _lib  # noqa: E402
+from paper_2405_01814_b200.dist import (HeadShardedAttention, PeerShardedAttention,  # noqa: E402
+                                        ShardGeometry, shard_inputs, stitch_outputs)
 from paper_2405_01814_b200.kvcache import PagedKVCache  # noqa: E402
 
 L, B_LOCAL, HQ, HKV, D, MB, P = 3, 8, 64, 8, 128, 2, 64
@@ -75,13 +76,42 @@ def main():
                    page_table=cache.page_table[sl], max_len=int(row_lens.max()), out=out,
                    k_new=k, v_new=v)
 
-    eng = (HeadShardedAttention(geo, dist, None, attend_fused, dev, torch.bfloat16) if fused
-           else HeadShardedAttention(geo, dist, append, attend, dev, torch.bfloat16))
     mine = slice(rank * B_LOCAL, (rank + 1) * B_LOCAL)
     qkv_in = shard_inputs(q[:, mine], kn[:, mine], vn[:, mine], world, MB).to(dev)
-    out = torch.zeros(geo.q_shape(), dtype=torch.bfloat16, device=dev)
-    eng.step(qkv_in, out)
-    torch.cuda.synchronize()
+    if os.environ.get("LAM_TEST_TRANSPORT", "nccl") == "peer":
+        # peer-memory transport: zero-copy pull of q/k/v, outputs stored into the model worker
+        ctx = _lib.context(dev.index)
+
+        def launch_args(layer, m):
+            sl = slice(m * geo.B_mb, (m + 1) * geo.B_mb)
+            qd = torch.empty((geo.B_mb, geo.hq_l, D), dtype=torch.bfloat16, device=dev)
+            a, _ = dec.make_args(qd, cache.k[layer], cache.v[layer], cache.seq_lens[sl],
+                                 page_table=cache.page_table[sl], max_len=int(row_lens.max()),
+                                 out=qd)
+            return a
+
+        eng = PeerShardedAttention(geo, dist, ctx, launch_args, dev, torch.bfloat16)
+        eng.qkv_in.copy_(qkv_in)
+        eng.out.zero_()
+        host_io = os.environ.get("LAM_TEST_HOST", "0") == "1"
+        if host_io:  # from pinned host buffers, as the end-to-end bench runs it
+            h_in = qkv_in.cpu().pin_memory()
+            h_out = torch.zeros(geo.q_shape(), dtype=torch.bfloat16).pin_memory()
+            eng.qkv_in.zero_()
+            torch.cuda.synchronize()
+            eng.step(host_in=h_in, host_out=h_out)
+        else:
+            eng.step()
+        torch.cuda.synchronize()
+        out = h_out if host_io else eng.out.clone()
+        dist.barrier()
+        eng.close()
+    else:
+        eng = (HeadShardedAttention(geo, dist, None, attend_fused, dev, torch.bfloat16) if fused
+               else HeadShardedAttention(geo, dist, append, attend, dev, torch.bfloat16))
+        out = torch.zeros(geo.q_shape(), dtype=torch.bfloat16, device=dev)
+        eng.step(qkv_in, out)
+        torch.cuda.synchronize()
     got = stitch_outputs(out).float().cpu().numpy()
     worst = 0.0
     for layer in range(L):

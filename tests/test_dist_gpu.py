@@ -12,15 +12,17 @@ ROOT = Path(__file__).resolve().parent.parent
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("fused", ["1", "0"])
+@pytest.mark.parametrize("transport,fused,host", [("nccl", "1", "0"), ("nccl", "0", "0"),
+                                                  ("peer", "1", "0"), ("peer", "1", "1")])
 @pytest.mark.parametrize("nproc", [2, 4])
-def test_sharded_engine_matches_oracle(built, nproc, fused):
+def test_sharded_engine_matches_oracle(built, nproc, transport, fused, host):
     if torch.cuda.device_count() < nproc:
         pytest.skip(f"needs {nproc} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1", "--master-port=29531",
            str(ROOT / "tests" / "dist_gpu_worker.py")]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
-                       env=dict(os.environ, PYTHONPATH=str(ROOT), LAM_TEST_FUSED=fused))
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT,
+                       env=dict(os.environ, PYTHONPATH=str(ROOT), LAM_TEST_FUSED=fused,
+                                LAM_TEST_TRANSPORT=transport, LAM_TEST_HOST=host))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count("OK") == nproc
