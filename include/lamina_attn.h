@@ -261,6 +261,16 @@ typedef struct lam_peer_io {
   void* out_dst[LAM_MAX_PEERS];
   int64_t k_new_offset;
   int64_t v_new_offset;
+  /* Optional in-kernel sequence numbers (no stream operations around the launch): every CTA
+   * waits until each wait_flags[i] >= wait_value (i < n_wait) before its first load, and the
+   * launch stores done_value to each done_flags[i] (i < n_done, local or peer) once all of
+   * its output rows are globally visible.  n_wait = n_done = 0 disables both. */
+  int32_t n_wait;
+  int32_t n_done;
+  uint32_t wait_value;
+  uint32_t done_value;
+  const uint32_t* wait_flags[LAM_MAX_PEERS];
+  uint32_t* done_flags[LAM_MAX_PEERS];
 } lam_peer_io;
 
 /* lam_decode whose q / k_new / v_new / out come from lam_peer_io (args->q, k_new, v_new and out

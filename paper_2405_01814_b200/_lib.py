@@ -76,6 +76,12 @@ class PeerIO(C.Structure):
         ("out_dst", C.c_void_p * LAM_MAX_PEERS),
         ("k_new_offset", C.c_int64),
         ("v_new_offset", C.c_int64),
+        ("n_wait", C.c_int32),
+        ("n_done", C.c_int32),
+        ("wait_value", C.c_uint32),
+        ("done_value", C.c_uint32),
+        ("wait_flags", C.c_void_p * LAM_MAX_PEERS),
+        ("done_flags", C.c_void_p * LAM_MAX_PEERS),
     ]
 
 

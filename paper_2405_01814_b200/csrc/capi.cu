@@ -28,7 +28,7 @@ struct lam_ctx {
   int32_t* counters = nullptr;
   int64_t counters_cap = 0;
   int32_t* err = nullptr;  // device error word for the instance API
-  int32_t* work = nullptr; // [2] persistent-kernel work counters (self-resetting)
+  int32_t* work = nullptr; // [4] persistent-kernel counters: items, producers, epilogues (self-resetting)
   void* scratch = nullptr; // instance API: logits workspace
   int64_t scratch_cap = 0; // bytes
   int64_t* offs = nullptr; // instance API: logit offsets
@@ -161,8 +161,8 @@ struct Plan {
 // whose item counts (512, 1024) divide evenly there (up to +4 % over a full 148-CTA grid).
 void choose_splits(Plan& pl, int64_t units, int max_len, int max_ctas, int split_tokens,
                    double bytes_per_token) {
-  static const double BW_CHIP = 7.0e12, RATE_SM = env_int("LAM_PLAN_RATE_SM", 56) * 1e9,
-                      C_ITEM = env_int("LAM_PLAN_CITEM_NS", 4000) * 1e-9;
+  static const double BW_CHIP = 7.0e12, RATE_SM = env_int("LAM_PLAN_RATE_SM", 50) * 1e9,
+                      C_ITEM = env_int("LAM_PLAN_CITEM_NS", 2000) * 1e-9;
   const int tiles_total = std::max(1, (max_len + pl.tile - 1) / pl.tile);
   const int occ_per_sm = std::max(1, max_ctas / 148);
   double best = 1e300;
@@ -368,8 +368,8 @@ int lam_ctx_create(int device, lam_ctx** out) {
   cudaError_t e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (e == cudaSuccess) e = cudaMalloc(&c->err, sizeof(int32_t));
   if (e == cudaSuccess) e = cudaMemset(c->err, 0, sizeof(int32_t));
-  if (e == cudaSuccess) e = cudaMalloc(&c->work, 2 * sizeof(int32_t));
-  if (e == cudaSuccess) e = cudaMemset(c->work, 0, 2 * sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&c->work, 4 * sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMemset(c->work, 0, 4 * sizeof(int32_t));
   if (e != cudaSuccess) {
     delete c;
     return cuda_fail(e, "lam_ctx_create");
@@ -729,6 +729,21 @@ int decode_impl(lam_ctx* ctx, const lam_decode_args* a, const lam_peer_io* io, v
                                            : static_cast<int64_t>(a->num_kv_heads) * D;
     p.k_pool_w = const_cast<void*>(a->k_pool);
     p.v_pool_w = const_cast<void*>(a->v_pool);
+    if (io->n_wait < 0 || io->n_wait > LAM_MAX_PEERS || io->n_done < 0 || io->n_done > LAM_MAX_PEERS)
+      return fail(LAM_ERR_VALIDATION, "peer io: n_wait / n_done out of range");
+    for (int i = 0; i < io->n_wait; ++i) {
+      if (!io->wait_flags[i]) return fail(LAM_ERR_VALIDATION, "peer io: null wait flag");
+      p.wait_flag[i] = io->wait_flags[i];
+    }
+    for (int i = 0; i < io->n_done; ++i) {
+      if (!io->done_flags[i]) return fail(LAM_ERR_VALIDATION, "peer io: null done flag");
+      p.done_flag[i] = io->done_flags[i];
+    }
+    p.n_wait = io->n_wait;
+    p.n_done = io->n_done;
+    p.wait_value = io->wait_value;
+    p.done_value = io->done_value;
+    p.done_ctr = ctx->work + 2;
   }
   p.flags = env_int("LAM_DECODE_FLAGS", 0);
   p.scale = a->scale;

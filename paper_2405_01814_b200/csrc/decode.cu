@@ -37,12 +37,15 @@ template <typename T, int D, int GQ, int NW, int TILE, int STAGES>
 int simt_occ() {
   using C = SimtCfg<T, D, GQ, NW, TILE, STAGES>;
   static std::atomic<uint64_t> done{0};
+  static std::atomic<int> cached{0};  // queried once per process (one device model)
+  if (const int c = cached.load(std::memory_order_relaxed); c > 0) return c;
   auto* k = decode_simt_kernel<T, D, GQ, NW, TILE, STAGES>;
   if (ensure_smem_attr(k, C::SMEM_BYTES, done) != cudaSuccess) return 0;
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, C::THREADS, C::SMEM_BYTES) !=
       cudaSuccess)
     return 0;
+  cached.store(n, std::memory_order_relaxed);
   return n;
 }
 
@@ -62,12 +65,15 @@ template <typename T, int NW, int STAGES>
 int mma_occ_v() {
   using C = MmaCfg<NW, STAGES>;
   static std::atomic<uint64_t> done{0};
+  static std::atomic<int> cached{0};  // queried once per process (one device model)
+  if (const int c = cached.load(std::memory_order_relaxed); c > 0) return c;
   auto* k = decode_gqa_mma_kernel<T, NW, STAGES>;
   if (ensure_smem_attr(k, C::SMEM_BYTES, done) != cudaSuccess) return 0;
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, C::THREADS, C::SMEM_BYTES) !=
       cudaSuccess)
     return 0;
+  cached.store(n, std::memory_order_relaxed);
   return n;
 }
 

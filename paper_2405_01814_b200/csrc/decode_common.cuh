@@ -67,7 +67,41 @@ struct DecodeParams {
   const void* q_src[LAM_MAX_PEERS];
   void* out_dst[LAM_MAX_PEERS];
   int64_t new_off[2];
+  // device-side sequence numbers (optional): the producer of every CTA waits until each
+  // wait_flag[i] >= wait_value before its first load; the last CTA to finish its epilogue
+  // stores done_value to every done_flag[i] after all CTAs' output stores (system scope).
+  int32_t n_wait, n_done;
+  uint32_t wait_value, done_value;
+  const uint32_t* wait_flag[LAM_MAX_PEERS];
+  uint32_t* done_flag[LAM_MAX_PEERS];
+  int32_t* done_ctr;        // epilogue arrival counter (self-resetting)
 };
+
+// Spin until the inputs of this launch are published (peer transport).  ~10 s without progress
+// traps the kernel instead of hanging the device.
+__device__ __forceinline__ void wait_inputs(const DecodeParams& p) {
+  if (p.n_wait <= 0) return;
+  const long long t0 = clock64();
+  for (int i = 0; i < p.n_wait; ++i) {
+    while (static_cast<int32_t>(ld_acquire_sys(p.wait_flag[i]) - p.wait_value) < 0) {
+      __nanosleep(200);
+      if (clock64() - t0 > (20ll << 30)) __trap();
+    }
+  }
+  fence_proxy_async_global();
+}
+
+// Called by every CTA's epilogue warp after its last output store.
+__device__ __forceinline__ void signal_outputs(const DecodeParams& p) {
+  if (p.n_done <= 0) return;
+  __syncwarp();
+  if (threadIdx.x % 32 != 0) return;
+  __threadfence_system();
+  if (atomicAdd(p.done_ctr, 1) != static_cast<int>(gridDim.x) - 1) return;
+  *p.done_ctr = 0;  // ready for the next launch (stream-ordered)
+  __threadfence_system();
+  for (int i = 0; i < p.n_done; ++i) st_release_sys(p.done_flag[i], p.done_value);
+}
 
 // Start of request b's q rows / new k (which = 0) or v (1) rows, local or on a peer.
 template <typename T>
@@ -165,6 +199,7 @@ template <int STAGES, int TILE, class Issue>
 __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* full,
                                               uint64_t* empty, int4* meta, long long* meta_row,
                                               Issue issue) {
+  wait_inputs(p);
   int i = 0;
   auto acquire = [&](int k) {
     const int s = k % STAGES;
@@ -389,6 +424,7 @@ __device__ __forceinline__ void epilogue_loop(const DecodeParams& p, const RedPi
       if (threadIdx.x % 32 == 0) mbar_arrive(r.empty);
     });
   }
+  signal_outputs(p);
 }
 
 }  // namespace lam

@@ -267,10 +267,15 @@ class PeerShardedAttention:
 
     `launch_args(layer, m)` returns the lam_decode_args of the local launch (pools, page table,
     seq_lens, order of micro-batch m's rows); q / out / k_new / v_new come from the peers.
+
+    sync="kernel" (default): the decode kernel itself waits for qkv_ready (every CTA's producer
+    polls before its first load) and publishes out_ready (the last CTA to finish, after a
+    system-scope fence), so the compute stream carries nothing but back-to-back decode
+    launches.  sync="stream": the same sequence numbers as stream operations around each launch.
     """
 
     def __init__(self, geo: ShardGeometry, dist, ctx, launch_args: Callable, device: torch.device,
-                 dtype: torch.dtype):
+                 dtype: torch.dtype, sync: str = "kernel"):
         import ctypes as C
 
         from . import _lib
@@ -345,6 +350,15 @@ class PeerShardedAttention:
         # local flags to wait on: every source's qkv_ready[m][*], every worker's out_ready[m][*]
         self.wait_qkv = [Ptrs(*[fl(j, 0, m, s) for s in range(N)]) for m in range(MB)]
         self.wait_out = [Ptrs(*[fl(j, 1, m, s) for s in range(N)]) for m in range(MB)]
+        if sync not in ("kernel", "stream"):
+            raise ValueError("sync must be 'kernel' or 'stream'")
+        self.sync = sync
+        if sync == "kernel":
+            for (layer, m), io in self.io.items():
+                io.n_wait = io.n_done = N
+                for i in range(N):
+                    io.wait_flags[i] = self.wait_qkv[m][i]
+                    io.done_flags[i] = self.sig_out[m][i]
 
     def close(self):
         if self.peer:
@@ -391,15 +405,21 @@ class PeerShardedAttention:
                     _lib.check(lib.lam_stream_wait(h, self.wait_out[m], N, ep - 1, ms))
                 _lib.check(lib.lam_stream_signal(h, self.sig_qkv[m], N, ep, ms))
             for m in range(MB):
-                _lib.check(lib.lam_stream_wait(h, self.wait_qkv[m], N, ep, cs))
+                io = self.io[layer, m]
+                in_kernel = self.sync == "kernel"
+                if in_kernel:
+                    io.wait_value = io.done_value = ep
+                else:
+                    _lib.check(lib.lam_stream_wait(h, self.wait_qkv[m], N, ep, cs))
                 e = ev[k] if ev is not None else None
                 k += 1
                 if e is not None:
                     e[0].record(comp)
-                _lib.check(lib.lam_decode_peer(h, self.args[layer, m], self.io[layer, m], cs))
+                _lib.check(lib.lam_decode_peer(h, self.args[layer, m], io, cs))
                 if e is not None:
                     e[1].record(comp)
-                _lib.check(lib.lam_stream_signal(h, self.sig_out[m], N, ep, cs))
+                if not in_kernel:
+                    _lib.check(lib.lam_stream_signal(h, self.sig_out[m], N, ep, cs))
                 if host_out is not None:
                     ds = self.d2h.cuda_stream
                     _lib.check(lib.lam_stream_wait(h, self.wait_out[m], N, ep, ds))

@@ -90,7 +90,8 @@ def main():
                                  out=qd)
             return a
 
-        eng = PeerShardedAttention(geo, dist, ctx, launch_args, dev, torch.bfloat16)
+        eng = PeerShardedAttention(geo, dist, ctx, launch_args, dev, torch.bfloat16,
+                                   sync=os.environ.get("LAM_TEST_SYNC", "kernel"))
         eng.qkv_in.copy_(qkv_in)
         eng.out.zero_()
         host_io = os.environ.get("LAM_TEST_HOST", "0") == "1"

@@ -12,10 +12,11 @@ ROOT = Path(__file__).resolve().parent.parent
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("transport,fused,host", [("nccl", "1", "0"), ("nccl", "0", "0"),
-                                                  ("peer", "1", "0"), ("peer", "1", "1")])
+@pytest.mark.parametrize("transport,fused,host,sync", [
+    ("nccl", "1", "0", "-"), ("nccl", "0", "0", "-"), ("peer", "1", "0", "kernel"),
+    ("peer", "1", "1", "kernel"), ("peer", "1", "0", "stream"), ("peer", "1", "1", "stream")])
 @pytest.mark.parametrize("nproc", [2, 4])
-def test_sharded_engine_matches_oracle(built, nproc, transport, fused, host):
+def test_sharded_engine_matches_oracle(built, nproc, transport, fused, host, sync):
     if torch.cuda.device_count() < nproc:
         pytest.skip(f"needs {nproc} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
@@ -23,6 +24,7 @@ def test_sharded_engine_matches_oracle(built, nproc, transport, fused, host):
            str(ROOT / "tests" / "dist_gpu_worker.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT,
                        env=dict(os.environ, PYTHONPATH=str(ROOT), LAM_TEST_FUSED=fused,
-                                LAM_TEST_TRANSPORT=transport, LAM_TEST_HOST=host))
+                                LAM_TEST_TRANSPORT=transport, LAM_TEST_HOST=host,
+                                LAM_TEST_SYNC=sync))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count("OK") == nproc
