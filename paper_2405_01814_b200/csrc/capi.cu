@@ -18,6 +18,8 @@
 #include "decode_common.cuh"
 #include "lam_internal.h"
 
+constexpr int kSlots = 4;  // launches that may overlap (programmatic dependent launch)
+
 struct lam_ctx {
   int device = 0;
   int num_sms = 0;
@@ -28,7 +30,12 @@ struct lam_ctx {
   int32_t* counters = nullptr;
   int64_t counters_cap = 0;
   int32_t* err = nullptr;  // device error word for the instance API
-  int32_t* work = nullptr; // [4] persistent-kernel counters: items, producers, epilogues (self-resetting)
+  // launch slots of the persistent decode kernels (see DecodeParams::slot): device counters
+  // [kSlots][2] and the host's shadow of where each slot's next launch starts
+  unsigned long long* slots = nullptr;
+  uint64_t item_base[kSlots] = {};
+  uint64_t done_base[kSlots] = {};
+  uint64_t seq = 0;
   void* scratch = nullptr; // instance API: logits workspace
   int64_t scratch_cap = 0; // bytes
   int64_t* offs = nullptr; // instance API: logit offsets
@@ -368,8 +375,8 @@ int lam_ctx_create(int device, lam_ctx** out) {
   cudaError_t e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (e == cudaSuccess) e = cudaMalloc(&c->err, sizeof(int32_t));
   if (e == cudaSuccess) e = cudaMemset(c->err, 0, sizeof(int32_t));
-  if (e == cudaSuccess) e = cudaMalloc(&c->work, 4 * sizeof(int32_t));
-  if (e == cudaSuccess) e = cudaMemset(c->work, 0, 4 * sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&c->slots, kSlots * 2 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(c->slots, 0, kSlots * 2 * sizeof(unsigned long long));
   if (e != cudaSuccess) {
     delete c;
     return cuda_fail(e, "lam_ctx_create");
@@ -385,7 +392,7 @@ int lam_ctx_destroy(lam_ctx* c) {
   cudaFree(c->ws_ml);
   cudaFree(c->counters);
   cudaFree(c->err);
-  cudaFree(c->work);
+  cudaFree(c->slots);
   cudaFree(c->scratch);
   cudaFree(c->offs);
   delete c;
@@ -397,9 +404,22 @@ int lam_ctx_num_sms(const lam_ctx* c) { return c ? c->num_sms : 0; }
 int lam_ctx_reserve(lam_ctx* c, int64_t partial_rows, int32_t head_dim, int64_t counters) {
   if (!c) return fail(LAM_ERR_VALIDATION, "null context");
   LAM_CUDA(cudaSetDevice(c->device));
-  LAM_CUDA(grow(&c->ws_acc, &c->ws_acc_cap, partial_rows * head_dim, false));
-  LAM_CUDA(grow(&c->ws_ml, &c->ws_ml_cap, partial_rows * 2, false));
-  LAM_CUDA(grow(&c->counters, &c->counters_cap, counters, true));
+  // every launch slot has its own split workspace (capacities are per slot)
+  if (partial_rows * head_dim > c->ws_acc_cap) {
+    int64_t cap = 0;
+    LAM_CUDA(grow(&c->ws_acc, &cap, kSlots * partial_rows * head_dim, false));
+    c->ws_acc_cap = partial_rows * head_dim;
+  }
+  if (partial_rows * 2 > c->ws_ml_cap) {
+    int64_t cap = 0;
+    LAM_CUDA(grow(&c->ws_ml, &cap, kSlots * partial_rows * 2, false));
+    c->ws_ml_cap = partial_rows * 2;
+  }
+  if (counters > c->counters_cap) {
+    int64_t cap = 0;
+    LAM_CUDA(grow(&c->counters, &cap, kSlots * counters, true));
+    c->counters_cap = counters;
+  }
   return LAM_OK;
 }
 
@@ -692,7 +712,10 @@ int decode_impl(lam_ctx* ctx, const lam_decode_args* a, const lam_peer_io* io, v
   p.S = pl.S;
   p.QG = pl.QG;
   p.n_items = static_cast<int32_t>(static_cast<int64_t>(a->batch) * a->num_kv_heads * pl.QG * pl.S);
-  p.work = ctx->work;
+  const int slot = static_cast<int>(ctx->seq % kSlots);
+  p.slot = ctx->slots + 2 * slot;
+  p.item_base = ctx->item_base[slot];
+  p.done_base = ctx->done_base[slot];
   p.order = a->request_order;
   if (a->k_new != nullptr) {  // fused append
     if (a->v_new == nullptr) return fail(LAM_ERR_VALIDATION, "fused append needs both k_new and v_new");
@@ -743,7 +766,9 @@ int decode_impl(lam_ctx* ctx, const lam_decode_args* a, const lam_peer_io* io, v
     p.n_done = io->n_done;
     p.wait_value = io->wait_value;
     p.done_value = io->done_value;
-    p.done_ctr = ctx->work + 2;
+    // the launch carries its own input dependencies (sequence numbers), so it may overlap the
+    // previous kernel's drain
+    p.pdl = io->n_wait > 0 && env_int("LAM_PDL", 1) != 0;
   }
   p.flags = env_int("LAM_DECODE_FLAGS", 0);
   p.scale = a->scale;
@@ -757,9 +782,9 @@ int decode_impl(lam_ctx* ctx, const lam_decode_args* a, const lam_peer_io* io, v
                            std::max<int64_t>(cnt, ctx->counters_cap));
       if (rc != LAM_OK) return rc;
     }
-    p.ws_acc = ctx->ws_acc;
-    p.ws_ml = ctx->ws_ml;
-    p.counters = ctx->counters;
+    p.ws_acc = ctx->ws_acc + slot * ctx->ws_acc_cap;
+    p.ws_ml = ctx->ws_ml + slot * ctx->ws_ml_cap;
+    p.counters = ctx->counters + slot * ctx->counters_cap;
   }
   auto s = static_cast<cudaStream_t>(stream);
   if (pl.kernel == LAM_KERNEL_GQA_MMA) {
@@ -777,6 +802,11 @@ int decode_impl(lam_ctx* ctx, const lam_decode_args* a, const lam_peer_io* io, v
   } else {
     LAM_CUDA(lam::launch_decode_simt(a->kv_dtype, D, pl.GQ, pl.variant, p, pl.ctas, s));
   }
+  // the slot's next launch starts where this one ends (every CTA claims until one claim past
+  // the last item, and counts itself out once)
+  ctx->item_base[slot] += static_cast<uint64_t>(p.n_items) + pl.ctas;
+  ctx->done_base[slot] += static_cast<uint64_t>(pl.ctas);
+  ++ctx->seq;
   return LAM_OK;
 }
 

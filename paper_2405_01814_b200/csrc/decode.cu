@@ -22,6 +22,28 @@ cudaError_t ensure_smem_attr(K kernel, int bytes, std::atomic<uint64_t>& done_ma
   return e;
 }
 
+// Launch with programmatic dependent launch when p.pdl: the grid may start while the previous
+// kernel of the stream is still draining (its CTAs trigger once they run out of work items).
+template <typename K, typename... Args>
+cudaError_t launch_k(K kernel, const DecodeParams& p, int ctas, int threads, int smem,
+                     cudaStream_t stream, Args... args) {
+  if (!p.pdl) {
+    kernel<<<ctas, threads, smem, stream>>>(args...);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(ctas);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 template <typename T, int D, int GQ, int NW, int TILE, int STAGES>
 cudaError_t simt_launch(const DecodeParams& p, int ctas, cudaStream_t stream) {
   using C = SimtCfg<T, D, GQ, NW, TILE, STAGES>;
@@ -29,8 +51,7 @@ cudaError_t simt_launch(const DecodeParams& p, int ctas, cudaStream_t stream) {
   auto* k = decode_simt_kernel<T, D, GQ, NW, TILE, STAGES>;
   cudaError_t e = ensure_smem_attr(k, C::SMEM_BYTES, done);
   if (e != cudaSuccess) return e;
-  k<<<ctas, C::THREADS, C::SMEM_BYTES, stream>>>(p);
-  return cudaGetLastError();
+  return launch_k(k, p, ctas, C::THREADS, C::SMEM_BYTES, stream, p);
 }
 
 template <typename T, int D, int GQ, int NW, int TILE, int STAGES>
@@ -57,8 +78,7 @@ cudaError_t mma_launch_v(const DecodeParams& p, const CUtensorMap& kmap, const C
   auto* k = decode_gqa_mma_kernel<T, NW, STAGES>;
   cudaError_t e = ensure_smem_attr(k, C::SMEM_BYTES, done);
   if (e != cudaSuccess) return e;
-  k<<<ctas, C::THREADS, C::SMEM_BYTES, stream>>>(p, kmap, vmap);
-  return cudaGetLastError();
+  return launch_k(k, p, ctas, C::THREADS, C::SMEM_BYTES, stream, p, kmap, vmap);
 }
 
 template <typename T, int NW, int STAGES>

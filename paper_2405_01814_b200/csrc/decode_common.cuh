@@ -39,7 +39,13 @@ struct DecodeParams {
   float* ws_acc;            // [B*Hq*S][D] split partials (unnormalised acc)
   float* ws_ml;             // [B*Hq*S][2] (max in natural-log units, sum)
   int32_t* counters;        // [B*Hkv*QG] split arrival counters (self-resetting)
-  int32_t* work;            // [2] item counter, exited-producer counter (self-resetting)
+  // Launch slot (one of a small ring, so overlapping launches never share state): slot[0]
+  // counts item claims, slot[1] finished epilogues, both monotonic.  This launch owns claims
+  // [item_base, item_base + n_items + grid) and arrivals [done_base, done_base + grid); it
+  // starts only once the slot's previous launch has fully finished (slot[1] >= done_base).
+  unsigned long long* slot;
+  unsigned long long item_base, done_base;
+  int32_t pdl;              // launched with programmatic dependent launch
   int32_t B, Hq, Hkv, G, D;
   int32_t page_size, pt_stride;
   int32_t chunk;            // tokens per split (multiple of the kernel tile)
@@ -74,8 +80,22 @@ struct DecodeParams {
   uint32_t wait_value, done_value;
   const uint32_t* wait_flag[LAM_MAX_PEERS];
   uint32_t* done_flag[LAM_MAX_PEERS];
-  int32_t* done_ctr;        // epilogue arrival counter (self-resetting)
 };
+
+__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Wait until the previous launch on this slot has finished (normally long done).
+__device__ __forceinline__ void acquire_slot(const DecodeParams& p) {
+  const long long t0 = clock64();
+  while (ld_acquire_gpu_u64(p.slot + 1) < p.done_base) {
+    __nanosleep(100);
+    if (clock64() - t0 > (20ll << 30)) __trap();
+  }
+}
 
 // Spin until the inputs of this launch are published (peer transport).  ~10 s without progress
 // traps the kernel instead of hanging the device.
@@ -91,14 +111,17 @@ __device__ __forceinline__ void wait_inputs(const DecodeParams& p) {
   fence_proxy_async_global();
 }
 
-// Called by every CTA's epilogue warp after its last output store.
-__device__ __forceinline__ void signal_outputs(const DecodeParams& p) {
-  if (p.n_done <= 0) return;
+// Called by every CTA's epilogue warp after its last output / workspace store: count the CTA
+// out of the slot; the last CTA publishes the outputs (peer transport).
+__device__ __forceinline__ void finish_cta(const DecodeParams& p) {
   __syncwarp();
   if (threadIdx.x % 32 != 0) return;
-  __threadfence_system();
-  if (atomicAdd(p.done_ctr, 1) != static_cast<int>(gridDim.x) - 1) return;
-  *p.done_ctr = 0;  // ready for the next launch (stream-ordered)
+  if (p.n_done > 0)
+    __threadfence_system();
+  else
+    __threadfence();
+  const unsigned long long old = atomicAdd(p.slot + 1, 1ull);
+  if (p.n_done <= 0 || old - p.done_base != gridDim.x - 1) return;
   __threadfence_system();
   for (int i = 0; i < p.n_done; ++i) st_release_sys(p.done_flag[i], p.done_value);
 }
@@ -199,6 +222,7 @@ template <int STAGES, int TILE, class Issue>
 __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* full,
                                               uint64_t* empty, int4* meta, long long* meta_row,
                                               Issue issue) {
+  acquire_slot(p);
   wait_inputs(p);
   int i = 0;
   auto acquire = [&](int k) {
@@ -207,8 +231,9 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
     return s;
   };
   for (;;) {
-    const int idx = atomicAdd(p.work, 1);
-    if (idx >= p.n_items) break;
+    const long long claim = static_cast<long long>(atomicAdd(p.slot, 1ull) - p.item_base);
+    if (claim >= p.n_items) break;
+    const int idx = static_cast<int>(claim);
     const Item it = make_item(p, idx, TILE);
     if (it.ntiles == 0) {
       if (it.split == 0 && it.len == 0) {  // empty request: zero-output marker
@@ -229,11 +254,9 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
   const int s = acquire(i);
   meta[s] = make_int4(-1, 0, 0, 0);
   mbar_arrive(&full[s]);
-  // the last producer to leave resets the counters for the next launch
-  if (atomicAdd(p.work + 1, 1) == static_cast<int>(gridDim.x) - 1) {
-    p.work[0] = 0;
-    p.work[1] = 0;
-  }
+  // out of work: the next launch of the stream (programmatic dependent launch) may take this
+  // SM as soon as this CTA drains
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 // Element d of the output of (request b, q head h).
@@ -424,7 +447,7 @@ __device__ __forceinline__ void epilogue_loop(const DecodeParams& p, const RedPi
       if (threadIdx.x % 32 == 0) mbar_arrive(r.empty);
     });
   }
-  signal_outputs(p);
+  finish_cta(p);
 }
 
 }  // namespace lam

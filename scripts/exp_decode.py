@@ -34,6 +34,8 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--P", type=int, default=64)
     ap.add_argument("--no-order", action="store_true")
+    ap.add_argument("--fused", action="store_true", help="fused append (k_new / v_new)")
+    ap.add_argument("--nbuf", type=int, default=0, help="KV buffer sets to rotate (0: >= 2 GiB)")
     a = ap.parse_args()
     c = CFG[a.cfg]
     B, Hq, Hkv, L, dt, D, P = c["B"], c["Hq"], c["Hkv"], c["L"], c["dtype"], 128, a.P
@@ -46,7 +48,7 @@ def main():
     else:
         lens_np = np.full(B, L, np.int32)
     layer_bytes = 2 * int(lens_np.sum()) * Hkv * D * esz
-    nbuf = max(2, math.ceil(2 * 2**30 / layer_bytes))
+    nbuf = a.nbuf or max(2, math.ceil(2 * 2**30 / layer_bytes))
     g = torch.Generator(device="cuda").manual_seed(0)
     bufs = []
     for _ in range(nbuf):
@@ -64,6 +66,10 @@ def main():
     lens = torch.tensor(lens_np, dtype=torch.int32, device="cuda")
     order = None if (a.no_order or not c.get("mixed")) else dec.longest_first(lens)
     out = torch.empty_like(q)
+    kn = vn = None
+    if a.fused:
+        kn = torch.empty((B, Hkv, D), dtype=dt, device="cuda").uniform_(-1, 1, generator=g)
+        vn = torch.empty_like(kn).uniform_(-1, 1, generator=g)
     for kern in a.kernels.split(","):
         for st in [int(x) for x in a.splits.split(",")]:
             try:
@@ -75,7 +81,7 @@ def main():
             def run(i):
                 kp, vp, pt = bufs[i % nbuf]
                 dec.decode(q, kp, vp, lens, page_table=pt, max_len=L, out=out, kernel=kern,
-                           split_tokens=st, request_order=order)
+                           split_tokens=st, request_order=order, k_new=kn, v_new=vn)
             for i in range(5):
                 run(i)
             torch.cuda.synchronize()
