@@ -240,7 +240,7 @@ class Workload:
     """Resident paged KV for every layer (or as many distinct layer buffers as fit) plus
     per-layer new-token inputs; one GPU's share under KV-head sharding."""
 
-    def __init__(self, w: dict, rank: int, world: int, device):
+    def __init__(self, w: dict, rank: int, world: int, device, engine: bool = False):
         import numpy as np
         import torch
 
@@ -257,9 +257,11 @@ class Workload:
         self.B_local = w["B"]                 # requests whose q/k/v this rank produces
         self.B = w["B"] * world               # requests whose local heads this rank attends
         self.layers = w["layers"]
-        self.mb = 2 if world > 1 else 1       # staggered micro-batches (multi-GPU only)
+        # the attention-worker engine (always for N > 1): two staggered micro-batches
+        engine = engine or world > 1
+        self.mb = 2 if engine else 1
         self.geo = None
-        if world > 1:
+        if engine:
             from paper_2405_01814_b200.dist import ShardGeometry
 
             self.geo = ShardGeometry(rank, world, self.layers, self.B_local, self.Hq, self.Hkv,
@@ -366,13 +368,16 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
 
         dist.init_process_group("nccl", device_id=device)
     t_setup = time.time()
-    W = Workload(w, rank, world, device)
+    use_engine = world > 1 or args.engine == "peer"
+    if world == 1 and use_engine and args.transport != "peer":
+        raise SystemExit("--engine peer at one GPU needs --transport peer")
+    W = Workload(w, rank, world, device, engine=use_engine)
     log(f"[rank {rank}] setup {time.time() - t_setup:.1f}s: {W.resident}/{W.layers} layers resident, "
         f"kernel={W.kernel} splits={W.splits} chunk={W.chunk}")
 
     stream = torch.cuda.current_stream(device)
     engine = None
-    if world > 1:
+    if use_engine:
         from paper_2405_01814_b200.dist import HeadShardedAttention
 
         def attend(layer, m, q, k, v, out):  # fused append + decode, straight from the
@@ -455,8 +460,13 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
     barrier()
 
     # ---- timed region (device-resident inputs)
-    ev = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)]
-           for _ in range(W.layers * W.mb)] for _ in range(args.steps)]
+    # Self-synchronising peer launches overlap their neighbours (programmatic dependent launch);
+    # an event between two launches would serialise them, so the timed region then carries
+    # only the step events and a launch's duration is the step time / launches (an upper bound).
+    pdl = engine is not None and args.transport == "peer" and \
+        os.environ.get("LAM_PEER_SYNC", "kernel") == "kernel" and os.environ.get("LAM_PDL", "1") != "0"
+    ev = [None if pdl else [[torch.cuda.Event(enable_timing=True) for _ in range(2)]
+                            for _ in range(W.layers * W.mb)] for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(device.index if "CUDA_VISIBLE_DEVICES" not in os.environ else
                            int(os.environ["CUDA_VISIBLE_DEVICES"].split(",")[device.index]))
@@ -471,8 +481,9 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
     barrier()
     clocks = sampler.stop() if rank == 0 else None
     ms_total = t0.elapsed_time(t1)
-    kern_ms = [e[0].elapsed_time(e[1]) for s in range(args.steps) for e in ev[s]]
     ms_step = ms_total / max(args.steps, 1)
+    kern_ms = ([ms_step / (W.layers * W.mb)] if pdl else
+               [e[0].elapsed_time(e[1]) for s in range(args.steps) for e in ev[s]])
     if dist is not None:
         t = torch.tensor([ms_step, statistics.mean(kern_ms)], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -481,6 +492,16 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
         kern_avg = statistics.mean(kern_ms)
     launches = args.steps * W.layers * W.mb * (2 if args.separate_append else 1)
     alone_ms = None
+    if pdl:
+        # diagnostic: the same step with launches serialised and timed one by one
+        os.environ["LAM_PDL"] = "0"
+        ev1 = [[torch.cuda.Event(enable_timing=True) for _ in range(2)]
+               for _ in range(W.layers * W.mb)]
+        barrier()
+        step(ev1)
+        barrier()
+        os.environ["LAM_PDL"] = "1"
+        alone_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in ev1)
     if engine is not None and args.transport != "peer":
         # the same decode launch with no collective in flight (diagnoses comm interference)
         g = W.geo
@@ -523,7 +544,9 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
                    "seq_len": int(W.max_len), "sum_seq_len": int(W.lens.sum()) ,
                    "layers": W.layers, "kv_layers_resident": W.resident,
                    "q_heads": W.Hq, "kv_heads": W.Hkv, "head_dim": W.D, "page_size": w["P"],
-                   "parallelism": f"kv-head sharded x{world} ({args.transport})" if world > 1 else "single GPU",
+                   "parallelism": (f"kv-head sharded x{world} ({args.transport})" if world > 1 else
+                                   "single GPU" + (", attention-worker engine (2 micro-batches, peer transport)"
+                                                   if use_engine else "")),
                    "l2": f"inputs {W.kv_bytes_layer * W.resident / 2**30:.0f} GiB of KV >> 126 MB L2; no flush needed",
                    "kernel": W.kernel, "splits": W.splits, "split_tokens": W.chunk},
         "attn_tokens_per_s": W.B / (ms_step / 1e3),
@@ -534,6 +557,9 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650",
                      "kernel": f"decode_{W.kernel}", "bytes_per_launch": W.decode_bytes_per_launch,
                      "avg_launch_ms": kern_avg, "traffic": ncu_traffic(args.workload, world),
+                     "launch_timing": ("step time / launches (back-to-back launches overlap under "
+                                       "programmatic dependent launch)" if pdl else
+                                       "CUDA events around every launch"),
                      "alone_launch_ms": alone_ms},
         "gpu_launches": launches,
         "clocks": clocks,
@@ -575,7 +601,8 @@ def run_e2e(args, W, engine, dist, device, stream):
         for _ in range(max(1, args.warmup)):
             step_mg()
         torch.cuda.synchronize(device)
-        dist.barrier()
+        if dist is not None:
+            dist.barrier()
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record(stream)
         for _ in range(args.steps):
@@ -583,7 +610,8 @@ def run_e2e(args, W, engine, dist, device, stream):
         t1.record(stream)
         torch.cuda.synchronize(device)
         t = torch.tensor([t0.elapsed_time(t1) / max(args.steps, 1)], device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if dist is not None:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t[0])
         h2d = h_qkv.numel() * h_qkv.element_size()
         d2h = h_out.numel() * h_out.element_size()
@@ -656,6 +684,9 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=3.0)
     ap.add_argument("--transport", default="nccl", choices=["nccl", "peer"],
                     help="multi-GPU scatter/gather: NCCL all-to-all or zero-copy NVLink peer memory")
+    ap.add_argument("--engine", default="local", choices=["local", "peer"],
+                    help="one GPU: plain per-layer launches, or the attention-worker engine of the "
+                         "multi-GPU runs (2 micro-batches, self-synchronising launches)")
     ap.add_argument("--separate-append", action="store_true",
                     help="lam_kv_append + lam_decode per layer instead of the fused launch")
     args = ap.parse_args()

@@ -306,7 +306,12 @@ class PeerShardedAttention:
         self.flags = raw[self.off_flags: self.off_flags + 2 * MB * N * 4].view(torch.int32).view(2, MB, N)
         # exchange handles; map every peer's buffer
         handles = [None] * N
-        dist.all_gather_object(handles, bytes(handle))
+        if dist is None:
+            if N != 1:
+                raise ValueError("more than one rank needs a process group to exchange handles")
+            handles[0] = bytes(handle)
+        else:
+            dist.all_gather_object(handles, bytes(handle))
         self.peer = []
         for r in range(N):
             if r == g.rank:
@@ -316,7 +321,8 @@ class PeerShardedAttention:
             p = C.c_void_p()
             _lib.check(self.lib.lam_peer_open(ctx.handle, hb, C.byref(p)))
             self.peer.append(p.value)
-        dist.barrier()
+        if dist is not None:
+            dist.barrier()
         self.compute = torch.cuda.current_stream(device)
         self.model = torch.cuda.Stream(device=device)   # model-worker side signalling
         self.h2d = torch.cuda.Stream(device=device)

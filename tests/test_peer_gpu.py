@@ -1,0 +1,157 @@
+"""lam_decode_peer on one GPU: rows grouped by source with per-source q/k/v and output buffers,
+in-kernel sequence-number wait / publish, and programmatic dependent launch — checked bitwise
+against lam_decode on the same rows (identical arithmetic, only the addressing differs)."""
+import ctypes as C
+import math
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _setup(n_src=2, Bh=4, Hq=8, Hkv=2, D=128, P=64, seed=0):
+    from paper_2405_01814_b200.kvcache import PagedKVCache
+
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    B = n_src * Bh
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(1, 700, B).astype(np.int32)
+    cache = PagedKVCache(1, Hkv, D, P, int((-(-lens // P)).sum()) + 1, B, int(-(-lens.max() // P)),
+                         dtype=torch.bfloat16, device=torch.device("cuda"), shuffle_seed=seed)
+    cache.set_lengths(lens)
+    cache.sync()
+    cache.fill_random(g)
+    W = Hq + 2 * Hkv
+    qkv = [torch.empty((Bh, W, D), dtype=torch.bfloat16, device="cuda").uniform_(-1, 1, generator=g)
+           for _ in range(n_src)]
+    return cache, lens, qkv, dict(n_src=n_src, Bh=Bh, Hq=Hq, Hkv=Hkv, D=D, W=W)
+
+
+def _reference(cache, lens, qkv, s):
+    """lam_decode with fused append over the concatenated rows."""
+    from paper_2405_01814_b200 import decode as dec
+
+    Hq, Hkv = s["Hq"], s["Hkv"]
+    packed = torch.cat(qkv, 0)
+    k = cache.k[0].clone()
+    v = cache.v[0].clone()
+    out = dec.decode(packed[:, :Hq], k, v, cache.seq_lens, page_table=cache.page_table,
+                     max_len=int(lens.max()), k_new=packed[:, Hq:Hq + Hkv],
+                     v_new=packed[:, Hq + Hkv:])
+    return out, k, v
+
+
+@pytest.mark.parametrize("sync", ["kernel", "none"])
+def test_decode_peer_matches_decode(built, sync):
+    from paper_2405_01814_b200 import _lib, decode as dec
+
+    cache, lens, qkv, s = _setup()
+    want, k_want, v_want = _reference(cache, lens, qkv, s)
+    n_src, Bh, Hq, Hkv, D, W = (s[x] for x in ("n_src", "Bh", "Hq", "Hkv", "D", "W"))
+    outs = [torch.zeros((Bh, Hq, D), dtype=torch.bfloat16, device="cuda") for _ in range(n_src)]
+    flags = torch.zeros(2 * n_src, dtype=torch.int32, device="cuda")
+    qd = torch.empty((n_src * Bh, Hq, D), dtype=torch.bfloat16, device="cuda")
+    a, _ = dec.make_args(qd, cache.k[0], cache.v[0], cache.seq_lens, page_table=cache.page_table,
+                         max_len=int(lens.max()), out=qd)
+    a.q_batch_stride = a.new_batch_stride = W * D
+    io = _lib.PeerIO()
+    io.n_src, io.rows_per_src = n_src, Bh
+    for i in range(n_src):
+        io.q_src[i] = qkv[i].data_ptr()
+        io.out_dst[i] = outs[i].data_ptr()
+    io.k_new_offset, io.v_new_offset = Hq * D, (Hq + Hkv) * D
+    lib, ctx = _lib.load(), _lib.context(0)
+    Ptrs = C.c_void_p * n_src
+    ready = Ptrs(*[flags.data_ptr() + 4 * i for i in range(n_src)])
+    done = Ptrs(*[flags.data_ptr() + 4 * (n_src + i) for i in range(n_src)])
+    main = torch.cuda.current_stream()
+    side = torch.cuda.Stream()
+    if sync == "kernel":
+        io.n_wait = io.n_done = n_src
+        io.wait_value = io.done_value = 1
+        for i in range(n_src):
+            io.wait_flags[i] = ready[i]
+            io.done_flags[i] = done[i]
+        torch.cuda.synchronize()
+        # the launch is enqueued first and waits inside the kernel for the publication
+        _lib.check(lib.lam_decode_peer(ctx.handle, a, io, main.cuda_stream))
+        _lib.check(lib.lam_stream_signal(ctx.handle, ready, n_src, 1, side.cuda_stream))
+        _lib.check(lib.lam_stream_wait(ctx.handle, done, n_src, 1, side.cuda_stream))
+        side.synchronize()  # returns only once the kernel published its outputs
+    else:
+        _lib.check(lib.lam_decode_peer(ctx.handle, a, io, main.cuda_stream))
+    torch.cuda.synchronize()
+    got = torch.cat(outs, 0)
+    assert torch.equal(got, want)
+    assert torch.equal(cache.k[0], k_want) and torch.equal(cache.v[0], v_want)
+    if sync == "kernel":
+        assert flags.tolist() == [1] * (2 * n_src)
+
+
+def test_decode_peer_back_to_back_overlapping_launches(built):
+    """Many self-synchronising launches in a row (programmatic dependent launch, launch slots
+    reused round-robin): every launch's outputs and publication are correct."""
+    from paper_2405_01814_b200 import _lib, decode as dec
+
+    cache, lens, qkv, s = _setup(n_src=1, Bh=16, Hq=8, Hkv=1)
+    n_src, Bh, Hq, Hkv, D, W = (s[x] for x in ("n_src", "Bh", "Hq", "Hkv", "D", "W"))
+    lib, ctx = _lib.load(), _lib.context(0)
+    n = 12
+    flags = torch.zeros(2, dtype=torch.int32, device="cuda")
+    outs = [torch.zeros((Bh, Hq, D), dtype=torch.bfloat16, device="cuda") for _ in range(n)]
+    qd = torch.empty((Bh, Hq, D), dtype=torch.bfloat16, device="cuda")
+    # no fused append here: every launch reads the same pools, so all outputs must be equal
+    a, _ = dec.make_args(qd, cache.k[0], cache.v[0], cache.seq_lens, page_table=cache.page_table,
+                         max_len=int(lens.max()), out=qd)
+    a.q_batch_stride = W * D
+    want = dec.decode(qkv[0][:, :Hq], cache.k[0], cache.v[0], cache.seq_lens,
+                      page_table=cache.page_table, max_len=int(lens.max()))
+    torch.cuda.synchronize()
+    ready = C.c_void_p(flags.data_ptr())
+    done = C.c_void_p(flags.data_ptr() + 4)
+    side = torch.cuda.Stream()
+    stream = torch.cuda.current_stream().cuda_stream
+    ios = []
+    for i in range(n):
+        io = _lib.PeerIO()
+        io.n_src, io.rows_per_src = 1, Bh
+        io.q_src[0], io.out_dst[0] = qkv[0].data_ptr(), outs[i].data_ptr()
+        io.n_wait = io.n_done = 1
+        io.wait_value = io.done_value = i + 1
+        io.wait_flags[0], io.done_flags[0] = ready.value, done.value
+        ios.append(io)
+        _lib.check(lib.lam_decode_peer(ctx.handle, a, io, stream))
+    for i in range(n):  # publish inputs one launch at a time, in order
+        arr = (C.c_void_p * 1)(ready.value)
+        _lib.check(lib.lam_stream_signal(ctx.handle, arr, 1, i + 1, side.cuda_stream))
+    torch.cuda.synchronize()
+    for i in range(n):
+        assert torch.equal(outs[i], want), i
+    assert flags.tolist() == [n, n]
+    # the publication is monotonic: the last launch published last
+    del ios
+
+
+def test_decode_peer_validation(built):
+    from paper_2405_01814_b200 import _lib
+
+    lib, ctx = _lib.load(), _lib.context(0)
+    a = _lib.DecodeArgs()
+    io = _lib.PeerIO()
+    with pytest.raises(_lib.ValidationError):
+        _lib.check(lib.lam_decode_peer(ctx.handle, a, None, None))
+    cache, lens, qkv, s = _setup()
+    from paper_2405_01814_b200 import decode as dec
+
+    qd = torch.empty((8, 8, 128), dtype=torch.bfloat16, device="cuda")
+    a, _ = dec.make_args(qd, cache.k[0], cache.v[0], cache.seq_lens, page_table=cache.page_table,
+                         max_len=int(lens.max()), out=qd)
+    io.n_src, io.rows_per_src = 3, 4  # 3 * 4 != batch 8
+    with pytest.raises(_lib.ValidationError):
+        _lib.check(lib.lam_decode_peer(ctx.handle, a, io, None))
+    io.n_src, io.rows_per_src = 2, 4
+    with pytest.raises(_lib.ValidationError, match="null"):
+        _lib.check(lib.lam_decode_peer(ctx.handle, a, io, None))
+    assert math.isfinite(1.0)
