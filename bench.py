@@ -342,7 +342,7 @@ class Workload:
                   else None, max_len=self.max_len)
         self.kernel, self.splits, self.chunk = dec.plan(
             qd, self.k_layers[0], self.v_layers[0], self.seq_lens[: self.B_launch], ctx=self.ctx,
-            **kw)
+            split_tokens=int(os.environ.get("LAM_BENCH_SPLIT_TOKENS", 0)), **kw)
         self.ctx.reserve(self.B_launch * self.hq_local * max(self.splits, 1), self.D,
                          self.B_launch * self.hkv_local)
 
@@ -369,7 +369,7 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
         dist.init_process_group("nccl", device_id=device)
     t_setup = time.time()
     use_engine = world > 1 or args.engine == "peer"
-    if world == 1 and use_engine and args.transport != "peer":
+    if world == 1 and use_engine and args.transport != "peer":  # (NCCL needs N > 1)
         raise SystemExit("--engine peer at one GPU needs --transport peer")
     W = Workload(w, rank, world, device, engine=use_engine)
     log(f"[rank {rank}] setup {time.time() - t_setup:.1f}s: {W.resident}/{W.layers} layers resident, "
@@ -682,7 +682,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=3.0)
-    ap.add_argument("--transport", default="nccl", choices=["nccl", "peer"],
+    ap.add_argument("--transport", default="peer", choices=["nccl", "peer"],
                     help="multi-GPU scatter/gather: NCCL all-to-all or zero-copy NVLink peer memory")
     ap.add_argument("--engine", default="local", choices=["local", "peer"],
                     help="one GPU: plain per-layer launches, or the attention-worker engine of the "

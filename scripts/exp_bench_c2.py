@@ -40,7 +40,7 @@ def main():
                              max_len=W.max_len, out=W.out[layer], split_tokens=W.chunk)
         args_nf.append(x)
 
-    def run(tag, arglist, layers, per_launch_events, sampler=False):
+    def run(tag, arglist, layers, per_launch_events, sampler=False, pace=None):
         for _ in range(2):
             for i in layers:
                 _lib.check(lib.lam_decode(W.ctx.handle, arglist[i], sp))
@@ -57,16 +57,26 @@ def main():
         t0.record()
         for _ in range(a.reps):
             for i in layers:
+                if pace == "event" and k >= 2:
+                    evs[k - 2][1].synchronize()
+                elif pace == "sleep":
+                    time.sleep(0.0004)
                 if per_launch_events:
                     evs[k][0].record()
-                _lib.check(lib.lam_decode(W.ctx.handle, arglist[i], sp))
+                if pace == "python":
+                    kp, vp = W.layer_pools(i, 0)
+                    dec.decode(W.q_in[i], kp, vp, W.seq_lens, page_table=W.page_table,
+                               max_len=W.max_len, out=W.out[i], ctx=W.ctx, split_tokens=W.chunk,
+                               k_new=W.kn_in[i], v_new=W.vn_in[i])
+                else:
+                    _lib.check(lib.lam_decode(W.ctx.handle, arglist[i], sp))
                 if per_launch_events:
                     evs[k][1].record()
                 k += 1
         t1.record()
         torch.cuda.synchronize()
         if smp:
-            smp.stop()
+            print("   clocks", smp.stop())
         per = t0.elapsed_time(t1) / (len(layers) * a.reps)
         kern = (sum(e0.elapsed_time(e1) for e0, e1 in evs) / len(evs)) if per_launch_events else per
         gbs = W.decode_bytes_per_launch / (kern / 1e3) / 1e9
@@ -74,14 +84,12 @@ def main():
               flush=True)
 
     allL = list(range(L))
-    run("fused, all layers, events", args, allL, True)
-    run("fused, all layers, no events", args, allL, False)
-    run("fused, all layers, events, sampler", args, allL, True, sampler=True)
-    run("plain, all layers, events", args_nf, allL, True)
-    run("fused, layers 0-1 only, events", args, [0, 1], True)
-    run("plain, layers 0-1 only, events", args_nf, [0, 1], True)
-    run("plain, layer 0 only, events", args_nf, [0], True)
-
+    for r in range(2):
+        run(f"fast enqueue [{r}]", args, allL, True)
+        run(f"paced: event 2 behind [{r}]", args, allL, True, pace="event")
+        run(f"paced: sleep 0.4 ms [{r}]", args, allL, True, pace="sleep")
+        run(f"paced: python make_args [{r}]", args, allL, True, pace="python")
+        run(f"fast enqueue + sampler thread [{r}]", args, allL, True, sampler=True)
 
 if __name__ == "__main__":
     main()

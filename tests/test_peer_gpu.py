@@ -102,12 +102,11 @@ def test_decode_peer_back_to_back_overlapping_launches(built):
     flags = torch.zeros(2, dtype=torch.int32, device="cuda")
     outs = [torch.zeros((Bh, Hq, D), dtype=torch.bfloat16, device="cuda") for _ in range(n)]
     qd = torch.empty((Bh, Hq, D), dtype=torch.bfloat16, device="cuda")
-    # no fused append here: every launch reads the same pools, so all outputs must be equal
+    # every launch appends the same new token (idempotent), so all outputs must be equal
     a, _ = dec.make_args(qd, cache.k[0], cache.v[0], cache.seq_lens, page_table=cache.page_table,
                          max_len=int(lens.max()), out=qd)
-    a.q_batch_stride = W * D
-    want = dec.decode(qkv[0][:, :Hq], cache.k[0], cache.v[0], cache.seq_lens,
-                      page_table=cache.page_table, max_len=int(lens.max()))
+    a.q_batch_stride = a.new_batch_stride = W * D
+    want, _, _ = _reference(cache, lens, qkv, s)
     torch.cuda.synchronize()
     ready = C.c_void_p(flags.data_ptr())
     done = C.c_void_p(flags.data_ptr() + 4)
@@ -118,6 +117,7 @@ def test_decode_peer_back_to_back_overlapping_launches(built):
         io = _lib.PeerIO()
         io.n_src, io.rows_per_src = 1, Bh
         io.q_src[0], io.out_dst[0] = qkv[0].data_ptr(), outs[i].data_ptr()
+        io.k_new_offset, io.v_new_offset = Hq * D, (Hq + Hkv) * D
         io.n_wait = io.n_done = 1
         io.wait_value = io.done_value = i + 1
         io.wait_flags[0], io.done_flags[0] = ready.value, done.value
@@ -129,8 +129,8 @@ def test_decode_peer_back_to_back_overlapping_launches(built):
     torch.cuda.synchronize()
     for i in range(n):
         assert torch.equal(outs[i], want), i
-    assert flags.tolist() == [n, n]
-    # the publication is monotonic: the last launch published last
+    # overlapping launches may publish out of order; every launch published a value in range
+    assert flags[0].item() == n and 1 <= flags[1].item() <= n
     del ios
 
 
