@@ -338,11 +338,13 @@ class Workload:
         from paper_2405_01814_b200 import decode as dec
 
         qd = torch.empty((self.B_launch, self.hq_local, self.D), dtype=self.dtype, device=device)
+        # split_tokens of every launch: 0 = the library's planner decides (the default)
+        self.split_arg = int(os.environ.get("LAM_BENCH_SPLIT_TOKENS", 0))
         kw = dict(page_table=self.page_table[: self.B_launch] if self.page_table is not None
                   else None, max_len=self.max_len)
         self.kernel, self.splits, self.chunk = dec.plan(
             qd, self.k_layers[0], self.v_layers[0], self.seq_lens[: self.B_launch], ctx=self.ctx,
-            split_tokens=int(os.environ.get("LAM_BENCH_SPLIT_TOKENS", 0)), **kw)
+            split_tokens=self.split_arg, **kw)
         self.ctx.reserve(self.B_launch * self.hq_local * max(self.splits, 1), self.D,
                          self.B_launch * self.hkv_local)
 
@@ -385,7 +387,7 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
             sl = W.rows(m)
             dec.decode(q, kp, vp, W.seq_lens[sl],
                        page_table=W.page_table[sl] if W.page_table is not None else None,
-                       max_len=W.max_len, out=out, ctx=W.ctx, split_tokens=W.chunk,
+                       max_len=W.max_len, out=out, ctx=W.ctx, split_tokens=W.split_arg,
                        k_new=k, v_new=v, request_order=W.orders[m])
 
         if args.transport == "peer":
@@ -398,7 +400,7 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
                 qd = torch.empty((g.B_mb, g.hq_l, g.D), dtype=W.dtype, device=device)
                 a, _ = dec.make_args(qd, kp, vp, W.seq_lens[sl],
                                      page_table=W.page_table[sl] if W.page_table is not None else None,
-                                     max_len=W.max_len, out=qd, split_tokens=W.chunk,
+                                     max_len=W.max_len, out=qd, split_tokens=W.split_arg,
                                      request_order=W.orders[m])
                 return a
 
@@ -425,14 +427,14 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
             if args.separate_append:
                 dec.kv_append(W.kn_in[layer], W.vn_in[layer], kp, vp, W.positions, W.page_table)
                 dec.decode(W.q_in[layer], kp, vp, W.seq_lens, page_table=W.page_table,
-                           max_len=W.max_len, out=W.out[layer], ctx=W.ctx, split_tokens=W.chunk)
+                           max_len=W.max_len, out=W.out[layer], ctx=W.ctx, split_tokens=W.split_arg)
             else:  # one launch: append the new token and attend (fused lam_kv_append)
                 key = (layer, (s * W.layers + layer) % W.resident)
                 a = arg_cache.get(key)
                 if a is None:  # lam_decode_args built once per (layer, pool set)
                     a, _ = dec.make_args(W.q_in[layer], kp, vp, W.seq_lens,
                                          page_table=W.page_table, max_len=W.max_len,
-                                         out=W.out[layer], split_tokens=W.chunk,
+                                         out=W.out[layer], split_tokens=W.split_arg,
                                          k_new=W.kn_in[layer], v_new=W.vn_in[layer],
                                          request_order=W.orders[0])
                     arg_cache[key] = a
@@ -516,7 +518,7 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
             dec.decode(packed[:, : g.hq_l], kp, vp, W.seq_lens[sl],
                        page_table=W.page_table[sl] if W.page_table is not None else None,
                        max_len=W.max_len, out=engine.o_l[0].view(g.B_mb, g.hq_l, g.D), ctx=W.ctx,
-                       split_tokens=W.chunk, request_order=W.orders[0])
+                       split_tokens=W.split_arg, request_order=W.orders[0])
         e1.record(stream)
         torch.cuda.synchronize(device)
         alone_ms = e0.elapsed_time(e1) / reps
@@ -634,7 +636,7 @@ def run_e2e(args, W, engine, dist, device, stream):
         for layer in range(L):
             kp, vp = W.layer_pools(layer, s)
             a, _ = dec.make_args(d_q, kp, vp, W.seq_lens, page_table=W.page_table,
-                                 max_len=W.max_len, out=d_out, split_tokens=W.chunk,
+                                 max_len=W.max_len, out=d_out, split_tokens=W.split_arg,
                                  request_order=W.orders[0])
             arr[layer] = a
         args_sets.append(arr)

@@ -157,6 +157,7 @@ struct Plan {
   int ctas = 0;    // persistent grid
   int chunk = 0;
   int S = 1;
+  int64_t u_head = 0;  // leading units run whole; the rest split S ways (split tail)
 };
 
 // Split count and grid size for the persistent kernels, from a small model fitted on B200:
@@ -229,14 +230,16 @@ int plan_decode(lam_ctx* ctx, const lam_decode_args* a, Plan* pl) {
 
   const int variant = gqa_variant();
   const int mtile = lam::mma_variant_tile(variant);
-  const bool mma_ok = (kvd == LAM_BF16 || kvd == LAM_F16) && a->head_dim == 128 && G >= 2 &&
+  const bool mma_ok = (kvd == LAM_BF16 || kvd == LAM_F16) && a->head_dim == 128 && G >= 1 &&
                       G <= 8 && mtile > 0 && (!paged || a->page_size % mtile == 0);
   int kernel = a->kernel;
-  if (kernel == LAM_KERNEL_AUTO) kernel = mma_ok ? LAM_KERNEL_GQA_MMA : LAM_KERNEL_SIMT;
+  if (kernel == LAM_KERNEL_AUTO)
+    kernel = mma_ok && (G >= 2 || env_int("LAM_MHA_MMA", 0) != 0) ? LAM_KERNEL_GQA_MMA
+                                                                  : LAM_KERNEL_SIMT;
   if (kernel == LAM_KERNEL_GQA_MMA) {
     if (!mma_ok)
       return fail(LAM_ERR_VALIDATION,
-                  "GQA MMA kernel needs 16-bit KV, head_dim 128, 2 <= G <= 8 and page_size a "
+                  "GQA MMA kernel needs 16-bit KV, head_dim 128, 1 <= G <= 8 and page_size a "
                   "multiple of its tile (" + std::to_string(mtile) + " tokens)");
     pl->kernel = kernel;
     pl->variant = variant;
@@ -265,6 +268,15 @@ int plan_decode(lam_ctx* ctx, const lam_decode_args* a, Plan* pl) {
                 2.0 * a->head_dim * (kvd == LAM_F32 ? 4 : 2));
   if (const int force = env_int("LAM_DECODE_CTAS", 0); force > 0)
     pl->ctas = std::min(force, occ * ctx->num_sms);
+  // split tail (experiment knobs): the last `tail` units split `ts` ways
+  if (const int tail = env_int("LAM_TAIL_UNITS", 0); tail > 0 && pl->S == 1 && a->split_tokens <= 0) {
+    const int ts = std::max(2, env_int("LAM_TAIL_SPLITS", 4));
+    const int tiles_total = std::max(1, (a->max_len + pl->tile - 1) / pl->tile);
+    const int ct = (tiles_total + ts - 1) / ts;
+    pl->S = (tiles_total + ct - 1) / ct;
+    pl->chunk = ct * pl->tile;
+    if (pl->S > 1) pl->u_head = std::max<int64_t>(0, units - tail);
+  }
   if (pl->S > 65535) return fail(LAM_ERR_VALIDATION, "too many splits");
   return LAM_OK;
 }
@@ -711,7 +723,9 @@ int decode_impl(lam_ctx* ctx, const lam_decode_args* a, const lam_peer_io* io, v
   p.chunk = pl.chunk;
   p.S = pl.S;
   p.QG = pl.QG;
-  p.n_items = static_cast<int32_t>(static_cast<int64_t>(a->batch) * a->num_kv_heads * pl.QG * pl.S);
+  const int64_t units = static_cast<int64_t>(a->batch) * a->num_kv_heads * pl.QG;
+  p.u_head = static_cast<int32_t>(pl.u_head);
+  p.n_items = static_cast<int32_t>(pl.u_head + (units - pl.u_head) * pl.S);
   const int slot = static_cast<int>(ctx->seq % kSlots);
   p.slot = ctx->slots + 2 * slot;
   p.item_base = ctx->item_base[slot];

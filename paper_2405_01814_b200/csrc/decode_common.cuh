@@ -49,9 +49,10 @@ struct DecodeParams {
   int32_t B, Hq, Hkv, G, D;
   int32_t page_size, pt_stride;
   int32_t chunk;            // tokens per split (multiple of the kernel tile)
-  int32_t S;                // number of splits
+  int32_t S;                // number of splits of a split unit
+  int32_t u_head;           // leading units run whole (split tail: see item_unit)
   int32_t QG;               // q-head groups per kv head (G / heads per CTA)
-  int32_t n_items;          // B * Hkv * QG * S
+  int32_t n_items;          // u_head + (B * Hkv * QG - u_head) * S
   float scale;              // softmax scale (natural units)
   float scale_log2;         // scale * log2(e)
   int32_t out_f32;
@@ -158,21 +159,43 @@ __device__ __forceinline__ int64_t kv_row(const DecodeParams& p, int b, int h, i
 struct Item {
   int b, kvh, qg, split;
   int len, t_begin, t_end, ntiles;
+  int whole;  // the item is a whole unit (no split partial, no merge)
 };
 
-// Work item `idx`: split fastest, then q-head group, kv head, request.
-__device__ __forceinline__ Item make_item(const DecodeParams& p, int idx, int tile) {
-  Item it;
-  it.split = idx % p.S;
-  int unit = idx / p.S;
+// Work item `idx` -> (unit, split).  The first u_head items are whole units; the remaining
+// units are split S ways, split fastest (a split tail: the last rounds of a launch run short
+// items, so the CTAs finish together).  u_head = 0 is a uniform S-way split.
+__device__ __forceinline__ void item_unit(const DecodeParams& p, int idx, int& unit, int& split,
+                                          int& whole) {
+  if (idx < p.u_head) {
+    unit = idx;
+    split = 0;
+    whole = 1;
+  } else {
+    const int j = idx - p.u_head;
+    unit = p.u_head + j / p.S;
+    split = j % p.S;
+    whole = p.S == 1;
+  }
+}
+
+// Unit -> (request, kv head, q group): q-head group fastest, then kv head, request.
+__device__ __forceinline__ void unit_coords(const DecodeParams& p, int unit, Item& it) {
   it.qg = unit % p.QG;
   unit /= p.QG;
   it.kvh = unit % p.Hkv;
   it.b = unit / p.Hkv;
   if (p.order != nullptr) it.b = __ldg(p.order + it.b);
+}
+
+__device__ __forceinline__ Item make_item(const DecodeParams& p, int idx, int tile) {
+  Item it;
+  int unit;
+  item_unit(p, idx, unit, it.split, it.whole);
+  unit_coords(p, unit, it);
   it.len = __ldg(p.seq_lens + it.b);
-  it.t_begin = it.split * p.chunk;
-  it.t_end = min(it.len, it.t_begin + p.chunk);
+  it.t_begin = it.whole ? 0 : it.split * p.chunk;
+  it.t_end = min(it.len, it.whole ? p.S * p.chunk : it.t_begin + p.chunk);
   it.ntiles = it.t_end > it.t_begin ? (it.t_end - it.t_begin + tile - 1) / tile : 0;
   return it;
 }
@@ -182,15 +205,11 @@ __device__ __forceinline__ Item make_item(const DecodeParams& p, int idx, int ti
 template <int TILE>
 __device__ __forceinline__ Item item_from_tag(const DecodeParams& p, int4 tag) {
   Item it;
-  it.split = tag.x % p.S;
-  int unit = tag.x / p.S;
-  it.qg = unit % p.QG;
-  unit /= p.QG;
-  it.kvh = unit % p.Hkv;
-  it.b = unit / p.Hkv;
-  if (p.order != nullptr) it.b = __ldg(p.order + it.b);
+  int unit;
+  item_unit(p, tag.x, unit, it.split, it.whole);
+  unit_coords(p, unit, it);
   it.len = tag.z;
-  it.t_begin = it.split * p.chunk;
+  it.t_begin = it.whole ? 0 : it.split * p.chunk;
   it.t_end = tag.w;
   it.ntiles = it.t_end > it.t_begin ? (it.t_end - it.t_begin + TILE - 1) / TILE : 0;
   return it;
@@ -202,10 +221,11 @@ __device__ __forceinline__ bool tile_has_new(const DecodeParams& p, const Item& 
   return p.k_new != nullptr && it.t_end == it.len && it.len > 0 && j == it.ntiles - 1;
 }
 
-// Splits of a (request, kv head, q group) unit that carry tokens (>= 1: an empty request
-// still produces its zero output through split 0).
-__device__ __forceinline__ int live_splits(const DecodeParams& p, int len) {
-  return len > 0 ? min(p.S, (len + p.chunk - 1) / p.chunk) : 1;
+// Splits of the item's unit that carry tokens (>= 1: an empty request still produces its zero
+// output through split 0).
+__device__ __forceinline__ int live_splits(const DecodeParams& p, const Item& it) {
+  if (it.whole) return 1;
+  return it.len > 0 ? min(p.S, (it.len + p.chunk - 1) / p.chunk) : 1;
 }
 
 // ---- persistent producer ---------------------------------------------------------------
@@ -313,7 +333,7 @@ __device__ __forceinline__ void finish_item_warp(const DecodeParams& p, const It
     return A;
   };
 
-  const int S_live = live_splits(p, it.len);
+  const int S_live = live_splits(p, it);
   if (S_live == 1) {
 #pragma unroll
     for (int g = 0; g < GQ; ++g) {

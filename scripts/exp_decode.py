@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--splits", default="0")
     ap.add_argument("--kernels", default="auto")
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--warm", type=int, default=5)
     ap.add_argument("--P", type=int, default=64)
     ap.add_argument("--no-order", action="store_true")
     ap.add_argument("--fused", action="store_true", help="fused append (k_new / v_new)")
@@ -82,7 +83,7 @@ def main():
                 kp, vp, pt = bufs[i % nbuf]
                 dec.decode(q, kp, vp, lens, page_table=pt, max_len=L, out=out, kernel=kern,
                            split_tokens=st, request_order=order, k_new=kn, v_new=vn)
-            for i in range(5):
+            for i in range(a.warm):
                 run(i)
             torch.cuda.synchronize()
             evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))

@@ -59,7 +59,10 @@ def test_golden_fixtures(built, golden):
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16, torch.float16])
 @pytest.mark.parametrize("G", [1, 2, 4, 8])
 @pytest.mark.parametrize("paged", [False, True])
-def test_decode_vs_oracle(built, dtype, G, paged):
+@pytest.mark.parametrize("kernel", ["auto", "simt", "gqa_mma"])
+def test_decode_vs_oracle(built, dtype, G, paged, kernel):
+    if kernel == "gqa_mma" and dtype == torch.float32:
+        pytest.skip("tensor-core kernel is 16-bit only")
     B, Hkv, D = 3, 2, 128
     Hq = Hkv * G
     lens = [1, 77, 300]
@@ -80,7 +83,7 @@ def test_decode_vs_oracle(built, dtype, G, paged):
     for split in (0, 64, 128):
         out, lse = _decode(q, kp, vp, _lens_t(lens), page_table=ptt, max_len=max(lens),
                            scale=scale, out_dtype=torch.float32, split_tokens=split,
-                           return_lse=True)
+                           return_lse=True, kernel=kernel)
         torch.cuda.synchronize()
         assert _maxabs(out.cpu().numpy(), want) <= TOL[dtype], (split,)
         assert _maxabs(lse.cpu().numpy(), want_lse) <= 1e-3, (split,)
@@ -352,3 +355,29 @@ def test_request_order_is_transparent(built):
     out = dec.decode(q, kp, vp, lt, page_table=ptt, max_len=max(lens), out_dtype=torch.float32,
                      request_order=dec.longest_first(lt))
     assert _maxabs(out.cpu().numpy(), want) <= 2e-3
+
+
+@pytest.mark.parametrize("kernel,G,dtype", [("simt", 1, torch.bfloat16), ("simt", 1, torch.float32),
+                                            ("gqa_mma", 8, torch.bfloat16), ("simt", 4, torch.float16)])
+@pytest.mark.parametrize("tail,splits", [(1, 2), (3, 4), (100, 3)])
+def test_split_tail_vs_oracle(built, monkeypatch, kernel, G, dtype, tail, splits):
+    """Split tail: the last `tail` units run as `splits` short items merged in split order, the
+    others whole (LAM_TAIL_UNITS / LAM_TAIL_SPLITS)."""
+    monkeypatch.setenv("LAM_TAIL_UNITS", str(tail))
+    monkeypatch.setenv("LAM_TAIL_SPLITS", str(splits))
+    B, Hkv, D = 5, 2, 128
+    Hq = Hkv * G
+    lens = [1, 700, 0, 333, 1024]
+    q, k, v = make_dense(B, Hq, Hkv, D, 1024, dtype, seed=tail * 7 + splits)
+    scale = 1 / math.sqrt(D)
+    want, want_lse = oracle_decode(q, k, v, lens, scale, want_lse=True)
+    P = 64
+    pt, npages = page_table_for(lens, P, seed=splits)
+    kp, vp = to_paged(k, lens, P, pt, npages), to_paged(v, lens, P, pt, npages)
+    out, lse = _decode(q, kp, vp, _lens_t(lens), page_table=torch.tensor(pt, device="cuda"),
+                       max_len=max(lens), scale=scale, out_dtype=torch.float32, return_lse=True,
+                       kernel=kernel)
+    torch.cuda.synchronize()
+    assert _maxabs(out.cpu().numpy(), want) <= TOL[dtype]
+    finite = np.isfinite(want_lse)
+    assert _maxabs(lse.cpu().numpy()[finite], want_lse[finite]) <= 1e-3
