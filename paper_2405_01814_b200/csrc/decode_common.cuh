@@ -56,7 +56,7 @@ struct DecodeParams {
   float scale;              // softmax scale (natural units)
   float scale_log2;         // scale * log2(e)
   int32_t out_f32;
-  int32_t flags;            // reserved (tuning experiments)
+  int32_t flags;            // diagnostics: bit 4 = consumers skip the math (streaming only)
   // fused append (optional): the new token of request b (position seq_lens[b] - 1) comes from
   // k_new/v_new (request b, kv head h at + b * new_stride + h * D); the kernel attends over it
   // from shared memory and writes it into the pools for later steps.
@@ -401,12 +401,33 @@ __device__ __forceinline__ void finish_item_warp(const DecodeParams& p, const It
     float A[DPL];
 #pragma unroll
     for (int e = 0; e < DPL; ++e) A[e] = 0.f;
-    const int n = min(32, S_live);
-    for (int j = 0; j < n; ++j) {
-      const float wj = __shfl_sync(0xffffffffu, w, j);
-      const float* src = p.ws_acc + (row0 + j) * D + lane;
+    constexpr int kBatch = 8;  // splits whose slices are all in flight at once
+    if (S_live <= kBatch) {
+      // every live split's slice is loaded before the first use: one L2 round trip per head
+      // instead of one per split (the merge runs on the epilogue warp, which the consumers
+      // wait for at their next hand-off)
+      float v[kBatch][DPL];
 #pragma unroll
-      for (int e = 0; e < DPL; ++e) A[e] = fmaf(wj, __ldcg(src + e * 32), A[e]);
+      for (int j = 0; j < kBatch; ++j)
+#pragma unroll
+        for (int e = 0; e < DPL; ++e)
+          v[j][e] = j < S_live ? __ldcg(p.ws_acc + (row0 + j) * D + lane + e * 32) : 0.f;
+#pragma unroll
+      for (int j = 0; j < kBatch; ++j) {
+        const float wj = __shfl_sync(0xffffffffu, w, j);
+        if (j < S_live) {
+#pragma unroll
+          for (int e = 0; e < DPL; ++e) A[e] = fmaf(wj, v[j][e], A[e]);
+        }
+      }
+    } else {
+      const int n = min(32, S_live);
+      for (int j = 0; j < n; ++j) {
+        const float wj = __shfl_sync(0xffffffffu, w, j);
+        const float* src = p.ws_acc + (row0 + j) * D + lane;
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) A[e] = fmaf(wj, __ldcg(src + e * 32), A[e]);
+      }
     }
     for (int s0 = 32; s0 < S_live; s0 += 32) {  // more than 32 splits (rare)
       float w2 = 0.f, m2 = -INFINITY;

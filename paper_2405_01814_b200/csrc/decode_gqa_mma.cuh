@@ -175,7 +175,7 @@ __global__ void __launch_bounds__((NW_ + 2) * 32)
     const int new_r = tile_has_new<TILE>(p, it, mt.y) ? it.len - 1 - (it.t_begin + mt.y * TILE)
                                                       : -1;
     const bool my_new = new_r >= warp * 16 && new_r < warp * 16 + 16;
-    if (nval > 0) {
+    if (nval > 0 && !(p.flags & 16)) {  // (flags bit 4: streaming-only diagnostic)
       if (my_new) {
         const uint8_t* kn = qslot + s * C::SLOT_BYTES + C::Q_BYTES;
         const int c = lane & 15;

@@ -145,7 +145,7 @@ __global__ void __launch_bounds__((NW + 2) * 32)
         for (int e = 0; e < VEC; ++e) acc[g][e] = 0.f;
       }
     }
-    if (it.ntiles > 0) {
+    if (it.ntiles > 0 && !(p.flags & 16)) {  // (flags bit 4: streaming-only diagnostic)
       const int tile_tok = it.t_begin + mt.y * TILE;
       const uint32_t k_addr = ring_addr + s * 2 * C::TILE_BYTES;
       const uint32_t v_addr = k_addr + C::TILE_BYTES;
