@@ -165,12 +165,16 @@ struct Plan {
 // with dynamic claiming, `full` rounds of items run on every CTA and the remaining `rem` items
 // run on rem CTAs at min(BW_CHIP / rem, RATE_SM); every item boundary costs ~C_ITEM.
 //   T(S, ctas) = full * t_item(ctas) + [rem > 0] t_item(rem) + ceil(items / ctas) * C_ITEM
-// Measured choices: C1, C2, C3 -> S = 1; C4 -> S = 4; grid 128-132 CTAs for the GQA shapes
-// whose item counts (512, 1024) divide evenly there (up to +4 % over a full 148-CTA grid).
+// Measured choices (scripts/call46.sh, call47.sh): C1, C2, C3, C5 -> S = 1; C4 -> S = 4; the
+// 512-unit and 128-unit sharded GQA launches (c3n8, c4n8) -> S = 1.
 void choose_splits(Plan& pl, int64_t units, int max_len, int max_ctas, int split_tokens,
                    double bytes_per_token) {
+  // An item boundary costs the tensor-core kernel more (8 q heads of epilogue per item, and the
+  // split partial / merge round trips): measured ~2.5-5 us per extra item vs ~0.5-2 us (SIMT).
   static const double BW_CHIP = 7.0e12, RATE_SM = env_int("LAM_PLAN_RATE_SM", 50) * 1e9,
-                      C_ITEM = env_int("LAM_PLAN_CITEM_NS", 2000) * 1e-9;
+                      C_ITEM_SIMT = env_int("LAM_PLAN_CITEM_NS", 2000) * 1e-9,
+                      C_ITEM_MMA = env_int("LAM_PLAN_CITEM_MMA_NS", 5000) * 1e-9;
+  const double C_ITEM = pl.kernel == LAM_KERNEL_GQA_MMA ? C_ITEM_MMA : C_ITEM_SIMT;
   const int tiles_total = std::max(1, (max_len + pl.tile - 1) / pl.tile);
   const int occ_per_sm = std::max(1, max_ctas / 148);
   double best = 1e300;

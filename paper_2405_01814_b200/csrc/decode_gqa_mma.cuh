@@ -47,7 +47,7 @@ __device__ __forceinline__ uint32_t swz(int r, int c) {
 }
 
 template <typename T, int NW_, int STAGES_>
-__global__ void __launch_bounds__((NW_ + 2) * 32)
+__global__ void __launch_bounds__((NW_ + 2) * 32, 1)
     decode_gqa_mma_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap kmap,
                           const __grid_constant__ CUtensorMap vmap) {
   using C = MmaCfg<NW_, STAGES_>;

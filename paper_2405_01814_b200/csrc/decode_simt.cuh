@@ -48,7 +48,7 @@ struct SimtCfg {
 };
 
 template <typename T, int D, int GQ, int NW, int TILE, int STAGES>
-__global__ void __launch_bounds__((NW + 2) * 32)
+__global__ void __launch_bounds__((NW + 2) * 32, 1)
     decode_simt_kernel(const DecodeParams p) {
   using C = SimtCfg<T, D, GQ, NW, TILE, STAGES>;
   constexpr int VEC = C::VEC, LPR = C::LPR, RPI = C::RPI, TPW = C::TPW, ITER = C::ITER;
