@@ -237,8 +237,13 @@ int plan_decode(lam_ctx* ctx, const lam_decode_args* a, Plan* pl) {
   const bool mma_ok = (kvd == LAM_BF16 || kvd == LAM_F16) && a->head_dim == 128 && G >= 1 &&
                       G <= 8 && mtile > 0 && (!paged || a->page_size % mtile == 0);
   int kernel = a->kernel;
+  // 16-bit KV with D = 128 runs on the tensor-core kernel for every group size, MHA (G = 1)
+  // included: both kernels stream at the same rate when timed alone (7226 GB/s, C2), but under
+  // a sustained step the SIMT kernel's FMA/shuffle load draws more SM power, the clocks drop
+  // further under sw_power_cap (1736-1814 vs 1822-1886 MHz) and the step is 5 % slower
+  // (scripts/call49.sh).  LAM_MHA_MMA=0 restores the SIMT kernel for G = 1.
   if (kernel == LAM_KERNEL_AUTO)
-    kernel = mma_ok && (G >= 2 || env_int("LAM_MHA_MMA", 0) != 0) ? LAM_KERNEL_GQA_MMA
+    kernel = mma_ok && (G >= 2 || env_int("LAM_MHA_MMA", 1) != 0) ? LAM_KERNEL_GQA_MMA
                                                                   : LAM_KERNEL_SIMT;
   if (kernel == LAM_KERNEL_GQA_MMA) {
     if (!mma_ok)
