@@ -56,7 +56,8 @@ struct DecodeParams {
   float scale;              // softmax scale (natural units)
   float scale_log2;         // scale * log2(e)
   int32_t out_f32;
-  int32_t flags;            // diagnostics: bit 4 = consumers skip the math (streaming only)
+  int32_t flags;            // diagnostics: bit 4 = consumers skip the math (streaming only),
+                            // bit 5 = the epilogue warp skips its work
   // fused append (optional): the new token of request b (position seq_lens[b] - 1) comes from
   // k_new/v_new (request b, kv head h at + b * new_stride + h * D); the kernel attends over it
   // from shared memory and writes it into the pools for later steps.
@@ -279,9 +280,41 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-// Element d of the output of (request b, q head h).
-template <typename T, int D>
-__device__ __forceinline__ void store_out(const DecodeParams& p, int b, int h, int d, float v) {
+// N contiguous floats (N = 2 or 4, 8- or 16-byte aligned) from shared / global memory.
+template <int N>
+__device__ __forceinline__ void ld_vec(const float* src, float (&v)[N]) {
+  static_assert(N == 2 || N == 4, "vector width");
+  if constexpr (N == 4) {
+    const float4 x = *reinterpret_cast<const float4*>(src);
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+  } else {
+    const float2 x = *reinterpret_cast<const float2*>(src);
+    v[0] = x.x; v[1] = x.y;
+  }
+}
+template <int N>
+__device__ __forceinline__ void ldcg_vec(const float* src, float (&v)[N]) {  // L2, not L1
+  if constexpr (N == 4) {
+    const float4 x = __ldcg(reinterpret_cast<const float4*>(src));
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+  } else {
+    const float2 x = __ldcg(reinterpret_cast<const float2*>(src));
+    v[0] = x.x; v[1] = x.y;
+  }
+}
+template <int N>
+__device__ __forceinline__ void st_vec(float* dst, const float (&v)[N]) {
+  if constexpr (N == 4)
+    *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+  else
+    *reinterpret_cast<float2*>(dst) = make_float2(v[0], v[1]);
+}
+
+// Elements [d, d + N) of the output of (request b, q head h), local or in the source rank's
+// buffer (peer transport); fp32 or the KV type.
+template <typename T, int D, int N>
+__device__ __forceinline__ void store_out_vec(const DecodeParams& p, int b, int h, int d,
+                                              const float (&v)[N]) {
   void* base = p.out;
   if (p.src_rows > 0) {
     const int s = b / p.src_rows;
@@ -289,23 +322,46 @@ __device__ __forceinline__ void store_out(const DecodeParams& p, int b, int h, i
     b -= s * p.src_rows;
   }
   const int64_t idx = (static_cast<int64_t>(b) * p.Hq + h) * D + d;
-  if (p.out_f32)
-    static_cast<float*>(base)[idx] = v;
-  else
-    static_cast<T*>(base)[idx] = Elem<T>::from_float(v);
+  if (sizeof(T) == 4 || p.out_f32) {
+    st_vec<N>(static_cast<float*>(base) + idx, v);
+  } else if constexpr (sizeof(T) == 2) {
+    T* dst = static_cast<T*>(base) + idx;
+    if constexpr (N == 4)
+      *reinterpret_cast<uint2*>(dst) =
+          make_uint2(Elem<T>::pack2(v[0], v[1]), Elem<T>::pack2(v[2], v[3]));
+    else
+      *reinterpret_cast<uint32_t*>(dst) = Elem<T>::pack2(v[0], v[1]);
+  }
+}
+
+__device__ __forceinline__ int atom_add_acq_rel_gpu(int32_t* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v)
+               : "memory");
+  return old;
 }
 
 // Split-K epilogue of one work item, run by the CTA's dedicated epilogue warp while the
 // consumer warps already stream the next item.  red_m/red_l/red_acc hold the NW per-warp
 // partials for GQ q heads: red_m[w*GQ+g] (log2 units if kLog2, else natural), red_l[w*GQ+g],
-// red_acc[(w*GQ+g)*D + d].  `nvalid` q heads of the group are real (the MMA kernel pads to 8).
-template <typename T, int D, int GQ, int NW, bool kLog2, class Release>
+// red_acc[(w*GQ+g)*RS + d] (row stride RS >= D floats, a multiple of 4).  `nvalid` q heads of
+// the group are real (the MMA kernel pads to 8).
+//
+// Lane l owns the D/32 contiguous dims [l*D/32, (l+1)*D/32) of every head, so the warp
+// partials, the split partials and the outputs all move as 8- or 16-byte vectors.  The split
+// partial is published with one acq_rel atomic by lane 0 after a warp barrier (no full
+// sequentially-consistent fence), and the last split of a unit merges the live partials in
+// split order (merge, attention.cpp:100-118, identity early-out: an empty split weighs 0).
+template <typename T, int D, int GQ, int NW, bool kLog2, int RS, class Release>
 __device__ __forceinline__ void finish_item_warp(const DecodeParams& p, const Item& it,
                                                  int nvalid, const float* red_m,
                                                  const float* red_l, const float* red_acc,
                                                  Release release) {
   constexpr float kLn2 = 0.6931471805599453f;
+  constexpr int DPL = D / 32;  // contiguous output dims per lane
+  static_assert(RS % 4 == 0 && RS >= D, "partial row stride");
   const int lane = threadIdx.x % 32;
+  const int d0 = lane * DPL;
   const int b = it.b;
   const int qh0 = it.kvh * p.G + it.qg * GQ;
 
@@ -326,25 +382,33 @@ __device__ __forceinline__ void finish_item_warp(const DecodeParams& p, const It
     cta_m[g] = (M == -INFINITY) ? -INFINITY : (kLog2 ? M * kLn2 : M);  // natural units
     cta_l[g] = L;
   }
-  auto merged_acc = [&](int g, int d) {
-    float A = 0.f;
+  auto merged_acc = [&](int g, float (&A)[DPL]) {
 #pragma unroll
-    for (int w = 0; w < NW; ++w) A = fmaf(wsc[g][w], red_acc[(w * GQ + g) * D + d], A);
-    return A;
+    for (int e = 0; e < DPL; ++e) A[e] = 0.f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      float x[DPL];
+      ld_vec<DPL>(red_acc + (w * GQ + g) * RS + d0, x);
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) A[e] = fmaf(wsc[g][w], x[e], A[e]);
+    }
   };
 
   const int S_live = live_splits(p, it);
   if (S_live == 1) {
 #pragma unroll
     for (int g = 0; g < GQ; ++g) {
-      if (g >= nvalid) break;
-      for (int d = lane; d < D; d += 32) {
+      if (g < nvalid) {
+        float A[DPL];
+        merged_acc(g, A);
         const float L = cta_l[g];
-        store_out<T, D>(p, b, qh0 + g, d, L > 0.f ? merged_acc(g, d) / L : 0.f);
+        const float inv = L > 0.f ? 1.f / L : 0.f;
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) A[e] *= inv;
+        store_out_vec<T, D, DPL>(p, b, qh0 + g, d0, A);
+        if (lane == 0 && p.lse != nullptr)
+          p.lse[static_cast<int64_t>(b) * p.Hq + qh0 + g] = L > 0.f ? cta_m[g] + logf(L) : -INFINITY;
       }
-      if (lane == 0 && p.lse != nullptr)
-        p.lse[static_cast<int64_t>(b) * p.Hq + qh0 + g] =
-            cta_l[g] > 0.f ? cta_m[g] + logf(cta_l[g]) : -INFINITY;
     }
     release();
     return;
@@ -353,28 +417,25 @@ __device__ __forceinline__ void finish_item_warp(const DecodeParams& p, const It
   // 2. write this split's partial, then count it in.
 #pragma unroll
   for (int g = 0; g < GQ; ++g) {
-    if (g >= nvalid) break;
-    const int64_t row = (static_cast<int64_t>(b) * p.Hq + qh0 + g) * p.S + it.split;
-    for (int d = lane; d < D; d += 32) p.ws_acc[row * D + d] = merged_acc(g, d);
-    if (lane == 0) {
-      p.ws_ml[row * 2 + 0] = cta_m[g];
-      p.ws_ml[row * 2 + 1] = cta_l[g];
+    if (g < nvalid) {
+      const int64_t row = (static_cast<int64_t>(b) * p.Hq + qh0 + g) * p.S + it.split;
+      float A[DPL];
+      merged_acc(g, A);
+      st_vec<DPL>(p.ws_acc + row * D + d0, A);
+      if (lane == 0)
+        *reinterpret_cast<float2*>(p.ws_ml + row * 2) = make_float2(cta_m[g], cta_l[g]);
     }
   }
   release();  // the consumers may refill red_* while this warp counts and merges splits
-  __threadfence();
-  __syncwarp();
+  __syncwarp();  // every lane's partial stores precede lane 0's release
   int32_t* counter = p.counters + (static_cast<int64_t>(b) * p.Hkv + it.kvh) * p.QG + it.qg;
   int last = 0;
-  if (lane == 0) last = (atomicAdd(counter, 1) == S_live - 1);
+  if (lane == 0) last = (atom_add_acq_rel_gpu(counter, 1) == S_live - 1);
   last = __shfl_sync(0xffffffffu, last, 0);
   if (!last) return;
-  __threadfence();
 
-  // 3. last split of this unit: merge the live partials in split order and finalize.
-  //    The split statistics of every q head are loaded together (lane s holds split s), so a
-  //    merge costs a couple of L2 round trips, not one chain per head.
-  constexpr int DPL = D / 32;  // output dims per lane
+  // 3. last split of this unit: merge the live partials in split order and finalize.  Lane s
+  //    holds split s's statistics; every live split's slice of a head is loaded before use.
   float ms[GQ], ls[GQ];
 #pragma unroll
   for (int g = 0; g < GQ; ++g) {
@@ -389,66 +450,67 @@ __device__ __forceinline__ void finish_item_warp(const DecodeParams& p, const It
   }
 #pragma unroll
   for (int g = 0; g < GQ; ++g) {
-    if (g >= nvalid) break;
+    if (g >= nvalid) continue;
     const int64_t row0 = (static_cast<int64_t>(b) * p.Hq + qh0 + g) * p.S;
     float M = ms[g];
     for (int s0 = 32 + lane; s0 < S_live; s0 += 32) M = fmaxf(M, __ldcg(p.ws_ml + (row0 + s0) * 2));
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-    // lanes >= S_live hold -inf and weigh nothing; splits beyond 32 take a slow path
+    // lanes >= S_live hold -inf and weigh nothing
     const float w = ms[g] == -INFINITY ? 0.f : expf(ms[g] - M);
     float L = w * ls[g];
     float A[DPL];
 #pragma unroll
     for (int e = 0; e < DPL; ++e) A[e] = 0.f;
-    constexpr int kBatch = 8;  // splits whose slices are all in flight at once
+    constexpr int kBatch = 8;
     if (S_live <= kBatch) {
-      // every live split's slice is loaded before the first use: one L2 round trip per head
-      // instead of one per split (the merge runs on the epilogue warp, which the consumers
-      // wait for at their next hand-off)
       float v[kBatch][DPL];
 #pragma unroll
-      for (int j = 0; j < kBatch; ++j)
+      for (int j = 0; j < kBatch; ++j) {
+        if (j < S_live) {
+          ldcg_vec<DPL>(p.ws_acc + (row0 + j) * D + d0, v[j]);
+        } else {
 #pragma unroll
-        for (int e = 0; e < DPL; ++e)
-          v[j][e] = j < S_live ? __ldcg(p.ws_acc + (row0 + j) * D + lane + e * 32) : 0.f;
+          for (int e = 0; e < DPL; ++e) v[j][e] = 0.f;
+        }
+      }
 #pragma unroll
       for (int j = 0; j < kBatch; ++j) {
         const float wj = __shfl_sync(0xffffffffu, w, j);
-        if (j < S_live) {
 #pragma unroll
-          for (int e = 0; e < DPL; ++e) A[e] = fmaf(wj, v[j][e], A[e]);
-        }
+        for (int e = 0; e < DPL; ++e) A[e] = fmaf(wj, v[j][e], A[e]);
       }
     } else {
       const int n = min(32, S_live);
       for (int j = 0; j < n; ++j) {
         const float wj = __shfl_sync(0xffffffffu, w, j);
-        const float* src = p.ws_acc + (row0 + j) * D + lane;
+        float v[DPL];
+        ldcg_vec<DPL>(p.ws_acc + (row0 + j) * D + d0, v);
 #pragma unroll
-        for (int e = 0; e < DPL; ++e) A[e] = fmaf(wj, __ldcg(src + e * 32), A[e]);
+        for (int e = 0; e < DPL; ++e) A[e] = fmaf(wj, v[e], A[e]);
       }
     }
     for (int s0 = 32; s0 < S_live; s0 += 32) {  // more than 32 splits (rare)
-      float w2 = 0.f, m2 = -INFINITY;
+      float w2 = 0.f;
       if (s0 + lane < S_live) {
         const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + (row0 + s0 + lane) * 2));
-        m2 = ml.x;
         w2 = ml.x == -INFINITY ? 0.f : expf(ml.x - M);
         L += w2 * ml.y;
       }
-      (void)m2;
       for (int j = 0; j < min(32, S_live - s0); ++j) {
         const float wj = __shfl_sync(0xffffffffu, w2, j);
-        const float* src = p.ws_acc + (row0 + s0 + j) * D + lane;
+        float v[DPL];
+        ldcg_vec<DPL>(p.ws_acc + (row0 + s0 + j) * D + d0, v);
 #pragma unroll
-        for (int e = 0; e < DPL; ++e) A[e] = fmaf(wj, __ldcg(src + e * 32), A[e]);
+        for (int e = 0; e < DPL; ++e) A[e] = fmaf(wj, v[e], A[e]);
       }
     }
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
+    const float inv = L > 0.f ? 1.f / L : 0.f;
 #pragma unroll
-    for (int e = 0; e < DPL; ++e) store_out<T, D>(p, b, qh0 + g, lane + e * 32, L > 0.f ? A[e] / L : 0.f);
+    for (int e = 0; e < DPL; ++e) A[e] *= inv;
+    store_out_vec<T, D, DPL>(p, b, qh0 + g, d0, A);
     if (lane == 0 && p.lse != nullptr)
       p.lse[static_cast<int64_t>(b) * p.Hq + qh0 + g] = L > 0.f ? M + logf(L) : -INFINITY;
   }
@@ -474,7 +536,7 @@ __device__ __forceinline__ void red_commit(const RedPipe& r) {
 }
 
 // Epilogue warp main loop.
-template <typename T, int D, int GQ, int NW, bool kLog2, int TILE>
+template <typename T, int D, int GQ, int NW, bool kLog2, int TILE, int RS>
 __device__ __forceinline__ void epilogue_loop(const DecodeParams& p, const RedPipe& r,
                                               int nvalid, const float* red_m,
                                               const float* red_l, const float* red_acc) {
@@ -483,7 +545,12 @@ __device__ __forceinline__ void epilogue_loop(const DecodeParams& p, const RedPi
     const int idx = r.item[0];
     if (idx < 0) break;
     const Item it = item_from_tag<TILE>(p, make_int4(idx, 0, r.item[1], r.item[2]));
-    finish_item_warp<T, D, GQ, NW, kLog2>(p, it, nvalid, red_m, red_l, red_acc, [&] {
+    if (p.flags & 32) {  // diagnostic: no epilogue work (outputs are not written)
+      __syncwarp();
+      if (threadIdx.x % 32 == 0) mbar_arrive(r.empty);
+      continue;
+    }
+    finish_item_warp<T, D, GQ, NW, kLog2, RS>(p, it, nvalid, red_m, red_l, red_acc, [&] {
       __syncwarp();
       if (threadIdx.x % 32 == 0) mbar_arrive(r.empty);
     });

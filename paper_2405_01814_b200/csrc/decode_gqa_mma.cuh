@@ -32,7 +32,10 @@ struct MmaCfg {
   static constexpr int Q_BYTES = GQ * D * 2;        // one item's (padded) q rows
   static constexpr int ROW_BYTES = D * 2;
   static constexpr int SLOT_BYTES = Q_BYTES + 2 * ROW_BYTES;  // q rows + fused new k, v rows
-  static constexpr int RED_FLOATS = NW * GQ * (D + 2);
+  // warp partial rows padded to D + 4 floats: the fragment-layout stores of the 4 column
+  // pairs of a lane quad land in distinct banks, and rows stay 16-byte aligned
+  static constexpr int RS = D + 4;
+  static constexpr int RED_FLOATS = NW * GQ * (RS + 2);
   static constexpr int SMEM_BYTES = RING_BYTES + STAGES * SLOT_BYTES + RED_FLOATS * 4 +
                                     STAGES * 16 + STAGES * 8 + (2 * STAGES + 4) * 8 + 16 + 64 +
                                     1024;  // +align slack
@@ -114,7 +117,7 @@ __global__ void __launch_bounds__((NW_ + 2) * 32, 1)
     return;
   }
   if (warp == NW + 1) {
-    epilogue_loop<T, D, GQ, NW, true, TILE>(p, red, G, red_m, red_l, red_acc);
+    epilogue_loop<T, D, GQ, NW, true, TILE, C::RS>(p, red, G, red_m, red_l, red_acc);
     return;
   }
 
@@ -269,10 +272,10 @@ __global__ void __launch_bounds__((NW_ + 2) * 32, 1)
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
         const int d = t * 16 + gr;
-        red_acc[(warp * GQ + gc) * D + d] = o[t][0];
-        red_acc[(warp * GQ + gc + 1) * D + d] = o[t][1];
-        red_acc[(warp * GQ + gc) * D + d + 8] = o[t][2];
-        red_acc[(warp * GQ + gc + 1) * D + d + 8] = o[t][3];
+        red_acc[(warp * GQ + gc) * C::RS + d] = o[t][0];
+        red_acc[(warp * GQ + gc + 1) * C::RS + d] = o[t][1];
+        red_acc[(warp * GQ + gc) * C::RS + d + 8] = o[t][2];
+        red_acc[(warp * GQ + gc + 1) * C::RS + d + 8] = o[t][3];
       }
       if (warp == 0 && lane == 0) {
         red.item[0] = mt.x;

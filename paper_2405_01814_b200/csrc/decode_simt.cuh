@@ -109,7 +109,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, 1)
     return;
   }
   if (warp == NW + 1) {
-    epilogue_loop<T, D, GQ, NW, C::kLog2, TILE>(p, red, GQ, red_m, red_l, red_acc);
+    epilogue_loop<T, D, GQ, NW, C::kLog2, TILE, D>(p, red, GQ, red_m, red_l, red_acc);
     return;
   }
 
@@ -246,7 +246,9 @@ __global__ void __launch_bounds__((NW + 2) * 32, 1)
 #pragma unroll
         for (int g = 0; g < GQ; ++g) {
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) red_acc[(warp * GQ + g) * D + sub * VEC + e] = acc[g][e];
+          for (int e = 0; e < VEC; e += 4)
+            *reinterpret_cast<float4*>(red_acc + (warp * GQ + g) * D + sub * VEC + e) =
+                make_float4(acc[g][e], acc[g][e + 1], acc[g][e + 2], acc[g][e + 3]);
           if (sub == 0) {
             red_m[warp * GQ + g] = m[g];
             red_l[warp * GQ + g] = l[g];
