@@ -135,7 +135,7 @@ class HeadShardedAttention:
                 for m in range(MB):
                     self._scatter(layer, m, qkv_in)
                     self._attend(layer, m, None)
-                    self._a2a(out[layer, m], self.o_l[m])
+                    self._gather(layer, m, out)
             return
         comm, comp = self.comm, self.compute
         comm.wait_stream(comp)  # inputs produced on the compute stream are visible
@@ -167,7 +167,7 @@ class HeadShardedAttention:
         def gather(layer, m):
             with torch.cuda.stream(comm):
                 comm.wait_event(done[layer][m])
-                self._a2a(out[layer, m], self.o_l[m])
+                self._gather(layer, m, out)
                 gath[m].record(comm)
             if host_out is not None:
                 self.d2h.wait_event(gath[m])
@@ -198,6 +198,9 @@ class HeadShardedAttention:
     def _scatter(self, layer, m, qkv_in):
         self._a2a(self.qkv_r[m], qkv_in[layer, m])
 
+    def _gather(self, layer, m, out):
+        self._a2a(out[layer, m], self.o_l[m])
+
     def _attend(self, layer, m, e):
         g = self.geo
         packed = self.qkv_r[m].view(g.B_mb, g.W, g.D)
@@ -215,6 +218,160 @@ class HeadShardedAttention:
             self.attend_fn(layer, m, q, out)
         if e is not None:
             e[1].record(self.compute)
+
+
+class RequestGeometry:
+    """Request-level partition of the attention worker pool (§8(f) row 4): every rank owns ALL
+    KV heads of the requests `request_partition` (attention.cpp:179-203, greedy longest-first
+    bin packing over KV sizes) assigns to it.  This is the fallback when num_kv_heads is not
+    divisible by the number of devices (head_partition's ValidationError, attention.cpp:167-170),
+    and it balances mixed-length batches by KV bytes instead of by head count.
+
+    Global request r = s * B_local + b lives on model worker s; micro-batch m of every model
+    worker is its local requests [m * Bh, (m + 1) * Bh).  Per (layer, micro-batch):
+      * scatter: model worker s sends each of its micro-batch requests' packed QKV-projection
+        rows [Hq + 2 Hkv][D] to owner[r] (one variable-split all-to-all); its send order is
+        `send_order[m]`, i.e. its requests grouped by destination;
+      * the owner decodes the rows it received — grouped by source, in the senders' order —
+        over its KV store, where micro-batch m occupies rows [row_off[m], row_off[m] + n_recv[m]);
+      * gather: the reverse all-to-all returns the outputs [Hq][D] in the sender's send order.
+    """
+
+    def __init__(self, rank: int, world: int, layers: int, B_local: int, Hq: int, Hkv: int,
+                 D: int, owner, micro_batches: int = 2):
+        if Hq % Hkv:
+            raise ValueError("query heads must be a multiple of KV heads")
+        if B_local % micro_batches:
+            raise ValueError("B_local must split evenly into micro-batches")
+        owner = [int(x) for x in owner]
+        if len(owner) != world * B_local or any(not 0 <= d < world for d in owner):
+            raise ValueError("owner must map every global request to a rank")
+        self.rank, self.world, self.layers = rank, world, layers
+        self.B_local, self.Hq, self.Hkv, self.D = B_local, Hq, Hkv, D
+        self.micro_batches, self.owner = micro_batches, owner
+        Bh = self.Bh
+        # model-worker side: this rank's micro-batch requests grouped by destination (stable)
+        self.send_order, self.send_counts = [], []
+        # attention side: requests received per micro-batch, grouped by source, sender order
+        self.recv_reqs, self.recv_counts, self.row_off = [], [], []
+        off = 0
+        for m in range(micro_batches):
+            mb = range(m * Bh, (m + 1) * Bh)
+            order = sorted(mb, key=lambda b: (owner[rank * B_local + b], b))
+            self.send_order.append(order)
+            self.send_counts.append([sum(owner[rank * B_local + b] == d for b in mb)
+                                     for d in range(world)])
+            reqs, counts = [], []
+            for s in range(world):
+                got = [s * B_local + b for b in sorted(range(m * Bh, (m + 1) * Bh),
+                                                        key=lambda b: (owner[s * B_local + b], b))
+                       if owner[s * B_local + b] == rank]
+                reqs += got
+                counts.append(len(got))
+            self.recv_reqs.append(reqs)
+            self.recv_counts.append(counts)
+            self.row_off.append(off)
+            off += len(reqs)
+        self.B_attn = off  # requests this rank attends to (all micro-batches)
+
+    @property
+    def Bh(self) -> int:
+        return self.B_local // self.micro_batches
+
+    @property
+    def W(self) -> int:
+        return self.Hq + 2 * self.Hkv
+
+    @property
+    def rows(self) -> list:
+        """attention-side KV rows: global request of every row of this rank's store"""
+        return [r for reqs in self.recv_reqs for r in reqs]
+
+    def q_shape(self):
+        return (self.layers, self.micro_batches, self.Bh, self.Hq, self.D)
+
+    def qkv_shape(self):
+        return (self.layers, self.micro_batches, self.Bh, self.W, self.D)
+
+
+class RequestShardedAttention(HeadShardedAttention):
+    """The attention worker pool partitioned by request (RequestGeometry) with the same two
+    staggered micro-batches and streams as HeadShardedAttention; only the exchange differs:
+    variable-split all-to-alls of whole requests instead of equal head shards.
+
+    qkv_in [L, MB, Bh, Hq + 2 Hkv, D] and out [L, MB, Bh, Hq, D] are in each micro-batch's
+    send order (geo.send_order; `pack_request_inputs` / `unpack_request_outputs` convert).
+    attend(layer, m, q, k, v, out) (fused) or append + attend work on the n_recv[m] rows that
+    start at geo.row_off[m] of the local store, with all Hq / Hkv heads.
+    """
+
+    def __init__(self, geo: RequestGeometry, dist, append: Callable, attend: Callable,
+                 device: torch.device, dtype: torch.dtype):
+        self.geo, self.dist = geo, dist
+        self.append_fn, self.attend_fn = append, attend
+        self.device, self.dtype = device, dtype
+        g = geo
+        self.qkv_r = [torch.empty((sum(g.recv_counts[m]), g.W, g.D), dtype=dtype, device=device)
+                      for m in range(g.micro_batches)]
+        self.o_l = [torch.empty((sum(g.recv_counts[m]), g.Hq, g.D), dtype=dtype, device=device)
+                    for m in range(g.micro_batches)]
+        self.cuda = device.type == "cuda"
+        if self.cuda:
+            self.comm = torch.cuda.Stream(device=device)
+            self.compute = torch.cuda.current_stream(device)
+            self.h2d = torch.cuda.Stream(device=device)
+            self.d2h = torch.cuda.Stream(device=device)
+
+    def _scatter(self, layer, m, qkv_in):
+        g = self.geo
+        self.dist.all_to_all_single(self.qkv_r[m], qkv_in[layer, m],
+                                    output_split_sizes=g.recv_counts[m],
+                                    input_split_sizes=g.send_counts[m])
+
+    def _gather(self, layer, m, out):
+        g = self.geo
+        self.dist.all_to_all_single(out[layer, m], self.o_l[m],
+                                    output_split_sizes=g.send_counts[m],
+                                    input_split_sizes=g.recv_counts[m])
+
+    def _attend(self, layer, m, e):
+        g = self.geo
+        if self.qkv_r[m].shape[0] == 0:
+            return
+        packed = self.qkv_r[m]
+        q = packed[:, : g.Hq]
+        k = packed[:, g.Hq: g.Hq + g.Hkv]
+        v = packed[:, g.Hq + g.Hkv:]
+        out = self.o_l[m]
+        if self.append_fn is not None:
+            self.append_fn(layer, m, k, v)
+        if e is not None:
+            e[0].record(self.compute)
+        if self.append_fn is None:
+            self.attend_fn(layer, m, q, k, v, out)
+        else:
+            self.attend_fn(layer, m, q, out)
+        if e is not None:
+            e[1].record(self.compute)
+
+
+def pack_request_inputs(geo: RequestGeometry, q: torch.Tensor, kn: torch.Tensor,
+                        vn: torch.Tensor) -> torch.Tensor:
+    """[L, B_local, H, D] model-worker tensors -> [L, MB, Bh, Hq + 2 Hkv, D] in send order."""
+    idx = torch.tensor([b for m in range(geo.micro_batches) for b in geo.send_order[m]],
+                       dtype=torch.long, device=q.device)
+    x = torch.cat([q, kn, vn], dim=2).index_select(1, idx)
+    return x.view(q.shape[0], geo.micro_batches, geo.Bh, geo.W, geo.D).contiguous()
+
+
+def unpack_request_outputs(geo: RequestGeometry, out: torch.Tensor) -> torch.Tensor:
+    """[L, MB, Bh, Hq, D] in send order -> [L, B_local, Hq, D] in local request order."""
+    L = out.shape[0]
+    flat = out.reshape(L, geo.B_local, geo.Hq, geo.D)
+    idx = [b for m in range(geo.micro_batches) for b in geo.send_order[m]]
+    inv = torch.empty(geo.B_local, dtype=torch.long)
+    inv[torch.tensor(idx)] = torch.arange(geo.B_local)
+    return flat.index_select(1, inv.to(out.device))
 
 
 def stitch_outputs(out: torch.Tensor) -> torch.Tensor:

@@ -22,7 +22,83 @@ from paper_2405_01814_b200.kvcache import PagedKVCache  # noqa: E402
 L, B_LOCAL, HQ, HKV, D, MB, P = 3, 8, 64, 8, 128, 2, 64
 
 
+def main_request():
+    """Request-partitioned pool (dist.RequestShardedAttention): every rank holds all KV heads of
+    the requests request_partition gives it; Hkv = 3 is not divisible by the world size."""
+    from paper_2405_01814_b200.attention import request_partition
+    from paper_2405_01814_b200.dist import (RequestGeometry, RequestShardedAttention,
+                                            pack_request_inputs, unpack_request_outputs)
+
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    dev = torch.device("cuda", int(os.environ["LOCAL_RANK"]))
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", device_id=dev)
+    hq, hkv = 24, 3
+    rng = np.random.default_rng(13)
+    B = world * B_LOCAL
+    lens = np.exp(rng.uniform(np.log(8), np.log(2000), B)).astype(np.int32)  # mixed lengths
+    owner = request_partition((lens + 1).astype(np.float64), world).device_of
+    geo = RequestGeometry(rank, world, L, B_LOCAL, hq, hkv, D, owner, MB)
+    lmax = int(lens.max()) + 1
+    bf = lambda x: torch.from_numpy(x).to(torch.bfloat16)  # noqa: E731
+    ck = bf(rng.uniform(-1, 1, (L, B, hkv, lmax, D)).astype(np.float32))
+    cv = bf(rng.uniform(-1, 1, (L, B, hkv, lmax, D)).astype(np.float32))
+    q = bf(rng.uniform(-1, 1, (L, B, hq, D)).astype(np.float32))
+    kn = bf(rng.uniform(-1, 1, (L, B, hkv, D)).astype(np.float32))
+    vn = bf(rng.uniform(-1, 1, (L, B, hkv, D)).astype(np.float32))
+    rows = np.array(geo.rows, np.int64)
+    row_lens = lens[rows] + 1
+    n_rows = max(len(rows), 1)
+    cache = PagedKVCache(L, hkv, D, P, int((-(-row_lens // P)).sum()) + 2, n_rows,
+                         int(-(-row_lens.max() // P)) if len(rows) else 1, dtype=torch.bfloat16,
+                         device=dev, shuffle_seed=rank)
+    if len(rows):
+        cache.set_lengths(row_lens)
+    cache.sync()
+    pt = cache.page_table_host
+    for layer in range(L):
+        for r, req in enumerate(rows):
+            n = int(lens[req])
+            for p0 in range(0, n, P):
+                t1 = min(n, p0 + P)
+                cache.k[layer, pt[r, p0 // P], :, : t1 - p0] = ck[layer, req, :, p0:t1].to(dev)
+                cache.v[layer, pt[r, p0 // P], :, : t1 - p0] = cv[layer, req, :, p0:t1].to(dev)
+    max_len = int(row_lens.max()) if len(rows) else 1
+
+    def attend_fused(layer, m, qr, k, v, out):
+        sl = slice(geo.row_off[m], geo.row_off[m] + qr.shape[0])
+        dec.decode(qr, cache.k[layer], cache.v[layer], cache.seq_lens[sl],
+                   page_table=cache.page_table[sl], max_len=max_len, out=out, k_new=k, v_new=v)
+
+    eng = RequestShardedAttention(geo, dist, None, attend_fused, dev, torch.bfloat16)
+    mine = slice(rank * B_LOCAL, (rank + 1) * B_LOCAL)
+    qkv_in = pack_request_inputs(geo, q[:, mine], kn[:, mine], vn[:, mine]).to(dev)
+    out = torch.zeros(geo.q_shape(), dtype=torch.bfloat16, device=dev)
+    eng.step(qkv_in, out)
+    torch.cuda.synchronize()
+    got = unpack_request_outputs(geo, out).float().cpu().numpy()
+    worst = 0.0
+    for layer in range(L):
+        for b in range(B_LOCAL):
+            req = rank * B_LOCAL + b
+            k = ck[layer, req:req + 1].float().numpy().copy()
+            v = cv[layer, req:req + 1].float().numpy().copy()
+            k[0, :, lens[req]] = kn[layer, req].float().numpy()
+            v[0, :, lens[req]] = vn[layer, req].float().numpy()
+            want = O.decode_dense(q[layer, req:req + 1].float().numpy(), k, v, [lens[req] + 1],
+                                  1 / math.sqrt(D))[0]
+            worst = max(worst, float(np.abs(got[layer, b] - want).max()))
+    ok = worst <= 2e-3 + 2 ** -9
+    print(f"rank {rank} request-sharded worst max-abs {worst:.3e} {'OK' if ok else 'FAIL'}",
+          flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
 def main():
+    if os.environ.get("LAM_TEST_SHARD", "head") == "request":
+        return main_request()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     dev = torch.device("cuda", int(os.environ["LOCAL_RANK"]))
     torch.cuda.set_device(dev)

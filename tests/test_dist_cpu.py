@@ -117,3 +117,103 @@ def test_geometry_validation():
     assert (g.hq_l, g.hkv_l, g.Bh, g.B_mb, g.B_attn) == (16, 2, 64, 256, 512)
     rows = sorted(g.kv_row(s, b) for s in range(4) for b in range(128))
     assert rows == list(range(512))
+
+
+# ---- request-level partition (dist.RequestShardedAttention), KV heads not divisible by N ----
+RQ_HQ, RQ_HKV = 6, 3  # head_partition would reject 3 KV heads over 2 ranks
+
+
+def _req_problem(seed=11):
+    rng = np.random.default_rng(seed)
+    B = WORLD * B_LOCAL
+    lens = rng.integers(1, 40, B).astype(np.int32)
+    lmax = int(lens.max()) + 1
+    ck = rng.uniform(-1, 1, (L, B, RQ_HKV, lmax, D)).astype(np.float32)
+    cv = rng.uniform(-1, 1, (L, B, RQ_HKV, lmax, D)).astype(np.float32)
+    q = rng.uniform(-1, 1, (L, B, RQ_HQ, D)).astype(np.float32)
+    kn = rng.uniform(-1, 1, (L, B, RQ_HKV, D)).astype(np.float32)
+    vn = rng.uniform(-1, 1, (L, B, RQ_HKV, D)).astype(np.float32)
+    return lens, ck, cv, q, kn, vn
+
+
+def _req_owner(lens):
+    from paper_2405_01814_b200.attention import request_partition
+
+    return request_partition((lens + 1).astype(np.float64), WORLD).device_of
+
+
+def _req_worker(rank, port, result_dir):
+    sys.path.insert(0, str(ROOT))
+    import torch.distributed as dist
+
+    from oracle import oracle as O
+    from paper_2405_01814_b200.dist import (RequestGeometry, RequestShardedAttention,
+                                            pack_request_inputs, unpack_request_outputs)
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    lens, ck, cv, q, kn, vn = _req_problem()
+    geo = RequestGeometry(rank, WORLD, L, B_LOCAL, RQ_HQ, RQ_HKV, D, _req_owner(lens), MB)
+    rows = np.array(geo.rows, np.int64)
+    store_k, store_v = ck[:, rows].copy(), cv[:, rows].copy()  # all heads of owned requests
+    pos = lens[rows]
+
+    def attend(layer, m, qr, k, v, out):  # fused: append the new token, then attend
+        sl = slice(geo.row_off[m], geo.row_off[m] + qr.shape[0])
+        for i, r in enumerate(range(sl.start, sl.stop)):
+            store_k[layer, r, :, pos[r]] = k[i].contiguous().numpy()
+            store_v[layer, r, :, pos[r]] = v[i].contiguous().numpy()
+        res = O.decode_dense(qr.contiguous().numpy(), store_k[layer, sl], store_v[layer, sl],
+                             pos[sl] + 1, 1 / np.sqrt(D))
+        out.copy_(torch.from_numpy(res))
+
+    eng = RequestShardedAttention(geo, dist, None, attend, torch.device("cpu"), torch.float32)
+    mine = slice(rank * B_LOCAL, (rank + 1) * B_LOCAL)
+    qkv_in = pack_request_inputs(geo, torch.from_numpy(q[:, mine]), torch.from_numpy(kn[:, mine]),
+                                 torch.from_numpy(vn[:, mine]))
+    out = torch.zeros(geo.q_shape())
+    eng.step(qkv_in, out)
+    np.save(Path(result_dir) / f"rq{rank}.npy", unpack_request_outputs(geo, out).numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_request_sharded_exchange_matches_oracle(tmp_path):
+    import torch.multiprocessing as mp
+
+    from oracle import oracle as O
+
+    lens, ck, cv, q, kn, vn = _req_problem()
+    owner = _req_owner(lens)
+    assert sorted(set(owner)) == [0, 1]  # both ranks attend, with requests from both sources
+    os.environ["PYTHONPATH"] = str(ROOT) + os.pathsep + os.environ.get("PYTHONPATH", "")
+    mp.spawn(_req_worker, args=(_free_port(), str(tmp_path)), nprocs=WORLD, join=True)
+    for rank in range(WORLD):
+        got = np.load(tmp_path / f"rq{rank}.npy")          # [L, B_local, Hq, D]
+        for layer in range(L):
+            for b in range(B_LOCAL):
+                req = rank * B_LOCAL + b
+                k = ck[layer, req:req + 1].copy()
+                v = cv[layer, req:req + 1].copy()
+                k[0, :, lens[req]] = kn[layer, req]
+                v[0, :, lens[req]] = vn[layer, req]
+                want = O.decode_dense(q[layer, req:req + 1], k, v, [lens[req] + 1], 1 / np.sqrt(D))[0]
+                assert np.allclose(got[layer, b], want, rtol=0, atol=1e-6)
+
+
+def test_request_geometry():
+    from paper_2405_01814_b200.attention import request_partition
+    from paper_2405_01814_b200.dist import RequestGeometry
+
+    # the reference's imbalance case (test_attention.cpp:271-282): sizes 8192 + 7 x 512 over 2
+    sizes = [8192] + [512] * 7
+    a = request_partition(sizes, 2)
+    geos = [RequestGeometry(r, 2, 1, 4, 8, 1, 128, a.device_of) for r in range(2)]
+    # every request is attended exactly once, and every send count meets a receive count
+    assert sorted(r for g in geos for r in g.rows) == list(range(8))
+    for m in range(2):
+        for s in range(2):
+            for d in range(2):
+                assert geos[s].send_counts[m][d] == geos[d].recv_counts[m][s]
+    with pytest.raises(ValueError):
+        RequestGeometry(0, 2, 1, 4, 8, 1, 128, [0] * 7)
