@@ -138,8 +138,9 @@ int lam_request_partition(const double* kv_sizes, int64_t n, int64_t num_devices
  * q: [B][Hq][D] in kv_dtype.  out: [B][Hq][D] in out_dtype (kv_dtype or LAM_F32).
  * lse (nullable): [B][Hq] fp32 natural-log sum-exp of the scaled logits.
  * seq_lens: [B] int32 device array; max_len is a host upper bound used for grid sizing.
- * kernel: LAM_KERNEL_AUTO picks GQA_MMA for 16-bit KV with Hq/Hkv == 8 (or 4, 2), SIMT
- *         otherwise.  split_tokens: tokens per split-K chunk (0 = auto). */
+ * kernel: LAM_KERNEL_AUTO picks GQA_MMA (tensor cores) for 16-bit KV with D = 128 and
+ *         1 <= Hq/Hkv <= 8 — MHA included, unless the environment sets LAM_MHA_MMA=0 — and
+ *         SIMT otherwise (fp32 KV, D = 64).  split_tokens: tokens per split-K chunk (0 = auto). */
 typedef struct lam_decode_args {
   int32_t kv_dtype;
   int32_t out_dtype;
