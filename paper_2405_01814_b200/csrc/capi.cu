@@ -134,17 +134,13 @@ int make_pool_map(CUtensorMap* map, int dtype, const void* base, int64_t rows, i
 }
 
 // Kernel variants (decode.cu LAM_MMA_VARIANTS / LAM_SIMT_VARIANTS); variant 0 is the tuned
-// default, LAM_GQA_VARIANT / LAM_SIMT_VARIANT / LAM_ITEMS_PER_CTA override it for tuning.
+// default, LAM_GQA_VARIANT / LAM_SIMT_VARIANT override it for tuning.
 int gqa_variant() {
   static int v = env_int("LAM_GQA_VARIANT", 0);
   return v;
 }
 int simt_variant() {
   static int v = env_int("LAM_SIMT_VARIANT", 0);
-  return v;
-}
-int items_per_cta() {
-  static int v = env_int("LAM_ITEMS_PER_CTA", 4);
   return v;
 }
 
@@ -160,17 +156,20 @@ struct Plan {
   int64_t u_head = 0;  // leading units run whole; the rest split S ways (split tail)
 };
 
-// Split count and grid size for the persistent kernels, from a small model fitted on B200:
-// the chip streams ~BW_CHIP, one SM at most ~RATE_SM (so fewer CTAs can each stream faster);
-// with dynamic claiming, `full` rounds of items run on every CTA and the remaining `rem` items
-// run on rem CTAs at min(BW_CHIP / rem, RATE_SM); every item boundary costs ~C_ITEM.
-//   T(S, ctas) = full * t_item(ctas) + [rem > 0] t_item(rem) + ceil(items / ctas) * C_ITEM
-// Measured choices (scripts/call46.sh, call47.sh): C1, C2, C3, C5 -> S = 1; C4 -> S = 4; the
-// 512-unit and 128-unit sharded GQA launches (c3n8, c4n8) -> S = 1.
+// Split count and grid size for the persistent kernels, from a small model fitted on B200.
+// With dynamic claiming a launch of `items` equal items on `ctas` CTAs runs
+// k = ceil(items / ctas) rounds; a partial last round is not measurably faster than a full
+// one.  So for a given item count the grid is the smallest one that still needs only
+// k = ceil(items / max_ctas) rounds, ctas = ceil(items / k): the rounds are as even as they
+// can be, and each CTA streams at min(BW_CHIP / ctas, RATE_SM) (C1: 256 items on 128 CTAs
+// beat 143 CTAs by 4 %, scripts/call56.sh).  Every item boundary costs ~C_ITEM; it costs the
+// tensor-core kernel more (8 q heads of epilogue per item, split partial and merge round trips).
+//   T(S) = k * (item_bytes / min(BW_CHIP / ctas, RATE_SM) + C_ITEM)
+// The grid shrinks only by more than 5 %.  Measured choices (call46/47/54/56/57): C1 -> S = 1 on
+// 128 CTAs (+3-4 %); C2, C3, C5 -> S = 1; C4 -> S = 4; the sharded GQA launches c3n8
+// (512 units) -> S = 1 on 128 CTAs (+1.5 %), c4n8 (128 units) -> S = 1 on 128 CTAs.
 void choose_splits(Plan& pl, int64_t units, int max_len, int max_ctas, int split_tokens,
                    double bytes_per_token) {
-  // An item boundary costs the tensor-core kernel more (8 q heads of epilogue per item, and the
-  // split partial / merge round trips): measured ~2.5-5 us per extra item vs ~0.5-2 us (SIMT).
   static const double BW_CHIP = 7.0e12, RATE_SM = env_int("LAM_PLAN_RATE_SM", 50) * 1e9,
                       C_ITEM_SIMT = env_int("LAM_PLAN_CITEM_NS", 2000) * 1e-9,
                       C_ITEM_MMA = env_int("LAM_PLAN_CITEM_MMA_NS", 5000) * 1e-9;
@@ -186,21 +185,18 @@ void choose_splits(Plan& pl, int64_t units, int max_len, int max_ctas, int split
     const int s_eff = (tiles_total + c - 1) / c;
     if (split_tokens <= 0 && s_eff != s) continue;
     const double item_bytes = static_cast<double>(c) * pl.tile * bytes_per_token;
-    const int64_t items = units * s_eff;
-    const int lo = std::max(1, (max_ctas * 3) / 4);
-    for (int ctas = max_ctas; ctas >= lo; --ctas) {
-      const double rate = [&](double n) { return std::min(BW_CHIP / n, RATE_SM * occ_per_sm); }(ctas);
-      const int64_t full = items / ctas, rem = items % ctas;
-      double t = static_cast<double>(full) * item_bytes / rate;
-      if (rem > 0) t += item_bytes / std::min(BW_CHIP / static_cast<double>(rem), RATE_SM * occ_per_sm);
-      t += static_cast<double>((items + ctas - 1) / ctas) * C_ITEM *
-           (items_per_cta() > 0 ? items_per_cta() / 4.0 : 1.0);
-      // a smaller grid or more splits must win by >= 1.5 % (model noise)
-      if (t < best * (1 - 0.015)) {
-        best = t;
-        best_ct = c;
-        best_ctas = ctas;
-      }
+    const int64_t items = std::max<int64_t>(1, units * s_eff);
+    const int64_t k = (items + max_ctas - 1) / max_ctas;
+    int ctas = static_cast<int>((items + k - 1) / k);
+    // shrink only when it evens the rounds out by a margin (C3: 147 CTAs lose 0.6 % to 148)
+    if (ctas > max_ctas * 95 / 100) ctas = max_ctas;
+    const double rate = std::min(BW_CHIP / ctas, RATE_SM * occ_per_sm);
+    const double t = static_cast<double>(k) * (item_bytes / rate + C_ITEM);
+    // more splits must win by >= 1.5 % (model noise)
+    if (t < best * (1 - 0.015)) {
+      best = t;
+      best_ct = c;
+      best_ctas = ctas;
     }
   }
   pl.chunk = best_ct * pl.tile;
