@@ -683,7 +683,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=3.0)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="CPU reference sample length for cpu_baseline (seconds of CPU work)")
     ap.add_argument("--transport", default="peer", choices=["nccl", "peer"],
                     help="multi-GPU scatter/gather: NCCL all-to-all or zero-copy NVLink peer memory")
     ap.add_argument("--engine", default="local", choices=["local", "peer"],
