@@ -217,3 +217,78 @@ def test_request_geometry():
                 assert geos[s].send_counts[m][d] == geos[d].recv_counts[m][s]
     with pytest.raises(ValueError):
         RequestGeometry(0, 2, 1, 4, 8, 1, 128, [0] * 7)
+
+
+# ---- the head-sharded exchange at 8 ranks (the driver's largest scaling point), gloo ----
+W8, HQ8, HKV8, B8 = 8, 16, 8, 2
+
+
+def _w8_problem(seed=5):
+    rng = np.random.default_rng(seed)
+    B = W8 * B8
+    lens = rng.integers(1, 12, B).astype(np.int32)
+    lmax = int(lens.max()) + 1
+    ck = rng.uniform(-1, 1, (1, B, HKV8, lmax, D)).astype(np.float32)
+    cv = rng.uniform(-1, 1, (1, B, HKV8, lmax, D)).astype(np.float32)
+    q = rng.uniform(-1, 1, (1, B, HQ8, D)).astype(np.float32)
+    kn = rng.uniform(-1, 1, (1, B, HKV8, D)).astype(np.float32)
+    vn = rng.uniform(-1, 1, (1, B, HKV8, D)).astype(np.float32)
+    return lens, ck, cv, q, kn, vn
+
+
+def _w8_worker(rank, port, result_dir):
+    sys.path.insert(0, str(ROOT))
+    import torch.distributed as dist
+
+    from oracle import oracle as O
+    from paper_2405_01814_b200.dist import (HeadShardedAttention, ShardGeometry, shard_inputs,
+                                            stitch_outputs)
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=W8)
+    geo = ShardGeometry(rank, W8, 1, B8, HQ8, HKV8, D, 2)
+    lens, ck, cv, q, kn, vn = _w8_problem()
+    h0, h1 = rank * geo.hkv_l, (rank + 1) * geo.hkv_l
+    row_req = np.zeros(geo.B_attn, np.int64)
+    for src in range(W8):
+        for b in range(B8):
+            row_req[geo.kv_row(src, b)] = src * B8 + b
+    sk, sv = ck[:, row_req, h0:h1].copy(), cv[:, row_req, h0:h1].copy()
+    pos = lens[row_req]
+
+    def attend(layer, m, qr, k, v, out):
+        sl = slice(m * geo.B_mb, (m + 1) * geo.B_mb)
+        for i, r in enumerate(range(sl.start, sl.stop)):
+            sk[layer, r, :, pos[r]] = k[i].contiguous().numpy()
+            sv[layer, r, :, pos[r]] = v[i].contiguous().numpy()
+        out.copy_(torch.from_numpy(O.decode_dense(qr.contiguous().numpy(), sk[layer, sl],
+                                                  sv[layer, sl], pos[sl] + 1, 1 / np.sqrt(D))))
+
+    eng = HeadShardedAttention(geo, dist, None, attend, torch.device("cpu"), torch.float32)
+    mine = slice(rank * B8, (rank + 1) * B8)
+    qkv_in = shard_inputs(torch.from_numpy(q[:, mine]), torch.from_numpy(kn[:, mine]),
+                          torch.from_numpy(vn[:, mine]), W8, 2)
+    out = torch.zeros(geo.q_shape())
+    eng.step(qkv_in, out)
+    np.save(Path(result_dir) / f"w8_{rank}.npy", stitch_outputs(out).numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_head_sharded_exchange_8_ranks(tmp_path):
+    import torch.multiprocessing as mp
+
+    from oracle import oracle as O
+
+    os.environ["PYTHONPATH"] = str(ROOT) + os.pathsep + os.environ.get("PYTHONPATH", "")
+    mp.spawn(_w8_worker, args=(_free_port(), str(tmp_path)), nprocs=W8, join=True)
+    lens, ck, cv, q, kn, vn = _w8_problem()
+    for rank in range(W8):
+        got = np.load(tmp_path / f"w8_{rank}.npy")
+        for b in range(B8):
+            req = rank * B8 + b
+            k, v = ck[0, req:req + 1].copy(), cv[0, req:req + 1].copy()
+            k[0, :, lens[req]] = kn[0, req]
+            v[0, :, lens[req]] = vn[0, req]
+            want = O.decode_dense(q[0, req:req + 1], k, v, [lens[req] + 1], 1 / np.sqrt(D))[0]
+            assert np.allclose(got[0, b], want, rtol=0, atol=1e-6)
