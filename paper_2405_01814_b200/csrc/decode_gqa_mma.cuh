@@ -237,13 +237,20 @@ __global__ void __launch_bounds__((NW_ + 2) * 32, 1)
       l1 = l1 * al1 + (r1 + r3);
       const uint32_t b0 = movmatrix_trans(plo);
       const uint32_t b1 = movmatrix_trans(phi);
-      // O^T = O^T * alpha + V^T · P^T
+      // O^T = O^T * alpha + V^T · P^T.  Once the running max has settled, alpha is exactly 1
+      // for the whole warp on most tiles: skipping the 32 multiplies then changes no bit and
+      // saves SM issue slots (and power, which bounds the sustained step under sw_power_cap).
+      if (__any_sync(0xffffffffu, al0 != 1.f || al1 != 1.f)) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          o[t][0] *= al0;
+          o[t][1] *= al1;
+          o[t][2] *= al0;
+          o[t][3] *= al1;
+        }
+      }
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
-        o[t][0] *= al0;
-        o[t][1] *= al1;
-        o[t][2] *= al0;
-        o[t][3] *= al1;
         uint32_t a0, a1, a2, a3;
         ldmatrix_x4_trans(vb + swz<C::BOX_BYTES>(warp * 16 + v_row, t * 2 + v_chk), a0, a1, a2, a3);
         Mma16816<T>::run(o[t], a0, a1, a2, a3, b0, b1);
