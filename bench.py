@@ -374,6 +374,11 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
     if world == 1 and use_engine and args.transport != "peer":  # (NCCL needs N > 1)
         raise SystemExit("--engine peer at one GPU needs --transport peer")
     W = Workload(w, rank, world, device, engine=use_engine)
+    if args.overlap_layers is None:
+        # consecutive launches of a step are different layers (their pools are disjoint) only
+        # when the model has more than one layer; a one-layer stream would have each launch
+        # read the rows its predecessor appended, which overlap_prev's contract excludes
+        args.overlap_layers = int(W.layers >= 2 and engine_is_local(args, world))
     log(f"[rank {rank}] setup {time.time() - t_setup:.1f}s: {W.resident}/{W.layers} layers resident, "
         f"kernel={W.kernel} splits={W.splits} chunk={W.chunk}")
 
@@ -436,7 +441,8 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
                                          page_table=W.page_table, max_len=W.max_len,
                                          out=W.out[layer], split_tokens=W.split_arg,
                                          k_new=W.kn_in[layer], v_new=W.vn_in[layer],
-                                         request_order=W.orders[0])
+                                         request_order=W.orders[0],
+                                         overlap_prev=args.overlap_layers)
                     arg_cache[key] = a
                 _lib.check(lib.lam_decode(W.ctx.handle, a, sp))
             if ev is not None:
@@ -467,6 +473,7 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
     # only the step events and a launch's duration is the step time / launches (an upper bound).
     pdl = engine is not None and args.transport == "peer" and \
         os.environ.get("LAM_PEER_SYNC", "kernel") == "kernel" and os.environ.get("LAM_PDL", "1") != "0"
+    pdl = pdl or (engine is None and args.overlap_layers and not args.separate_append)
     ev = [None if pdl else [[torch.cuda.Event(enable_timing=True) for _ in range(2)]
                             for _ in range(W.layers * W.mb)] for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -550,7 +557,8 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
                                    "single GPU" + (", attention-worker engine (2 micro-batches, peer transport)"
                                                    if use_engine else "")),
                    "l2": f"inputs {W.kv_bytes_layer * W.resident / 2**30:.0f} GiB of KV >> 126 MB L2; no flush needed",
-                   "kernel": W.kernel, "splits": W.splits, "split_tokens": W.chunk},
+                   "kernel": W.kernel, "splits": W.splits, "split_tokens": W.chunk,
+                   "overlap_layers": bool(args.overlap_layers)},
         "attn_tokens_per_s": W.B / (ms_step / 1e3),
         "frac_of_hbm_roofline": value / world / peak,
         "frac_of_hbm_spec_8tbs": value / world / 8000.0,
@@ -576,6 +584,11 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def engine_is_local(args, world: int) -> bool:
+    """plain per-layer launches on one GPU (no attention-worker engine)"""
+    return world == 1 and args.engine == "local" and not args.separate_append
 
 
 def run_e2e(args, W, engine, dist, device, stream):
@@ -690,6 +703,11 @@ def main():
     ap.add_argument("--engine", default="local", choices=["local", "peer"],
                     help="one GPU: plain per-layer launches, or the attention-worker engine of the "
                          "multi-GPU runs (2 micro-batches, self-synchronising launches)")
+    ap.add_argument("--overlap-layers", type=int, default=None, choices=[0, 1],
+                    help="one GPU: each layer's launch may stream its first KV tiles while the "
+                         "previous layer's launch drains (lam_decode_args.overlap_prev; q / k_new "
+                         "/ v_new are read only after the previous launch completes).  Default: on "
+                         "for multi-layer workloads, off for one layer (c1)")
     ap.add_argument("--separate-append", action="store_true",
                     help="lam_kv_append + lam_decode per layer instead of the fused launch")
     args = ap.parse_args()

@@ -177,6 +177,12 @@ typedef struct lam_decode_args {
    * in this order (longest-processing-time-first keeps mixed-length batches balanced, in the
    * spirit of request_partition, attention.cpp:185-196).  NULL = request order. */
   const int32_t* request_order;
+  /* Overlap with the preceding kernel of the stream (programmatic dependent launch): the launch
+   * may start while that kernel drains and stream its first KV tiles, but it reads q, k_new and
+   * v_new only after that kernel has completed (griddepcontrol.wait).  The caller guarantees the
+   * preceding kernel writes neither page_table, seq_lens, request_order nor the KV rows this
+   * launch reads — e.g. consecutive layers of a decode step.  0 = ordinary stream order. */
+  int32_t overlap_prev;
 } lam_decode_args;
 
 int lam_decode(lam_ctx* ctx, const lam_decode_args* args, void* stream);

@@ -59,6 +59,7 @@ class DecodeArgs(C.Structure):
         ("v_new", C.c_void_p),
         ("new_batch_stride", C.c_int64),
         ("request_order", C.c_void_p),
+        ("overlap_prev", C.c_int32),
     ]
 
 

@@ -789,6 +789,11 @@ int decode_impl(lam_ctx* ctx, const lam_decode_args* a, const lam_peer_io* io, v
     // previous kernel's drain
     p.pdl = io->n_wait > 0 && env_int("LAM_PDL", 1) != 0;
   }
+  if (a->overlap_prev != 0 && io == nullptr) {
+    // stream the first KV tiles while the preceding kernel drains; q / k_new / v_new wait for it
+    p.pdl = 1;
+    p.defer_inputs = 1;
+  }
   p.flags = env_int("LAM_DECODE_FLAGS", 0);
   p.scale = a->scale;
   p.scale_log2 = a->scale * 1.4426950408889634f;

@@ -46,6 +46,8 @@ struct DecodeParams {
   unsigned long long* slot;
   unsigned long long item_base, done_base;
   int32_t pdl;              // launched with programmatic dependent launch
+  int32_t defer_inputs;     // (with pdl) KV tiles of the first item may stream before the
+                            // preceding grid completes; q / k_new / v_new loads wait for it
   int32_t B, Hq, Hkv, G, D;
   int32_t page_size, pt_stride;
   int32_t chunk;            // tokens per split (multiple of the kernel tile)
@@ -157,6 +159,8 @@ __device__ __forceinline__ int64_t kv_row(const DecodeParams& p, int b, int h, i
   return (blk * p.Hkv + h) * p.page_size + (t % p.page_size);
 }
 
+enum IssueMode { kIssueAll = 0, kIssueKV = 1, kIssueInputs = 2 };
+
 struct Item {
   int b, kvh, qg, split;
   int len, t_begin, t_end, ntiles;
@@ -232,8 +236,17 @@ __device__ __forceinline__ int live_splits(const DecodeParams& p, const Item& it
 // ---- persistent producer ---------------------------------------------------------------
 // meta[s] = {item, tile index, request length, item end token}; item < 0 ends the work.
 // meta_row[s] = first pool row of the stage's tile (consumers write the fused new token there).
-// `issue(s, it, j, row)` must arrive on full[s] with expect_tx and start the stage's TMA
-// copies of tile j, whose first KV row is `row`.
+// `issue(s, it, j, row, mode)` must arrive on full[s] with expect_tx for all of the stage's
+// bytes and start the stage's TMA copies of tile j, whose first KV row is `row`: mode
+// kIssueAll = every copy, kIssueKV = the K/V tile only, kIssueInputs = only the copies of
+// request inputs (q rows, fused new K/V rows) of a stage issued before with kIssueKV.
+//
+// Deferred inputs (p.defer_inputs, programmatic dependent launch): the KV cache does not depend
+// on the stream's preceding kernel but q / k_new / v_new may, so the producer streams the first
+// item's KV tiles into the free ring (at most STAGES of them, without waiting on any stage),
+// then waits for the preceding grid (griddepcontrol.wait) and issues the deferred input copies.
+// The consumers cannot finish a stage before its inputs land, so the producer must not need a
+// recycled stage before that: the prefetch stops at the ring size or the end of the item.
 //
 // Items are claimed from a global counter right after the previous item's tiles are issued.
 // Measured on B200 this dynamic schedule beats a static round-robin split by 2-3 % (per-SM
@@ -251,12 +264,17 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
     if (k >= STAGES) mbar_wait(&empty[s], ((k / STAGES) - 1) & 1);
     return s;
   };
+  bool deferring = p.defer_inputs != 0;  // first item: KV now, inputs after griddep_wait
   for (;;) {
     const long long claim = static_cast<long long>(atomicAdd(p.slot, 1ull) - p.item_base);
     if (claim >= p.n_items) break;
     const int idx = static_cast<int>(claim);
     const Item it = make_item(p, idx, TILE);
     if (it.ntiles == 0) {
+      if (deferring) {  // nothing to prefetch
+        griddep_wait();
+        deferring = false;
+      }
       if (it.split == 0 && it.len == 0) {  // empty request: zero-output marker
         const int s = acquire(i++);
         meta[s] = make_int4(idx, 0, 0, 0);
@@ -264,14 +282,28 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
       }                                    // (an empty split has nothing to merge)
       continue;
     }
+    const int i0 = i;  // first stage index of this item
     for (int j = 0; j < it.ntiles; ++j) {
+      if (deferring && i >= STAGES) {  // ring full: the inputs must land before any reuse
+        griddep_wait();
+        for (int jj = 0; jj < j; ++jj)
+          issue((i0 + jj) % STAGES, it, jj, meta_row[(i0 + jj) % STAGES], kIssueInputs);
+        deferring = false;
+      }
       const int s = acquire(i++);
       const int64_t row = kv_row(p, it.b, it.kvh, it.t_begin + j * TILE);
       meta[s] = make_int4(idx, j, it.len, it.t_end);
       meta_row[s] = row;
-      issue(s, it, j, row);
+      issue(s, it, j, row, deferring ? kIssueKV : kIssueAll);
+    }
+    if (deferring) {  // the whole (short) first item is in the ring
+      griddep_wait();
+      for (int jj = 0; jj < it.ntiles; ++jj)
+        issue((i0 + jj) % STAGES, it, jj, meta_row[(i0 + jj) % STAGES], kIssueInputs);
+      deferring = false;
     }
   }
+  if (deferring) griddep_wait();  // no work: still order the launch after its predecessor
   const int s = acquire(i);
   meta[s] = make_int4(-1, 0, 0, 0);
   mbar_arrive(&full[s]);

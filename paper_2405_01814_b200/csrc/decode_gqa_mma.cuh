@@ -90,23 +90,25 @@ __global__ void __launch_bounds__((NW_ + 2) * 32, 1)
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
       producer_loop<STAGES, TILE>(p, full, empty, meta, meta_row,
-                                  [&](int s, const Item& it, int j, int64_t row) {
+                                  [&](int s, const Item& it, int j, int64_t row, int mode) {
         uint8_t* st = smem + s * C::STAGE_BYTES;
         const uint32_t qb = static_cast<uint32_t>(G) * D * 2;
         const bool fused = tile_has_new<TILE>(p, it, j);
-        mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES + (j == 0 ? qb : 0) +
-                                            (fused ? 2 * C::ROW_BYTES : 0));
-        if (fused) {
+        if (mode != kIssueInputs)
+          mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES + (j == 0 ? qb : 0) +
+                                              (fused ? 2 * C::ROW_BYTES : 0));
+        if (mode != kIssueKV && fused) {
           const int64_t off = static_cast<int64_t>(it.kvh) * D;
           uint8_t* kn = qslot + s * C::SLOT_BYTES + C::Q_BYTES;
           tma_load_1d(kn, new_rows<T>(p, 0, it.b) + off, C::ROW_BYTES, &full[s], pol);
           tma_load_1d(kn + C::ROW_BYTES, new_rows<T>(p, 1, it.b) + off, C::ROW_BYTES, &full[s],
                       pol);
         }
-        if (j == 0)
+        if (mode != kIssueKV && j == 0)
           tma_load_1d(qslot + s * C::SLOT_BYTES,
                       q_rows<T>(p, it.b) + static_cast<int64_t>(it.kvh) * G * D,
                       qb, &full[s], pol);
+        if (mode == kIssueInputs) return;
         const int32_t r32 = static_cast<int32_t>(row);
         tma_load_2d(st, &kmap, 0, r32, &full[s], pol);
         tma_load_2d(st + C::BOX_BYTES, &kmap, 64, r32, &full[s], pol);

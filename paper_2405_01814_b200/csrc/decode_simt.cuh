@@ -83,25 +83,27 @@ __global__ void __launch_bounds__((NW + 2) * 32, 1)
       const T* kp = static_cast<const T*>(p.k_pool);
       const T* vp = static_cast<const T*>(p.v_pool);
       producer_loop<STAGES, TILE>(p, full, empty, meta, meta_row,
-                                  [&](int s, const Item& it, int j, int64_t row) {
+                                  [&](int s, const Item& it, int j, int64_t row, int mode) {
         const int tok = it.t_begin + j * TILE;
         const int rows = min(TILE, it.t_end - tok);
         const uint32_t bytes = static_cast<uint32_t>(rows) * D * sizeof(T);
         T* ks = ring + static_cast<size_t>(s) * 2 * TILE * D;
         const bool fused = tile_has_new<TILE>(p, it, j);
-        mbar_arrive_expect_tx(&full[s], 2 * bytes + (j == 0 ? C::Q_BYTES : 0) +
-                                            (fused ? 2 * C::ROW_BYTES : 0));
+        if (mode != kIssueInputs)
+          mbar_arrive_expect_tx(&full[s], 2 * bytes + (j == 0 ? C::Q_BYTES : 0) +
+                                              (fused ? 2 * C::ROW_BYTES : 0));
         uint8_t* slot = qslot + s * C::SLOT_BYTES;
-        if (j == 0) {
+        if (mode != kIssueKV && j == 0) {
           const T* qsrc = q_rows<T>(p, it.b) + static_cast<int64_t>(it.kvh * p.G + it.qg * GQ) * D;
           tma_load_1d(slot, qsrc, C::Q_BYTES, &full[s], pol);
         }
-        if (fused) {
+        if (mode != kIssueKV && fused) {
           const int64_t off = static_cast<int64_t>(it.kvh) * D;
           tma_load_1d(slot + C::Q_BYTES, new_rows<T>(p, 0, it.b) + off, C::ROW_BYTES, &full[s], pol);
           tma_load_1d(slot + C::Q_BYTES + C::ROW_BYTES, new_rows<T>(p, 1, it.b) + off,
                       C::ROW_BYTES, &full[s], pol);
         }
+        if (mode == kIssueInputs) return;
         tma_load_1d(ks, kp + row * D, bytes, &full[s], pol);
         tma_load_1d(ks + TILE * D, vp + row * D, bytes, &full[s], pol);
       });

@@ -41,7 +41,8 @@ def make_args(q: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor,
               lse: torch.Tensor | None = None, kernel: str = "auto",
               split_tokens: int = 0, k_new: torch.Tensor | None = None,
               v_new: torch.Tensor | None = None,
-              request_order: torch.Tensor | None = None) -> tuple[DecodeArgs, torch.Tensor]:
+              request_order: torch.Tensor | None = None,
+              overlap_prev: bool = False) -> tuple[DecodeArgs, torch.Tensor]:
     """Fill lam_decode_args from tensors; returns (args, out).  With k_new/v_new ([B, Hkv, D],
     a shared batch stride allowed) the launch also appends each request's new token at
     position seq_lens[b] - 1 (fused lam_kv_append)."""
@@ -101,23 +102,25 @@ def make_args(q: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor,
         if request_order.dtype != torch.int32 or request_order.shape != (B,):
             raise _lib.ValidationError("request_order must be int32 [B]")
         a.request_order = request_order.data_ptr()
+    a.overlap_prev = 1 if overlap_prev else 0
     return a, out
 
 
 def decode(q, k_pool, v_pool, seq_lens, *, page_table=None, max_len=None, scale=None, out=None,
            out_dtype=None, return_lse=False, kernel="auto", split_tokens=0, ctx=None,
-           stream=None, k_new=None, v_new=None, request_order=None):
+           stream=None, k_new=None, v_new=None, request_order=None, overlap_prev=False):
     """softmax(q K^T scale) V per (request, q head) over the request's first seq_lens[b]
     tokens; q head h reads KV head h // (Hq // Hkv).  With k_new / v_new the request's new
     token (position seq_lens[b] - 1) is taken from them and appended to the pools in the same
-    launch."""
+    launch.  overlap_prev: see lam_decode_args.overlap_prev (the launch may start streaming KV
+    while the stream's preceding kernel drains; q / k_new / v_new are read after it completes)."""
     lse = None
     if return_lse:
         lse = torch.empty(q.shape[:2], dtype=torch.float32, device=q.device)
     a, out = make_args(q, k_pool, v_pool, seq_lens, page_table=page_table, max_len=max_len,
                        scale=scale, out=out, out_dtype=out_dtype, lse=lse, kernel=kernel,
                        split_tokens=split_tokens, k_new=k_new, v_new=v_new,
-                       request_order=request_order)
+                       request_order=request_order, overlap_prev=overlap_prev)
     ctx = ctx or _lib.context(q.device.index or 0)
     check(_lib.load().lam_decode(ctx.handle, a, _stream_ptr(stream)))
     return (out, lse) if return_lse else out

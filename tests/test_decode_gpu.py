@@ -381,3 +381,48 @@ def test_split_tail_vs_oracle(built, monkeypatch, kernel, G, dtype, tail, splits
     assert _maxabs(out.cpu().numpy(), want) <= TOL[dtype]
     finite = np.isfinite(want_lse)
     assert _maxabs(lse.cpu().numpy()[finite], want_lse[finite]) <= 1e-3
+
+
+@pytest.mark.parametrize("kernel,dtype,G", [("gqa_mma", torch.bfloat16, 8), ("gqa_mma", torch.bfloat16, 1),
+                                            ("simt", torch.float32, 1), ("simt", torch.bfloat16, 2)])
+@pytest.mark.parametrize("lmax", [40, 300, 3000])
+def test_overlap_prev_orders_inputs_after_preceding_kernel(built, kernel, dtype, G, lmax):
+    """overlap_prev (programmatic dependent launch): a chain of launches over different pools
+    where each launch's q and fused new K/V rows are the PRECEDING launch's output — so they
+    must be read only after it completes — equals the same chain with ordinary stream order,
+    bitwise.  Covers first items shorter than the ring (all inputs deferred to the end of the
+    item) and longer ones (deferred at the ring boundary)."""
+    from paper_2405_01814_b200 import decode as dec
+
+    B, Hkv, D, P, L = 24, 4, 128, 64, 6
+    Hq = Hkv * G
+    g = torch.Generator(device="cuda").manual_seed(3)
+    lens = torch.randint(1, lmax, (B,), generator=g, device="cuda", dtype=torch.int32)
+    lens[0] = lmax
+    npg = (lmax + P - 1) // P
+    pools = [(torch.empty((B * npg, Hkv, P, D), device="cuda").uniform_(-1, 1, generator=g).to(dtype),
+              torch.empty((B * npg, Hkv, P, D), device="cuda").uniform_(-1, 1, generator=g).to(dtype))
+             for _ in range(L)]
+    pt = torch.randperm(B * npg, generator=g, device="cuda").to(torch.int32).view(B, npg)
+    q0 = torch.empty((B, Hq, D), device="cuda").uniform_(-1, 1, generator=g).to(dtype)
+
+    def chain(overlap):
+        kv = [(k.clone(), v.clone()) for k, v in pools]
+        outs, q = [], q0
+        for layer in range(L):
+            out = torch.empty((B, Hq, D), dtype=dtype, device="cuda")
+            dec.decode(q, kv[layer][0], kv[layer][1], lens, page_table=pt, max_len=lmax, out=out,
+                       kernel=kernel, k_new=q[:, :Hkv], v_new=q[:, Hkv - 1: 2 * Hkv - 1]
+                       if Hq >= 2 * Hkv else q[:, :Hkv], overlap_prev=overlap and layer > 0)
+            outs.append(out)
+            q = out
+        torch.cuda.synchronize()
+        return outs, kv
+
+    want, kv_want = chain(False)
+    for _ in range(3):
+        got, kv_got = chain(True)
+        for layer in range(L):
+            assert torch.equal(got[layer], want[layer]), layer
+            assert torch.equal(kv_got[layer][0], kv_want[layer][0])
+            assert torch.equal(kv_got[layer][1], kv_want[layer][1])
