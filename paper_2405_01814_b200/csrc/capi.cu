@@ -788,6 +788,10 @@ int decode_impl(lam_ctx* ctx, const lam_decode_args* a, const lam_peer_io* io, v
     // the launch carries its own input dependencies (sequence numbers), so it may overlap the
     // previous kernel's drain
     p.pdl = io->n_wait > 0 && env_int("LAM_PDL", 1) != 0;
+    // LAM_PEER_PREFETCH=1: stream the first KV tiles (local pool) before the inputs' sequence
+    // numbers arrive.  Off by default: the inputs are normally published before the launch
+    // starts, and the deferred issue cost 0.3-0.6 % at N = 2 (scripts/call61.sh).
+    if (io->n_wait > 0 && env_int("LAM_PEER_PREFETCH", 0) != 0) p.defer_inputs = 2;
   }
   if (a->overlap_prev != 0 && io == nullptr) {
     // stream the first KV tiles while the preceding kernel drains; q / k_new / v_new wait for it

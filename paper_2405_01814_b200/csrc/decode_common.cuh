@@ -46,8 +46,9 @@ struct DecodeParams {
   unsigned long long* slot;
   unsigned long long item_base, done_base;
   int32_t pdl;              // launched with programmatic dependent launch
-  int32_t defer_inputs;     // (with pdl) KV tiles of the first item may stream before the
-                            // preceding grid completes; q / k_new / v_new loads wait for it
+  int32_t defer_inputs;     // KV tiles of the first item may stream before the inputs are
+                            // ready; q / k_new / v_new loads wait for them: 1 = the preceding
+                            // grid (overlap_prev), 2 = the peer sequence numbers (wait_flag)
   int32_t B, Hq, Hkv, G, D;
   int32_t page_size, pt_stride;
   int32_t chunk;            // tokens per split (multiple of the kernel tile)
@@ -257,7 +258,15 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
                                               uint64_t* empty, int4* meta, long long* meta_row,
                                               Issue issue) {
   acquire_slot(p);
-  wait_inputs(p);
+  // peer transport: the inputs' sequence numbers are awaited like the preceding grid of an
+  // overlap_prev launch — after the first KV tiles are in flight (p.defer_inputs = 2)
+  auto inputs_ready = [&] {
+    if (p.defer_inputs == 2)
+      wait_inputs(p);
+    else
+      griddep_wait();
+  };
+  if (p.defer_inputs != 2) wait_inputs(p);
   int i = 0;
   auto acquire = [&](int k) {
     const int s = k % STAGES;
@@ -272,7 +281,7 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
     const Item it = make_item(p, idx, TILE);
     if (it.ntiles == 0) {
       if (deferring) {  // nothing to prefetch
-        griddep_wait();
+        inputs_ready();
         deferring = false;
       }
       if (it.split == 0 && it.len == 0) {  // empty request: zero-output marker
@@ -285,7 +294,7 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
     const int i0 = i;  // first stage index of this item
     for (int j = 0; j < it.ntiles; ++j) {
       if (deferring && i >= STAGES) {  // ring full: the inputs must land before any reuse
-        griddep_wait();
+        inputs_ready();
         for (int jj = 0; jj < j; ++jj)
           issue((i0 + jj) % STAGES, it, jj, meta_row[(i0 + jj) % STAGES], kIssueInputs);
         deferring = false;
@@ -297,13 +306,13 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
       issue(s, it, j, row, deferring ? kIssueKV : kIssueAll);
     }
     if (deferring) {  // the whole (short) first item is in the ring
-      griddep_wait();
+      inputs_ready();
       for (int jj = 0; jj < it.ntiles; ++jj)
         issue((i0 + jj) % STAGES, it, jj, meta_row[(i0 + jj) % STAGES], kIssueInputs);
       deferring = false;
     }
   }
-  if (deferring) griddep_wait();  // no work: still order the launch after its predecessor
+  if (deferring) inputs_ready();  // no work: still order the launch after its inputs
   const int s = acquire(i);
   meta[s] = make_int4(-1, 0, 0, 0);
   mbar_arrive(&full[s]);
