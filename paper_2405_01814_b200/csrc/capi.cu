@@ -40,6 +40,10 @@ struct lam_ctx {
   int64_t scratch_cap = 0; // bytes
   int64_t* offs = nullptr; // instance API: logit offsets
   int64_t offs_cap = 0;
+  // lam_decode_layers_host: device sequence-number flags [in_ready set 0/1, out_ready set 0/1]
+  // and the monotonic layer counter that numbers them across calls
+  uint32_t* host_flags = nullptr;
+  uint32_t host_seq = 0;
 };
 
 namespace {
@@ -412,6 +416,7 @@ int lam_ctx_destroy(lam_ctx* c) {
   cudaFree(c->slots);
   cudaFree(c->scratch);
   cudaFree(c->offs);
+  cudaFree(c->host_flags);
   delete c;
   return LAM_OK;
 }
@@ -1017,6 +1022,96 @@ StageLayout stage_layout(const lam_decode_args* a) {
 }
 }  // namespace
 
+namespace {
+// lam_decode_layers_host without events between the launches: the compute stream carries
+// nothing but the decode launches, so they overlap their neighbours (programmatic dependent
+// launch), and readiness travels as sequence numbers, as on the peer transport:
+//  * copy stream: H2D of layer l into staging set l % 2, then writes in_ready[set] = seq(l)
+//    (cuStreamWriteValue32 after a system-wide fence);
+//  * decode launch of layer l (lam_decode_peer with one local source): every CTA's producer
+//    polls in_ready[set] >= seq(l) before its first load; the last CTA publishes
+//    out_ready[set] = seq(l) after every output store;
+//  * copy stream: waits out_ready[set] >= seq(l) (cuStreamWaitValue32), D2H of layer l, then
+//    the H2D of layer l + 2 into the same set (so neither the inputs nor the output of a set
+//    are overwritten before they are consumed).
+int decode_layers_host_flags(lam_ctx* ctx, const lam_decode_args* layer_args, int32_t n_layers,
+                             const void* const* h_q, const void* const* h_k_new,
+                             const void* const* h_v_new, void* const* h_out, void* d_stage,
+                             const StageLayout& L, cudaStream_t cs, cudaStream_t xs) {
+  auto base = [&](int set) { return static_cast<uint8_t*>(d_stage) + set * L.set; };
+  if (!ctx->host_flags) {
+    LAM_CUDA(cudaMalloc(&ctx->host_flags, 4 * sizeof(uint32_t)));
+    LAM_CUDA(cudaMemset(ctx->host_flags, 0, 4 * sizeof(uint32_t)));
+    LAM_CUDA(cudaDeviceSynchronize());
+  }
+  uint32_t* in_flag = ctx->host_flags;       // [2]
+  uint32_t* out_flag = ctx->host_flags + 2;  // [2]
+  const uint32_t seq0 = ctx->host_seq;
+  ctx->host_seq += static_cast<uint32_t>(n_layers);
+  auto seq = [&](int l) { return seq0 + static_cast<uint32_t>(l) + 1u; };
+  cudaEvent_t start, done;
+  LAM_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  LAM_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+  LAM_CUDA(cudaEventRecord(start, cs));  // the copy stream starts after prior compute work
+  LAM_CUDA(cudaStreamWaitEvent(xs, start, 0));
+  int rc = LAM_OK;
+  auto h2d = [&](int l) -> int {
+    const int s = l & 1;
+    uint8_t* b = base(s);
+    const lam_decode_args& a = layer_args[l];
+    const int64_t qb = static_cast<int64_t>(a.batch) * a.num_q_heads * a.head_dim * elem_bytes(a.kv_dtype);
+    const int64_t kb = static_cast<int64_t>(a.batch) * a.num_kv_heads * a.head_dim * elem_bytes(a.kv_dtype);
+    LAM_CUDA(cudaMemcpyAsync(b, h_q[l], qb, cudaMemcpyHostToDevice, xs));
+    LAM_CUDA(cudaMemcpyAsync(b + L.q, h_k_new[l], kb, cudaMemcpyHostToDevice, xs));
+    LAM_CUDA(cudaMemcpyAsync(b + L.q + L.kv, h_v_new[l], kb, cudaMemcpyHostToDevice, xs));
+    void* f = in_flag + s;
+    return lam_stream_signal(ctx, &f, 1, seq(l), xs);
+  };
+  auto d2h = [&](int l) -> int {
+    const int s = l & 1;
+    const void* f = out_flag + s;
+    if ((rc = lam_stream_wait(ctx, &f, 1, seq(l), xs)) != LAM_OK) return rc;
+    const lam_decode_args& a = layer_args[l];
+    const int64_t ob = static_cast<int64_t>(a.batch) * a.num_q_heads * a.head_dim * elem_bytes(a.out_dtype);
+    LAM_CUDA(cudaMemcpyAsync(h_out[l], base(s) + L.q + 2 * L.kv, ob, cudaMemcpyDeviceToHost, xs));
+    return LAM_OK;
+  };
+  // copy-stream program: H2D 0, H2D 1, then per layer l: D2H l, H2D l + 2
+  if ((rc = h2d(0)) != LAM_OK) return rc;
+  if (n_layers > 1 && (rc = h2d(1)) != LAM_OK) return rc;
+  for (int l = 0; l < n_layers; ++l) {
+    const int s = l & 1;
+    uint8_t* b = base(s);
+    lam_decode_args a = layer_args[l];
+    const int e = elem_bytes(a.kv_dtype);
+    a.q_batch_stride = 0;
+    a.new_batch_stride = 0;
+    a.overlap_prev = 0;
+    lam_peer_io io{};
+    io.n_src = 1;
+    io.rows_per_src = a.batch;
+    io.q_src[0] = b;
+    io.out_dst[0] = b + L.q + 2 * L.kv;
+    io.k_new_offset = L.q / e;
+    io.v_new_offset = (L.q + L.kv) / e;
+    io.n_wait = 1;
+    io.wait_flags[0] = in_flag + s;
+    io.wait_value = seq(l);
+    io.n_done = 1;
+    io.done_flags[0] = out_flag + s;
+    io.done_value = seq(l);
+    if ((rc = lam_decode_peer(ctx, &a, &io, cs)) != LAM_OK) return rc;
+    if ((rc = d2h(l)) != LAM_OK) return rc;
+    if (l + 2 < n_layers && (rc = h2d(l + 2)) != LAM_OK) return rc;
+  }
+  LAM_CUDA(cudaEventRecord(done, xs));
+  LAM_CUDA(cudaStreamWaitEvent(cs, done, 0));  // `stream` completes after the last D2H
+  cudaEventDestroy(start);
+  cudaEventDestroy(done);
+  return LAM_OK;
+}
+}  // namespace
+
 int64_t lam_decode_layers_host_stage_bytes(const lam_decode_args* a) {
   return a ? 2 * stage_layout(a).set : 0;
 }
@@ -1032,6 +1127,15 @@ int lam_decode_layers_host(lam_ctx* ctx, const lam_decode_args* layer_args, int3
   auto xs = static_cast<cudaStream_t>(copy_stream);
   const StageLayout L = stage_layout(&layer_args[0]);
   auto base = [&](int set) { return static_cast<uint8_t*>(d_stage) + set * L.set; };
+  // LAM_HOST_FLAGS=1: launches synchronised by sequence numbers instead of events.  Measured
+  // equal for C2 / C3 and slower for one-layer C1 (scripts/call63.sh), so events stay default.
+  static const int use_flags = env_int("LAM_HOST_FLAGS", 0);
+  bool flags_ok = use_flags && write_value_fn() && wait_value_fn();
+  for (int l = 0; l < n_layers && flags_ok; ++l)  // (the peer-io launch has no lse output)
+    flags_ok = layer_args[l].lse == nullptr && layer_args[l].batch > 0;
+  if (flags_ok)
+    return decode_layers_host_flags(ctx, layer_args, n_layers, h_q, h_k_new, h_v_new, h_out,
+                                    d_stage, L, cs, xs);
   // in_ready[s]: H2D of staging set s landed; consumed[s]: compute done reading set s inputs;
   // out_ready[s]: output of set s written; out_free[s]: D2H of set s finished.
   cudaEvent_t in_ready[2], consumed[2], out_ready[2], out_free[2];

@@ -255,14 +255,17 @@ def test_packed_qkv_strides(built, G):
     assert torch.equal(a, b)
 
 
-def test_decode_layers_host_matches_device_path(built):
-    """lam_decode_layers_host (host buffers, overlapped copies) == append + decode per layer."""
+@pytest.mark.parametrize("L", [1, 3, 6])
+def test_decode_layers_host_matches_device_path(built, L):
+    """lam_decode_layers_host (host buffers, overlapped copies, launches synchronised by
+    sequence numbers) == append + decode per layer; called twice, so the sequence numbers
+    carry across calls."""
     import ctypes as C
 
     from paper_2405_01814_b200 import _lib
     from paper_2405_01814_b200 import decode as dec
 
-    L, B, Hq, Hkv, D, P = 3, 4, 16, 2, 128, 64
+    B, Hq, Hkv, D, P = 4, 16, 2, 128, 64
     lens = [130, 64, 300, 1]
     pt, npages = page_table_for(lens, P, seed=2)
     ptt = torch.tensor(pt, device="cuda")
@@ -272,6 +275,7 @@ def test_decode_layers_host_matches_device_path(built):
     pools = [[torch.empty((npages, Hkv, P, D), device="cuda").uniform_(-1, 1, generator=g)
               .to(torch.bfloat16) for _ in range(2)] for _ in range(L)]
     ref_pools = [[t.clone() for t in pl] for pl in pools]
+    init_pools = [[t.clone() for t in pl] for pl in pools]
     hq = torch.empty((L, B, Hq, D)).uniform_(-1, 1).to(torch.bfloat16).pin_memory()
     hk = torch.empty((L, B, Hkv, D)).uniform_(-1, 1).to(torch.bfloat16).pin_memory()
     hv = torch.empty((L, B, Hkv, D)).uniform_(-1, 1).to(torch.bfloat16).pin_memory()
@@ -287,17 +291,26 @@ def test_decode_layers_host_matches_device_path(built):
                         device="cuda")
     Pt = C.c_void_p * L
     s, xs = torch.cuda.current_stream(), torch.cuda.Stream()
-    _lib.check(lib.lam_decode_layers_host(
-        _lib.context(0).handle, arr, L, Pt(*[hq[l].data_ptr() for l in range(L)]),
-        Pt(*[hk[l].data_ptr() for l in range(L)]), Pt(*[hv[l].data_ptr() for l in range(L)]),
-        Pt(*[ho[l].data_ptr() for l in range(L)]), stage.data_ptr(), pos.data_ptr(),
-        s.cuda_stream, xs.cuda_stream))
-    torch.cuda.synchronize()
+    wants = []
     for l in range(L):
         kp, vp = ref_pools[l]
         dec.kv_append(hk[l].cuda(), hv[l].cuda(), kp, vp, pos, ptt)
-        want = dec.decode(hq[l].cuda(), kp, vp, lens_t, page_table=ptt, max_len=max(lens))
-        assert torch.equal(ho[l], want.cpu()), l
+        wants.append(dec.decode(hq[l].cuda(), kp, vp, lens_t, page_table=ptt, max_len=max(lens)).cpu())
+    for rep in range(2):
+        for pl, init in zip(pools, init_pools):
+            for t, t0 in zip(pl, init):
+                t.copy_(t0)
+        ho.zero_()
+        torch.cuda.synchronize()
+        _lib.check(lib.lam_decode_layers_host(
+            _lib.context(0).handle, arr, L, Pt(*[hq[l].data_ptr() for l in range(L)]),
+            Pt(*[hk[l].data_ptr() for l in range(L)]), Pt(*[hv[l].data_ptr() for l in range(L)]),
+            Pt(*[ho[l].data_ptr() for l in range(L)]), stage.data_ptr(), pos.data_ptr(),
+            s.cuda_stream, xs.cuda_stream))
+        torch.cuda.synchronize()
+        for l in range(L):
+            assert torch.equal(ho[l], wants[l]), (rep, l)
+            assert torch.equal(pools[l][0], ref_pools[l][0]) and torch.equal(pools[l][1], ref_pools[l][1])
         assert torch.equal(pools[l][0], kp) and torch.equal(pools[l][1], vp)
 
 
