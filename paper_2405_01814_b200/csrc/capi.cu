@@ -1129,7 +1129,7 @@ int lam_decode_layers_host(lam_ctx* ctx, const lam_decode_args* layer_args, int3
   auto base = [&](int set) { return static_cast<uint8_t*>(d_stage) + set * L.set; };
   // LAM_HOST_FLAGS=1: launches synchronised by sequence numbers instead of events.  Measured
   // equal for C2 / C3 and slower for one-layer C1 (scripts/call63.sh), so events stay default.
-  static const int use_flags = env_int("LAM_HOST_FLAGS", 0);
+  const int use_flags = env_int("LAM_HOST_FLAGS", 0);
   bool flags_ok = use_flags && write_value_fn() && wait_value_fn();
   for (int l = 0; l < n_layers && flags_ok; ++l)  // (the peer-io launch has no lse output)
     flags_ok = layer_args[l].lse == nullptr && layer_args[l].batch > 0;
