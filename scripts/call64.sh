@@ -1,0 +1,6 @@
+#!/bin/bash
+# full GPU test suite + smoke on the current tree
+mkdir -p gpurun_out
+exec > gpurun_out/call64.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -q 2>&1 | tail -3
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
