@@ -189,6 +189,8 @@ int lam_decode(lam_ctx* ctx, const lam_decode_args* args, void* stream);
 /* Kernel family and split count lam_decode would use for these arguments. */
 int lam_decode_plan(lam_ctx* ctx, const lam_decode_args* args, int32_t* kernel,
                     int32_t* num_splits, int32_t* split_tokens);
+/* Persistent grid (CTAs) lam_decode would launch for these arguments. */
+int lam_decode_plan_grid(lam_ctx* ctx, const lam_decode_args* args, int32_t* ctas);
 
 /* Write the new token of every request into the paged pools (bit-exact copy):
  *   k_pool[page_table[b][pos/P]][h][pos%P][:] = k_new[b*new_batch_stride + h*D ...], same for V,

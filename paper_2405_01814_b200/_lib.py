@@ -110,6 +110,7 @@ SIGNATURES = {
     "lam_request_partition": (C.c_int, [_P, _I64, _I64, _P, _P, _P]),
     "lam_decode": (C.c_int, [_P, C.POINTER(DecodeArgs), _P]),
     "lam_decode_plan": (C.c_int, [_P, C.POINTER(DecodeArgs), _P, _P, _P]),
+    "lam_decode_plan_grid": (C.c_int, [_P, C.POINTER(DecodeArgs), _P]),
     "lam_kv_append": (C.c_int, [_I32, _I32, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _I64, _P, _P,
                                 _P]),
     "lam_kv_gather": (C.c_int, [_I32, _I32, _I32, _I32, _I32, _I32, _P, _P, _I32, _P, _P, _P]),

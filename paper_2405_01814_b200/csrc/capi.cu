@@ -123,7 +123,9 @@ int make_pool_map(CUtensorMap* map, int dtype, const void* base, int64_t rows, i
   const cuuint32_t estr[2] = {1, 1};
   const CUtensorMapDataType dt =
       dtype == LAM_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-  static const int promo = env_int("LAM_TMAP_PROMOTION", 3);  // 0 none, 1 64B, 2 128B, 3 256B
+  // 0 none, 1 64B, 2 128B, 3 256B.  None: the 8 KB boxes are whole 128-byte rows already; in
+  // the sustained (power-capped) step it beat 256B by 0.8 % on C3, 0.2 % on C2 (call66.sh)
+  static const int promo = env_int("LAM_TMAP_PROMOTION", 0);
   const CUtensorMapL2promotion pr =
       promo == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
                  : promo == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
@@ -700,6 +702,16 @@ int lam_decode_plan(lam_ctx* ctx, const lam_decode_args* a, int32_t* kernel, int
   if (kernel) *kernel = pl.kernel;
   if (num_splits) *num_splits = pl.S;
   if (split_tokens) *split_tokens = pl.chunk;
+  return LAM_OK;
+}
+
+int lam_decode_plan_grid(lam_ctx* ctx, const lam_decode_args* a, int32_t* ctas) {
+  if (!ctx) return fail(LAM_ERR_VALIDATION, "null context");
+  LAM_CUDA(cudaSetDevice(ctx->device));
+  Plan pl;
+  int rc = plan_decode(ctx, a, &pl);
+  if (rc != LAM_OK) return rc;
+  if (ctas) *ctas = pl.ctas;
   return LAM_OK;
 }
 

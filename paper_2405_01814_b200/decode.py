@@ -143,6 +143,17 @@ def plan(q, k_pool, v_pool, seq_lens, **kw):
     return names[k.value], s.value, t.value
 
 
+def plan_grid(q, k_pool, v_pool, seq_lens, **kw) -> int:
+    """Persistent grid size (CTAs) lam_decode would launch."""
+    ctx = kw.pop("ctx", None) or _lib.context(q.device.index or 0)
+    a, _ = make_args(q, k_pool, v_pool, seq_lens, **kw)
+    import ctypes as C
+
+    n = C.c_int32()
+    check(_lib.load().lam_decode_plan_grid(ctx.handle, a, C.byref(n)))
+    return n.value
+
+
 def kv_append(k_new, v_new, k_pool, v_pool, positions, page_table=None, stream=None):
     """k_pool[page(b, pos)][h][pos % P] = k_new[b][h] (and V), pos = positions[b].
     k_new / v_new are [B, Hkv, D] with contiguous heads; a batch stride (e.g. slices of a packed

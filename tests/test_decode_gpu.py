@@ -441,3 +441,34 @@ def test_overlap_prev_orders_inputs_after_preceding_kernel(built, kernel, dtype,
             assert torch.equal(got[layer], want[layer]), layer
             assert torch.equal(kv_got[layer][0], kv_want[layer][0])
             assert torch.equal(kv_got[layer][1], kv_want[layer][1])
+
+
+@pytest.mark.parametrize("name,B,Hq,Hkv,L,dtype,paged,want", [
+    # (kernel, splits, CTAs) the planner picks for the BASELINE launch shapes, measured best on
+    # B200 (profiles/r01b/SUMMARY.md §2, §7): C1 on 128 CTAs (2 even rounds), C4 split 4 ways,
+    # the 512-unit sharded GQA launch unsplit on 128 CTAs, the rest unsplit on the full grid.
+    ("c1", 8, 32, 32, 1024, torch.float32, False, ("simt", 1, 128)),
+    ("c2", 64, 32, 32, 4096, torch.bfloat16, True, ("gqa_mma", 1, 148)),
+    ("c3", 128, 64, 8, 4096, torch.bfloat16, True, ("gqa_mma", 1, 148)),
+    ("c4", 32, 64, 8, 32768, torch.bfloat16, True, ("gqa_mma", 4, 148)),
+    ("c3n8", 512, 8, 1, 4096, torch.bfloat16, True, ("gqa_mma", 1, 128)),
+])
+def test_planner_choices_for_baseline_shapes(built, name, B, Hq, Hkv, L, dtype, paged, want):
+    from paper_2405_01814_b200 import decode as dec
+
+    if torch.cuda.get_device_properties(0).multi_processor_count != 148:
+        pytest.skip("choices are pinned for the 148-SM B200")
+    D, P = 128, 64
+    q = torch.empty((B, Hq, D), dtype=dtype, device="cuda")
+    lens = torch.full((B,), L, dtype=torch.int32, device="cuda")
+    if paged:
+        npg = B * L // P
+        pool = torch.empty((npg, Hkv, P, D), dtype=dtype, device="cuda")
+        pt = torch.zeros((B, L // P), dtype=torch.int32, device="cuda")
+        kw = dict(page_table=pt, max_len=L)
+    else:
+        pool = torch.empty((B, Hkv, L, D), dtype=dtype, device="cuda")
+        kw = dict(max_len=L)
+    kern, splits, _ = dec.plan(q, pool, pool, lens, **kw)
+    ctas = dec.plan_grid(q, pool, pool, lens, **kw)
+    assert (kern, splits, ctas) == want
