@@ -12,10 +12,17 @@ context — one fused lam_decode launch (k_new/v_new), or lam_kv_append + lam_de
 Default workload (N=1): BASELINE config 2, LLaMA-2-7B all 32 layers, bf16, B=64, l=4096 —
 137 GB of KV resident in HBM (far above the 126 MB L2, so no flush is needed).
 With N>1 (torchrun, one rank per GPU) the KV heads are sharded over ranks
-(head_partition, attention.cpp:164-177) and the global batch grows with N (weak scaling):
-each rank is the model worker of B requests and the attention worker of Hkv/N heads of all
-N*B requests; Q/K/V are scattered and outputs gathered by NCCL all-to-all, overlapped with
-attention across two staggered micro-batches.
+(head_partition, attention.cpp:164-177).  --scaling strong (the default for N>1) keeps the
+workload's global batch fixed — each rank is the model worker of B/N requests and the attention
+worker of Hkv/N heads of all B requests, so T1/(N*TN) is the parallel efficiency of BASELINE.md
+§3 — and --scaling weak gives every rank B requests (global batch N*B).  Q/K/V reach the head
+owners and outputs return over NVLink peer memory (or NCCL all-to-all with --transport nccl),
+overlapped with attention across two staggered micro-batches.
+
+After the timed regions the bench checks its own outputs (--check 1, the default): on seeded
+(request, q head) pairs of three layers, the output of the benchmarked launch configuration
+against the CPU oracle (oracle/, the restatement of attention.cpp:48-70) on the same pool
+contents, within the north-star bound, and the fused append bit-exact.
 """
 from __future__ import annotations
 
@@ -214,10 +221,14 @@ def run_reference(args, w: dict, rank: int, world: int) -> None:
     step_bytes = PF.attn_cost(spec, w["B"], w["l"]).bytes
     line = {"metric": METRIC, "value": value, "unit": "GB/s", "impl": "reference",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": step_bytes / (value * 1e9) * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "ms_per_step": step_bytes / (value * 1e9) * 1e3,
+            "ms_per_step_basis": ("extrapolated: the step's attn_cost bytes / the rate measured on "
+                                  "the bounded sample (one layer, a subset of units); not timed "
+                                  "over a whole step"),
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic U(-1,1)",
-            "config": {"workload": f"{args.workload}: {w['desc']}", "global_batch": w["B"],
+            "config": {"workload": f"{args.workload}: {w['desc']}",
+                       "global_batch": w["B"] * (world if args.scaling == "weak" else 1),
                        "seq_len": w["l"], "layers": w["layers"],
                        "parallelism": "host threads"},
             "attn_tokens_per_s": value * 1e9 / (PF.kv_bytes_per_token(spec) * w["l"]),
@@ -240,7 +251,8 @@ class Workload:
     """Resident paged KV for every layer (or as many distinct layer buffers as fit) plus
     per-layer new-token inputs; one GPU's share under KV-head sharding."""
 
-    def __init__(self, w: dict, rank: int, world: int, device, engine: bool = False):
+    def __init__(self, w: dict, rank: int, world: int, device, engine: bool = False,
+                 strong: bool = False):
         import numpy as np
         import torch
 
@@ -254,8 +266,16 @@ class Workload:
         if self.Hkv % world:
             raise SystemExit(f"{self.Hkv} KV heads do not shard over {world} GPUs")
         self.hq_local, self.hkv_local = self.Hq // world, self.Hkv // world
-        self.B_local = w["B"]                 # requests whose q/k/v this rank produces
-        self.B = w["B"] * world               # requests whose local heads this rank attends
+        # requests whose q/k/v this rank produces: a share of the fixed global batch (strong
+        # scaling) or a full batch per rank (weak scaling)
+        from paper_2405_01814_b200.dist import local_batch
+
+        try:
+            self.B_local = local_batch(w["B"], world, "strong" if strong else "weak",
+                                       2 if (engine or world > 1) else 1)
+        except ValueError as e:
+            raise SystemExit(str(e))
+        self.B = self.B_local * world         # requests whose local heads this rank attends
         self.layers = w["layers"]
         # the attention-worker engine (always for N > 1): two staggered micro-batches
         engine = engine or world > 1
@@ -266,9 +286,14 @@ class Workload:
 
             self.geo = ShardGeometry(rank, world, self.layers, self.B_local, self.Hq, self.Hkv,
                                      self.D, self.mb)
-        # per-source request lengths; attention-side rows are micro-batch major
-        src_lens = [mixed_lengths(w["B"], 2024 + r) if w.get("mixed")
-                    else np.full(w["B"], w["l"], np.int32) for r in range(world)]
+        # per-source request lengths; attention-side rows are micro-batch major.  Strong scaling
+        # deals one global draw out to the sources (the same requests at every N).
+        if w.get("mixed") and strong:
+            glob = mixed_lengths(self.B, 2024)
+            src_lens = [glob[r * self.B_local:(r + 1) * self.B_local] for r in range(world)]
+        else:
+            src_lens = [mixed_lengths(w["B"], 2024 + r) if w.get("mixed")
+                        else np.full(w["B"], w["l"], np.int32) for r in range(world)]
         self.lens = np.zeros(self.B, np.int32)
         for src in range(world):
             for b in range(self.B_local):
@@ -356,6 +381,65 @@ class Workload:
         return self.k_layers[i], self.v_layers[i]
 
 
+def check_outputs(W, engine, step_fn, counter, layers_hint=None, pairs_per_layer=4, seed=7):
+    """Checker, outside every timed region: run one more step of the benchmarked launch
+    configuration and compare its outputs on seeded (request, q head) pairs of three layers with
+    the CPU oracle (exact_attention<float> restated, attention.cpp:48-70, on the exactly upcast
+    pool contents) — max-abs within the north-star bound — and the fused append bit-exact (the
+    pool row at seq_len - 1 equals the new token).  Each rank checks the rows it both produced
+    (model worker) and attended (attention worker).  Returns (max_abs_err, n_pairs, append_ok)."""
+    import numpy as np
+    import torch
+
+    from oracle import oracle as O
+
+    s = counter[0]
+    step_fn()
+    torch.cuda.synchronize(W.device)
+    rng = np.random.default_rng(seed + W.rank)
+    L = W.layers
+    layers = sorted({0, min(1, L - 1), L - 1} if layers_hint is None else set(layers_hint))
+    G = W.Hq // W.Hkv
+    scale = 1.0 / math.sqrt(W.D)
+    P = W.w["P"]
+    worst, n, append_ok = 0.0, 0, True
+    for layer in layers:
+        if engine is None:  # plain per-layer launches: rows are requests, all heads local
+            kp, vp = W.layer_pools(layer, s)
+            cand = [(b, b) for b in range(W.B)]
+        else:  # engine: this rank's own requests, its own head shard
+            kp, vp = W.layer_pools(layer)
+            g = W.geo
+            cand = [(g.kv_row(W.rank, bl), bl) for bl in range(W.B_local)]
+        for _ in range(pairs_per_layer):
+            row, bl = cand[int(rng.integers(len(cand)))]
+            h = int(rng.integers(W.hq_local))
+            kvh = h // G
+            ln = int(W.lens[row])
+            if engine is None:
+                q = W.q_in[layer, bl, h]
+                k_new, v_new = W.kn_in[layer, bl, kvh], W.vn_in[layer, bl, kvh]
+                out = W.out[layer, bl, h]
+            else:
+                m, i = divmod(bl, g.Bh)
+                rows = W.qkv_in[layer, m, W.rank, i]
+                q, k_new, v_new = rows[h], rows[g.hq_l + kvh], rows[g.hq_l + g.hkv_l + kvh]
+                out = W.out[layer, m, W.rank, i, h]
+            if W.page_table is not None:
+                npg = -(-ln // P)
+                pages = W.page_table[row, :npg].long()
+                kd = kp[pages, kvh].reshape(-1, W.D)[:ln]
+                vd = vp[pages, kvh].reshape(-1, W.D)[:ln]
+            else:
+                kd, vd = kp[row, kvh, :ln], vp[row, kvh, :ln]
+            append_ok &= bool(torch.equal(kd[ln - 1], k_new) and torch.equal(vd[ln - 1], v_new))
+            want = O.decode_dense(q.float().cpu().numpy()[None, None], kd.float().cpu().numpy()[None, None],
+                                  vd.float().cpu().numpy()[None, None], np.array([ln], np.int32), scale)
+            err = float(np.abs(out.float().cpu().numpy() - want[0, 0]).max())
+            worst, n = max(worst, err), n + 1
+    return worst, n, append_ok
+
+
 def run_ours(args, w: dict, rank: int, world: int) -> None:
     import numpy as np
     import torch
@@ -373,7 +457,8 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
     use_engine = world > 1 or args.engine == "peer"
     if world == 1 and use_engine and args.transport != "peer":  # (NCCL needs N > 1)
         raise SystemExit("--engine peer at one GPU needs --transport peer")
-    W = Workload(w, rank, world, device, engine=use_engine)
+    strong = args.scaling == "strong"
+    W = Workload(w, rank, world, device, engine=use_engine, strong=strong)
     if args.overlap_layers is None:
         # consecutive launches of a step are different layers (their pools are disjoint) only
         # when the model has more than one layer; a one-layer stream would have each launch
@@ -544,6 +629,22 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
     if not args.no_e2e:
         e2e = run_e2e(args, W, engine, dist, device, stream)
 
+    # ---- output check of the benchmarked launch configuration (outside the timed regions)
+    check = None
+    if args.check:
+        tol = {"bfloat16": 2e-3, "float16": 2e-3, "float32": 1e-5}[w["dtype"]]
+        if w["dtype"] != "float32" and W.out.dtype != torch.float32:
+            tol += 2.0 ** -9  # the bench's outputs are stored in bf16 (|out| < 1)
+        err, n, app = check_outputs(W, engine, step, counter)
+        t = torch.tensor([err, float(not app)], device=device, dtype=torch.float64)
+        if dist is not None:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        err, app = float(t[0]), not bool(t[1])
+        check = {"checker": "CPU oracle (oracle/: exact_attention<float> restated, attention.cpp:48-70) on the "
+                            "upcast pool contents after one more step; outside the timed regions",
+                 "pairs_per_rank": n, "max_abs": err, "tol": tol, "append_bit_exact": app,
+                 "ok": bool(err <= tol and app)}
+
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -555,7 +656,7 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": {"bfloat16": "bf16", "float32": "f32", "float16": "f16"}[w["dtype"]],
         "data": "synthetic: q, k, v ~ U(-1,1) (bench_attention.cpp:11-27 law), shuffled page placement",
         "config": {"workload": f"{args.workload}: {w['desc']}", "global_batch": W.B,
@@ -586,6 +687,8 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
     }
     if e2e is not None:
         line["e2e"] = e2e
+    if check is not None:
+        line["check"] = check
     if not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline(w, target_s=args.cpu_seconds)
@@ -594,6 +697,8 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+    if check is not None and not check["ok"]:
+        raise SystemExit("output check FAILED: the numbers above are not valid")
 
 
 def engine_is_local(args, world: int) -> bool:
@@ -720,6 +825,11 @@ def main():
                          "for multi-layer workloads, off for one layer (c1)")
     ap.add_argument("--separate-append", action="store_true",
                     help="lam_kv_append + lam_decode per layer instead of the fused launch")
+    ap.add_argument("--scaling", default=None, choices=["strong", "weak"],
+                    help="N>1: fixed global batch (strong, the default) or B requests per rank (weak)")
+    ap.add_argument("--check", type=int, default=1, choices=[0, 1],
+                    help="after the timed regions, check the benchmarked launches' outputs against "
+                         "the CPU oracle on seeded (request, head) pairs of three layers")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -727,6 +837,8 @@ def main():
         log(f"--gpus {args.gpus} requested without torchrun: running one rank")
         args.gpus = 1
     w = WORKLOADS[args.workload]
+    if args.scaling is None:  # (at N = 1 both mean the same workload)
+        args.scaling = "strong"
     if args.impl == "reference":
         run_reference(args, w, rank, world)
     else:

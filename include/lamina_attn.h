@@ -62,6 +62,18 @@ int lam_ctx_reserve(lam_ctx* ctx, int64_t partial_rows, int32_t head_dim, int64_
 /* Number of SMs of the context's device (148 on B200). */
 int lam_ctx_num_sms(const lam_ctx* ctx);
 
+/* Bounded device-side spins.  A decode launch that waits for its input sequence numbers
+ * (lam_peer_io.wait_flags) or for its launch slot longer than the timeout gives up instead of
+ * trapping: it records a LAM_STATUS_* code in the context's status word, completes (outputs
+ * unspecified) and still publishes its done flags, so no waiter on another GPU hangs and the
+ * CUDA context stays usable.  Default 10 s, or LAM_SPIN_TIMEOUT_MS at lam_ctx_create; 0 waits
+ * forever.  lam_ctx_status synchronises the device and reads (and optionally clears) the word. */
+#define LAM_STATUS_OK 0
+#define LAM_STATUS_INPUT_TIMEOUT 1
+#define LAM_STATUS_SLOT_TIMEOUT 2
+int lam_ctx_set_spin_timeout(lam_ctx* ctx, int64_t timeout_ns);
+int lam_ctx_status(lam_ctx* ctx, int32_t* status, int32_t clear);
+
 /* ---- reference operator API, device pointers -----------------------------
  * One "instance" is one AttnInstance (attention.hpp:20-30): a query vector of d
  * elements and its key/value rows.  Keys/values of all instances live in two row
@@ -284,7 +296,11 @@ typedef struct lam_peer_io {
 
 /* lam_decode whose q / k_new / v_new / out come from lam_peer_io (args->q, k_new, v_new and out
  * are ignored; fused append is implied; args->lse must be NULL).  batch == n_src *
- * rows_per_src. */
+ * rows_per_src.  With n_wait > 0 and args->overlap_prev the launch uses programmatic dependent
+ * launch and never waits for the preceding kernel of the stream: its inputs are ordered by the
+ * sequence numbers alone, and the overlap_prev contract (the preceding kernel writes none of
+ * page_table, seq_lens, request_order or the KV rows this launch reads or appends) orders the
+ * rest.  Without overlap_prev the launch follows ordinary stream order. */
 int lam_decode_peer(lam_ctx* ctx, const lam_decode_args* args, const lam_peer_io* io,
                     void* stream);
 

@@ -16,6 +16,7 @@ DROPIN_PATH = LIB_DIR / "libdisagg_attention.so"
 LAM_OK, LAM_ERR_ERROR, LAM_ERR_VALIDATION, LAM_ERR_CUDA = 0, 1, 2, 3
 LAM_F32, LAM_F64, LAM_BF16, LAM_F16 = 0, 1, 2, 3
 LAM_KERNEL_AUTO, LAM_KERNEL_SIMT, LAM_KERNEL_GQA_MMA = 0, 1, 2
+LAM_STATUS_OK, LAM_STATUS_INPUT_TIMEOUT, LAM_STATUS_SLOT_TIMEOUT = 0, 1, 2
 
 
 class Error(RuntimeError):
@@ -96,6 +97,8 @@ SIGNATURES = {
     "lam_ctx_destroy": (C.c_int, [_P]),
     "lam_ctx_reserve": (C.c_int, [_P, _I64, _I32, _I64]),
     "lam_ctx_num_sms": (C.c_int, [_P]),
+    "lam_ctx_set_spin_timeout": (C.c_int, [_P, _I64]),
+    "lam_ctx_status": (C.c_int, [_P, _P, _I32]),
     "lam_exact_attention": (C.c_int, [_P, C.c_int, _I64, _I32, _P, _P, _P, _P, _P, _P, _P, _P]),
     "lam_partial_attention": (C.c_int, [_P, C.c_int, _I64, _I32, _P, _P, _P, _P, _P, _P, _P, _P,
                                         _P, _P, _P, _P, _P]),
@@ -174,6 +177,15 @@ class Context:
     @property
     def num_sms(self) -> int:
         return self._lib.lam_ctx_num_sms(self.handle)
+
+    def set_spin_timeout(self, ns: int) -> None:
+        check(self._lib.lam_ctx_set_spin_timeout(self.handle, int(ns)))
+
+    def status(self, clear: bool = True) -> int:
+        """LAM_STATUS_* word of the context (synchronises the device)."""
+        st = C.c_int32()
+        check(self._lib.lam_ctx_status(self.handle, C.byref(st), int(clear)))
+        return st.value
 
     def reserve(self, partial_rows: int, head_dim: int, counters: int) -> None:
         check(self._lib.lam_ctx_reserve(self.handle, partial_rows, head_dim, counters))

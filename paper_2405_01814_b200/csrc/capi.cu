@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <numeric>
 #include <string>
@@ -44,6 +45,9 @@ struct lam_ctx {
   // and the monotonic layer counter that numbers them across calls
   uint32_t* host_flags = nullptr;
   uint32_t host_seq = 0;
+  // bounded device-side spins of the decode kernels (lam_ctx_status / lam_ctx_set_spin_timeout)
+  int32_t* status = nullptr;
+  unsigned long long spin_timeout_ns = 10ull * 1000 * 1000 * 1000;
 };
 
 namespace {
@@ -96,6 +100,24 @@ int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
   return e ? std::atoi(e) : dflt;
 }
+
+// Makes `device` current for the scope of a C-ABI call and restores the caller's device after.
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int device) {
+    err = cudaGetDevice(&prev);
+    if (err == cudaSuccess && prev != device) err = cudaSetDevice(device);
+    else if (err == cudaSuccess) prev = -1;  // nothing to restore
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+#define LAM_DEVICE(ctx)                                               \
+  DeviceGuard device_guard_((ctx)->device);                           \
+  if (device_guard_.err != cudaSuccess) return cuda_fail(device_guard_.err, "cudaSetDevice")
 
 // ---- driver entry point for tensor maps (no -lcuda link dependency) ----
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
@@ -168,7 +190,7 @@ struct Plan {
 // one.  So for a given item count the grid is the smallest one that still needs only
 // k = ceil(items / max_ctas) rounds, ctas = ceil(items / k): the rounds are as even as they
 // can be, and each CTA streams at min(BW_CHIP / ctas, RATE_SM) (C1: 256 items on 128 CTAs
-// beat 143 CTAs by 4 %, scripts/call56.sh).  Every item boundary costs ~C_ITEM; it costs the
+// beat 143 CTAs by 4 %, experiments/r01/call56.sh).  Every item boundary costs ~C_ITEM; it costs the
 // tensor-core kernel more (8 q heads of epilogue per item, split partial and merge round trips).
 //   T(S) = k * (item_bytes / min(BW_CHIP / ctas, RATE_SM) + C_ITEM)
 // The grid shrinks only by more than 5 %.  Measured choices (call46/47/54/56/57): C1 -> S = 1 on
@@ -243,7 +265,7 @@ int plan_decode(lam_ctx* ctx, const lam_decode_args* a, Plan* pl) {
   // included: both kernels stream at the same rate when timed alone (7226 GB/s, C2), but under
   // a sustained step the SIMT kernel's FMA/shuffle load draws more SM power, the clocks drop
   // further under sw_power_cap (1736-1814 vs 1822-1886 MHz) and the step is 5 % slower
-  // (scripts/call49.sh).  LAM_MHA_MMA=0 restores the SIMT kernel for G = 1.
+  // (experiments/r01/call49.sh).  LAM_MHA_MMA=0 restores the SIMT kernel for G = 1.
   if (kernel == LAM_KERNEL_AUTO)
     kernel = mma_ok && (G >= 2 || env_int("LAM_MHA_MMA", 1) != 0) ? LAM_KERNEL_GQA_MMA
                                                                   : LAM_KERNEL_SIMT;
@@ -331,7 +353,16 @@ struct HostStage {
   }
 };
 
-thread_local HostStage g_stage;
+// one staging area (and context) per device and thread: a thread that moves between devices
+// stages and launches on the device that is current at each call
+HostStage& host_stage() {
+  thread_local std::vector<std::unique_ptr<HostStage>> stages;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) dev = 0;
+  if (static_cast<size_t>(dev) >= stages.size()) stages.resize(dev + 1);
+  if (!stages[dev]) stages[dev] = std::make_unique<HostStage>();
+  return *stages[dev];
+}
 
 int check_err_word(lam_ctx* ctx, cudaStream_t stream, const char* empty_msg) {
   int32_t h = 0;
@@ -353,7 +384,7 @@ int run_instances(lam_ctx* ctx, int dtype, int64_t n_inst, int32_t d, const void
   if (d < 1) return fail(LAM_ERR_VALIDATION, "query must be non-empty");
   if (n_inst < 0) return fail(LAM_ERR_VALIDATION, "negative instance count");
   if (n_inst == 0) return LAM_OK;
-  LAM_CUDA(cudaSetDevice(ctx->device));
+  LAM_DEVICE(ctx);
   LAM_CUDA(grow(&ctx->offs, &ctx->offs_cap, n_inst + 1, false));
   LAM_CUDA(lam::launch_count_scan(n_inst, kv_len, exact ? nullptr : idx_off, ctx->offs, stream));
   int64_t total = 0;
@@ -389,7 +420,8 @@ int lam_ctx_create(int device, lam_ctx** out) {
   int n = 0;
   LAM_CUDA(cudaGetDeviceCount(&n));
   if (device < 0 || device >= n) return fail(LAM_ERR_VALIDATION, "no such CUDA device");
-  LAM_CUDA(cudaSetDevice(device));
+  DeviceGuard guard(device);
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
   int major = 0;
   LAM_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
   if (major < 10) return fail(LAM_ERR_CUDA, "liblamina_attn is built for sm_100a (B200) only");
@@ -400,6 +432,10 @@ int lam_ctx_create(int device, lam_ctx** out) {
   if (e == cudaSuccess) e = cudaMemset(c->err, 0, sizeof(int32_t));
   if (e == cudaSuccess) e = cudaMalloc(&c->slots, kSlots * 2 * sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMemset(c->slots, 0, kSlots * 2 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMalloc(&c->status, sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMemset(c->status, 0, sizeof(int32_t));
+  if (const char* t = std::getenv("LAM_SPIN_TIMEOUT_MS"))
+    c->spin_timeout_ns = static_cast<unsigned long long>(std::max(0.0, std::atof(t)) * 1e6);
   if (e != cudaSuccess) {
     delete c;
     return cuda_fail(e, "lam_ctx_create");
@@ -410,7 +446,8 @@ int lam_ctx_create(int device, lam_ctx** out) {
 
 int lam_ctx_destroy(lam_ctx* c) {
   if (!c) return LAM_OK;
-  cudaSetDevice(c->device);
+  DeviceGuard guard(c->device);
+  cudaFree(c->status);
   cudaFree(c->ws_acc);
   cudaFree(c->ws_ml);
   cudaFree(c->counters);
@@ -425,9 +462,24 @@ int lam_ctx_destroy(lam_ctx* c) {
 
 int lam_ctx_num_sms(const lam_ctx* c) { return c ? c->num_sms : 0; }
 
+int lam_ctx_set_spin_timeout(lam_ctx* c, int64_t timeout_ns) {
+  if (!c || timeout_ns < 0) return fail(LAM_ERR_VALIDATION, "bad spin timeout");
+  c->spin_timeout_ns = static_cast<unsigned long long>(timeout_ns);
+  return LAM_OK;
+}
+
+int lam_ctx_status(lam_ctx* c, int32_t* status, int32_t clear) {
+  if (!c || !status) return fail(LAM_ERR_VALIDATION, "null context or status");
+  LAM_DEVICE(c);
+  LAM_CUDA(cudaDeviceSynchronize());
+  LAM_CUDA(cudaMemcpy(status, c->status, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if (clear) LAM_CUDA(cudaMemset(c->status, 0, sizeof(int32_t)));
+  return LAM_OK;
+}
+
 int lam_ctx_reserve(lam_ctx* c, int64_t partial_rows, int32_t head_dim, int64_t counters) {
   if (!c) return fail(LAM_ERR_VALIDATION, "null context");
-  LAM_CUDA(cudaSetDevice(c->device));
+  LAM_DEVICE(c);
   // every launch slot has its own split workspace (capacities are per slot)
   if (partial_rows * head_dim > c->ws_acc_cap) {
     int64_t cap = 0;
@@ -477,7 +529,7 @@ int lam_merge(lam_ctx* ctx, int dtype, int64_t n, int32_t d, const void* a_acc,
   if (dtype != LAM_F32 && dtype != LAM_F64)
     return fail(LAM_ERR_VALIDATION, "merge supports f32 and f64");
   if (d < 0 || n < 0) return fail(LAM_ERR_VALIDATION, "negative size");
-  LAM_CUDA(cudaSetDevice(ctx->device));
+  LAM_DEVICE(ctx);
   auto s = static_cast<cudaStream_t>(stream);
   LAM_CUDA(lam::launch_merge(dtype, n, d, a_acc, a_max, a_log_denom, a_count, b_acc, b_max,
                              b_log_denom, b_count, o_acc, o_max, o_log_denom, o_count, ctx->err,
@@ -490,7 +542,7 @@ int lam_finalize(lam_ctx* ctx, int dtype, int64_t n, int32_t d, const void* acc,
   if (!ctx) return fail(LAM_ERR_VALIDATION, "null context");
   if (dtype != LAM_F32 && dtype != LAM_F64)
     return fail(LAM_ERR_VALIDATION, "finalize supports f32 and f64");
-  LAM_CUDA(cudaSetDevice(ctx->device));
+  LAM_DEVICE(ctx);
   auto s = static_cast<cudaStream_t>(stream);
   LAM_CUDA(cudaMemsetAsync(ctx->err, 0, sizeof(int32_t), s));
   LAM_CUDA(lam::launch_finalize(dtype, n, d, acc, log_denom, count, out, ctx->err, s));
@@ -509,10 +561,10 @@ int stage_in(int slot0, std::initializer_list<HostCopy> items, std::vector<void*
   int i = slot0;
   for (const auto& it : items) {
     void* d = nullptr;
-    int rc = g_stage.get(i++, it.bytes, &d);
+    int rc = host_stage().get(i++, it.bytes, &d);
     if (rc != LAM_OK) return rc;
     if (it.host && it.bytes > 0)
-      LAM_CUDA(cudaMemcpyAsync(d, it.host, it.bytes, cudaMemcpyHostToDevice, g_stage.stream));
+      LAM_CUDA(cudaMemcpyAsync(d, it.host, it.bytes, cudaMemcpyHostToDevice, host_stage().stream));
     dev.push_back(d);
   }
   return LAM_OK;
@@ -522,7 +574,7 @@ int stage_in(int slot0, std::initializer_list<HostCopy> items, std::vector<void*
 int lam_exact_attention_host(int dtype, int64_t n_inst, int32_t d, const void* q, int64_t n_rows,
                              const void* k_rows, const void* v_rows, const int64_t* kv_row0,
                              const int64_t* kv_len, const void* scale, void* out) {
-  int rc = g_stage.init();
+  int rc = host_stage().init();
   if (rc != LAM_OK) return rc;
   const int e = elem_bytes(dtype);
   if (e == 0) return fail(LAM_ERR_VALIDATION, "bad dtype");
@@ -538,12 +590,12 @@ int lam_exact_attention_host(int dtype, int64_t n_inst, int32_t d, const void* q
                  {nullptr, n_inst * d * e}},
                 dv);
   if (rc != LAM_OK) return rc;
-  rc = lam_exact_attention(g_stage.ctx, dtype, n_inst, d, dv[0], dv[1], dv[2],
+  rc = lam_exact_attention(host_stage().ctx, dtype, n_inst, d, dv[0], dv[1], dv[2],
                            static_cast<int64_t*>(dv[3]), static_cast<int64_t*>(dv[4]), dv[5], dv[6],
-                           g_stage.stream);
+                           host_stage().stream);
   if (rc != LAM_OK) return rc;
-  LAM_CUDA(cudaMemcpyAsync(out, dv[6], n_inst * d * e, cudaMemcpyDeviceToHost, g_stage.stream));
-  LAM_CUDA(cudaStreamSynchronize(g_stage.stream));
+  LAM_CUDA(cudaMemcpyAsync(out, dv[6], n_inst * d * e, cudaMemcpyDeviceToHost, host_stage().stream));
+  LAM_CUDA(cudaStreamSynchronize(host_stage().stream));
   return LAM_OK;
 }
 
@@ -553,7 +605,7 @@ int lam_partial_attention_host(int dtype, int64_t n_inst, int32_t d, const void*
                                const int64_t* idx, const int64_t* idx_off, const void* scale,
                                void* acc, void* max_logit, void* log_denom,
                                int64_t* token_count) {
-  int rc = g_stage.init();
+  int rc = host_stage().init();
   if (rc != LAM_OK) return rc;
   const int e = elem_bytes(dtype);
   if (e == 0) return fail(LAM_ERR_VALIDATION, "bad dtype");
@@ -575,12 +627,12 @@ int lam_partial_attention_host(int dtype, int64_t n_inst, int32_t d, const void*
                  {nullptr, n_inst * 8}},
                 dv);
   if (rc != LAM_OK) return rc;
-  rc = lam_partial_attention(g_stage.ctx, dtype, n_inst, d, dv[0], dv[1], dv[2],
+  rc = lam_partial_attention(host_stage().ctx, dtype, n_inst, d, dv[0], dv[1], dv[2],
                              static_cast<int64_t*>(dv[3]), static_cast<int64_t*>(dv[4]),
                              static_cast<int64_t*>(dv[5]), static_cast<int64_t*>(dv[6]), dv[7],
-                             dv[8], dv[9], dv[10], static_cast<int64_t*>(dv[11]), g_stage.stream);
+                             dv[8], dv[9], dv[10], static_cast<int64_t*>(dv[11]), host_stage().stream);
   if (rc != LAM_OK) return rc;
-  auto s = g_stage.stream;
+  auto s = host_stage().stream;
   LAM_CUDA(cudaMemcpyAsync(acc, dv[8], n_inst * d * e, cudaMemcpyDeviceToHost, s));
   LAM_CUDA(cudaMemcpyAsync(max_logit, dv[9], n_inst * e, cudaMemcpyDeviceToHost, s));
   LAM_CUDA(cudaMemcpyAsync(log_denom, dv[10], n_inst * e, cudaMemcpyDeviceToHost, s));
@@ -593,7 +645,7 @@ int lam_merge_host(int dtype, int64_t n, int32_t d, const void* a_acc, const voi
                    const void* a_log_denom, const int64_t* a_count, const void* b_acc,
                    const void* b_max, const void* b_log_denom, const int64_t* b_count,
                    void* o_acc, void* o_max, void* o_log_denom, int64_t* o_count) {
-  int rc = g_stage.init();
+  int rc = host_stage().init();
   if (rc != LAM_OK) return rc;
   const int e = elem_bytes(dtype);
   if (e == 0) return fail(LAM_ERR_VALIDATION, "bad dtype");
@@ -614,11 +666,11 @@ int lam_merge_host(int dtype, int64_t n, int32_t d, const void* a_acc, const voi
                  {nullptr, n * 8}},
                 dv);
   if (rc != LAM_OK) return rc;
-  rc = lam_merge(g_stage.ctx, dtype, n, d, dv[0], dv[1], dv[2], static_cast<int64_t*>(dv[3]),
+  rc = lam_merge(host_stage().ctx, dtype, n, d, dv[0], dv[1], dv[2], static_cast<int64_t*>(dv[3]),
                  dv[4], dv[5], dv[6], static_cast<int64_t*>(dv[7]), dv[8], dv[9], dv[10],
-                 static_cast<int64_t*>(dv[11]), g_stage.stream);
+                 static_cast<int64_t*>(dv[11]), host_stage().stream);
   if (rc != LAM_OK) return rc;
-  auto s = g_stage.stream;
+  auto s = host_stage().stream;
   LAM_CUDA(cudaMemcpyAsync(o_acc, dv[8], n * d * e, cudaMemcpyDeviceToHost, s));
   LAM_CUDA(cudaMemcpyAsync(o_max, dv[9], n * e, cudaMemcpyDeviceToHost, s));
   LAM_CUDA(cudaMemcpyAsync(o_log_denom, dv[10], n * e, cudaMemcpyDeviceToHost, s));
@@ -629,7 +681,7 @@ int lam_merge_host(int dtype, int64_t n, int32_t d, const void* a_acc, const voi
 
 int lam_finalize_host(int dtype, int64_t n, int32_t d, const void* acc, const void* log_denom,
                       const int64_t* count, void* out) {
-  int rc = g_stage.init();
+  int rc = host_stage().init();
   if (rc != LAM_OK) return rc;
   const int e = elem_bytes(dtype);
   if (e == 0) return fail(LAM_ERR_VALIDATION, "bad dtype");
@@ -638,11 +690,11 @@ int lam_finalize_host(int dtype, int64_t n, int32_t d, const void* acc, const vo
   rc = stage_in(0, {{acc, n * d * e}, {log_denom, n * e}, {count, n * 8}, {nullptr, n * d * e}},
                 dv);
   if (rc != LAM_OK) return rc;
-  rc = lam_finalize(g_stage.ctx, dtype, n, d, dv[0], dv[1], static_cast<int64_t*>(dv[2]), dv[3],
-                    g_stage.stream);
+  rc = lam_finalize(host_stage().ctx, dtype, n, d, dv[0], dv[1], static_cast<int64_t*>(dv[2]), dv[3],
+                    host_stage().stream);
   if (rc != LAM_OK) return rc;
-  LAM_CUDA(cudaMemcpyAsync(out, dv[3], n * d * e, cudaMemcpyDeviceToHost, g_stage.stream));
-  LAM_CUDA(cudaStreamSynchronize(g_stage.stream));
+  LAM_CUDA(cudaMemcpyAsync(out, dv[3], n * d * e, cudaMemcpyDeviceToHost, host_stage().stream));
+  LAM_CUDA(cudaStreamSynchronize(host_stage().stream));
   return LAM_OK;
 }
 
@@ -695,7 +747,7 @@ int lam_request_partition(const double* kv_sizes, int64_t n, int64_t num_devices
 int lam_decode_plan(lam_ctx* ctx, const lam_decode_args* a, int32_t* kernel, int32_t* num_splits,
                     int32_t* split_tokens) {
   if (!ctx) return fail(LAM_ERR_VALIDATION, "null context");
-  LAM_CUDA(cudaSetDevice(ctx->device));
+  LAM_DEVICE(ctx);
   Plan pl;
   int rc = plan_decode(ctx, a, &pl);
   if (rc != LAM_OK) return rc;
@@ -707,7 +759,7 @@ int lam_decode_plan(lam_ctx* ctx, const lam_decode_args* a, int32_t* kernel, int
 
 int lam_decode_plan_grid(lam_ctx* ctx, const lam_decode_args* a, int32_t* ctas) {
   if (!ctx) return fail(LAM_ERR_VALIDATION, "null context");
-  LAM_CUDA(cudaSetDevice(ctx->device));
+  LAM_DEVICE(ctx);
   Plan pl;
   int rc = plan_decode(ctx, a, &pl);
   if (rc != LAM_OK) return rc;
@@ -719,6 +771,7 @@ namespace {
 
 int decode_impl(lam_ctx* ctx, const lam_decode_args* a, const lam_peer_io* io, void* stream) {
   if (!ctx) return fail(LAM_ERR_VALIDATION, "null context");
+  LAM_DEVICE(ctx);
   Plan pl;
   int rc = plan_decode(ctx, a, &pl);
   if (rc != LAM_OK) return rc;
@@ -753,6 +806,8 @@ int decode_impl(lam_ctx* ctx, const lam_decode_args* a, const lam_peer_io* io, v
   p.item_base = ctx->item_base[slot];
   p.done_base = ctx->done_base[slot];
   p.order = a->request_order;
+  p.status = ctx->status;
+  p.spin_timeout_ns = ctx->spin_timeout_ns;
   if (a->k_new != nullptr) {  // fused append
     if (a->v_new == nullptr) return fail(LAM_ERR_VALIDATION, "fused append needs both k_new and v_new");
     p.k_new = a->k_new;
@@ -802,12 +857,14 @@ int decode_impl(lam_ctx* ctx, const lam_decode_args* a, const lam_peer_io* io, v
     p.n_done = io->n_done;
     p.wait_value = io->wait_value;
     p.done_value = io->done_value;
-    // the launch carries its own input dependencies (sequence numbers), so it may overlap the
-    // previous kernel's drain
-    p.pdl = io->n_wait > 0 && env_int("LAM_PDL", 1) != 0;
+    // the launch carries its own input dependencies (sequence numbers), so with overlap_prev it
+    // may overlap the previous kernel's drain entirely: it never waits for that grid, which the
+    // caller's overlap_prev contract allows (the preceding kernel writes none of the page table,
+    // lengths, order or KV rows this launch touches)
+    p.pdl = io->n_wait > 0 && a->overlap_prev != 0 && env_int("LAM_PDL", 1) != 0;
     // LAM_PEER_PREFETCH=1: stream the first KV tiles (local pool) before the inputs' sequence
     // numbers arrive.  Off by default: the inputs are normally published before the launch
-    // starts, and the deferred issue cost 0.3-0.6 % at N = 2 (scripts/call61.sh).
+    // starts, and the deferred issue cost 0.3-0.6 % at N = 2 (experiments/r01/call61.sh).
     if (io->n_wait > 0 && env_int("LAM_PEER_PREFETCH", 0) != 0) p.defer_inputs = 2;
   }
   if (a->overlap_prev != 0 && io == nullptr) {
@@ -872,7 +929,7 @@ static_assert(sizeof(cudaIpcMemHandle_t) <= LAM_IPC_HANDLE_BYTES, "IPC handle si
 
 int lam_peer_alloc(lam_ctx* ctx, int64_t bytes, void** dptr, void* handle) {
   if (!ctx || !dptr || !handle || bytes < 1) return fail(LAM_ERR_VALIDATION, "peer_alloc: bad arguments");
-  LAM_CUDA(cudaSetDevice(ctx->device));
+  LAM_DEVICE(ctx);
   void* p = nullptr;
   LAM_CUDA(cudaMalloc(&p, static_cast<size_t>(bytes)));
   cudaError_t e = cudaMemset(p, 0, static_cast<size_t>(bytes));
@@ -890,14 +947,14 @@ int lam_peer_alloc(lam_ctx* ctx, int64_t bytes, void** dptr, void* handle) {
 
 int lam_peer_free(lam_ctx* ctx, void* dptr) {
   if (!ctx) return fail(LAM_ERR_VALIDATION, "null context");
-  LAM_CUDA(cudaSetDevice(ctx->device));
+  LAM_DEVICE(ctx);
   LAM_CUDA(cudaFree(dptr));
   return LAM_OK;
 }
 
 int lam_peer_open(lam_ctx* ctx, const void* handle, void** dptr) {
   if (!ctx || !handle || !dptr) return fail(LAM_ERR_VALIDATION, "peer_open: bad arguments");
-  LAM_CUDA(cudaSetDevice(ctx->device));
+  LAM_DEVICE(ctx);
   cudaIpcMemHandle_t h{};
   std::memcpy(&h, handle, sizeof(h));
   LAM_CUDA(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
@@ -906,7 +963,7 @@ int lam_peer_open(lam_ctx* ctx, const void* handle, void** dptr) {
 
 int lam_peer_close(lam_ctx* ctx, void* dptr) {
   if (!ctx) return fail(LAM_ERR_VALIDATION, "null context");
-  LAM_CUDA(cudaSetDevice(ctx->device));
+  LAM_DEVICE(ctx);
   LAM_CUDA(cudaIpcCloseMemHandle(dptr));
   return LAM_OK;
 }
@@ -1098,7 +1155,7 @@ int decode_layers_host_flags(lam_ctx* ctx, const lam_decode_args* layer_args, in
     const int e = elem_bytes(a.kv_dtype);
     a.q_batch_stride = 0;
     a.new_batch_stride = 0;
-    a.overlap_prev = 0;
+    a.overlap_prev = l > 0;  // consecutive layers: disjoint pools (overlap_prev contract)
     lam_peer_io io{};
     io.n_src = 1;
     io.rows_per_src = a.batch;
@@ -1134,13 +1191,19 @@ int lam_decode_layers_host(lam_ctx* ctx, const lam_decode_args* layer_args, int3
                            const int32_t* d_positions, void* stream, void* copy_stream) {
   if (!ctx || !layer_args || n_layers < 0) return fail(LAM_ERR_VALIDATION, "bad arguments");
   if (n_layers == 0) return LAM_OK;
-  LAM_CUDA(cudaSetDevice(ctx->device));
+  LAM_DEVICE(ctx);
   auto cs = static_cast<cudaStream_t>(stream);
   auto xs = static_cast<cudaStream_t>(copy_stream);
   const StageLayout L = stage_layout(&layer_args[0]);
+  for (int l = 1; l < n_layers; ++l) {  // both staging sets are sized from layer 0
+    const StageLayout Ll = stage_layout(&layer_args[l]);
+    if (Ll.q > L.q || Ll.kv > L.kv || Ll.out > L.out)
+      return fail(LAM_ERR_VALIDATION, "layer " + std::to_string(l) +
+                                          ": q / k_new / v_new / out larger than layer 0's staging");
+  }
   auto base = [&](int set) { return static_cast<uint8_t*>(d_stage) + set * L.set; };
   // LAM_HOST_FLAGS=1: launches synchronised by sequence numbers instead of events.  Measured
-  // equal for C2 / C3 and slower for one-layer C1 (scripts/call63.sh), so events stay default.
+  // equal for C2 / C3 and slower for one-layer C1 (experiments/r01/call63.sh), so events stay default.
   const int use_flags = env_int("LAM_HOST_FLAGS", 0);
   bool flags_ok = use_flags && write_value_fn() && wait_value_fn();
   for (int l = 0; l < n_layers && flags_ok; ++l)  // (the peer-io launch has no lse output)
@@ -1181,6 +1244,7 @@ int lam_decode_layers_host(lam_ctx* ctx, const lam_decode_args* layer_args, int3
     uint8_t* b = base(s);
     lam_decode_args a = layer_args[l];
     a.q = b;
+    a.q_batch_stride = 0;  // the staging set holds dense [B][Hq][D] rows
     a.out = b + L.q + 2 * L.kv;
     LAM_CUDA(cudaStreamWaitEvent(cs, in_ready[s], 0));
     if (l >= 2) LAM_CUDA(cudaStreamWaitEvent(cs, out_free[s], 0));

@@ -85,7 +85,14 @@ struct DecodeParams {
   uint32_t wait_value, done_value;
   const uint32_t* wait_flag[LAM_MAX_PEERS];
   uint32_t* done_flag[LAM_MAX_PEERS];
+  // bounded spins (see spin_expired): status word of the context and the timeout (0 = none)
+  int32_t* status;
+  unsigned long long spin_timeout_ns;
 };
+
+// lam_ctx_status codes (include/lamina_attn.h)
+constexpr int kStatusInputTimeout = 1;  // input sequence numbers never arrived
+constexpr int kStatusSlotTimeout = 2;   // the launch slot's previous launch never finished
 
 __device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
   unsigned long long v;
@@ -93,24 +100,43 @@ __device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned 
   return v;
 }
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// A spin that has seen no progress for p.spin_timeout_ns (0 = wait forever) gives up: it records
+// `code` in the context's status word (lam_ctx_status) and returns false.  The launch then
+// completes normally — its outputs are unspecified and its done flags are still published, so
+// no waiter on another GPU hangs — instead of trapping, which would leave a sticky error in the
+// CUDA context of every attention worker.
+__device__ __forceinline__ bool spin_expired(const DecodeParams& p, unsigned long long t0, int code) {
+  if (p.spin_timeout_ns == 0 || globaltimer_ns() - t0 < p.spin_timeout_ns) return false;
+  if (p.status != nullptr) atomicCAS(p.status, 0, code);
+  return true;
+}
+
 // Wait until the previous launch on this slot has finished (normally long done).
 __device__ __forceinline__ void acquire_slot(const DecodeParams& p) {
-  const long long t0 = clock64();
+  const unsigned long long t0 = globaltimer_ns();
   while (ld_acquire_gpu_u64(p.slot + 1) < p.done_base) {
     __nanosleep(100);
-    if (clock64() - t0 > (20ll << 30)) __trap();
+    if (spin_expired(p, t0, kStatusSlotTimeout)) return;
   }
 }
 
-// Spin until the inputs of this launch are published (peer transport).  ~10 s without progress
-// traps the kernel instead of hanging the device.
+// Spin until the inputs of this launch are published (peer transport).
 __device__ __forceinline__ void wait_inputs(const DecodeParams& p) {
   if (p.n_wait <= 0) return;
-  const long long t0 = clock64();
+  const unsigned long long t0 = globaltimer_ns();
   for (int i = 0; i < p.n_wait; ++i) {
     while (static_cast<int32_t>(ld_acquire_sys(p.wait_flag[i]) - p.wait_value) < 0) {
       __nanosleep(200);
-      if (clock64() - t0 > (20ll << 30)) __trap();
+      if (spin_expired(p, t0, kStatusInputTimeout)) {
+        i = p.n_wait;
+        break;
+      }
     }
   }
   fence_proxy_async_global();

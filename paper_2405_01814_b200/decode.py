@@ -66,9 +66,20 @@ def make_args(q: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor,
         raise _lib.ValidationError("seq_lens must be int32")
     if page_table is not None and page_table.dtype != torch.int32:
         raise _lib.ValidationError("page_table must be int32")
+    if seq_lens.shape != (B,):
+        raise _lib.ValidationError(f"seq_lens must be [B] = [{B}]")
+    if page_table is not None:
+        if page_table.dim() != 2 or page_table.shape[0] < B or not page_table[:B].is_contiguous():
+            raise _lib.ValidationError("page_table must be [>= B, pages] with contiguous rows")
+    elif k_pool.shape[0] < B:
+        raise _lib.ValidationError("dense KV pools need one [Hkv, l_max, D] block per request")
     odt = out_dtype or (out.dtype if out is not None else q.dtype)
+    if odt not in (q.dtype, torch.float32):
+        raise _lib.ValidationError("out dtype must be the KV dtype or float32")
     if out is None:
         out = torch.empty((B, Hq, D), dtype=odt, device=q.device)
+    elif out.shape != (B, Hq, D) or out.dtype != odt or not out.is_contiguous() or not out.is_cuda:
+        raise _lib.ValidationError(f"out must be a contiguous CUDA [{B}, {Hq}, {D}] {odt} tensor")
     a = DecodeArgs()
     a.kv_dtype = _DT[q.dtype]
     a.out_dtype = _DT[odt]

@@ -33,6 +33,23 @@ from typing import Callable
 import torch
 
 
+def local_batch(batch: int, world: int, scaling: str = "strong", micro_batches: int = 2) -> int:
+    """Requests each model worker produces.  strong: a fixed global batch is dealt out (request
+    g = rank * B_local + b), so T1 / (N * TN) is the parallel efficiency at a fixed global batch
+    (BASELINE.md §3); weak: every rank brings `batch` requests (global batch N * batch)."""
+    if scaling == "weak":
+        b = batch
+    elif scaling == "strong":
+        if batch % world:
+            raise ValueError(f"global batch {batch} does not split over {world} ranks")
+        b = batch // world
+    else:
+        raise ValueError("scaling must be 'strong' or 'weak'")
+    if b % micro_batches:
+        raise ValueError(f"{b} requests per rank do not split into {micro_batches} micro-batches")
+    return b
+
+
 @dataclass
 class ShardGeometry:
     rank: int
@@ -497,6 +514,10 @@ class PeerShardedAttention:
                 a.q_batch_stride = g.W * g.D
                 a.new_batch_stride = g.W * g.D
                 a.lse = None
+                # consecutive launches of a step touch disjoint pools / page-table rows, so they
+                # may overlap (lam_decode_peer + overlap_prev); the step's first launch follows
+                # whatever the stream ran before it (e.g. a length update) in stream order
+                a.overlap_prev = 0 if (layer, m) == (0, 0) else 1
                 io = _lib.PeerIO()
                 io.n_src, io.rows_per_src = N, g.Bh
                 blk = (layer * MB + m) * N + j

@@ -472,3 +472,93 @@ def test_planner_choices_for_baseline_shapes(built, name, B, Hq, Hkv, L, dtype, 
     kern, splits, _ = dec.plan(q, pool, pool, lens, **kw)
     ctas = dec.plan_grid(q, pool, pool, lens, **kw)
     assert (kern, splits, ctas) == want
+
+
+def _request_kv(pool, pt, b, kvh, ln, P):
+    pages = pt[b, : -(-ln // P)].long()
+    return pool[pages, kvh].reshape(-1, pool.shape[-1])[:ln]
+
+
+@pytest.mark.slow
+def test_c2_full_shape_overlap_chain_vs_oracle(built):
+    """BASELINE config 2 exactly as the bench launches it — B=64, l=4096, 32/32 heads, bf16,
+    paged P=64, the tensor-core kernel at G=1, fused append, overlap_prev — as a chain of three
+    layers where each layer's q and new K/V rows are the previous layer's output (so the
+    programmatic-dependent-launch ordering is load-bearing), against the oracle on seeded
+    (request, head) pairs of every layer; appends bit-exact."""
+    from paper_2405_01814_b200 import decode as dec
+
+    B, H, D, L, P, layers = 64, 32, 128, 4096, 64, 3
+    npg = B * L // P
+    g = torch.Generator(device="cuda").manual_seed(12)
+    perm = torch.randperm(npg, generator=torch.Generator().manual_seed(2)).to(torch.int32)
+    pt = perm.view(B, L // P).cuda()
+    lens = _lens_t([L] * B)
+    pools = [(torch.empty((npg, H, P, D), dtype=torch.bfloat16, device="cuda").uniform_(-1, 1, generator=g),
+              torch.empty((npg, H, P, D), dtype=torch.bfloat16, device="cuda").uniform_(-1, 1, generator=g))
+             for _ in range(layers)]
+    x0 = torch.empty((B, 3 * H, D), dtype=torch.bfloat16, device="cuda").uniform_(-1, 1, generator=g)
+    kern, splits, _ = dec.plan(x0[:, :H], pools[0][0], pools[0][1], lens, page_table=pt, max_len=L)
+    assert kern == "gqa_mma" and splits == 1
+    # layer 0 reads packed QKV rows; layer l > 0 reads q = k_new = v_new = layer l-1's output,
+    # straight from the launch before it (no kernel in between)
+    ins = [(x0[:, :H], x0[:, H:2 * H], x0[:, 2 * H:])]
+    outs = []
+    for layer in range(layers):
+        q, kn, vn = ins[layer]
+        o = dec.decode(q, pools[layer][0], pools[layer][1], lens, page_table=pt, max_len=L,
+                       k_new=kn, v_new=vn, overlap_prev=layer > 0)
+        outs.append(o)
+        ins.append((o, o, o))
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(4)
+    ptc = pt
+    for layer in range(layers):
+        kp, vp = pools[layer]
+        for _ in range(4):
+            b, h = int(rng.integers(B)), int(rng.integers(H))
+            kd = _request_kv(kp, ptc, b, h, L, P)
+            vd = _request_kv(vp, ptc, b, h, L, P)
+            q, kn, vn = ins[layer]
+            assert torch.equal(kd[L - 1], kn[b, h]) and torch.equal(vd[L - 1], vn[b, h])
+            want = oracle_decode(q[b:b + 1, h:h + 1], kd[None, None], vd[None, None], [L], 1 / math.sqrt(D))
+            got = outs[layer][b, h].float().cpu().numpy()
+            assert _maxabs(got, want[0, 0]) <= 2e-3 + 2.0 ** -9, (layer, b, h)
+
+
+@pytest.mark.slow
+def test_c5_full_shape_request_order_vs_oracle(built):
+    """BASELINE config 5's launch as the bench runs it (one micro-batch launch of the global
+    B=256 batch's first half is what the engine issues; here the whole batch in one launch):
+    LLaMA-2-70B GQA 64/8, bf16, log-uniform lengths on [128, 16384] (mt-seeded), paged,
+    fused append and longest-first request_order, against the oracle on seeded pairs that
+    include the longest and the shortest request."""
+    from paper_2405_01814_b200 import decode as dec
+
+    B, Hq, Hkv, D, P = 256, 64, 8, 128, 64
+    r = np.random.default_rng(2024)
+    lens = np.exp(r.uniform(math.log(128), math.log(16384), B)).astype(np.int32)
+    pt_np, npages = page_table_for(lens, P, seed=8)
+    pt = torch.tensor(pt_np, device="cuda")
+    g = torch.Generator(device="cuda").manual_seed(5)
+    kp = torch.empty((npages, Hkv, P, D), dtype=torch.bfloat16, device="cuda").uniform_(-1, 1, generator=g)
+    vp = torch.empty_like(kp).uniform_(-1, 1, generator=g)
+    x = torch.empty((B, Hq + 2 * Hkv, D), dtype=torch.bfloat16, device="cuda").uniform_(-1, 1, generator=g)
+    lt = _lens_t(lens)
+    out = dec.decode(x[:, :Hq], kp, vp, lt, page_table=pt, max_len=int(lens.max()),
+                     k_new=x[:, Hq:Hq + Hkv], v_new=x[:, Hq + Hkv:], out_dtype=torch.float32,
+                     request_order=dec.longest_first(lt))
+    torch.cuda.synchronize()
+    assert torch.isfinite(out).all()
+    rng = np.random.default_rng(6)
+    bs = [int(np.argmax(lens)), int(np.argmin(lens))] + [int(b) for b in rng.choice(B, 6, replace=False)]
+    for b in bs:
+        ln = int(lens[b])
+        kvh = int(rng.integers(Hkv))
+        kd = _request_kv(kp, pt, b, kvh, ln, P)
+        vd = _request_kv(vp, pt, b, kvh, ln, P)
+        assert torch.equal(kd[ln - 1], x[b, Hq + kvh]) and torch.equal(vd[ln - 1], x[b, Hq + Hkv + kvh])
+        heads = list(range(kvh * 8, kvh * 8 + 8))
+        want = oracle_decode(x[b:b + 1, heads], kd[None, None], vd[None, None], [ln],
+                             1 / math.sqrt(D))  # 8 q heads on one KV head (G = 8)
+        assert _maxabs(out[b, heads].cpu().numpy(), want[0]) <= 2e-3, b

@@ -292,3 +292,96 @@ def test_head_sharded_exchange_8_ranks(tmp_path):
             v[0, :, lens[req]] = vn[0, req]
             want = O.decode_dense(q[0, req:req + 1], k, v, [lens[req] + 1], 1 / np.sqrt(D))[0]
             assert np.allclose(got[0, b], want, rtol=0, atol=1e-6)
+
+
+# ---- strong scaling: one fixed global batch dealt out over 2, 4 and 8 ranks (gloo) ----
+BG, HQS, HKVS = 16, 16, 8
+
+
+def _strong_problem(seed=9):
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(1, 12, BG).astype(np.int32)
+    lmax = int(lens.max()) + 1
+    ck = rng.uniform(-1, 1, (2, BG, HKVS, lmax, D)).astype(np.float32)
+    cv = rng.uniform(-1, 1, (2, BG, HKVS, lmax, D)).astype(np.float32)
+    q = rng.uniform(-1, 1, (2, BG, HQS, D)).astype(np.float32)
+    kn = rng.uniform(-1, 1, (2, BG, HKVS, D)).astype(np.float32)
+    vn = rng.uniform(-1, 1, (2, BG, HKVS, D)).astype(np.float32)
+    return lens, ck, cv, q, kn, vn
+
+
+def _strong_worker(rank, world, port, result_dir):
+    sys.path.insert(0, str(ROOT))
+    import torch.distributed as dist
+
+    from oracle import oracle as O
+    from paper_2405_01814_b200.dist import (HeadShardedAttention, ShardGeometry, local_batch,
+                                            shard_inputs, stitch_outputs)
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    bl = local_batch(BG, world, "strong")
+    geo = ShardGeometry(rank, world, 2, bl, HQS, HKVS, D, 2)
+    assert geo.B_attn == BG  # every attention worker sees the whole global batch
+    lens, ck, cv, q, kn, vn = _strong_problem()
+    h0, h1 = rank * geo.hkv_l, (rank + 1) * geo.hkv_l
+    row_req = np.zeros(geo.B_attn, np.int64)
+    for src in range(world):
+        for b in range(bl):
+            row_req[geo.kv_row(src, b)] = src * bl + b
+    sk, sv = ck[:, row_req, h0:h1].copy(), cv[:, row_req, h0:h1].copy()
+    pos = lens[row_req]
+
+    def attend(layer, m, qr, k, v, out):
+        sl = slice(m * geo.B_mb, (m + 1) * geo.B_mb)
+        for i, r in enumerate(range(sl.start, sl.stop)):
+            sk[layer, r, :, pos[r]] = k[i].contiguous().numpy()
+            sv[layer, r, :, pos[r]] = v[i].contiguous().numpy()
+        out.copy_(torch.from_numpy(O.decode_dense(qr.contiguous().numpy(), sk[layer, sl],
+                                                  sv[layer, sl], pos[sl] + 1, 1 / np.sqrt(D))))
+
+    eng = HeadShardedAttention(geo, dist, None, attend, torch.device("cpu"), torch.float32)
+    mine = slice(rank * bl, (rank + 1) * bl)
+    qkv_in = shard_inputs(torch.from_numpy(q[:, mine]), torch.from_numpy(kn[:, mine]),
+                          torch.from_numpy(vn[:, mine]), world, 2)
+    out = torch.zeros(geo.q_shape())
+    eng.step(qkv_in, out)
+    np.save(Path(result_dir) / f"strong{world}_{rank}.npy", stitch_outputs(out).numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_strong_scaling_geometry_same_global_batch(tmp_path, world):
+    """The bench's --scaling strong geometry: the same 16 requests dealt out over N ranks (8 KV
+    heads, 1-4 per rank, two micro-batches) give, per global request, the single-process oracle
+    over all heads — the same outputs at every N."""
+    import torch.multiprocessing as mp
+
+    from oracle import oracle as O
+
+    os.environ["PYTHONPATH"] = str(ROOT) + os.pathsep + os.environ.get("PYTHONPATH", "")
+    mp.spawn(_strong_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    lens, ck, cv, q, kn, vn = _strong_problem()
+    bl = BG // world
+    for rank in range(world):
+        got = np.load(tmp_path / f"strong{world}_{rank}.npy")
+        for layer in range(2):
+            for b in range(bl):
+                req = rank * bl + b
+                k, v = ck[layer, req:req + 1].copy(), cv[layer, req:req + 1].copy()
+                k[0, :, lens[req]] = kn[layer, req]
+                v[0, :, lens[req]] = vn[layer, req]
+                want = O.decode_dense(q[layer, req:req + 1], k, v, [lens[req] + 1], 1 / np.sqrt(D))[0]
+                assert np.allclose(got[layer, b], want, rtol=0, atol=1e-6)
+
+
+def test_local_batch():
+    from paper_2405_01814_b200.dist import local_batch
+
+    assert local_batch(128, 8) == 16 and local_batch(128, 1) == 128
+    assert local_batch(64, 4, "weak") == 64
+    with pytest.raises(ValueError):
+        local_batch(32, 3)
+    with pytest.raises(ValueError):
+        local_batch(8, 8)  # one request per rank cannot form two micro-batches

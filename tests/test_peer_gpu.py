@@ -106,6 +106,7 @@ def test_decode_peer_back_to_back_overlapping_launches(built):
     a, _ = dec.make_args(qd, cache.k[0], cache.v[0], cache.seq_lens, page_table=cache.page_table,
                          max_len=int(lens.max()), out=qd)
     a.q_batch_stride = a.new_batch_stride = W * D
+    a.overlap_prev = 1  # consecutive launches may overlap (programmatic dependent launch)
     want, _, _ = _reference(cache, lens, qkv, s)
     torch.cuda.synchronize()
     ready = C.c_void_p(flags.data_ptr())
@@ -155,3 +156,110 @@ def test_decode_peer_validation(built):
     with pytest.raises(_lib.ValidationError, match="null"):
         _lib.check(lib.lam_decode_peer(ctx.handle, a, io, None))
     assert math.isfinite(1.0)
+
+
+def _peer_io(n_src, Bh, Hq, Hkv, D, qkv, outs, flags=None, value=1):
+    from paper_2405_01814_b200 import _lib
+
+    io = _lib.PeerIO()
+    io.n_src, io.rows_per_src = n_src, Bh
+    for i in range(n_src):
+        io.q_src[i] = qkv[i].data_ptr()
+        io.out_dst[i] = outs[i].data_ptr()
+    io.k_new_offset, io.v_new_offset = Hq * D, (Hq + Hkv) * D
+    if flags is not None:
+        io.n_wait = io.n_done = n_src
+        io.wait_value = io.done_value = value
+        for i in range(n_src):
+            io.wait_flags[i] = flags.data_ptr() + 4 * i
+            io.done_flags[i] = flags.data_ptr() + 4 * (n_src + i)
+    return io
+
+
+@pytest.mark.parametrize("n_src,Bh,G", [(2, 3, 8), (3, 2, 1), (5, 2, 8), (8, 2, 8), (8, 1, 4)])
+def test_decode_peer_vs_oracle(built, n_src, Bh, G):
+    """The peer-transport launch (rows grouped by source, q / k_new / v_new read from each
+    source's packed rows, outputs stored into each source's buffer, in-kernel sequence numbers)
+    against the CPU oracle: fused append bit-exact (the oracle's byte paging of the pool equals
+    the dense cache with the new token at seq_len - 1) and attention within the bf16 bound
+    (exact_attention<float> on the upcast values, attention.cpp:48-70)."""
+    from oracle import oracle as O
+    from paper_2405_01814_b200 import _lib, decode as dec
+    from tests.helpers import oracle_decode
+
+    Hkv, D = 2, 128
+    Hq = Hkv * G
+    cache, lens, qkv, s = _setup(n_src=n_src, Bh=Bh, Hq=Hq, Hkv=Hkv, D=D, seed=n_src * 10 + G)
+    B, W, P = n_src * Bh, s["W"], cache.k.shape[3]
+    lmax = int(lens.max())
+    pt = cache.page_table.cpu().numpy()
+    # the cache before the step, dense, with each request's new token written at len - 1
+    k_dense = dec.kv_gather(cache.k[0], cache.page_table, cache.seq_lens, lmax).cpu()
+    v_dense = dec.kv_gather(cache.v[0], cache.page_table, cache.seq_lens, lmax).cpu()
+    packed = torch.cat(qkv, 0).cpu()
+    for b in range(B):
+        k_dense[b, :, lens[b] - 1] = packed[b, Hq:Hq + Hkv]
+        v_dense[b, :, lens[b] - 1] = packed[b, Hq + Hkv:]
+    outs = [torch.zeros((Bh, Hq, D), dtype=torch.float32, device="cuda") for _ in range(n_src)]
+    flags = torch.zeros(2 * n_src, dtype=torch.int32, device="cuda")
+    qd = torch.empty((B, Hq, D), dtype=torch.bfloat16, device="cuda")
+    a, _ = dec.make_args(qd, cache.k[0], cache.v[0], cache.seq_lens, page_table=cache.page_table,
+                         max_len=lmax, out=torch.empty((B, Hq, D), device="cuda"))
+    a.q_batch_stride = a.new_batch_stride = W * D
+    io = _peer_io(n_src, Bh, Hq, Hkv, D, qkv, outs, flags, value=7)
+    lib, ctx = _lib.load(), _lib.context(0)
+    torch.cuda.synchronize()
+    _lib.check(lib.lam_decode_peer(ctx.handle, a, io, torch.cuda.current_stream().cuda_stream))
+    side = torch.cuda.Stream()
+    ready = (C.c_void_p * n_src)(*[flags.data_ptr() + 4 * i for i in range(n_src)])
+    _lib.check(lib.lam_stream_signal(ctx.handle, ready, n_src, 7, side.cuda_stream))
+    torch.cuda.synchronize()
+    assert flags.tolist() == [7] * (2 * n_src)
+    assert ctx.status() == _lib.LAM_STATUS_OK
+    # append: byte-exact against the oracle's page gather of the pool the kernel wrote
+    for pool, dense in ((cache.k[0], k_dense), (cache.v[0], v_dense)):
+        pool_bytes = pool.view(torch.uint8).cpu().numpy().reshape(pool.shape[0], Hkv, P, D * 2)
+        got = O.page_gather(pool_bytes, pt, lens, lmax)
+        assert np.array_equal(got, dense.view(torch.uint8).numpy().reshape(got.shape))
+    want = oracle_decode(packed[:, :Hq], k_dense, v_dense, lens, 1 / math.sqrt(D))
+    got = torch.cat(outs, 0).cpu().numpy()
+    assert float(np.abs(got - want).max()) <= 2e-3
+
+
+def test_spin_timeout_reports_status_instead_of_trapping(built):
+    """A launch whose inputs are never published gives up after the context's spin timeout:
+    it records LAM_STATUS_INPUT_TIMEOUT, still publishes its done flags, and the context stays
+    usable for the next launch."""
+    from paper_2405_01814_b200 import _lib, decode as dec
+
+    cache, lens, qkv, s = _setup(n_src=2, Bh=2, Hq=8, Hkv=2)
+    n_src, Bh, Hq, Hkv, D, W = (s[x] for x in ("n_src", "Bh", "Hq", "Hkv", "D", "W"))
+    ctx = _lib.Context(0)  # own context: its timeout does not leak into other tests
+    try:
+        ctx.set_spin_timeout(20_000_000)  # 20 ms
+        outs = [torch.zeros((Bh, Hq, D), dtype=torch.bfloat16, device="cuda") for _ in range(n_src)]
+        flags = torch.zeros(2 * n_src, dtype=torch.int32, device="cuda")
+        qd = torch.empty((n_src * Bh, Hq, D), dtype=torch.bfloat16, device="cuda")
+        a, _ = dec.make_args(qd, cache.k[0].clone(), cache.v[0].clone(), cache.seq_lens,
+                             page_table=cache.page_table, max_len=int(lens.max()), out=qd)
+        a.q_batch_stride = a.new_batch_stride = W * D
+        io = _peer_io(n_src, Bh, Hq, Hkv, D, qkv, outs, flags, value=3)
+        lib = _lib.load()
+        _lib.check(lib.lam_decode_peer(ctx.handle, a, io, torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()  # returns: the kernel gave up instead of hanging or trapping
+        assert ctx.status() == _lib.LAM_STATUS_INPUT_TIMEOUT
+        assert flags[n_src:].tolist() == [3] * n_src
+        assert ctx.status() == _lib.LAM_STATUS_OK  # cleared by the read
+        # the context still works: publish and rerun
+        flags[:n_src] = 4
+        io.wait_value = io.done_value = 4
+        want, _, _ = _reference(cache, lens, qkv, s)
+        a2, _ = dec.make_args(qd, cache.k[0], cache.v[0], cache.seq_lens,
+                              page_table=cache.page_table, max_len=int(lens.max()), out=qd)
+        a2.q_batch_stride = a2.new_batch_stride = W * D
+        _lib.check(lib.lam_decode_peer(ctx.handle, a2, io, torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        assert ctx.status() == _lib.LAM_STATUS_OK
+        assert torch.equal(torch.cat(outs, 0), want)
+    finally:
+        ctx.close()
