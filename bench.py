@@ -398,7 +398,10 @@ def check_outputs(W, engine, step_fn, counter, layers_hint=None, pairs_per_layer
     torch.cuda.synchronize(W.device)
     rng = np.random.default_rng(seed + W.rank)
     L = W.layers
-    layers = sorted({0, min(1, L - 1), L - 1} if layers_hint is None else set(layers_hint))
+    # with fewer resident pool sets than layers, layers l and l + resident share a pool within a
+    # step and the later one's append is what the pool holds: check layers no later layer aliases
+    lo = max(0, L - W.resident)
+    layers = sorted({lo, min(lo + 1, L - 1), L - 1} if layers_hint is None else set(layers_hint))
     G = W.Hq // W.Hkv
     scale = 1.0 / math.sqrt(W.D)
     P = W.w["P"]

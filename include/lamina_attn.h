@@ -45,6 +45,7 @@ extern "C" {
 #define LAM_KERNEL_AUTO 0
 #define LAM_KERNEL_SIMT 1     /* warp-shuffle online softmax, CUDA cores (MHA) */
 #define LAM_KERNEL_GQA_MMA 2  /* tensor-core m16n8k16 over a GQA group of 8 q heads */
+#define LAM_KERNEL_GQA_TC 3   /* tcgen05.mma from the TMA ring, accumulators in TMEM */
 
 typedef struct lam_ctx lam_ctx;
 

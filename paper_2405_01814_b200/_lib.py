@@ -15,7 +15,7 @@ DROPIN_PATH = LIB_DIR / "libdisagg_attention.so"
 
 LAM_OK, LAM_ERR_ERROR, LAM_ERR_VALIDATION, LAM_ERR_CUDA = 0, 1, 2, 3
 LAM_F32, LAM_F64, LAM_BF16, LAM_F16 = 0, 1, 2, 3
-LAM_KERNEL_AUTO, LAM_KERNEL_SIMT, LAM_KERNEL_GQA_MMA = 0, 1, 2
+LAM_KERNEL_AUTO, LAM_KERNEL_SIMT, LAM_KERNEL_GQA_MMA, LAM_KERNEL_GQA_TC = 0, 1, 2, 3
 LAM_STATUS_OK, LAM_STATUS_INPUT_TIMEOUT, LAM_STATUS_SLOT_TIMEOUT = 0, 1, 2
 
 

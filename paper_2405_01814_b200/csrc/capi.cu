@@ -201,7 +201,7 @@ void choose_splits(Plan& pl, int64_t units, int max_len, int max_ctas, int split
   static const double BW_CHIP = 7.0e12, RATE_SM = env_int("LAM_PLAN_RATE_SM", 50) * 1e9,
                       C_ITEM_SIMT = env_int("LAM_PLAN_CITEM_NS", 2000) * 1e-9,
                       C_ITEM_MMA = env_int("LAM_PLAN_CITEM_MMA_NS", 5000) * 1e-9;
-  const double C_ITEM = pl.kernel == LAM_KERNEL_GQA_MMA ? C_ITEM_MMA : C_ITEM_SIMT;
+  const double C_ITEM = pl.kernel == LAM_KERNEL_SIMT ? C_ITEM_SIMT : C_ITEM_MMA;
   const int tiles_total = std::max(1, (max_len + pl.tile - 1) / pl.tile);
   const int occ_per_sm = std::max(1, max_ctas / 148);
   double best = 1e300;
@@ -260,16 +260,32 @@ int plan_decode(lam_ctx* ctx, const lam_decode_args* a, Plan* pl) {
   const int mtile = lam::mma_variant_tile(variant);
   const bool mma_ok = (kvd == LAM_BF16 || kvd == LAM_F16) && a->head_dim == 128 && G >= 1 &&
                       G <= 8 && mtile > 0 && (!paged || a->page_size % mtile == 0);
+  const bool tc_ok = (kvd == LAM_BF16 || kvd == LAM_F16) && a->head_dim == 128 && G >= 1 &&
+                     G <= 8 && a->page_size % lam::kTcBoxRows == 0;
   int kernel = a->kernel;
   // 16-bit KV with D = 128 runs on the tensor-core kernel for every group size, MHA (G = 1)
   // included: both kernels stream at the same rate when timed alone (7226 GB/s, C2), but under
   // a sustained step the SIMT kernel's FMA/shuffle load draws more SM power, the clocks drop
   // further under sw_power_cap (1736-1814 vs 1822-1886 MHz) and the step is 5 % slower
   // (experiments/r01/call49.sh).  LAM_MHA_MMA=0 restores the SIMT kernel for G = 1.
-  if (kernel == LAM_KERNEL_AUTO)
+  if (kernel == LAM_KERNEL_AUTO) {
     kernel = mma_ok && (G >= 2 || env_int("LAM_MHA_MMA", 1) != 0) ? LAM_KERNEL_GQA_MMA
                                                                   : LAM_KERNEL_SIMT;
-  if (kernel == LAM_KERNEL_GQA_MMA) {
+    // LAM_GQA_TC=1: the tcgen05 / TMEM kernel wherever it applies (A/B against mma.sync)
+    if (tc_ok && kernel == LAM_KERNEL_GQA_MMA && env_int("LAM_GQA_TC", 0) != 0)
+      kernel = LAM_KERNEL_GQA_TC;
+  }
+  if (kernel == LAM_KERNEL_GQA_TC) {
+    if (!tc_ok)
+      return fail(LAM_ERR_VALIDATION,
+                  "tcgen05 GQA kernel needs 16-bit KV, head_dim 128, 1 <= G <= 8 and page_size a "
+                  "multiple of 64");
+    pl->kernel = kernel;
+    pl->variant = 0;
+    pl->GQ = 8;
+    pl->QG = 1;
+    pl->tile = lam::kTcTile;
+  } else if (kernel == LAM_KERNEL_GQA_MMA) {
     if (!mma_ok)
       return fail(LAM_ERR_VALIDATION,
                   "GQA MMA kernel needs 16-bit KV, head_dim 128, 1 <= G <= 8 and page_size a "
@@ -292,9 +308,9 @@ int plan_decode(lam_ctx* ctx, const lam_decode_args* a, Plan* pl) {
   } else {
     return fail(LAM_ERR_VALIDATION, "unknown kernel family");
   }
-  const int occ = pl->kernel == LAM_KERNEL_GQA_MMA
-                      ? lam::occupancy_mma(kvd, pl->variant)
-                      : lam::occupancy_simt(kvd, a->head_dim, pl->GQ, pl->variant);
+  const int occ = pl->kernel == LAM_KERNEL_GQA_MMA  ? lam::occupancy_mma(kvd, pl->variant)
+                  : pl->kernel == LAM_KERNEL_GQA_TC ? lam::occupancy_tc(kvd)
+                                                    : lam::occupancy_simt(kvd, a->head_dim, pl->GQ, pl->variant);
   if (occ <= 0) return fail(LAM_ERR_CUDA, "decode kernel cannot be resident on this device");
   const int64_t units = static_cast<int64_t>(a->batch) * a->num_kv_heads * pl->QG;
   choose_splits(*pl, units, a->max_len, occ * ctx->num_sms, a->split_tokens,
@@ -889,18 +905,22 @@ int decode_impl(lam_ctx* ctx, const lam_decode_args* a, const lam_peer_io* io, v
     p.counters = ctx->counters + slot * ctx->counters_cap;
   }
   auto s = static_cast<cudaStream_t>(stream);
-  if (pl.kernel == LAM_KERNEL_GQA_MMA) {
+  if (pl.kernel == LAM_KERNEL_GQA_MMA || pl.kernel == LAM_KERNEL_GQA_TC) {
     const int64_t rows = a->page_table
                              ? a->num_pages * a->num_kv_heads * static_cast<int64_t>(a->page_size)
                              : static_cast<int64_t>(a->batch) * a->num_kv_heads * a->page_size;
     if (rows >= (int64_t{1} << 31))
       return fail(LAM_ERR_VALIDATION, "pool exceeds 2^31 rows for the tensor map");
     CUtensorMap kmap, vmap;
-    rc = make_pool_map(&kmap, a->kv_dtype, a->k_pool, rows, D, pl.tile);
+    const int box_rows = pl.kernel == LAM_KERNEL_GQA_TC ? lam::kTcBoxRows : pl.tile;
+    rc = make_pool_map(&kmap, a->kv_dtype, a->k_pool, rows, D, box_rows);
     if (rc != LAM_OK) return rc;
-    rc = make_pool_map(&vmap, a->kv_dtype, a->v_pool, rows, D, pl.tile);
+    rc = make_pool_map(&vmap, a->kv_dtype, a->v_pool, rows, D, box_rows);
     if (rc != LAM_OK) return rc;
-    LAM_CUDA(lam::launch_decode_mma(a->kv_dtype, pl.variant, p, kmap, vmap, pl.ctas, s));
+    if (pl.kernel == LAM_KERNEL_GQA_TC)
+      LAM_CUDA(lam::launch_decode_tc(a->kv_dtype, p, kmap, vmap, pl.ctas, s));
+    else
+      LAM_CUDA(lam::launch_decode_mma(a->kv_dtype, pl.variant, p, kmap, vmap, pl.ctas, s));
   } else {
     LAM_CUDA(lam::launch_decode_simt(a->kv_dtype, D, pl.GQ, pl.variant, p, pl.ctas, s));
   }

@@ -1,7 +1,9 @@
 // decode.cu — instantiations and launchers of the decode kernels.
 #include <atomic>
+#include <cstdlib>
 
 #include "decode_gqa_mma.cuh"
+#include "decode_gqa_tc.cuh"
 #include "decode_simt.cuh"
 #include "lam_internal.h"
 
@@ -88,6 +90,49 @@ int mma_occ_v() {
   static std::atomic<int> cached{0};  // queried once per process (one device model)
   if (const int c = cached.load(std::memory_order_relaxed); c > 0) return c;
   auto* k = decode_gqa_mma_kernel<T, NW, STAGES>;
+  if (ensure_smem_attr(k, C::SMEM_BYTES, done) != cudaSuccess) return 0;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, C::THREADS, C::SMEM_BYTES) !=
+      cudaSuccess)
+    return 0;
+  cached.store(n, std::memory_order_relaxed);
+  return n;
+}
+
+template <typename T, int ST>
+cudaError_t tc_launch_v(const DecodeParams& p, const CUtensorMap& kmap, const CUtensorMap& vmap,
+                        int ctas, cudaStream_t stream) {
+  using C = TcCfg<ST>;
+  static std::atomic<uint64_t> done{0};
+  auto* k = decode_gqa_tc_kernel<T, ST>;
+  cudaError_t e = ensure_smem_attr(k, C::SMEM_BYTES, done);
+  if (e != cudaSuccess) return e;
+  return launch_k(k, p, ctas, C::THREADS, C::SMEM_BYTES, stream, p, kmap, vmap);
+}
+
+// LAM_TC_STAGES=2: the two-stage ring (tuning); 3 is the default
+int tc_stages() {
+  static const int st = [] {
+    const char* e = std::getenv("LAM_TC_STAGES");
+    return e && std::atoi(e) == 2 ? 2 : 3;
+  }();
+  return st;
+}
+
+template <typename T>
+cudaError_t tc_launch(const DecodeParams& p, const CUtensorMap& kmap, const CUtensorMap& vmap,
+                      int ctas, cudaStream_t stream) {
+  if (tc_stages() == 2) return tc_launch_v<T, 2>(p, kmap, vmap, ctas, stream);
+  return tc_launch_v<T, 3>(p, kmap, vmap, ctas, stream);
+}
+
+template <typename T>
+int tc_occ() {
+  using C = TcCfg<3>;
+  static std::atomic<uint64_t> done{0};
+  static std::atomic<int> cached{0};
+  if (const int c = cached.load(std::memory_order_relaxed); c > 0) return c;
+  auto* k = decode_gqa_tc_kernel<T, 3>;
   if (ensure_smem_attr(k, C::SMEM_BYTES, done) != cudaSuccess) return 0;
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, C::THREADS, C::SMEM_BYTES) !=
@@ -206,6 +251,19 @@ cudaError_t launch_decode_mma(int kv_dtype, int variant, const DecodeParams& p,
   if (kv_dtype == 2) return mma_launch<__nv_bfloat16>(variant, p, kmap, vmap, grid_x, stream);
   if (kv_dtype == 3) return mma_launch<__half>(variant, p, kmap, vmap, grid_x, stream);
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_decode_tc(int kv_dtype, const DecodeParams& p, const CUtensorMap& kmap,
+                             const CUtensorMap& vmap, int grid_x, cudaStream_t stream) {
+  if (kv_dtype == 2) return tc_launch<__nv_bfloat16>(p, kmap, vmap, grid_x, stream);
+  if (kv_dtype == 3) return tc_launch<__half>(p, kmap, vmap, grid_x, stream);
+  return cudaErrorInvalidValue;
+}
+
+int occupancy_tc(int kv_dtype) {
+  if (kv_dtype == 2) return tc_occ<__nv_bfloat16>();
+  if (kv_dtype == 3) return tc_occ<__half>();
+  return 0;
 }
 
 int occupancy_mma(int kv_dtype, int variant) {

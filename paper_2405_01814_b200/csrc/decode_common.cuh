@@ -263,8 +263,11 @@ __device__ __forceinline__ int live_splits(const DecodeParams& p, const Item& it
 // ---- persistent producer ---------------------------------------------------------------
 // meta[s] = {item, tile index, request length, item end token}; item < 0 ends the work.
 // meta_row[s] = first pool row of the stage's tile (consumers write the fused new token there).
-// `issue(s, it, j, row, mode)` must arrive on full[s] with expect_tx for all of the stage's
-// bytes and start the stage's TMA copies of tile j, whose first KV row is `row`: mode
+// A tile is NSUB chunks of TILE / NSUB tokens, each contiguous in the pool (a chunk never
+// crosses a page); the chunks' first pool rows are looked up together (independent loads).
+// `issue(s, it, j, rows, mode)` must arrive on full[s] with expect_tx for all of the stage's
+// bytes and start the stage's TMA copies of tile j, whose chunk c starts at pool row rows[c]
+// (chunks past the item end are not loaded; rows[c] = -1): mode
 // kIssueAll = every copy, kIssueKV = the K/V tile only, kIssueInputs = only the copies of
 // request inputs (q rows, fused new K/V rows) of a stage issued before with kIssueKV.
 //
@@ -279,7 +282,9 @@ __device__ __forceinline__ int live_splits(const DecodeParams& p, const Item& it
 // Measured on B200 this dynamic schedule beats a static round-robin split by 2-3 % (per-SM
 // streaming rates differ across the two dies) and beats claiming one item ahead (that costs up
 // to one item of tail imbalance); the stage ring covers the claim's round trips.
-template <int STAGES, int TILE, class Issue>
+// META = meta slots (a multiple of STAGES; tile i's tag lives in meta[i % META]): more slots than
+// stages keep a tile's tag readable after its stage has been handed back for the next load.
+template <int STAGES, int TILE, int NSUB = 1, int META = STAGES, class Issue>
 __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* full,
                                               uint64_t* empty, int4* meta, long long* meta_row,
                                               Issue issue) {
@@ -311,8 +316,9 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
         deferring = false;
       }
       if (it.split == 0 && it.len == 0) {  // empty request: zero-output marker
+        const int ms = i % META;
         const int s = acquire(i++);
-        meta[s] = make_int4(idx, 0, 0, 0);
+        meta[ms] = make_int4(idx, 0, 0, 0);
         mbar_arrive(&full[s]);
       }                                    // (an empty split has nothing to merge)
       continue;
@@ -322,25 +328,31 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
       if (deferring && i >= STAGES) {  // ring full: the inputs must land before any reuse
         inputs_ready();
         for (int jj = 0; jj < j; ++jj)
-          issue((i0 + jj) % STAGES, it, jj, meta_row[(i0 + jj) % STAGES], kIssueInputs);
+          issue((i0 + jj) % STAGES, it, jj, &meta_row[(i0 + jj) % META], kIssueInputs);
         deferring = false;
       }
+      const int ms = i % META;
       const int s = acquire(i++);
-      const int64_t row = kv_row(p, it.b, it.kvh, it.t_begin + j * TILE);
-      meta[s] = make_int4(idx, j, it.len, it.t_end);
-      meta_row[s] = row;
-      issue(s, it, j, row, deferring ? kIssueKV : kIssueAll);
+      long long rows[NSUB];
+#pragma unroll
+      for (int c = 0; c < NSUB; ++c) {
+        const int t = it.t_begin + j * TILE + c * (TILE / NSUB);
+        rows[c] = (c == 0 || t < it.t_end) ? kv_row(p, it.b, it.kvh, t) : -1;
+      }
+      meta[ms] = make_int4(idx, j, it.len, it.t_end);
+      meta_row[ms] = rows[0];
+      issue(s, it, j, static_cast<const long long*>(rows), deferring ? kIssueKV : kIssueAll);
     }
     if (deferring) {  // the whole (short) first item is in the ring
       inputs_ready();
       for (int jj = 0; jj < it.ntiles; ++jj)
-        issue((i0 + jj) % STAGES, it, jj, meta_row[(i0 + jj) % STAGES], kIssueInputs);
+        issue((i0 + jj) % STAGES, it, jj, &meta_row[(i0 + jj) % META], kIssueInputs);
       deferring = false;
     }
   }
   if (deferring) inputs_ready();  // no work: still order the launch after its inputs
   const int s = acquire(i);
-  meta[s] = make_int4(-1, 0, 0, 0);
+  meta[i % META] = make_int4(-1, 0, 0, 0);
   mbar_arrive(&full[s]);
   // out of work: the next launch of the stream (programmatic dependent launch) may take this
   // SM as soon as this CTA drains

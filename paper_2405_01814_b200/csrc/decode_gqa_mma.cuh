@@ -90,7 +90,8 @@ __global__ void __launch_bounds__((NW_ + 2) * 32, 1)
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
       producer_loop<STAGES, TILE>(p, full, empty, meta, meta_row,
-                                  [&](int s, const Item& it, int j, int64_t row, int mode) {
+                                  [&](int s, const Item& it, int j, const long long* rows, int mode) {
+        const int64_t row = rows[0];
         uint8_t* st = smem + s * C::STAGE_BYTES;
         const uint32_t qb = static_cast<uint32_t>(G) * D * 2;
         const bool fused = tile_has_new<TILE>(p, it, j);

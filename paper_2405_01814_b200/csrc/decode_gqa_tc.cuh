@@ -1,0 +1,552 @@
+// decode_gqa_tc.cuh — split-K GQA decode attention on the 5th-generation tensor cores
+// (tcgen05.mma, accumulators in tensor memory).
+//
+// The contraction is the one of decode_gqa_mma.cuh (attention.cpp:141-162 with the G q heads
+// that share a KV head stacked as the N dimension):
+//   S[128 tok x 16]  = K[128 tok x 128 d] · Q^T[128 d x 16]      (q heads padded to N = 16)
+//   O^T[128 d x 16]  = V^T[128 d x 128 tok] · P^T[128 tok x 16]  (one fresh accumulator per tile)
+// but neither operand passes through the register file: one elected thread issues
+// tcgen05.mma straight from the TMA ring (K K-major, V MN-major, both 128-byte swizzled), and
+// the results land in TMEM.  The consumer warpgroup only touches 8 fp32 logits and 8 fp32
+// output values per thread and tile:
+//
+//   warp 0-3  softmax warpgroup: thread t owns token row t of S (TMEM lane t) and output row
+//             d = t of O^T.  Per tile: tcgen05.ld its 8 logits, the tile max per q head across
+//             the warpgroup, the online-softmax update, P (bf16) into shared memory as the MMA's
+//             B operand; then tcgen05.ld the previous tile's O^T row and fold it into the
+//             register accumulator with that tile's rescale factor.
+//   warp 4    MMA issuer: stages q (and the fused new K/V row) into the MMA operand layouts,
+//             issues S(i) as soon as tile i has landed and O(i-1) once P(i-1) is written;
+//             tcgen05.commit signals S-ready, O-ready and frees the ring stage.
+//   warp 5    TMA producer (decode_common.cuh:producer_loop), 128-token tiles as two 64-row
+//             chunks (one page each at page_size 64).
+//   warp 6    epilogue (decode_common.cuh:finish_item_warp): output, LSE or split partials.
+//
+// S and O^T are double-buffered in TMEM (4 x 16 of 64 allocated columns) and P in shared memory,
+// so the tensor core computes S(i+1) and O(i) while the warpgroup runs the softmax of tile i.
+// Online softmax semantics are those of the reference's partial form (attention.cpp:72-127):
+// running max, exp-weights, the sum taken over the rounded weights fed to the MMA.
+#pragma once
+
+#include <type_traits>
+
+#include "decode_common.cuh"
+
+namespace lam {
+
+// ---- tcgen05 wrappers -----------------------------------------------------------------
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// Arrive on `bar` once every tcgen05 operation this thread issued before has completed.
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+// D[tmem] (+)= A[smem] · B[smem], kind::f16 (bf16 / fp16 in, fp32 accumulate).
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// 32 TMEM lanes x 8 consecutive 32-bit columns -> 8 registers per thread (lane = thread of the
+// warp, relative to the lane base encoded in taddr).
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  // the registers are valid only after wait::ld: both in one asm statement, so no use of them
+  // can be scheduled in between
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Shared-memory matrix descriptor (sm_100 layout): start >> 4 in [0,14), leading byte offset >> 4
+// in [16,30), stride byte offset >> 4 in [32,46), version 1 in [46,48), layout type in [61,64)
+// (0 = no swizzle, 2 = 128-byte swizzle).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo,
+                                              uint32_t layout) {
+  return static_cast<uint64_t>((addr >> 4) & 0x3FFFu) |
+         (static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16) |
+         (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) |
+         (static_cast<uint64_t>(layout) << 61);
+}
+
+// Instruction descriptor, kind::f16: fp32 accumulator, A/B bf16 (1) or fp16 (0), M, N, majors
+// (0 = K-major, 1 = MN-major).
+template <typename T>
+__host__ __device__ constexpr uint32_t tc_idesc(int M, int N, int a_mn, int b_mn) {
+  constexpr uint32_t fmt = std::is_same<T, __half>::value ? 0u : 1u;  // fp16 : bf16
+  return (1u << 4) | (fmt << 7) | (fmt << 10) | (static_cast<uint32_t>(a_mn) << 15) |
+         (static_cast<uint32_t>(b_mn) << 16) | (static_cast<uint32_t>(N >> 3) << 17) |
+         (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+template <int STAGES_>
+struct TcCfg {
+  static constexpr int STAGES = STAGES_;
+  static constexpr int TILE = 128;  // tokens per stage = MMA M of S = MMA K of O
+  static constexpr int SUB = 64;    // rows per TMA box (a page chunk)
+  static constexpr int D = 128, GQ = 8, NPAD = 16;
+  static constexpr int BOX_BYTES = TILE * 128;       // [128 rows][64 cols] 16-bit, swizzled
+  static constexpr int MAT_BYTES = 2 * BOX_BYTES;    // one K (or V) tile, 32 KB
+  static constexpr int STAGE_BYTES = 2 * MAT_BYTES;  // K + V
+  static constexpr int RING_BYTES = STAGES * STAGE_BYTES;
+  static constexpr int QBOX = NPAD * 128;            // q rows as the S MMA's B operand: 2 boxes
+  static constexpr int QBUF_BYTES = 2 * QBOX;
+  static constexpr int PBUF_BYTES = TILE * 16;       // P rows (8 bf16 per token) per parity
+  static constexpr int Q_BYTES = GQ * D * 2;         // an item's q rows as loaded (row-major)
+  static constexpr int ROW_BYTES = D * 2;
+  static constexpr int SLOT_BYTES = Q_BYTES + 2 * ROW_BYTES;  // + fused new k, v rows
+  static constexpr int RS = D + 4;                   // epilogue partial row stride (floats)
+  static constexpr int OFF_QBUF = RING_BYTES;                      // [2 item parities]
+  static constexpr int OFF_PBUF = OFF_QBUF + 2 * QBUF_BYTES;       // P0, P1, zero block
+  static constexpr int OFF_SLOT = OFF_PBUF + 3 * PBUF_BYTES;       // [STAGES]
+  static constexpr int OFF_RED = OFF_SLOT + STAGES * SLOT_BYTES;
+  // red_m[8], red_l[8], red_lw[4][8], red_acc[8][RS], tmax[2][4][8]
+  static constexpr int RED_FLOATS = GQ + GQ + 4 * GQ + GQ * RS + 2 * 4 * GQ;
+  static constexpr int OFF_META = OFF_RED + RED_FLOATS * 4;
+  static constexpr int META = 2 * STAGES;  // tags outlive the K half of their stage
+  static constexpr int OFF_BAR = OFF_META + META * 16 + META * 8;
+  // fullK, emptyK, fullV, emptyV (per stage); s, p, o, ofree (x2); red full / empty
+  static constexpr int N_BARS = 4 * STAGES + 10;
+  static constexpr int SMEM_BYTES = OFF_BAR + N_BARS * 8 + 32 + 1024;  // + align slack
+  static constexpr int THREADS = 7 * 32;
+  static constexpr int TMEM_COLS = 64;  // S[2] and O[2], 16 columns each
+};
+
+template <typename T, int STAGES_>
+__global__ void __launch_bounds__(7 * 32, 1)
+    decode_gqa_tc_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap kmap,
+                         const __grid_constant__ CUtensorMap vmap) {
+  using C = TcCfg<STAGES_>;
+  constexpr int STAGES = C::STAGES, TILE = C::TILE, SUB = C::SUB, D = C::D, GQ = C::GQ;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* qbuf = smem + C::OFF_QBUF;
+  uint8_t* pbuf = smem + C::OFF_PBUF;
+  uint8_t* qslot = smem + C::OFF_SLOT;
+  float* red_m = reinterpret_cast<float*>(smem + C::OFF_RED);
+  float* red_l = red_m + GQ;
+  float* red_lw = red_l + GQ;           // [4 warps][8]
+  float* red_acc = red_lw + 4 * GQ;     // [8][RS]
+  float* tmax = red_acc + GQ * C::RS;   // [2][4 warps][8]
+  int4* meta = reinterpret_cast<int4*>(smem + C::OFF_META);
+  long long* meta_row = reinterpret_cast<long long*>(meta + C::META);
+  // K and V halves of a stage have their own barriers: K is handed back as soon as S has read
+  // it, V only after the O MMA, so the next K loads start a softmax + O-MMA earlier
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);  // K half (+ q, new rows)
+  uint64_t* empty = full + STAGES;
+  uint64_t* fullv = empty + STAGES;
+  uint64_t* emptyv = fullv + STAGES;
+  uint64_t* sbar = emptyv + STAGES;  // S(i) in TMEM           [2]
+  uint64_t* pbar = sbar + 2;         // P(i) in smem           [2]
+  uint64_t* obar = pbar + 2;         // O(i) in TMEM           [2]
+  uint64_t* ofree = obar + 2;        // O(i) read out          [2]
+  RedPipe red{ofree + 2, ofree + 3, reinterpret_cast<int*>(ofree + 4)};
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ofree + 6);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int G = p.G;  // real q heads of the group (<= 8); the MMA's other N rows are zero
+  const bool nomath = p.flags & 16;  // diagnostic: no MMAs, no TMEM reads (pipeline only)
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);   // tcgen05.commit after the S MMA
+      mbar_init(&fullv[s], 1);
+      mbar_init(&emptyv[s], 1);  // tcgen05.commit after the O MMA
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sbar[b], 1);
+      mbar_init(&pbar[b], 4);
+      mbar_init(&obar[b], 1);
+      mbar_init(&ofree[b], 4);
+    }
+    mbar_init(red.full, 4);
+    mbar_init(red.empty, 1);
+    fence_barrier_init();
+  }
+  if (warp == 5 && lane == 0) {
+    prefetch_tensormap(&kmap);
+    prefetch_tensormap(&vmap);
+  }
+  if (warp == 4) {  // TMEM: S[2], O[2] (the allocating warp also frees it)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(C::TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  // zero the padding the MMAs read: q rows G..15 of both q buffers and the P zero block
+  for (int i = threadIdx.x; i < (2 * C::QBUF_BYTES + 3 * C::PBUF_BYTES) / 16; i += blockDim.x) {
+    const int off = i * 16;
+    if (off >= 2 * C::QBUF_BYTES) {
+      if (off >= 2 * C::QBUF_BYTES + 2 * C::PBUF_BYTES)
+        *reinterpret_cast<uint4*>(qbuf + off) = make_uint4(0u, 0u, 0u, 0u);
+    } else if ((off % C::QBOX) / 128 >= G) {
+      *reinterpret_cast<uint4*>(qbuf + off) = make_uint4(0u, 0u, 0u, 0u);
+    }
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 5) {  // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      uint32_t v_used = 0, v_par = 0;  // per stage: V half loaded before / emptyv parity to wait
+      producer_loop<STAGES, TILE, 2, C::META>(
+          p, full, empty, meta, meta_row,
+          [&](int s, const Item& it, int j, const long long* rows, int mode) {
+            uint8_t* st = smem + s * C::STAGE_BYTES;
+            const uint32_t qb = static_cast<uint32_t>(G) * D * 2;
+            const bool fused = tile_has_new<TILE>(p, it, j);
+            const bool two = mode != kIssueInputs && rows[1] >= 0;
+            if (mode != kIssueInputs)
+              mbar_arrive_expect_tx(&full[s], (two ? 2 : 1) * 2 * SUB * 128 + (j == 0 ? qb : 0) +
+                                                  (fused ? 2 * C::ROW_BYTES : 0));
+            if (mode != kIssueKV && fused) {
+              const int64_t off = static_cast<int64_t>(it.kvh) * D;
+              uint8_t* kn = qslot + s * C::SLOT_BYTES + C::Q_BYTES;
+              tma_load_1d(kn, new_rows<T>(p, 0, it.b) + off, C::ROW_BYTES, &full[s], pol);
+              tma_load_1d(kn + C::ROW_BYTES, new_rows<T>(p, 1, it.b) + off, C::ROW_BYTES,
+                          &full[s], pol);
+            }
+            if (mode != kIssueKV && j == 0)
+              tma_load_1d(qslot + s * C::SLOT_BYTES,
+                          q_rows<T>(p, it.b) + static_cast<int64_t>(it.kvh) * G * D, qb, &full[s],
+                          pol);
+            if (mode == kIssueInputs) return;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              if (c == 1 && !two) break;
+              uint8_t* kd = st + c * SUB * 128;
+              tma_load_2d(kd, &kmap, 0, static_cast<int32_t>(rows[c]), &full[s], pol);
+              tma_load_2d(kd + C::BOX_BYTES, &kmap, 64, static_cast<int32_t>(rows[c]), &full[s], pol);
+            }
+            // the V half: wait until the O MMA of the stage's previous tile has read it
+            if (v_used >> s & 1) {
+              mbar_wait(&emptyv[s], (v_par >> s) & 1);
+              v_par ^= 1u << s;
+            }
+            v_used |= 1u << s;
+            mbar_arrive_expect_tx(&fullv[s], (two ? 2 : 1) * 2 * SUB * 128);
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              if (c == 1 && !two) break;
+              uint8_t* vd = st + C::MAT_BYTES + c * SUB * 128;
+              tma_load_2d(vd, &vmap, 0, static_cast<int32_t>(rows[c]), &fullv[s], pol);
+              tma_load_2d(vd + C::BOX_BYTES, &vmap, 64, static_cast<int32_t>(rows[c]), &fullv[s], pol);
+            }
+          });
+    }
+    return;
+  }
+  if (warp == 6) {  // ---------------- epilogue ----------------
+    for (int k = 0;; ++k) {
+      mbar_wait(red.full, k & 1);
+      const int idx = red.item[0];
+      if (idx < 0) break;
+      const Item it = item_from_tag<TILE>(p, make_int4(idx, 0, red.item[1], red.item[2]));
+      if (lane < GQ)  // the four warps' partial sums of the softmax denominator
+        red_l[lane] = red_lw[lane] + red_lw[GQ + lane] + red_lw[2 * GQ + lane] + red_lw[3 * GQ + lane];
+      __syncwarp();
+      finish_item_warp<T, D, GQ, 1, true, C::RS>(p, it, G, red_m, red_l, red_acc, [&] {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(red.empty);
+      });
+    }
+    finish_cta(p);
+    return;
+  }
+
+  constexpr uint32_t IDESC_S = tc_idesc<T>(128, C::NPAD, 0, 0);  // K-major A and B
+  constexpr uint32_t IDESC_O = tc_idesc<T>(128, C::NPAD, 1, 1);  // MN-major A and B
+  // TMEM columns: S(parity b) at b * 16, O(parity b) at 32 + b * 16
+  auto s_tmem = [&](int b) { return tmem + static_cast<uint32_t>(b) * 16; };
+  auto o_tmem = [&](int b) { return tmem + 32 + static_cast<uint32_t>(b) * 16; };
+
+  if (warp == 4) {  // ---------------- MMA issuer ----------------
+    const uint32_t ring = smem_u32(smem);
+    const uint32_t qb0 = smem_u32(qbuf), pb0 = smem_u32(pbuf);
+    Item it{};
+    int k_item = -1, prev_s = 0;
+    bool prev_real = false;
+    uint32_t v_par = 0;  // per stage: parity of the fullv phase of its next loaded V half
+    for (int i = 0;; ++i) {
+      const int s = i % STAGES;
+      mbar_wait(&full[s], (i / STAGES) & 1);
+      const int4 mt = meta[i % C::META];
+      const bool sentinel = mt.x < 0;
+      const bool real = !sentinel && mt.z > 0;  // (an empty request's marker carries no data)
+      if (real) {
+        if (mt.y == 0) {  // new item: its q rows into the S MMA's B layout (K-major, 128B swizzle)
+          it = item_from_tag<TILE>(p, mt);
+          ++k_item;
+          uint8_t* qb = qbuf + (k_item & 1) * C::QBUF_BYTES;
+          const uint8_t* src = qslot + s * C::SLOT_BYTES;
+          for (int c = lane; c < G * 16; c += 32) {
+            const int r = c >> 4, ch = c & 15;
+            *reinterpret_cast<uint4*>(qb + (ch >> 3) * C::QBOX + r * 128 + (((ch & 7) ^ (r & 7)) << 4)) =
+                *reinterpret_cast<const uint4*>(src + r * C::ROW_BYTES + ch * 16);
+          }
+        }
+        if (tile_has_new<TILE>(p, it, mt.y)) {  // fused append: the new K / V row into the tile and the pools
+          mbar_wait(&fullv[s], (v_par >> s) & 1);  // the V half must have landed first
+          const int r = it.len - 1 - (it.t_begin + mt.y * TILE);
+          const int ch = lane & 15, is_v = lane >> 4;
+          const uint4 val = *reinterpret_cast<const uint4*>(qslot + s * C::SLOT_BYTES + C::Q_BYTES +
+                                                            is_v * C::ROW_BYTES + ch * 16);
+          *reinterpret_cast<uint4*>(smem + s * C::STAGE_BYTES + is_v * C::MAT_BYTES +
+                                    (ch >> 3) * C::BOX_BYTES + r * 128 + (((ch & 7) ^ (r & 7)) << 4)) = val;
+          T* pool = static_cast<T*>(is_v ? p.v_pool_w : p.k_pool_w);
+          *reinterpret_cast<uint4*>(pool + kv_row(p, it.b, it.kvh, it.len - 1) * D + ch * 8) = val;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {  // S(i) = K(i) · Q^T
+          tc_fence_after();
+          const uint32_t kb = ring + s * C::STAGE_BYTES;
+          const uint32_t qb = qb0 + (k_item & 1) * C::QBUF_BYTES;
+          if (!nomath) {
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint32_t off = (kk >> 2) * C::BOX_BYTES + (kk & 3) * 32;
+              const uint32_t qoff = (kk >> 2) * C::QBOX + (kk & 3) * 32;
+              tc_mma(s_tmem(i & 1), smem_desc(kb + off, 16, 1024, 2),
+                     smem_desc(qb + qoff, 16, 1024, 2), IDESC_S, kk > 0);
+            }
+          }
+          tc_commit(&sbar[i & 1]);
+          if (!(p.flags & 64)) tc_commit(&empty[s]);  // the K half is free once S has read it
+        }
+      } else if (lane == 0) {
+        mbar_arrive(&sbar[i & 1]);  // marker / end of work: the warpgroup reads the tag
+        if (!sentinel) mbar_arrive(&empty[s]);
+      }
+      __syncwarp();
+      if (i >= 1) {  // O(i-1) = V(i-1)^T · P(i-1)^T
+        const int j = i - 1;
+        mbar_wait(&pbar[j & 1], (j >> 1) & 1);
+        if (j >= 2) mbar_wait(&ofree[j & 1], ((j - 2) >> 1) & 1);
+        if (prev_real) {
+          mbar_wait(&fullv[prev_s], (v_par >> prev_s) & 1);
+          v_par ^= 1u << prev_s;
+        }
+        if (lane == 0) {
+          tc_fence_after();
+          if (prev_real) {
+            const uint32_t vb = ring + prev_s * C::STAGE_BYTES + C::MAT_BYTES;
+            const uint32_t pb = pb0 + (j & 1) * C::PBUF_BYTES;
+            // the zero block (q heads 8..15 of P^T) sits right after P1
+            const uint32_t sbo = pb0 + 2 * C::PBUF_BYTES - pb;
+            if (!nomath) {
+#pragma unroll
+              for (int kk = 0; kk < TILE / 16; ++kk)
+                tc_mma(o_tmem(j & 1), smem_desc(vb + kk * 16 * 128, C::BOX_BYTES, 1024, 2),
+                       smem_desc(pb + kk * 256, 128, sbo, 0), IDESC_O, kk > 0);
+            }
+            tc_commit(&obar[j & 1]);
+            tc_commit(&emptyv[prev_s]);
+            if (p.flags & 64) tc_commit(&empty[prev_s]);  // diagnostic: K held until the O MMA
+          } else {
+            mbar_arrive(&obar[j & 1]);
+          }
+        }
+        __syncwarp();
+      }
+      if (sentinel) break;
+      prev_s = s;
+      prev_real = real;
+    }
+    named_bar_sync(3, 5 * 32);  // the warpgroup has read every result
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                   "n"(C::TMEM_COLS)
+                   : "memory");
+    return;
+  }
+
+  // ---------------- softmax warpgroup (warps 0-3) ----------------
+  const int t = warp * 32 + lane;  // token row of S / dim row of O^T = TMEM lane
+  const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+  const float sl2 = p.scale_log2;
+  float m[GQ], l[GQ], o[GQ], a_prev[GQ];  // running max (log2 units), sum, output row
+  float m_st[GQ], l_st[GQ];               // the finished item's statistics until its O lands
+  int4 tag{}, tag_st{};                   // {item, len, t_end} of the current / finished item
+  Item it{};
+  bool prev_real = false, prev_first = false, prev_last = false;
+  int k_item = 0, bpar = 0;
+  uint32_t v_par = 0;  // per stage: fullv parity of its next loaded V half
+#pragma unroll
+  for (int g = 0; g < GQ; ++g) { m[g] = -INFINITY; l[g] = 0.f; o[g] = 0.f; a_prev[g] = 0.f; }
+  for (int i = 0;; ++i) {
+    const int s = i % STAGES;
+    mbar_wait(&sbar[i & 1], (i >> 1) & 1);
+    tc_fence_after();
+    const int4 mt = meta[i % C::META];
+    const bool sentinel = mt.x < 0;
+    bool real = false, first = false, last = false;
+    float a_cur[GQ];
+#pragma unroll
+    for (int g = 0; g < GQ; ++g) a_cur[g] = 0.f;
+    if (sentinel || mt.y == 0) {  // an item ends: keep its statistics until its last O lands
+#pragma unroll
+      for (int g = 0; g < GQ; ++g) { m_st[g] = m[g]; l_st[g] = l[g]; m[g] = -INFINITY; l[g] = 0.f; }
+      tag_st = tag;
+    }
+    if (!sentinel) {
+      first = mt.y == 0;
+      if (first) {
+        it = item_from_tag<TILE>(p, mt);
+        tag = make_int4(mt.x, mt.z, mt.w, 0);
+      }
+      real = mt.z > 0;
+      last = mt.y == max(it.ntiles, 1) - 1;
+      if (real) {
+        float x[GQ];
+        tmem_ld8(s_tmem(i & 1) + lane_base, x);
+        const int tok = it.t_begin + mt.y * TILE + t;
+        const bool valid = tok < it.t_end;
+#pragma unroll
+        for (int g = 0; g < GQ; ++g) x[g] = valid ? x[g] * sl2 : -INFINITY;
+        // warp max of the 8 columns in 9 shuffles: halve the columns per step, then reduce;
+        // lanes 4g .. 4g+3 end up with column g's max
+        float h4[4], h2[2], h1;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const bool up = lane & 16;
+          const float send = up ? x[j] : x[j + 4];
+          h4[j] = fmaxf(up ? x[j + 4] : x[j], __shfl_xor_sync(0xffffffffu, send, 16));
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const bool up = lane & 8;
+          const float send = up ? h4[j] : h4[j + 2];
+          h2[j] = fmaxf(up ? h4[j + 2] : h4[j], __shfl_xor_sync(0xffffffffu, send, 8));
+        }
+        {
+          const bool up = lane & 4;
+          const float send = up ? h2[0] : h2[1];
+          h1 = fmaxf(up ? h2[1] : h2[0], __shfl_xor_sync(0xffffffffu, send, 4));
+        }
+        h1 = fmaxf(h1, __shfl_xor_sync(0xffffffffu, h1, 2));
+        h1 = fmaxf(h1, __shfl_xor_sync(0xffffffffu, h1, 1));
+        float* tm = tmax + bpar * 4 * GQ;
+        if ((lane & 3) == 0) tm[warp * GQ + (lane >> 2)] = h1;
+        named_bar_sync(1, 128);
+        bpar ^= 1;
+        uint32_t pw[GQ / 2];
+#pragma unroll
+        for (int g = 0; g < GQ; ++g) {
+          const float mx = fmaxf(fmaxf(tm[g], tm[GQ + g]), fmaxf(tm[2 * GQ + g], tm[3 * GQ + g]));
+          const float mn = fmaxf(m[g], mx);  // finite: the tile has a valid token
+          a_cur[g] = m[g] == -INFINITY ? 0.f : exp2f(m[g] - mn);
+          m[g] = mn;
+        }
+#pragma unroll
+        for (int g = 0; g < GQ; g += 2) {
+          pw[g / 2] = Elem<T>::pack2(exp2f(x[g] - m[g]), exp2f(x[g + 1] - m[g + 1]));
+          float r0, r1;  // the sum uses the rounded weights the MMA sees
+          Elem<T>::unpack2(pw[g / 2], r0, r1);
+          l[g] = l[g] * a_cur[g] + r0;
+          l[g + 1] = l[g + 1] * a_cur[g + 1] + r1;
+        }
+        *reinterpret_cast<uint4*>(pbuf + (i & 1) * C::PBUF_BYTES + t * 16) =
+            make_uint4(pw[0], pw[1], pw[2], pw[3]);
+        // stale rows past the end may hold non-finite values and p = 0 must meet 0: zero them,
+        // once the tile's V half has landed (it is loaded after the previous O MMA read the
+        // slot, so S — and this softmax — can run ahead of it)
+        if (it.t_begin + mt.y * TILE + TILE > it.t_end) mbar_wait(&fullv[s], (v_par >> s) & 1);
+        if (!valid) {
+          uint8_t* vrow = smem + s * C::STAGE_BYTES + C::MAT_BYTES + t * 128;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            *reinterpret_cast<uint4*>(vrow + c * 16) = make_uint4(0u, 0u, 0u, 0u);
+            *reinterpret_cast<uint4*>(vrow + C::BOX_BYTES + c * 16) = make_uint4(0u, 0u, 0u, 0u);
+          }
+        }
+        fence_proxy_async_smem();
+      }
+      if (real) v_par ^= 1u << s;
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pbar[i & 1]);
+    }
+    if (i >= 1) {  // fold O(i-1) into the output rows
+      const int j = i - 1;
+      mbar_wait(&obar[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      if (prev_real) {
+        float ot[GQ];
+        tmem_ld8(o_tmem(j & 1) + lane_base, ot);
+#pragma unroll
+        for (int g = 0; g < GQ; ++g) o[g] = prev_first ? ot[g] : fmaf(o[g], a_prev[g], ot[g]);
+      } else {
+#pragma unroll
+        for (int g = 0; g < GQ; ++g) o[g] = 0.f;  // an empty request's zero output
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ofree[j & 1]);
+      if (prev_last) {  // hand the finished item to the epilogue warp
+        float ls[GQ];
+#pragma unroll
+        for (int g = 0; g < GQ; ++g) {
+          float v = l_st[g];
+#pragma unroll
+          for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+          ls[g] = v;
+        }
+        red_acquire(red, k_item);
+        if (lane == 0) {
+          float4* lw = reinterpret_cast<float4*>(red_lw + warp * GQ);
+          lw[0] = make_float4(ls[0], ls[1], ls[2], ls[3]);
+          lw[1] = make_float4(ls[4], ls[5], ls[6], ls[7]);
+          if (warp == 0) {
+            float4* rm = reinterpret_cast<float4*>(red_m);
+            rm[0] = make_float4(m_st[0], m_st[1], m_st[2], m_st[3]);
+            rm[1] = make_float4(m_st[4], m_st[5], m_st[6], m_st[7]);
+          }
+        }
+#pragma unroll
+        for (int g = 0; g < GQ; ++g) red_acc[g * C::RS + t] = o[g];
+        if (warp == 0 && lane == 0) {
+          red.item[0] = tag_st.x;
+          red.item[1] = tag_st.y;
+          red.item[2] = tag_st.z;
+        }
+        red_commit(red);
+        ++k_item;
+      }
+    }
+    if (sentinel) break;
+#pragma unroll
+    for (int g = 0; g < GQ; ++g) a_prev[g] = real ? a_cur[g] : 0.f;
+    prev_real = real;
+    prev_first = first;
+    prev_last = last;
+  }
+  red_acquire(red, k_item);
+  if (warp == 0 && lane == 0) red.item[0] = -1;
+  red_commit(red);
+  named_bar_sync(3, 5 * 32);
+}
+
+}  // namespace lam

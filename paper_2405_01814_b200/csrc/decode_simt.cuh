@@ -83,7 +83,8 @@ __global__ void __launch_bounds__((NW + 2) * 32, 1)
       const T* kp = static_cast<const T*>(p.k_pool);
       const T* vp = static_cast<const T*>(p.v_pool);
       producer_loop<STAGES, TILE>(p, full, empty, meta, meta_row,
-                                  [&](int s, const Item& it, int j, int64_t row, int mode) {
+                                  [&](int s, const Item& it, int j, const long long* row0, int mode) {
+        const int64_t row = row0[0];
         const int tok = it.t_begin + j * TILE;
         const int rows = min(TILE, it.t_end - tok);
         const uint32_t bytes = static_cast<uint32_t>(rows) * D * sizeof(T);

@@ -18,6 +18,11 @@ cudaError_t launch_decode_mma(int kv_dtype, int variant, const DecodeParams& p,
                               const CUtensorMap& kmap, const CUtensorMap& vmap, int grid_x,
                               cudaStream_t stream);
 int mma_variant_tile(int variant);  // tokens per stage of a GQA kernel variant (0 = invalid)
+// tcgen05 / TMEM GQA kernel: 128-token stages fed as 64-row TMA boxes
+cudaError_t launch_decode_tc(int kv_dtype, const DecodeParams& p, const CUtensorMap& kmap,
+                             const CUtensorMap& vmap, int grid_x, cudaStream_t stream);
+int occupancy_tc(int kv_dtype);
+constexpr int kTcTile = 128, kTcBoxRows = 64;
 // resident CTAs per SM for an instantiation (0 if unsupported)
 int occupancy_simt(int kv_dtype, int D, int GQ, int variant);
 int occupancy_mma(int kv_dtype, int variant);

@@ -20,7 +20,7 @@ from ._lib import DecodeArgs, check
 
 _DT = {torch.float32: _lib.LAM_F32, torch.bfloat16: _lib.LAM_BF16, torch.float16: _lib.LAM_F16}
 _KERNELS = {"auto": _lib.LAM_KERNEL_AUTO, "simt": _lib.LAM_KERNEL_SIMT,
-            "gqa_mma": _lib.LAM_KERNEL_GQA_MMA}
+            "gqa_mma": _lib.LAM_KERNEL_GQA_MMA, "gqa_tc": _lib.LAM_KERNEL_GQA_TC}
 
 
 def _stream_ptr(stream) -> int:
@@ -150,7 +150,8 @@ def plan(q, k_pool, v_pool, seq_lens, **kw):
 
     k, s, t = C.c_int32(), C.c_int32(), C.c_int32()
     check(_lib.load().lam_decode_plan(ctx.handle, a, C.byref(k), C.byref(s), C.byref(t)))
-    names = {_lib.LAM_KERNEL_SIMT: "simt", _lib.LAM_KERNEL_GQA_MMA: "gqa_mma"}
+    names = {_lib.LAM_KERNEL_SIMT: "simt", _lib.LAM_KERNEL_GQA_MMA: "gqa_mma",
+             _lib.LAM_KERNEL_GQA_TC: "gqa_tc"}
     return names[k.value], s.value, t.value
 
 
