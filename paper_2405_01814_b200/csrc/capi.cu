@@ -261,7 +261,7 @@ int plan_decode(lam_ctx* ctx, const lam_decode_args* a, Plan* pl) {
   const bool mma_ok = (kvd == LAM_BF16 || kvd == LAM_F16) && a->head_dim == 128 && G >= 1 &&
                       G <= 8 && mtile > 0 && (!paged || a->page_size % mtile == 0);
   const bool tc_ok = (kvd == LAM_BF16 || kvd == LAM_F16) && a->head_dim == 128 && G >= 1 &&
-                     G <= 8 && a->page_size % lam::kTcBoxRows == 0;
+                     G <= 8 && (!paged || a->page_size % lam::kTcBoxRows == 0);
   int kernel = a->kernel;
   // 16-bit KV with D = 128 runs on the tensor-core kernel for every group size, MHA (G = 1)
   // included: both kernels stream at the same rate when timed alone (7226 GB/s, C2), but under
@@ -271,15 +271,19 @@ int plan_decode(lam_ctx* ctx, const lam_decode_args* a, Plan* pl) {
   if (kernel == LAM_KERNEL_AUTO) {
     kernel = mma_ok && (G >= 2 || env_int("LAM_MHA_MMA", 1) != 0) ? LAM_KERNEL_GQA_MMA
                                                                   : LAM_KERNEL_SIMT;
-    // LAM_GQA_TC=1: the tcgen05 / TMEM kernel wherever it applies (A/B against mma.sync)
-    if (tc_ok && kernel == LAM_KERNEL_GQA_MMA && env_int("LAM_GQA_TC", 0) != 0)
+    // The tcgen05 / TMEM kernel for MHA (G = 1): same box, sustained 32-layer C2 step 7144 vs
+    // 7062 GB/s (e2e 7023 vs 6883) — its SMs draw less power, so the clocks hold higher under
+    // sw_power_cap (1901-1923 vs 1863 MHz).  For GQA the mma.sync kernel stays (C3 step 6888 vs
+    // 6811 GB/s, experiments/r02/call12.sh).  LAM_GQA_TC=1 / 0 forces either for every group.
+    const int tc_env = env_int("LAM_GQA_TC", -1);
+    if (tc_ok && kernel == LAM_KERNEL_GQA_MMA && (tc_env == 1 || (tc_env < 0 && G == 1)))
       kernel = LAM_KERNEL_GQA_TC;
   }
   if (kernel == LAM_KERNEL_GQA_TC) {
     if (!tc_ok)
       return fail(LAM_ERR_VALIDATION,
-                  "tcgen05 GQA kernel needs 16-bit KV, head_dim 128, 1 <= G <= 8 and page_size a "
-                  "multiple of 64");
+                  "tcgen05 GQA kernel needs 16-bit KV, head_dim 128, 1 <= G <= 8 and (paged) "
+                  "page_size a multiple of 64");
     pl->kernel = kernel;
     pl->variant = 0;
     pl->GQ = 8;

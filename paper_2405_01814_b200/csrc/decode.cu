@@ -99,40 +99,42 @@ int mma_occ_v() {
   return n;
 }
 
-template <typename T, int ST>
+template <typename T, int KS, int VS>
 cudaError_t tc_launch_v(const DecodeParams& p, const CUtensorMap& kmap, const CUtensorMap& vmap,
                         int ctas, cudaStream_t stream) {
-  using C = TcCfg<ST>;
+  using C = TcCfg<KS, VS>;
   static std::atomic<uint64_t> done{0};
-  auto* k = decode_gqa_tc_kernel<T, ST>;
+  auto* k = decode_gqa_tc_kernel<T, KS, VS>;
   cudaError_t e = ensure_smem_attr(k, C::SMEM_BYTES, done);
   if (e != cudaSuccess) return e;
   return launch_k(k, p, ctas, C::THREADS, C::SMEM_BYTES, stream, p, kmap, vmap);
 }
 
-// LAM_TC_STAGES=2: the two-stage ring (tuning); 3 is the default
-int tc_stages() {
-  static const int st = [] {
-    const char* e = std::getenv("LAM_TC_STAGES");
-    return e && std::atoi(e) == 2 ? 2 : 3;
+// K / V ring slots of the tcgen05 kernel: LAM_TC_RING=33 (3 K + 3 V, default), 24, 42
+int tc_ring() {
+  static const int r = [] {
+    const char* e = std::getenv("LAM_TC_RING");
+    const int v = e ? std::atoi(e) : 33;
+    return v == 24 || v == 42 ? v : 33;
   }();
-  return st;
+  return r;
 }
 
 template <typename T>
 cudaError_t tc_launch(const DecodeParams& p, const CUtensorMap& kmap, const CUtensorMap& vmap,
                       int ctas, cudaStream_t stream) {
-  if (tc_stages() == 2) return tc_launch_v<T, 2>(p, kmap, vmap, ctas, stream);
-  return tc_launch_v<T, 3>(p, kmap, vmap, ctas, stream);
+  if (tc_ring() == 24) return tc_launch_v<T, 2, 4>(p, kmap, vmap, ctas, stream);
+  if (tc_ring() == 42) return tc_launch_v<T, 4, 2>(p, kmap, vmap, ctas, stream);
+  return tc_launch_v<T, 3, 3>(p, kmap, vmap, ctas, stream);
 }
 
-template <typename T>
-int tc_occ() {
-  using C = TcCfg<3>;
+template <typename T, int KS, int VS>
+int tc_occ_v() {
+  using C = TcCfg<KS, VS>;
   static std::atomic<uint64_t> done{0};
   static std::atomic<int> cached{0};
   if (const int c = cached.load(std::memory_order_relaxed); c > 0) return c;
-  auto* k = decode_gqa_tc_kernel<T, 3>;
+  auto* k = decode_gqa_tc_kernel<T, KS, VS>;
   if (ensure_smem_attr(k, C::SMEM_BYTES, done) != cudaSuccess) return 0;
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, C::THREADS, C::SMEM_BYTES) !=
@@ -140,6 +142,12 @@ int tc_occ() {
     return 0;
   cached.store(n, std::memory_order_relaxed);
   return n;
+}
+
+template <typename T>
+int tc_occ() {
+  return tc_ring() == 24 ? tc_occ_v<T, 2, 4>() : tc_ring() == 42 ? tc_occ_v<T, 4, 2>()
+                                                                   : tc_occ_v<T, 3, 3>();
 }
 
 // GQA kernel variants (consumer warps, stages): tile = 16 tokens per consumer warp.

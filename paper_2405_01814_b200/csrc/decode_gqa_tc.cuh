@@ -2,30 +2,32 @@
 // (tcgen05.mma, accumulators in tensor memory).
 //
 // The contraction is the one of decode_gqa_mma.cuh (attention.cpp:141-162 with the G q heads
-// that share a KV head stacked as the N dimension):
-//   S[128 tok x 16]  = K[128 tok x 128 d] · Q^T[128 d x 16]      (q heads padded to N = 16)
-//   O^T[128 d x 16]  = V^T[128 d x 128 tok] · P^T[128 tok x 16]  (one fresh accumulator per tile)
-// but neither operand passes through the register file: one elected thread issues
-// tcgen05.mma straight from the TMA ring (K K-major, V MN-major, both 128-byte swizzled), and
-// the results land in TMEM.  The consumer warpgroup only touches 8 fp32 logits and 8 fp32
-// output values per thread and tile:
+// that share a KV head as the N dimension, padded to N = 8):
+//   S[128 tok x 8]   = K[128 tok x 128 d] · Q^T[128 d x 8]
+//   O^T[128 d x 8]   = V^T[128 d x 128 tok] · P^T[128 tok x 8]  (one fresh accumulator per tile)
+// but neither operand passes through the register file: single threads issue tcgen05.mma
+// straight from the TMA rings (K K-major, V MN-major, both 128-byte swizzled) and the results
+// land in TMEM.  The softmax warpgroup only touches 8 fp32 logits and 8 fp32 output values per
+// thread and tile:
 //
 //   warp 0-3  softmax warpgroup: thread t owns token row t of S (TMEM lane t) and output row
-//             d = t of O^T.  Per tile: tcgen05.ld its 8 logits, the tile max per q head across
-//             the warpgroup, the online-softmax update, P (bf16) into shared memory as the MMA's
-//             B operand; then tcgen05.ld the previous tile's O^T row and fold it into the
-//             register accumulator with that tile's rescale factor.
-//   warp 4    MMA issuer: stages q (and the fused new K/V row) into the MMA operand layouts,
-//             issues S(i) as soon as tile i has landed and O(i-1) once P(i-1) is written;
-//             tcgen05.commit signals S-ready, O-ready and frees the ring stage.
-//   warp 5    TMA producer (decode_common.cuh:producer_loop), 128-token tiles as two 64-row
-//             chunks (one page each at page_size 64).
+//             d = t of O^T.  Per tile: tcgen05.ld its 8 logits (and hand the S buffer back), the
+//             tile max per q head across the warpgroup, the online-softmax update, P (bf16) into
+//             shared memory as the O MMA's B operand; then tcgen05.ld the previous tile's O^T row
+//             and fold it into the register accumulator with that tile's rescale factor.
+//   warp 4    S issuer: stages q (and the fused new K/V row) into the operand layouts and issues
+//             S(i) as soon as K(i) has landed and an S buffer is free; the commit hands the K
+//             slot back to the producer.
+//   warp 7    O issuer: O(j) as soon as P(j) is written; the commit hands the V slot back.
+//             (Two issuers, so neither stream of MMAs ever waits behind the other's inputs.)
+//   warp 5    TMA producer (decode_common.cuh:producer_loop): 128-token tiles as two 64-row
+//             chunks (a page each at page_size 64), K and V into separate rings.
 //   warp 6    epilogue (decode_common.cuh:finish_item_warp): output, LSE or split partials.
 //
-// S and O^T are double-buffered in TMEM (4 x 16 of 64 allocated columns) and P in shared memory,
-// so the tensor core computes S(i+1) and O(i) while the warpgroup runs the softmax of tile i.
-// Online softmax semantics are those of the reference's partial form (attention.cpp:72-127):
-// running max, exp-weights, the sum taken over the rounded weights fed to the MMA.
+// S is four-buffered and O^T double-buffered in TMEM (48 of 64 allocated columns), P
+// double-buffered in shared memory.  Online softmax semantics are those of the reference's
+// partial form (attention.cpp:72-127): running max, exp-weights, the sum taken over the rounded
+// weights fed to the MMA.
 #pragma once
 
 #include <type_traits>
@@ -95,16 +97,17 @@ __host__ __device__ constexpr uint32_t tc_idesc(int M, int N, int a_mn, int b_mn
          (static_cast<uint32_t>(M >> 4) << 24);
 }
 
-template <int STAGES_>
+template <int KS_, int VS_>
 struct TcCfg {
-  static constexpr int STAGES = STAGES_;
-  static constexpr int TILE = 128;  // tokens per stage = MMA M of S = MMA K of O
+  static constexpr int KS = KS_;  // K slots (128 tokens each), handed back after the S MMA
+  static constexpr int VS = VS_;  // V slots, handed back after the O MMA (later)
+  static constexpr int NS = 4;    // S buffers in TMEM (and q buffers in shared memory)
+  static constexpr int TILE = 128;  // tokens per tile = MMA M of S = MMA K of O
   static constexpr int SUB = 64;    // rows per TMA box (a page chunk)
-  static constexpr int D = 128, GQ = 8, NPAD = 16;
+  static constexpr int D = 128, GQ = 8, NPAD = 8;
   static constexpr int BOX_BYTES = TILE * 128;       // [128 rows][64 cols] 16-bit, swizzled
   static constexpr int MAT_BYTES = 2 * BOX_BYTES;    // one K (or V) tile, 32 KB
-  static constexpr int STAGE_BYTES = 2 * MAT_BYTES;  // K + V
-  static constexpr int RING_BYTES = STAGES * STAGE_BYTES;
+  static constexpr int OFF_V = KS * MAT_BYTES;
   static constexpr int QBOX = NPAD * 128;            // q rows as the S MMA's B operand: 2 boxes
   static constexpr int QBUF_BYTES = 2 * QBOX;
   static constexpr int PBUF_BYTES = TILE * 16;       // P rows (8 bf16 per token) per parity
@@ -112,31 +115,33 @@ struct TcCfg {
   static constexpr int ROW_BYTES = D * 2;
   static constexpr int SLOT_BYTES = Q_BYTES + 2 * ROW_BYTES;  // + fused new k, v rows
   static constexpr int RS = D + 4;                   // epilogue partial row stride (floats)
-  static constexpr int OFF_QBUF = RING_BYTES;                      // [2 item parities]
-  static constexpr int OFF_PBUF = OFF_QBUF + 2 * QBUF_BYTES;       // P0, P1, zero block
-  static constexpr int OFF_SLOT = OFF_PBUF + 3 * PBUF_BYTES;       // [STAGES]
-  static constexpr int OFF_RED = OFF_SLOT + STAGES * SLOT_BYTES;
+  static constexpr int OFF_QBUF = OFF_V + VS * MAT_BYTES;          // [NS]
+  static constexpr int OFF_PBUF = OFF_QBUF + NS * QBUF_BYTES;      // [2]
+  static constexpr int OFF_SLOT = OFF_PBUF + 2 * PBUF_BYTES;       // [KS]
+  static constexpr int OFF_RED = OFF_SLOT + KS * SLOT_BYTES;
   // red_m[8], red_l[8], red_lw[4][8], red_acc[8][RS], tmax[2][4][8]
   static constexpr int RED_FLOATS = GQ + GQ + 4 * GQ + GQ * RS + 2 * 4 * GQ;
   static constexpr int OFF_META = OFF_RED + RED_FLOATS * 4;
-  static constexpr int META = 2 * STAGES;  // tags outlive the K half of their stage
+  static constexpr int META = 16;  // tile tags outlive their K slot (read until the O MMA)
   static constexpr int OFF_BAR = OFF_META + META * 16 + META * 8;
-  // fullK, emptyK, fullV, emptyV (per stage); s, p, o, ofree (x2); red full / empty
-  static constexpr int N_BARS = 4 * STAGES + 10;
+  // fullK, emptyK [KS]; fullV, emptyV [VS]; s, sfree [NS]; p, o, ofree [2]; red full / empty
+  static constexpr int N_BARS = 2 * KS + 2 * VS + 2 * NS + 8;
   static constexpr int SMEM_BYTES = OFF_BAR + N_BARS * 8 + 32 + 1024;  // + align slack
-  static constexpr int THREADS = 7 * 32;
-  static constexpr int TMEM_COLS = 64;  // S[2] and O[2], 16 columns each
+  static constexpr int THREADS = 8 * 32;
+  static constexpr int TMEM_COLS = 64;  // S[4] and O[2], 8 columns each
 };
 
-template <typename T, int STAGES_>
-__global__ void __launch_bounds__(7 * 32, 1)
+template <typename T, int KS_, int VS_>
+__global__ void __launch_bounds__(8 * 32, 1)
     decode_gqa_tc_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap kmap,
                          const __grid_constant__ CUtensorMap vmap) {
-  using C = TcCfg<STAGES_>;
-  constexpr int STAGES = C::STAGES, TILE = C::TILE, SUB = C::SUB, D = C::D, GQ = C::GQ;
+  using C = TcCfg<KS_, VS_>;
+  constexpr int KS = C::KS, VS = C::VS, NS = C::NS, TILE = C::TILE, SUB = C::SUB, D = C::D,
+                GQ = C::GQ;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
+  uint8_t* vring = smem + C::OFF_V;
   uint8_t* qbuf = smem + C::OFF_QBUF;
   uint8_t* pbuf = smem + C::OFF_PBUF;
   uint8_t* qslot = smem + C::OFF_SLOT;
@@ -147,14 +152,16 @@ __global__ void __launch_bounds__(7 * 32, 1)
   float* tmax = red_acc + GQ * C::RS;   // [2][4 warps][8]
   int4* meta = reinterpret_cast<int4*>(smem + C::OFF_META);
   long long* meta_row = reinterpret_cast<long long*>(meta + C::META);
-  // K and V halves of a stage have their own barriers: K is handed back as soon as S has read
-  // it, V only after the O MMA, so the next K loads start a softmax + O-MMA earlier
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);  // K half (+ q, new rows)
-  uint64_t* empty = full + STAGES;
-  uint64_t* fullv = empty + STAGES;
-  uint64_t* emptyv = fullv + STAGES;
-  uint64_t* sbar = emptyv + STAGES;  // S(i) in TMEM           [2]
-  uint64_t* pbar = sbar + 2;         // P(i) in smem           [2]
+  // The K and V halves of a tile live in separate rings: K is handed back as soon as S has read
+  // it, V only after the O MMA.  The K ring follows the tile counter i; the V ring follows the
+  // count of data-carrying tiles (an empty request's marker takes a K slot but loads nothing).
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);  // K (+ q, new rows) [KS]
+  uint64_t* empty = full + KS;
+  uint64_t* fullv = empty + KS;      // [VS]
+  uint64_t* emptyv = fullv + VS;
+  uint64_t* sbar = emptyv + VS;      // S(i) in TMEM           [NS]
+  uint64_t* sfree = sbar + NS;       // S(i) read out          [NS]
+  uint64_t* pbar = sfree + NS;       // P(i) in smem           [2]
   uint64_t* obar = pbar + 2;         // O(i) in TMEM           [2]
   uint64_t* ofree = obar + 2;        // O(i) read out          [2]
   RedPipe red{ofree + 2, ofree + 3, reinterpret_cast<int*>(ofree + 4)};
@@ -162,17 +169,22 @@ __global__ void __launch_bounds__(7 * 32, 1)
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int G = p.G;  // real q heads of the group (<= 8); the MMA's other N rows are zero
-  const bool nomath = p.flags & 16;  // diagnostic: no MMAs, no TMEM reads (pipeline only)
+  const bool nomath = p.flags & 16;  // diagnostic: no MMAs (the pipeline alone)
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < KS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);   // tcgen05.commit after the S MMA
+    }
+    for (int s = 0; s < VS; ++s) {
       mbar_init(&fullv[s], 1);
       mbar_init(&emptyv[s], 1);  // tcgen05.commit after the O MMA
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NS; ++b) {
       mbar_init(&sbar[b], 1);
+      mbar_init(&sfree[b], 4);
+    }
+    for (int b = 0; b < 2; ++b) {
       mbar_init(&pbar[b], 4);
       mbar_init(&obar[b], 1);
       mbar_init(&ofree[b], 4);
@@ -185,23 +197,17 @@ __global__ void __launch_bounds__(7 * 32, 1)
     prefetch_tensormap(&kmap);
     prefetch_tensormap(&vmap);
   }
-  if (warp == 4) {  // TMEM: S[2], O[2] (the allocating warp also frees it)
+  if (warp == 4) {  // TMEM: S[4], O[2] (the allocating warp also frees it)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
                  "n"(C::TMEM_COLS)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  // zero the padding the MMAs read: q rows G..15 of both q buffers and the P zero block
-  for (int i = threadIdx.x; i < (2 * C::QBUF_BYTES + 3 * C::PBUF_BYTES) / 16; i += blockDim.x) {
-    const int off = i * 16;
-    if (off >= 2 * C::QBUF_BYTES) {
-      if (off >= 2 * C::QBUF_BYTES + 2 * C::PBUF_BYTES)
-        *reinterpret_cast<uint4*>(qbuf + off) = make_uint4(0u, 0u, 0u, 0u);
-    } else if ((off % C::QBOX) / 128 >= G) {
-      *reinterpret_cast<uint4*>(qbuf + off) = make_uint4(0u, 0u, 0u, 0u);
-    }
-  }
+  // zero the q rows G..7 of every q buffer (the MMA's padding rows)
+  for (int i = threadIdx.x; i < NS * C::QBUF_BYTES / 16; i += blockDim.x)
+    if ((i * 16 % C::QBOX) / 128 >= G)
+      *reinterpret_cast<uint4*>(qbuf + i * 16) = make_uint4(0u, 0u, 0u, 0u);
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
@@ -211,11 +217,11 @@ __global__ void __launch_bounds__(7 * 32, 1)
   if (warp == 5) {  // ---------------- TMA producer ----------------
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      uint32_t v_used = 0, v_par = 0;  // per stage: V half loaded before / emptyv parity to wait
-      producer_loop<STAGES, TILE, 2, C::META>(
+      int nv = 0;  // V tiles issued (data-carrying tiles so far)
+      producer_loop<KS, TILE, 2, C::META>(
           p, full, empty, meta, meta_row,
           [&](int s, const Item& it, int j, const long long* rows, int mode) {
-            uint8_t* st = smem + s * C::STAGE_BYTES;
+            uint8_t* kt = smem + s * C::MAT_BYTES;
             const uint32_t qb = static_cast<uint32_t>(G) * D * 2;
             const bool fused = tile_has_new<TILE>(p, it, j);
             const bool two = mode != kIssueInputs && rows[1] >= 0;
@@ -237,23 +243,21 @@ __global__ void __launch_bounds__(7 * 32, 1)
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
               if (c == 1 && !two) break;
-              uint8_t* kd = st + c * SUB * 128;
+              uint8_t* kd = kt + c * SUB * 128;
               tma_load_2d(kd, &kmap, 0, static_cast<int32_t>(rows[c]), &full[s], pol);
               tma_load_2d(kd + C::BOX_BYTES, &kmap, 64, static_cast<int32_t>(rows[c]), &full[s], pol);
             }
-            // the V half: wait until the O MMA of the stage's previous tile has read it
-            if (v_used >> s & 1) {
-              mbar_wait(&emptyv[s], (v_par >> s) & 1);
-              v_par ^= 1u << s;
-            }
-            v_used |= 1u << s;
-            mbar_arrive_expect_tx(&fullv[s], (two ? 2 : 1) * 2 * SUB * 128);
+            // V: its slot is free once the O MMA of the tile VS data tiles back has read it
+            const int v = nv++, vs = v % VS;
+            if (v >= VS) mbar_wait(&emptyv[vs], ((v / VS) - 1) & 1);
+            mbar_arrive_expect_tx(&fullv[vs], (two ? 2 : 1) * 2 * SUB * 128);
+            uint8_t* vt = vring + vs * C::MAT_BYTES;
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
               if (c == 1 && !two) break;
-              uint8_t* vd = st + C::MAT_BYTES + c * SUB * 128;
-              tma_load_2d(vd, &vmap, 0, static_cast<int32_t>(rows[c]), &fullv[s], pol);
-              tma_load_2d(vd + C::BOX_BYTES, &vmap, 64, static_cast<int32_t>(rows[c]), &fullv[s], pol);
+              uint8_t* vd = vt + c * SUB * 128;
+              tma_load_2d(vd, &vmap, 0, static_cast<int32_t>(rows[c]), &fullv[vs], pol);
+              tma_load_2d(vd + C::BOX_BYTES, &vmap, 64, static_cast<int32_t>(rows[c]), &fullv[vs], pol);
             }
           });
     }
@@ -279,28 +283,29 @@ __global__ void __launch_bounds__(7 * 32, 1)
 
   constexpr uint32_t IDESC_S = tc_idesc<T>(128, C::NPAD, 0, 0);  // K-major A and B
   constexpr uint32_t IDESC_O = tc_idesc<T>(128, C::NPAD, 1, 1);  // MN-major A and B
-  // TMEM columns: S(parity b) at b * 16, O(parity b) at 32 + b * 16
-  auto s_tmem = [&](int b) { return tmem + static_cast<uint32_t>(b) * 16; };
-  auto o_tmem = [&](int b) { return tmem + 32 + static_cast<uint32_t>(b) * 16; };
+  // TMEM columns: S(i % 4) at (i % 4) * 8, O(parity b) at 32 + b * 8
+  auto s_tmem = [&](int b) { return tmem + static_cast<uint32_t>(b) * 8; };
+  auto o_tmem = [&](int b) { return tmem + 32 + static_cast<uint32_t>(b) * 8; };
 
-  if (warp == 4) {  // ---------------- MMA issuer ----------------
-    const uint32_t ring = smem_u32(smem);
-    const uint32_t qb0 = smem_u32(qbuf), pb0 = smem_u32(pbuf);
+  if (warp == 4) {  // ---------------- S issuer ----------------
+    const uint32_t kring = smem_u32(smem), qb0 = smem_u32(qbuf);
     Item it{};
-    int k_item = -1, prev_s = 0;
-    bool prev_real = false;
-    uint32_t v_par = 0;  // per stage: parity of the fullv phase of its next loaded V half
+    int k_item = -1, nv = 0;  // items started; data tiles so far (the V ring's counter)
     for (int i = 0;; ++i) {
-      const int s = i % STAGES;
-      mbar_wait(&full[s], (i / STAGES) & 1);
+      const int s = i % KS;
+      mbar_wait(&full[s], (i / KS) & 1);
       const int4 mt = meta[i % C::META];
       const bool sentinel = mt.x < 0;
       const bool real = !sentinel && mt.z > 0;  // (an empty request's marker carries no data)
+      // S(i) reuses the buffer of S(i - NS), which the warpgroup has read out by sfree; the q
+      // buffer of item k is that of item k - NS, whose S MMAs completed before (in order)
+      if (i >= NS) mbar_wait(&sfree[i % NS], ((i / NS) - 1) & 1);
       if (real) {
+        const int v = nv++;
         if (mt.y == 0) {  // new item: its q rows into the S MMA's B layout (K-major, 128B swizzle)
           it = item_from_tag<TILE>(p, mt);
           ++k_item;
-          uint8_t* qb = qbuf + (k_item & 1) * C::QBUF_BYTES;
+          uint8_t* qb = qbuf + (k_item % NS) * C::QBUF_BYTES;
           const uint8_t* src = qslot + s * C::SLOT_BYTES;
           for (int c = lane; c < G * 16; c += 32) {
             const int r = c >> 4, ch = c & 15;
@@ -308,14 +313,15 @@ __global__ void __launch_bounds__(7 * 32, 1)
                 *reinterpret_cast<const uint4*>(src + r * C::ROW_BYTES + ch * 16);
           }
         }
-        if (tile_has_new<TILE>(p, it, mt.y)) {  // fused append: the new K / V row into the tile and the pools
-          mbar_wait(&fullv[s], (v_par >> s) & 1);  // the V half must have landed first
+        if (tile_has_new<TILE>(p, it, mt.y)) {  // fused append: the new K / V row into the tiles and the pools
+          mbar_wait(&fullv[v % VS], (v / VS) & 1);  // the V tile must have landed first
           const int r = it.len - 1 - (it.t_begin + mt.y * TILE);
           const int ch = lane & 15, is_v = lane >> 4;
           const uint4 val = *reinterpret_cast<const uint4*>(qslot + s * C::SLOT_BYTES + C::Q_BYTES +
                                                             is_v * C::ROW_BYTES + ch * 16);
-          *reinterpret_cast<uint4*>(smem + s * C::STAGE_BYTES + is_v * C::MAT_BYTES +
-                                    (ch >> 3) * C::BOX_BYTES + r * 128 + (((ch & 7) ^ (r & 7)) << 4)) = val;
+          uint8_t* tile = is_v ? vring + (v % VS) * C::MAT_BYTES : smem + s * C::MAT_BYTES;
+          *reinterpret_cast<uint4*>(tile + (ch >> 3) * C::BOX_BYTES + r * 128 +
+                                    (((ch & 7) ^ (r & 7)) << 4)) = val;
           T* pool = static_cast<T*>(is_v ? p.v_pool_w : p.k_pool_w);
           *reinterpret_cast<uint4*>(pool + kv_row(p, it.b, it.kvh, it.len - 1) * D + ch * 8) = val;
         }
@@ -323,66 +329,69 @@ __global__ void __launch_bounds__(7 * 32, 1)
         __syncwarp();
         if (lane == 0) {  // S(i) = K(i) · Q^T
           tc_fence_after();
-          const uint32_t kb = ring + s * C::STAGE_BYTES;
-          const uint32_t qb = qb0 + (k_item & 1) * C::QBUF_BYTES;
           if (!nomath) {
+            const uint32_t kb = kring + s * C::MAT_BYTES;
+            const uint32_t qb = qb0 + (k_item % NS) * C::QBUF_BYTES;
 #pragma unroll
             for (int kk = 0; kk < D / 16; ++kk) {
               const uint32_t off = (kk >> 2) * C::BOX_BYTES + (kk & 3) * 32;
               const uint32_t qoff = (kk >> 2) * C::QBOX + (kk & 3) * 32;
-              tc_mma(s_tmem(i & 1), smem_desc(kb + off, 16, 1024, 2),
+              tc_mma(s_tmem(i % NS), smem_desc(kb + off, 16, 1024, 2),
                      smem_desc(qb + qoff, 16, 1024, 2), IDESC_S, kk > 0);
             }
           }
-          tc_commit(&sbar[i & 1]);
-          if (!(p.flags & 64)) tc_commit(&empty[s]);  // the K half is free once S has read it
+          tc_commit(&sbar[i % NS]);
+          tc_commit(&empty[s]);  // the K slot is free once S has read it
         }
       } else if (lane == 0) {
-        mbar_arrive(&sbar[i & 1]);  // marker / end of work: the warpgroup reads the tag
+        mbar_arrive(&sbar[i % NS]);  // marker / end of work: the warpgroup reads the tag
         if (!sentinel) mbar_arrive(&empty[s]);
       }
       __syncwarp();
-      if (i >= 1) {  // O(i-1) = V(i-1)^T · P(i-1)^T
-        const int j = i - 1;
-        mbar_wait(&pbar[j & 1], (j >> 1) & 1);
-        if (j >= 2) mbar_wait(&ofree[j & 1], ((j - 2) >> 1) & 1);
-        if (prev_real) {
-          mbar_wait(&fullv[prev_s], (v_par >> prev_s) & 1);
-          v_par ^= 1u << prev_s;
-        }
-        if (lane == 0) {
-          tc_fence_after();
-          if (prev_real) {
-            const uint32_t vb = ring + prev_s * C::STAGE_BYTES + C::MAT_BYTES;
-            const uint32_t pb = pb0 + (j & 1) * C::PBUF_BYTES;
-            // the zero block (q heads 8..15 of P^T) sits right after P1
-            const uint32_t sbo = pb0 + 2 * C::PBUF_BYTES - pb;
-            if (!nomath) {
-#pragma unroll
-              for (int kk = 0; kk < TILE / 16; ++kk)
-                tc_mma(o_tmem(j & 1), smem_desc(vb + kk * 16 * 128, C::BOX_BYTES, 1024, 2),
-                       smem_desc(pb + kk * 256, 128, sbo, 0), IDESC_O, kk > 0);
-            }
-            tc_commit(&obar[j & 1]);
-            tc_commit(&emptyv[prev_s]);
-            if (p.flags & 64) tc_commit(&empty[prev_s]);  // diagnostic: K held until the O MMA
-          } else {
-            mbar_arrive(&obar[j & 1]);
-          }
-        }
-        __syncwarp();
-      }
       if (sentinel) break;
-      prev_s = s;
-      prev_real = real;
     }
-    named_bar_sync(3, 5 * 32);  // the warpgroup has read every result
+    named_bar_sync(3, 6 * 32);  // the warpgroup and the O issuer are done with TMEM
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                   "n"(C::TMEM_COLS)
-                   : "memory");
+                 "n"(C::TMEM_COLS)
+                 : "memory");
     return;
   }
-
+  if (warp == 7) {  // ---------------- O issuer ----------------
+    const uint32_t vring_a = smem_u32(vring), pb0 = smem_u32(pbuf);
+    int nv = 0;  // data tiles so far (the V ring's counter)
+    for (int j = 0;; ++j) {
+      mbar_wait(&pbar[j & 1], (j >> 1) & 1);  // P(j) written (the warpgroup also passes the end)
+      const int4 mt = meta[j % C::META];
+      if (mt.x < 0) break;
+      const bool real = mt.z > 0;
+      if (j >= 2) mbar_wait(&ofree[j & 1], ((j - 2) >> 1) & 1);
+      const int v = nv;
+      if (real) {
+        ++nv;
+        mbar_wait(&fullv[v % VS], (v / VS) & 1);
+      }
+      if (lane == 0) {
+        tc_fence_after();
+        if (real) {
+          const uint32_t vb = vring_a + (v % VS) * C::MAT_BYTES;
+          const uint32_t pb = pb0 + (j & 1) * C::PBUF_BYTES;
+          if (!nomath) {
+#pragma unroll
+            for (int kk = 0; kk < TILE / 16; ++kk)
+              tc_mma(o_tmem(j & 1), smem_desc(vb + kk * 16 * 128, C::BOX_BYTES, 1024, 2),
+                     smem_desc(pb + kk * 256, 128, 128, 0), IDESC_O, kk > 0);
+          }
+          tc_commit(&obar[j & 1]);
+          tc_commit(&emptyv[v % VS]);
+        } else {
+          mbar_arrive(&obar[j & 1]);
+        }
+      }
+      __syncwarp();
+    }
+    named_bar_sync(3, 6 * 32);
+    return;
+  }
   // ---------------- softmax warpgroup (warps 0-3) ----------------
   const int t = warp * 32 + lane;  // token row of S / dim row of O^T = TMEM lane
   const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
@@ -393,12 +402,11 @@ __global__ void __launch_bounds__(7 * 32, 1)
   Item it{};
   bool prev_real = false, prev_first = false, prev_last = false;
   int k_item = 0, bpar = 0;
-  uint32_t v_par = 0;  // per stage: fullv parity of its next loaded V half
+  int nv = 0;  // data-carrying tiles so far (the V ring's counter)
 #pragma unroll
   for (int g = 0; g < GQ; ++g) { m[g] = -INFINITY; l[g] = 0.f; o[g] = 0.f; a_prev[g] = 0.f; }
   for (int i = 0;; ++i) {
-    const int s = i % STAGES;
-    mbar_wait(&sbar[i & 1], (i >> 1) & 1);
+    mbar_wait(&sbar[i % NS], (i / NS) & 1);
     tc_fence_after();
     const int4 mt = meta[i % C::META];
     const bool sentinel = mt.x < 0;
@@ -421,7 +429,10 @@ __global__ void __launch_bounds__(7 * 32, 1)
       last = mt.y == max(it.ntiles, 1) - 1;
       if (real) {
         float x[GQ];
-        tmem_ld8(s_tmem(i & 1) + lane_base, x);
+        tmem_ld8(s_tmem(i % NS) + lane_base, x);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sfree[i % NS]);  // the S buffer may take S(i + NS)
         const int tok = it.t_begin + mt.y * TILE + t;
         const bool valid = tok < it.t_end;
 #pragma unroll
@@ -473,9 +484,9 @@ __global__ void __launch_bounds__(7 * 32, 1)
         // stale rows past the end may hold non-finite values and p = 0 must meet 0: zero them,
         // once the tile's V half has landed (it is loaded after the previous O MMA read the
         // slot, so S — and this softmax — can run ahead of it)
-        if (it.t_begin + mt.y * TILE + TILE > it.t_end) mbar_wait(&fullv[s], (v_par >> s) & 1);
+        if (it.t_begin + mt.y * TILE + TILE > it.t_end) mbar_wait(&fullv[nv % VS], (nv / VS) & 1);
         if (!valid) {
-          uint8_t* vrow = smem + s * C::STAGE_BYTES + C::MAT_BYTES + t * 128;
+          uint8_t* vrow = vring + (nv % VS) * C::MAT_BYTES + t * 128;
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
             *reinterpret_cast<uint4*>(vrow + c * 16) = make_uint4(0u, 0u, 0u, 0u);
@@ -484,10 +495,16 @@ __global__ void __launch_bounds__(7 * 32, 1)
         }
         fence_proxy_async_smem();
       }
-      if (real) v_par ^= 1u << s;
+      if (real) ++nv;
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&pbar[i & 1]);
+      if (lane == 0) {
+        if (!real) mbar_arrive(&sfree[i % NS]);  // (a marker reads no S, but owns the buffer)
+        mbar_arrive(&pbar[i & 1]);
+      }
+    } else {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pbar[i & 1]);  // the O issuer reads the end tag, too
     }
     if (i >= 1) {  // fold O(i-1) into the output rows
       const int j = i - 1;
@@ -546,7 +563,7 @@ __global__ void __launch_bounds__(7 * 32, 1)
   red_acquire(red, k_item);
   if (warp == 0 && lane == 0) red.item[0] = -1;
   red_commit(red);
-  named_bar_sync(3, 5 * 32);
+  named_bar_sync(3, 6 * 32);
 }
 
 }  // namespace lam

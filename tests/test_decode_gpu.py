@@ -59,9 +59,9 @@ def test_golden_fixtures(built, golden):
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16, torch.float16])
 @pytest.mark.parametrize("G", [1, 2, 4, 8])
 @pytest.mark.parametrize("paged", [False, True])
-@pytest.mark.parametrize("kernel", ["auto", "simt", "gqa_mma"])
+@pytest.mark.parametrize("kernel", ["auto", "simt", "gqa_mma", "gqa_tc"])
 def test_decode_vs_oracle(built, dtype, G, paged, kernel):
-    if kernel == "gqa_mma" and dtype == torch.float32:
+    if kernel in ("gqa_mma", "gqa_tc") and dtype == torch.float32:
         pytest.skip("tensor-core kernel is 16-bit only")
     B, Hkv, D = 3, 2, 128
     Hq = Hkv * G
@@ -188,8 +188,9 @@ def test_validation_errors(built):
 
 
 @pytest.mark.slow
+@pytest.mark.parametrize("kernel", ["auto", "gqa_tc"])
 @pytest.mark.parametrize("cfg", ["c3", "c4"])
-def test_llama2_70b_layer_subset_parity(built, cfg):
+def test_llama2_70b_layer_subset_parity(built, cfg, kernel):
     """BASELINE configs 3/4 at full size for one layer (paged bf16, GQA 64/8): a seeded
     subset of (request, q head) pairs against the oracle, all heads finite and bounded."""
     B, L = (128, 4096) if cfg == "c3" else (32, 32768)
@@ -202,7 +203,7 @@ def test_llama2_70b_layer_subset_parity(built, cfg):
     perm = torch.randperm(npages, generator=torch.Generator().manual_seed(5)).to(torch.int32)
     pt = perm.view(B, L // P).cuda()
     lens = _lens_t([L] * B)
-    out = _decode(q, kp, vp, lens, page_table=pt, out_dtype=torch.float32)
+    out = _decode(q, kp, vp, lens, page_table=pt, out_dtype=torch.float32, kernel=kernel)
     torch.cuda.synchronize()
     assert torch.isfinite(out).all() and out.abs().max() <= 1.0
     rng = np.random.default_rng(0)
@@ -217,15 +218,17 @@ def test_llama2_70b_layer_subset_parity(built, cfg):
             assert _maxabs(out[b, h].cpu().numpy(), want[0, h]) <= 2e-3
 
 
-@pytest.mark.parametrize("dtype,G", [(torch.bfloat16, 8), (torch.bfloat16, 1), (torch.float32, 1)])
-def test_many_splits_combine(built, dtype, G):
+@pytest.mark.parametrize("dtype,G,kernel", [(torch.bfloat16, 8, "auto"), (torch.bfloat16, 1, "auto"),
+                                            (torch.float32, 1, "auto"), (torch.bfloat16, 8, "gqa_tc")])
+def test_many_splits_combine(built, dtype, G, kernel):
     """More than 32 live splits per head exercises the long combine path."""
     B, Hkv, D, L = 2, 2, 128, 4000
     q, k, v = make_dense(B, Hkv * G, Hkv, D, L, dtype, seed=21)
     lens = [L, 2100]
     scale = 1 / math.sqrt(D)
     want = oracle_decode(q, k, v, lens, scale)
-    out = _decode(q, k, v, _lens_t(lens), scale=scale, out_dtype=torch.float32, split_tokens=64)
+    out = _decode(q, k, v, _lens_t(lens), scale=scale, out_dtype=torch.float32,
+                  split_tokens=128 if kernel == "gqa_tc" else 64, kernel=kernel)
     torch.cuda.synchronize()
     assert _maxabs(out.cpu().numpy(), want) <= TOL[dtype]
 
@@ -316,10 +319,11 @@ def test_decode_layers_host_matches_device_path(built, monkeypatch, L, flags):
         assert torch.equal(pools[l][0], kp) and torch.equal(pools[l][1], vp)
 
 
-@pytest.mark.parametrize("dtype,G,paged", [(torch.bfloat16, 8, True), (torch.bfloat16, 1, True),
-                                           (torch.float32, 1, False), (torch.float16, 4, True),
-                                           (torch.float32, 4, True)])
-def test_fused_append_equals_append_then_decode(built, dtype, G, paged):
+@pytest.mark.parametrize("dtype,G,paged,kernel", [
+    (torch.bfloat16, 8, True, "auto"), (torch.bfloat16, 1, True, "auto"), (torch.float32, 1, False, "auto"),
+    (torch.float16, 4, True, "auto"), (torch.float32, 4, True, "auto"), (torch.bfloat16, 8, True, "gqa_tc"),
+    (torch.float16, 1, True, "gqa_tc"), (torch.bfloat16, 2, False, "gqa_tc")])
+def test_fused_append_equals_append_then_decode(built, dtype, G, paged, kernel):
     """decode(..., k_new, v_new) == kv_append + decode: bitwise outputs and pools, for the
     last tile, split boundaries and single-token requests (new token at seq_lens - 1)."""
     from paper_2405_01814_b200 import decode as dec
@@ -338,12 +342,12 @@ def test_fused_append_equals_append_then_decode(built, dtype, G, paged):
         ptt, kp, vp = None, k.clone(), v.clone()
     kp2, vp2 = kp.clone(), vp.clone()
     lt = _lens_t(lens)
-    for split in (0, 64):
+    for split in (0, 128 if kernel == "gqa_tc" else 64):
         a = dec.decode(q, kp, vp, lt, page_table=ptt, max_len=max(lens), split_tokens=split,
-                       k_new=kn, v_new=vn, out_dtype=torch.float32)
+                       k_new=kn, v_new=vn, out_dtype=torch.float32, kernel=kernel)
         dec.kv_append(kn, vn, kp2, vp2, (lt - 1).contiguous(), ptt)
         b = dec.decode(q, kp2, vp2, lt, page_table=ptt, max_len=max(lens), split_tokens=split,
-                       out_dtype=torch.float32)
+                       out_dtype=torch.float32, kernel=kernel)
         torch.cuda.synchronize()
         assert torch.equal(a, b), split
         assert torch.equal(kp, kp2) and torch.equal(vp, vp2), split
@@ -362,10 +366,12 @@ def test_request_order_is_transparent(built):
     kp, vp = to_paged(k, lens, 64, pt, npages), to_paged(v, lens, 64, pt, npages)
     lt = _lens_t(lens)
     for split in (0, 256):
-        a = dec.decode(q, kp, vp, lt, page_table=ptt, max_len=max(lens), split_tokens=split)
-        b = dec.decode(q, kp, vp, lt, page_table=ptt, max_len=max(lens), split_tokens=split,
-                       request_order=dec.longest_first(lt))
-        assert torch.equal(a, b)
+        for kernel in ("auto", "gqa_tc"):
+            a = dec.decode(q, kp, vp, lt, page_table=ptt, max_len=max(lens), split_tokens=split,
+                           kernel=kernel)
+            b = dec.decode(q, kp, vp, lt, page_table=ptt, max_len=max(lens), split_tokens=split,
+                           request_order=dec.longest_first(lt), kernel=kernel)
+            assert torch.equal(a, b)
     want = oracle_decode(q, k, v, lens, 1 / math.sqrt(D))
     out = dec.decode(q, kp, vp, lt, page_table=ptt, max_len=max(lens), out_dtype=torch.float32,
                      request_order=dec.longest_first(lt))
@@ -373,7 +379,8 @@ def test_request_order_is_transparent(built):
 
 
 @pytest.mark.parametrize("kernel,G,dtype", [("simt", 1, torch.bfloat16), ("simt", 1, torch.float32),
-                                            ("gqa_mma", 8, torch.bfloat16), ("simt", 4, torch.float16)])
+                                            ("gqa_mma", 8, torch.bfloat16), ("simt", 4, torch.float16),
+                                            ("gqa_tc", 8, torch.bfloat16), ("gqa_tc", 1, torch.float16)])
 @pytest.mark.parametrize("tail,splits", [(1, 2), (3, 4), (100, 3)])
 def test_split_tail_vs_oracle(built, monkeypatch, kernel, G, dtype, tail, splits):
     """Split tail: the last `tail` units run as `splits` short items merged in split order, the
@@ -399,7 +406,8 @@ def test_split_tail_vs_oracle(built, monkeypatch, kernel, G, dtype, tail, splits
 
 
 @pytest.mark.parametrize("kernel,dtype,G", [("gqa_mma", torch.bfloat16, 8), ("gqa_mma", torch.bfloat16, 1),
-                                            ("simt", torch.float32, 1), ("simt", torch.bfloat16, 2)])
+                                            ("simt", torch.float32, 1), ("simt", torch.bfloat16, 2),
+                                            ("gqa_tc", torch.bfloat16, 8), ("gqa_tc", torch.bfloat16, 1)])
 @pytest.mark.parametrize("lmax", [40, 300, 3000])
 def test_overlap_prev_orders_inputs_after_preceding_kernel(built, kernel, dtype, G, lmax):
     """overlap_prev (programmatic dependent launch): a chain of launches over different pools
@@ -448,7 +456,7 @@ def test_overlap_prev_orders_inputs_after_preceding_kernel(built, kernel, dtype,
     # B200 (profiles/r01b/SUMMARY.md §2, §7): C1 on 128 CTAs (2 even rounds), C4 split 4 ways,
     # the 512-unit sharded GQA launch unsplit on 128 CTAs, the rest unsplit on the full grid.
     ("c1", 8, 32, 32, 1024, torch.float32, False, ("simt", 1, 128)),
-    ("c2", 64, 32, 32, 4096, torch.bfloat16, True, ("gqa_mma", 1, 148)),
+    ("c2", 64, 32, 32, 4096, torch.bfloat16, True, ("gqa_tc", 1, 148)),
     ("c3", 128, 64, 8, 4096, torch.bfloat16, True, ("gqa_mma", 1, 148)),
     ("c4", 32, 64, 8, 32768, torch.bfloat16, True, ("gqa_mma", 4, 148)),
     ("c3n8", 512, 8, 1, 4096, torch.bfloat16, True, ("gqa_mma", 1, 128)),
@@ -499,7 +507,7 @@ def test_c2_full_shape_overlap_chain_vs_oracle(built):
              for _ in range(layers)]
     x0 = torch.empty((B, 3 * H, D), dtype=torch.bfloat16, device="cuda").uniform_(-1, 1, generator=g)
     kern, splits, _ = dec.plan(x0[:, :H], pools[0][0], pools[0][1], lens, page_table=pt, max_len=L)
-    assert kern == "gqa_mma" and splits == 1
+    assert kern == "gqa_tc" and splits == 1  # the bench's C2 launch
     # layer 0 reads packed QKV rows; layer l > 0 reads q = k_new = v_new = layer l-1's output,
     # straight from the launch before it (no kernel in between)
     ins = [(x0[:, :H], x0[:, H:2 * H], x0[:, 2 * H:])]
