@@ -305,6 +305,39 @@ typedef struct lam_peer_io {
 int lam_decode_peer(lam_ctx* ctx, const lam_decode_args* args, const lam_peer_io* io,
                     void* stream);
 
+/* ---- step launch: every layer (and micro-batch) of a decode step in one persistent grid ----
+ *
+ * Launch lm = layer * n_mb + mb (layer major) is `args` (which describes layer 0, micro-batch 0)
+ * with
+ *   - rows [mb * rows_per_mb, (mb + 1) * rows_per_mb) of page_table / seq_lens / request_order
+ *     (args->batch = n_mb * rows_per_mb; request_order holds indices local to the micro-batch);
+ *   - KV pool rows of pool layer (layer0 + layer) % pool_layers: every layer's pool is one slice
+ *     of one allocation, pool_layer_rows rows apart (pool viewed as [rows][D], i.e. num_pages *
+ *     Hkv * page_size rows per layer when paged);
+ *   - q / k_new / v_new / out offset by lm * lm_q_stride / lm * lm_new_stride / lm * lm_out_stride
+ *     elements (with io, the per-source buffers of lam_peer_io; its new rows follow q).
+ * With io, wait_flags / done_flags address micro-batch 0's sequence numbers and flag_mb_stride
+ * (uint32 elements) micro-batch mb's; launch lm waits for and publishes epoch + layer + 1 — a CTA
+ * waits when it first claims one of lm's items, and lm's flags are published as soon as all its
+ * units are stored.  There is no launch boundary between layers: a CTA that runs out of work in
+ * one layer goes on with the next.  Splits are not used (S = 1) and args->lse must be NULL. */
+typedef struct lam_step_layout {
+  int32_t n_layers;
+  int32_t n_mb;
+  int32_t rows_per_mb;
+  int32_t pool_layers;
+  int32_t layer0;
+  int32_t flag_mb_stride;
+  int64_t pool_layer_rows;
+  int64_t lm_q_stride;
+  int64_t lm_new_stride;
+  int64_t lm_out_stride;
+  uint32_t epoch;
+} lam_step_layout;
+
+int lam_decode_step(lam_ctx* ctx, const lam_decode_args* args, const lam_step_layout* step,
+                    const lam_peer_io* io, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

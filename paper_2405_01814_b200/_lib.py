@@ -87,6 +87,24 @@ class PeerIO(C.Structure):
     ]
 
 
+class StepLayout(C.Structure):
+    """lam_step_layout (include/lamina_attn.h)."""
+
+    _fields_ = [
+        ("n_layers", C.c_int32),
+        ("n_mb", C.c_int32),
+        ("rows_per_mb", C.c_int32),
+        ("pool_layers", C.c_int32),
+        ("layer0", C.c_int32),
+        ("flag_mb_stride", C.c_int32),
+        ("pool_layer_rows", C.c_int64),
+        ("lm_q_stride", C.c_int64),
+        ("lm_new_stride", C.c_int64),
+        ("lm_out_stride", C.c_int64),
+        ("epoch", C.c_uint32),
+    ]
+
+
 _P, _I32, _I64, _F64 = C.c_void_p, C.c_int32, C.c_int64, C.c_double
 
 # name -> (restype, argtypes)
@@ -129,6 +147,8 @@ SIGNATURES = {
     "lam_stream_signal": (C.c_int, [_P, _P, _I32, C.c_uint32, _P]),
     "lam_stream_wait": (C.c_int, [_P, _P, _I32, C.c_uint32, _P]),
     "lam_decode_peer": (C.c_int, [_P, C.POINTER(DecodeArgs), C.POINTER(PeerIO), _P]),
+    "lam_decode_step": (C.c_int, [_P, C.POINTER(DecodeArgs), C.POINTER(StepLayout),
+                                  C.POINTER(PeerIO), _P]),
 }
 
 _lib = None

@@ -45,6 +45,9 @@ struct lam_ctx {
   // and the monotonic layer counter that numbers them across calls
   uint32_t* host_flags = nullptr;
   uint32_t host_seq = 0;
+  // step launches: finished units per launch lm, per launch slot (zeroed before each launch)
+  int32_t* lm_done = nullptr;
+  int64_t lm_done_cap = 0;
   // bounded device-side spins of the decode kernels (lam_ctx_status / lam_ctx_set_spin_timeout)
   int32_t* status = nullptr;
   unsigned long long spin_timeout_ns = 10ull * 1000 * 1000 * 1000;
@@ -476,6 +479,7 @@ int lam_ctx_destroy(lam_ctx* c) {
   cudaFree(c->scratch);
   cudaFree(c->offs);
   cudaFree(c->host_flags);
+  cudaFree(c->lm_done);
   delete c;
   return LAM_OK;
 }
@@ -789,9 +793,29 @@ int lam_decode_plan_grid(lam_ctx* ctx, const lam_decode_args* a, int32_t* ctas) 
 
 namespace {
 
-int decode_impl(lam_ctx* ctx, const lam_decode_args* a, const lam_peer_io* io, void* stream) {
+int decode_impl(lam_ctx* ctx, const lam_decode_args* a_in, const lam_peer_io* io,
+                const lam_step_layout* st, void* stream) {
   if (!ctx) return fail(LAM_ERR_VALIDATION, "null context");
   LAM_DEVICE(ctx);
+  lam_decode_args a_step;
+  const lam_decode_args* a = a_in;
+  int n_lm = 1;
+  if (st != nullptr) {  // plan one launch lm: rows_per_mb requests, no splits
+    if (st->n_layers < 1 || st->n_mb < 1 || st->rows_per_mb < 1 ||
+        static_cast<int64_t>(st->n_mb) * st->rows_per_mb != a_in->batch)
+      return fail(LAM_ERR_VALIDATION, "step: need n_layers, n_mb, rows_per_mb >= 1 and batch == "
+                                      "n_mb * rows_per_mb");
+    if (st->pool_layers < 1 || st->layer0 < 0 || st->pool_layer_rows < 0)
+      return fail(LAM_ERR_VALIDATION, "step: bad pool layer layout");
+    if (a_in->lse != nullptr) return fail(LAM_ERR_VALIDATION, "step: lse is not supported");
+    if (io != nullptr && io->rows_per_src * io->n_src != st->rows_per_mb)
+      return fail(LAM_ERR_VALIDATION, "step: peer io must describe one micro-batch's rows");
+    a_step = *a_in;
+    a_step.batch = st->rows_per_mb;
+    a_step.split_tokens = std::max(1, a_in->max_len);  // S = 1
+    a = &a_step;
+    n_lm = st->n_layers * st->n_mb;
+  }
   Plan pl;
   int rc = plan_decode(ctx, a, &pl);
   if (rc != LAM_OK) return rc;
@@ -799,6 +823,9 @@ int decode_impl(lam_ctx* ctx, const lam_decode_args* a, const lam_peer_io* io, v
   const int G = a->num_q_heads / a->num_kv_heads;
   const int D = a->head_dim;
   lam::DecodeParams p{};
+  p.n_lm = 1;
+  p.n_mb = 1;
+  p.pool_layers = 1;
   p.q = a->q;
   p.q_stride = a->q_batch_stride > 0 ? a->q_batch_stride
                                      : static_cast<int64_t>(a->num_q_heads) * a->head_dim;
@@ -821,6 +848,25 @@ int decode_impl(lam_ctx* ctx, const lam_decode_args* a, const lam_peer_io* io, v
   const int64_t units = static_cast<int64_t>(a->batch) * a->num_kv_heads * pl.QG;
   p.u_head = static_cast<int32_t>(pl.u_head);
   p.n_items = static_cast<int32_t>(pl.u_head + (units - pl.u_head) * pl.S);
+  p.mb_rows = a->batch;
+  p.items_per_lm = p.n_items;
+  p.units_per_lm = static_cast<int32_t>(units);
+  if (st != nullptr) {
+    if (static_cast<int64_t>(p.n_items) * n_lm >= (int64_t{1} << 31))
+      return fail(LAM_ERR_VALIDATION, "step: too many work items");
+    p.B = a_in->batch;
+    p.n_lm = n_lm;
+    p.n_mb = st->n_mb;
+    p.n_items *= n_lm;
+    p.pool_layers = st->pool_layers;
+    p.layer0 = st->layer0;
+    p.layer_rows = st->pool_layer_rows;
+    p.lm_q_stride = st->lm_q_stride;
+    p.lm_new_stride = st->lm_new_stride;
+    p.lm_out_stride = st->lm_out_stride;
+    p.flag_mb_stride = st->flag_mb_stride;
+    p.epoch = st->epoch;
+  }
   const int slot = static_cast<int>(ctx->seq % kSlots);
   p.slot = ctx->slots + 2 * slot;
   p.item_base = ctx->item_base[slot];
@@ -875,6 +921,8 @@ int decode_impl(lam_ctx* ctx, const lam_decode_args* a, const lam_peer_io* io, v
     }
     p.n_wait = io->n_wait;
     p.n_done = io->n_done;
+    if (st != nullptr && (io->n_wait > 0 || io->n_done > 0) && st->flag_mb_stride < 0)
+      return fail(LAM_ERR_VALIDATION, "step: bad flag_mb_stride");
     p.wait_value = io->wait_value;
     p.done_value = io->done_value;
     // the launch carries its own input dependencies (sequence numbers), so with overlap_prev it
@@ -887,7 +935,8 @@ int decode_impl(lam_ctx* ctx, const lam_decode_args* a, const lam_peer_io* io, v
     // starts, and the deferred issue cost 0.3-0.6 % at N = 2 (experiments/r01/call61.sh).
     if (io->n_wait > 0 && env_int("LAM_PEER_PREFETCH", 0) != 0) p.defer_inputs = 2;
   }
-  if (a->overlap_prev != 0 && io == nullptr) {
+  if (st != nullptr) p.defer_inputs = 0;  // (inputs are awaited per launch lm)
+  if (a->overlap_prev != 0 && io == nullptr && st == nullptr) {
     // stream the first KV tiles while the preceding kernel drains; q / k_new / v_new wait for it
     p.pdl = 1;
     p.defer_inputs = 1;
@@ -909,10 +958,20 @@ int decode_impl(lam_ctx* ctx, const lam_decode_args* a, const lam_peer_io* io, v
     p.counters = ctx->counters + slot * ctx->counters_cap;
   }
   auto s = static_cast<cudaStream_t>(stream);
+  if (st != nullptr) {  // [n_lm] finished units, [n_mb] layers published
+    const int64_t need = n_lm + st->n_mb;
+    if (need > ctx->lm_done_cap) {
+      LAM_CUDA(grow(&ctx->lm_done, &ctx->lm_done_cap, static_cast<int64_t>(kSlots) * need, true));
+      ctx->lm_done_cap = need;
+    }
+    p.lm_done = ctx->lm_done + slot * ctx->lm_done_cap;
+    LAM_CUDA(cudaMemsetAsync(p.lm_done, 0, need * sizeof(int32_t), s));
+  }
   if (pl.kernel == LAM_KERNEL_GQA_MMA || pl.kernel == LAM_KERNEL_GQA_TC) {
-    const int64_t rows = a->page_table
-                             ? a->num_pages * a->num_kv_heads * static_cast<int64_t>(a->page_size)
-                             : static_cast<int64_t>(a->batch) * a->num_kv_heads * a->page_size;
+    int64_t rows = a->page_table
+                       ? a->num_pages * a->num_kv_heads * static_cast<int64_t>(a->page_size)
+                       : static_cast<int64_t>(a_in->batch) * a->num_kv_heads * a->page_size;
+    if (st != nullptr) rows = std::max(rows, st->pool_layers * st->pool_layer_rows);
     if (rows >= (int64_t{1} << 31))
       return fail(LAM_ERR_VALIDATION, "pool exceeds 2^31 rows for the tensor map");
     CUtensorMap kmap, vmap;
@@ -939,12 +998,18 @@ int decode_impl(lam_ctx* ctx, const lam_decode_args* a, const lam_peer_io* io, v
 }  // namespace
 
 int lam_decode(lam_ctx* ctx, const lam_decode_args* a, void* stream) {
-  return decode_impl(ctx, a, nullptr, stream);
+  return decode_impl(ctx, a, nullptr, nullptr, stream);
 }
 
 int lam_decode_peer(lam_ctx* ctx, const lam_decode_args* a, const lam_peer_io* io, void* stream) {
   if (!io) return fail(LAM_ERR_VALIDATION, "null peer io");
-  return decode_impl(ctx, a, io, stream);
+  return decode_impl(ctx, a, io, nullptr, stream);
+}
+
+int lam_decode_step(lam_ctx* ctx, const lam_decode_args* a, const lam_step_layout* step,
+                    const lam_peer_io* io, void* stream) {
+  if (!step) return fail(LAM_ERR_VALIDATION, "null step layout");
+  return decode_impl(ctx, a, io, step, stream);
 }
 
 // ---------------- peer-memory transport ----------------

@@ -88,6 +88,20 @@ struct DecodeParams {
   // bounded spins (see spin_expired): status word of the context and the timeout (0 = none)
   int32_t* status;
   unsigned long long spin_timeout_ns;
+  // Step launch (lam_decode_step*): the items of n_lm = layers x micro-batches launches, layer
+  // major, in one persistent grid.  Launch lm = layer * n_mb + mb owns attention rows
+  // [mb * mb_rows, (mb + 1) * mb_rows) of page_table / seq_lens / order (order holds local
+  // indices), pool rows offset by layer * layer_rows, and inputs / outputs offset by
+  // lm * lm_q_stride / lm * lm_out_stride elements.  Its input sequence numbers (wait flags +
+  // mb * flag_mb_stride) are awaited when a CTA first claims one of its items, and once all of
+  // its units are finished (lm_done) its done flags are published; both carry epoch + layer + 1.
+  // A single launch is n_lm = n_mb = 1, mb_rows = B, items_per_lm = n_items.
+  int32_t n_lm, n_mb, mb_rows, items_per_lm, units_per_lm;
+  int32_t pool_layers, layer0;  // pool layer of layer l: (layer0 + l) % pool_layers
+  int64_t layer_rows, lm_q_stride, lm_new_stride, lm_out_stride;
+  int32_t flag_mb_stride;
+  uint32_t epoch;
+  int32_t* lm_done;
 };
 
 // lam_ctx_status codes (include/lamina_attn.h)
@@ -98,6 +112,15 @@ __device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned 
   unsigned long long v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
+}
+
+__device__ __forceinline__ int32_t ld_acquire_gpu_s32(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu_s32(int32_t* p, int32_t v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -126,12 +149,15 @@ __device__ __forceinline__ void acquire_slot(const DecodeParams& p) {
   }
 }
 
-// Spin until the inputs of this launch are published (peer transport).
-__device__ __forceinline__ void wait_inputs(const DecodeParams& p) {
+// Spin until the inputs of this launch (of launch lm of a step launch) are published.
+__device__ __forceinline__ void wait_inputs(const DecodeParams& p, int lm = -1) {
   if (p.n_wait <= 0) return;
   const unsigned long long t0 = globaltimer_ns();
+  const int mb = lm >= 0 ? lm % p.n_mb : 0;
+  const uint32_t value = lm >= 0 ? p.epoch + static_cast<uint32_t>(lm / p.n_mb) + 1u : p.wait_value;
   for (int i = 0; i < p.n_wait; ++i) {
-    while (static_cast<int32_t>(ld_acquire_sys(p.wait_flag[i]) - p.wait_value) < 0) {
+    const uint32_t* f = p.wait_flag[i] + static_cast<int64_t>(mb) * p.flag_mb_stride;
+    while (static_cast<int32_t>(ld_acquire_sys(f) - value) < 0) {
       __nanosleep(200);
       if (spin_expired(p, t0, kStatusInputTimeout)) {
         i = p.n_wait;
@@ -152,47 +178,57 @@ __device__ __forceinline__ void finish_cta(const DecodeParams& p) {
   else
     __threadfence();
   const unsigned long long old = atomicAdd(p.slot + 1, 1ull);
-  if (p.n_done <= 0 || old - p.done_base != gridDim.x - 1) return;
+  if (p.n_done <= 0 || p.n_lm > 1 || old - p.done_base != gridDim.x - 1) return;
   __threadfence_system();
   for (int i = 0; i < p.n_done; ++i) st_release_sys(p.done_flag[i], p.done_value);
 }
 
-// Start of request b's q rows / new k (which = 0) or v (1) rows, local or on a peer.
-template <typename T>
-__device__ __forceinline__ const T* q_rows(const DecodeParams& p, int b) {
-  if (p.src_rows > 0) {
-    const int s = b / p.src_rows;
-    return static_cast<const T*>(p.q_src[s]) + static_cast<int64_t>(b - s * p.src_rows) * p.q_stride;
-  }
-  return static_cast<const T*>(p.q) + static_cast<int64_t>(b) * p.q_stride;
-}
-template <typename T>
-__device__ __forceinline__ const T* new_rows(const DecodeParams& p, int which, int b) {
-  if (p.src_rows > 0) {
-    const int s = b / p.src_rows;
-    return static_cast<const T*>(p.q_src[s]) + p.new_off[which] +
-           static_cast<int64_t>(b - s * p.src_rows) * p.new_stride;
-  }
-  return static_cast<const T*>(which ? p.v_new : p.k_new) + static_cast<int64_t>(b) * p.new_stride;
-}
-
-// Physical row of token t of (request b, kv head h) in a pool viewed as [rows][D].
-// Paged: pool[page][Hkv][P][D]; dense: pool[B][Hkv][P][D] (P = row capacity).
-__device__ __forceinline__ int64_t kv_row(const DecodeParams& p, int b, int h, int t) {
+// Physical row of token t of (request b, kv head h) of launch lm in a pool viewed as [rows][D].
+// Paged: pool[page][Hkv][P][D]; dense: pool[B][Hkv][P][D] (P = row capacity); step launches add
+// the layer's offset.
+__device__ __forceinline__ int64_t kv_row(const DecodeParams& p, int b, int h, int t, int lm = 0) {
   const int64_t blk =
       p.page_table ? static_cast<int64_t>(__ldg(p.page_table + static_cast<int64_t>(b) * p.pt_stride +
                                                 t / p.page_size))
                    : static_cast<int64_t>(b);
-  return (blk * p.Hkv + h) * p.page_size + (t % p.page_size);
+  return (blk * p.Hkv + h) * p.page_size + (t % p.page_size) +
+         (p.n_lm > 1 ? static_cast<int64_t>((p.layer0 + lm / p.n_mb) % p.pool_layers) * p.layer_rows
+                     : 0);
 }
 
 enum IssueMode { kIssueAll = 0, kIssueKV = 1, kIssueInputs = 2 };
 
 struct Item {
-  int b, kvh, qg, split;
+  int b, kvh, qg, split;  // b: the attention row (over every micro-batch of a step launch)
   int len, t_begin, t_end, ntiles;
   int whole;  // the item is a whole unit (no split partial, no merge)
+  int lm;     // launch of a step launch (layer * n_mb + micro-batch); 0 otherwise
 };
+
+// Start of request it.b's q rows / new k (which = 0) or v (1) rows, local or on a peer.
+template <typename T>
+__device__ __forceinline__ const T* q_rows(const DecodeParams& p, const Item& it) {
+  const int b = it.b - (it.lm % p.n_mb) * p.mb_rows;  // row within the launch
+  const int64_t lm_off = static_cast<int64_t>(it.lm) * p.lm_q_stride;
+  if (p.src_rows > 0) {
+    const int s = b / p.src_rows;
+    return static_cast<const T*>(p.q_src[s]) + lm_off +
+           static_cast<int64_t>(b - s * p.src_rows) * p.q_stride;
+  }
+  return static_cast<const T*>(p.q) + lm_off + static_cast<int64_t>(b) * p.q_stride;
+}
+template <typename T>
+__device__ __forceinline__ const T* new_rows(const DecodeParams& p, int which, const Item& it) {
+  const int b = it.b - (it.lm % p.n_mb) * p.mb_rows;
+  if (p.src_rows > 0) {  // (the new rows sit in the packed q block)
+    const int64_t lm_off = static_cast<int64_t>(it.lm) * p.lm_q_stride;
+    const int s = b / p.src_rows;
+    return static_cast<const T*>(p.q_src[s]) + lm_off + p.new_off[which] +
+           static_cast<int64_t>(b - s * p.src_rows) * p.new_stride;
+  }
+  return static_cast<const T*>(which ? p.v_new : p.k_new) +
+         static_cast<int64_t>(it.lm) * p.lm_new_stride + static_cast<int64_t>(b) * p.new_stride;
+}
 
 // Work item `idx` -> (unit, split).  The first u_head items are whole units; the remaining
 // units are split S ways, split fastest (a split tail: the last rounds of a launch run short
@@ -211,19 +247,28 @@ __device__ __forceinline__ void item_unit(const DecodeParams& p, int idx, int& u
   }
 }
 
-// Unit -> (request, kv head, q group): q-head group fastest, then kv head, request.
+// Unit of launch lm -> (request, kv head, q group): q-head group fastest, then kv head, request.
 __device__ __forceinline__ void unit_coords(const DecodeParams& p, int unit, Item& it) {
   it.qg = unit % p.QG;
   unit /= p.QG;
   it.kvh = unit % p.Hkv;
-  it.b = unit / p.Hkv;
-  if (p.order != nullptr) it.b = __ldg(p.order + it.b);
+  const int r0 = (it.lm % p.n_mb) * p.mb_rows;
+  int b = unit / p.Hkv;
+  if (p.order != nullptr) b = __ldg(p.order + r0 + b);
+  it.b = r0 + b;
+}
+
+// Item index (over the whole launch) -> launch lm and the unit / split within it.
+__device__ __forceinline__ void item_lm(const DecodeParams& p, int idx, int& lm, int& local) {
+  lm = p.n_lm > 1 ? idx / p.items_per_lm : 0;
+  local = idx - lm * p.items_per_lm;
 }
 
 __device__ __forceinline__ Item make_item(const DecodeParams& p, int idx, int tile) {
   Item it;
-  int unit;
-  item_unit(p, idx, unit, it.split, it.whole);
+  int unit, local;
+  item_lm(p, idx, it.lm, local);
+  item_unit(p, local, unit, it.split, it.whole);
   unit_coords(p, unit, it);
   it.len = __ldg(p.seq_lens + it.b);
   it.t_begin = it.whole ? 0 : it.split * p.chunk;
@@ -237,8 +282,9 @@ __device__ __forceinline__ Item make_item(const DecodeParams& p, int idx, int ti
 template <int TILE>
 __device__ __forceinline__ Item item_from_tag(const DecodeParams& p, int4 tag) {
   Item it;
-  int unit;
-  item_unit(p, tag.x, unit, it.split, it.whole);
+  int unit, local;
+  item_lm(p, tag.x, it.lm, local);
+  item_unit(p, local, unit, it.split, it.whole);
   unit_coords(p, unit, it);
   it.len = tag.z;
   it.t_begin = it.whole ? 0 : it.split * p.chunk;
@@ -297,7 +343,9 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
     else
       griddep_wait();
   };
-  if (p.defer_inputs != 2) wait_inputs(p);
+  const bool step = p.n_lm > 1;  // inputs are awaited per launch lm, at its first claim
+  if (p.defer_inputs != 2 && !step) wait_inputs(p);
+  int waited_lm = -1;
   int i = 0;
   auto acquire = [&](int k) {
     const int s = k % STAGES;
@@ -310,6 +358,10 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
     if (claim >= p.n_items) break;
     const int idx = static_cast<int>(claim);
     const Item it = make_item(p, idx, TILE);
+    if (step && it.lm != waited_lm) {  // (claims arrive in launch order: lm only grows)
+      wait_inputs(p, it.lm);
+      waited_lm = it.lm;
+    }
     if (it.ntiles == 0) {
       if (deferring) {  // nothing to prefetch
         inputs_ready();
@@ -337,7 +389,7 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
 #pragma unroll
       for (int c = 0; c < NSUB; ++c) {
         const int t = it.t_begin + j * TILE + c * (TILE / NSUB);
-        rows[c] = (c == 0 || t < it.t_end) ? kv_row(p, it.b, it.kvh, t) : -1;
+        rows[c] = (c == 0 || t < it.t_end) ? kv_row(p, it.b, it.kvh, t, it.lm) : -1;
       }
       meta[ms] = make_int4(idx, j, it.len, it.t_end);
       meta_row[ms] = rows[0];
@@ -392,15 +444,17 @@ __device__ __forceinline__ void st_vec(float* dst, const float (&v)[N]) {
 // Elements [d, d + N) of the output of (request b, q head h), local or in the source rank's
 // buffer (peer transport); fp32 or the KV type.
 template <typename T, int D, int N>
-__device__ __forceinline__ void store_out_vec(const DecodeParams& p, int b, int h, int d,
+__device__ __forceinline__ void store_out_vec(const DecodeParams& p, const Item& it, int h, int d,
                                               const float (&v)[N]) {
   void* base = p.out;
+  int b = it.b - (it.lm % p.n_mb) * p.mb_rows;
   if (p.src_rows > 0) {
     const int s = b / p.src_rows;
     base = p.out_dst[s];
     b -= s * p.src_rows;
   }
-  const int64_t idx = (static_cast<int64_t>(b) * p.Hq + h) * D + d;
+  const int64_t idx = static_cast<int64_t>(it.lm) * p.lm_out_stride +
+                      (static_cast<int64_t>(b) * p.Hq + h) * D + d;
   if (sizeof(T) == 4 || p.out_f32) {
     st_vec<N>(static_cast<float*>(base) + idx, v);
   } else if constexpr (sizeof(T) == 2) {
@@ -418,6 +472,33 @@ __device__ __forceinline__ int atom_add_acq_rel_gpu(int32_t* p, int v) {
   asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v)
                : "memory");
   return old;
+}
+
+// A unit's outputs are all stored (step launches): count it in for its launch lm; the last unit
+// publishes lm's done flags (epoch + layer + 1, micro-batch mb's flag of every model worker)
+// after a system-scope fence, so a model worker that sees the number also sees the outputs.
+// Flags of one micro-batch are published in layer order (lm_done[n_lm + mb] = layers published):
+// in a decode step layer l + 1's inputs follow layer l's outputs, so the wait is normally empty,
+// but with inputs published ahead a later layer could finish first and must not be announced
+// before the earlier one.
+__device__ __forceinline__ void unit_done(const DecodeParams& p, const Item& it) {
+  if (p.lm_done == nullptr) return;
+  __syncwarp();
+  if (threadIdx.x % 32 != 0) return;
+  __threadfence_system();
+  if (atomicAdd(p.lm_done + it.lm, 1) != p.units_per_lm - 1) return;
+  __threadfence_system();
+  const int layer = it.lm / p.n_mb, mb = it.lm % p.n_mb;
+  int32_t* published = p.lm_done + p.n_lm + mb;
+  const unsigned long long t0 = globaltimer_ns();
+  while (ld_acquire_gpu_s32(published) < layer) {
+    __nanosleep(100);
+    if (spin_expired(p, t0, kStatusInputTimeout)) break;
+  }
+  const uint32_t value = p.epoch + static_cast<uint32_t>(layer) + 1u;
+  const int64_t off = static_cast<int64_t>(mb) * p.flag_mb_stride;
+  for (int i = 0; i < p.n_done; ++i) st_release_sys(p.done_flag[i] + off, value);
+  st_release_gpu_s32(published, layer + 1);
 }
 
 // Split-K epilogue of one work item, run by the CTA's dedicated epilogue warp while the
@@ -484,12 +565,13 @@ __device__ __forceinline__ void finish_item_warp(const DecodeParams& p, const It
         const float inv = L > 0.f ? 1.f / L : 0.f;
 #pragma unroll
         for (int e = 0; e < DPL; ++e) A[e] *= inv;
-        store_out_vec<T, D, DPL>(p, b, qh0 + g, d0, A);
+        store_out_vec<T, D, DPL>(p, it, qh0 + g, d0, A);
         if (lane == 0 && p.lse != nullptr)
           p.lse[static_cast<int64_t>(b) * p.Hq + qh0 + g] = L > 0.f ? cta_m[g] + logf(L) : -INFINITY;
       }
     }
     release();
+    unit_done(p, it);
     return;
   }
 
@@ -589,11 +671,12 @@ __device__ __forceinline__ void finish_item_warp(const DecodeParams& p, const It
     const float inv = L > 0.f ? 1.f / L : 0.f;
 #pragma unroll
     for (int e = 0; e < DPL; ++e) A[e] *= inv;
-    store_out_vec<T, D, DPL>(p, b, qh0 + g, d0, A);
+    store_out_vec<T, D, DPL>(p, it, qh0 + g, d0, A);
     if (lane == 0 && p.lse != nullptr)
       p.lse[static_cast<int64_t>(b) * p.Hq + qh0 + g] = L > 0.f ? M + logf(L) : -INFINITY;
   }
   if (lane == 0) *counter = 0;  // ready for the next launch
+  unit_done(p, it);
 }
 
 // Hand-off of per-warp partials from the consumer warps to the epilogue warp.  Single

@@ -101,13 +101,13 @@ __global__ void __launch_bounds__((NW_ + 2) * 32, 1)
         if (mode != kIssueKV && fused) {
           const int64_t off = static_cast<int64_t>(it.kvh) * D;
           uint8_t* kn = qslot + s * C::SLOT_BYTES + C::Q_BYTES;
-          tma_load_1d(kn, new_rows<T>(p, 0, it.b) + off, C::ROW_BYTES, &full[s], pol);
-          tma_load_1d(kn + C::ROW_BYTES, new_rows<T>(p, 1, it.b) + off, C::ROW_BYTES, &full[s],
+          tma_load_1d(kn, new_rows<T>(p, 0, it) + off, C::ROW_BYTES, &full[s], pol);
+          tma_load_1d(kn + C::ROW_BYTES, new_rows<T>(p, 1, it) + off, C::ROW_BYTES, &full[s],
                       pol);
         }
         if (mode != kIssueKV && j == 0)
           tma_load_1d(qslot + s * C::SLOT_BYTES,
-                      q_rows<T>(p, it.b) + static_cast<int64_t>(it.kvh) * G * D,
+                      q_rows<T>(p, it) + static_cast<int64_t>(it.kvh) * G * D,
                       qb, &full[s], pol);
         if (mode == kIssueInputs) return;
         const int32_t r32 = static_cast<int32_t>(row);

@@ -231,13 +231,13 @@ __global__ void __launch_bounds__(8 * 32, 1)
             if (mode != kIssueKV && fused) {
               const int64_t off = static_cast<int64_t>(it.kvh) * D;
               uint8_t* kn = qslot + s * C::SLOT_BYTES + C::Q_BYTES;
-              tma_load_1d(kn, new_rows<T>(p, 0, it.b) + off, C::ROW_BYTES, &full[s], pol);
-              tma_load_1d(kn + C::ROW_BYTES, new_rows<T>(p, 1, it.b) + off, C::ROW_BYTES,
+              tma_load_1d(kn, new_rows<T>(p, 0, it) + off, C::ROW_BYTES, &full[s], pol);
+              tma_load_1d(kn + C::ROW_BYTES, new_rows<T>(p, 1, it) + off, C::ROW_BYTES,
                           &full[s], pol);
             }
             if (mode != kIssueKV && j == 0)
               tma_load_1d(qslot + s * C::SLOT_BYTES,
-                          q_rows<T>(p, it.b) + static_cast<int64_t>(it.kvh) * G * D, qb, &full[s],
+                          q_rows<T>(p, it) + static_cast<int64_t>(it.kvh) * G * D, qb, &full[s],
                           pol);
             if (mode == kIssueInputs) return;
 #pragma unroll
@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(8 * 32, 1)
           *reinterpret_cast<uint4*>(tile + (ch >> 3) * C::BOX_BYTES + r * 128 +
                                     (((ch & 7) ^ (r & 7)) << 4)) = val;
           T* pool = static_cast<T*>(is_v ? p.v_pool_w : p.k_pool_w);
-          *reinterpret_cast<uint4*>(pool + kv_row(p, it.b, it.kvh, it.len - 1) * D + ch * 8) = val;
+          *reinterpret_cast<uint4*>(pool + kv_row(p, it.b, it.kvh, it.len - 1, it.lm) * D + ch * 8) = val;
         }
         fence_proxy_async_smem();
         __syncwarp();

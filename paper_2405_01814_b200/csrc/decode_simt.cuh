@@ -95,13 +95,13 @@ __global__ void __launch_bounds__((NW + 2) * 32, 1)
                                               (fused ? 2 * C::ROW_BYTES : 0));
         uint8_t* slot = qslot + s * C::SLOT_BYTES;
         if (mode != kIssueKV && j == 0) {
-          const T* qsrc = q_rows<T>(p, it.b) + static_cast<int64_t>(it.kvh * p.G + it.qg * GQ) * D;
+          const T* qsrc = q_rows<T>(p, it) + static_cast<int64_t>(it.kvh * p.G + it.qg * GQ) * D;
           tma_load_1d(slot, qsrc, C::Q_BYTES, &full[s], pol);
         }
         if (mode != kIssueKV && fused) {
           const int64_t off = static_cast<int64_t>(it.kvh) * D;
-          tma_load_1d(slot + C::Q_BYTES, new_rows<T>(p, 0, it.b) + off, C::ROW_BYTES, &full[s], pol);
-          tma_load_1d(slot + C::Q_BYTES + C::ROW_BYTES, new_rows<T>(p, 1, it.b) + off,
+          tma_load_1d(slot + C::Q_BYTES, new_rows<T>(p, 0, it) + off, C::ROW_BYTES, &full[s], pol);
+          tma_load_1d(slot + C::Q_BYTES + C::ROW_BYTES, new_rows<T>(p, 1, it) + off,
                       C::ROW_BYTES, &full[s], pol);
         }
         if (mode == kIssueInputs) return;

@@ -16,7 +16,7 @@ import math
 import torch
 
 from . import _lib
-from ._lib import DecodeArgs, check
+from ._lib import DecodeArgs, StepLayout, check
 
 _DT = {torch.float32: _lib.LAM_F32, torch.bfloat16: _lib.LAM_BF16, torch.float16: _lib.LAM_F16}
 _KERNELS = {"auto": _lib.LAM_KERNEL_AUTO, "simt": _lib.LAM_KERNEL_SIMT,
@@ -135,6 +135,59 @@ def decode(q, k_pool, v_pool, seq_lens, *, page_table=None, max_len=None, scale=
     ctx = ctx or _lib.context(q.device.index or 0)
     check(_lib.load().lam_decode(ctx.handle, a, _stream_ptr(stream)))
     return (out, lse) if return_lse else out
+
+
+def step_layout(n_layers: int, n_mb: int, rows_per_mb: int, *, pool_layers: int | None = None,
+                layer0: int = 0, pool_layer_rows: int = 0, lm_q_stride: int = 0,
+                lm_new_stride: int = 0, lm_out_stride: int = 0, flag_mb_stride: int = 0,
+                epoch: int = 0) -> StepLayout:
+    """lam_step_layout: launch lm = layer * n_mb + mb of a step launch (see lamina_attn.h)."""
+    st = StepLayout()
+    st.n_layers, st.n_mb, st.rows_per_mb = n_layers, n_mb, rows_per_mb
+    st.pool_layers = pool_layers if pool_layers is not None else n_layers
+    st.layer0, st.pool_layer_rows = layer0, pool_layer_rows
+    st.lm_q_stride, st.lm_new_stride, st.lm_out_stride = lm_q_stride, lm_new_stride, lm_out_stride
+    st.flag_mb_stride, st.epoch = flag_mb_stride, epoch & 0xFFFFFFFF
+    return st
+
+
+def decode_step(q, k_pools, v_pools, seq_lens, *, n_mb=1, page_table=None, max_len=None,
+                scale=None, out=None, k_new=None, v_new=None, request_order=None, kernel="auto",
+                layer0=0, ctx=None, stream=None, overlap_prev=False):
+    """Every layer (and micro-batch) of a decode step in one persistent launch (lam_decode_step).
+
+    q [L, n_mb * rows, Hq, D] (row stride within a layer allowed), k_pools / v_pools
+    [pool_layers, pages, Hkv, P, D] (layer l uses pool layer (layer0 + l) % pool_layers),
+    k_new / v_new [L, n_mb * rows, Hkv, D] (optional fused append), out [L, n_mb * rows, Hq, D].
+    request_order [n_mb * rows] holds each micro-batch's permutation (indices local to it)."""
+    L, B = q.shape[0], q.shape[1]
+    if B % n_mb:
+        raise _lib.ValidationError("rows must split evenly into micro-batches")
+    if out is None:
+        out = torch.empty((L,) + tuple(q.shape[1:]), dtype=q.dtype, device=q.device)
+    a, _ = make_args(q[0], k_pools[0], v_pools[0], seq_lens, page_table=page_table, max_len=max_len,
+                     scale=scale, out=out[0], kernel=kernel,
+                     k_new=k_new[0] if k_new is not None else None,
+                     v_new=v_new[0] if v_new is not None else None, request_order=None,
+                     overlap_prev=overlap_prev)
+    if request_order is not None:
+        _require_cuda(request_order)
+        if request_order.dtype != torch.int32 or request_order.shape != (B,):
+            raise _lib.ValidationError("request_order must be int32 [B]")
+        a.request_order = request_order.data_ptr()
+    st = step_layout(L, n_mb, B // n_mb, pool_layers=k_pools.shape[0], layer0=layer0,
+                     pool_layer_rows=k_pools[0].numel() // k_pools.shape[-1])
+    # launch lm = layer * n_mb + mb starts rows * stride(1) elements after launch lm - 1, which
+    # needs each layer's rows stored back to back (stride(0) = n_mb * rows * stride(1))
+    rows = B // n_mb
+    for t, name in ((q, "lm_q_stride"), (out, "lm_out_stride")) + (
+            ((k_new, "lm_new_stride"),) if k_new is not None else ()):
+        if n_mb > 1 and t.stride(0) != n_mb * rows * t.stride(1):
+            raise _lib.ValidationError(f"{name}: a layer's rows must be stored back to back")
+        setattr(st, name, t.stride(0) if n_mb == 1 else rows * t.stride(1))
+    ctx = ctx or _lib.context(q.device.index or 0)
+    check(_lib.load().lam_decode_step(ctx.handle, a, st, None, _stream_ptr(stream)))
+    return out
 
 
 def longest_first(seq_lens: torch.Tensor) -> torch.Tensor:
