@@ -119,12 +119,13 @@ class ClockSampler:
                 "reasons": sorted(reasons)}
 
 
-def ncu_traffic(workload: str, world: int):
-    """DRAM bytes per decode launch from the committed ncu capture of this workload's kernel
-    (profiles/ncu_traffic.json), or None when no capture of this launch shape exists."""
+def ncu_traffic(workload: str, world: int, launch: str, kernel: str):
+    """DRAM bytes per decode launch from the committed ncu capture of this workload's launch
+    (profiles/ncu_traffic.json, keyed workload/launch/kernel), or None when no capture of this
+    launch shape exists."""
     p = ROOT / "profiles" / "ncu_traffic.json"
     try:
-        d = json.loads(p.read_text()).get(workload)
+        d = json.loads(p.read_text()).get(f"{workload}/{launch}/{kernel}")
     except Exception:
         return None
     return d["traffic"] if d and world == 1 else None
@@ -312,6 +313,8 @@ class Workload:
         # consecutive steps never find their KV in the 126 MB L2.
         want = max(self.layers, -(-2**30 // layer_bytes))
         self.resident = int(max(1, min(want, budget // layer_bytes)))
+        if os.environ.get("LAM_BENCH_RESIDENT"):  # experiments: fewer distinct pool layers
+            self.resident = min(self.resident, int(os.environ["LAM_BENCH_RESIDENT"]))
         self.kv_bytes_layer = layer_bytes
         self.ctx = _lib.context(device.index)
         if w["paged"]:
@@ -471,6 +474,10 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
         f"kernel={W.kernel} splits={W.splits} chunk={W.chunk}")
 
     stream = torch.cuda.current_stream(device)
+    # one persistent launch per step: for multi-layer paged workloads (one-layer C1 has no layer
+    # boundary to remove)
+    use_step = (args.launch == "step" and not args.separate_append and W.layers > 1
+                and W.page_table is not None)
     engine = None
     if use_engine:
         from paper_2405_01814_b200.dist import HeadShardedAttention
@@ -497,8 +504,19 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
                                      request_order=W.orders[m])
                 return a
 
+            def step_args():  # the step launch: every attention row, pool layer 0
+                kp, vp = W.layer_pools(0)
+                qd = torch.empty((W.B, W.geo.hq_l, W.D), dtype=W.dtype, device=device)
+                a, _ = dec.make_args(qd, kp, vp, W.seq_lens, page_table=W.page_table,
+                                     max_len=W.max_len, out=qd)
+                if W.orders[0] is not None:
+                    W.order_all = torch.cat(W.orders).contiguous()
+                    a.request_order = W.order_all.data_ptr()
+                return a, W.resident, kp.numel() // W.D
+
+            sync = os.environ.get("LAM_PEER_SYNC", "step" if use_step else "kernel")
             engine = PeerShardedAttention(W.geo, dist, W.ctx, launch_args, device, W.dtype,
-                                          sync=os.environ.get("LAM_PEER_SYNC", "kernel"))
+                                          sync=sync, step_args=step_args)
             engine.qkv_in.copy_(W.qkv_in)
             W.qkv_in = engine.qkv_in
             W.out = engine.out
@@ -510,9 +528,19 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
     lib, sp = _lib.load(), stream.cuda_stream
 
     def step_local(ev=None):
-        """world == 1: append + decode per layer on the current stream."""
+        """world == 1: append + decode per layer on the current stream (or all layers in one
+        step launch)."""
         s = counter[0]
         counter[0] += 1
+        if use_step:
+            if ev is not None:
+                ev[0][0].record(stream)
+            dec.decode_step(W.q_in, W.cache.k, W.cache.v, W.seq_lens, page_table=W.page_table, max_len=W.max_len, out=W.out,
+                            k_new=W.kn_in, v_new=W.vn_in, request_order=W.orders[0],
+                            layer0=(s * W.layers) % W.resident, ctx=W.ctx)
+            if ev is not None:
+                ev[0][1].record(stream)
+            return
         for layer in range(W.layers):
             kp, vp = W.layer_pools(layer, s)
             if ev is not None:
@@ -559,9 +587,12 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
     # Self-synchronising peer launches overlap their neighbours (programmatic dependent launch);
     # an event between two launches would serialise them, so the timed region then carries
     # only the step events and a launch's duration is the step time / launches (an upper bound).
-    pdl = engine is not None and args.transport == "peer" and \
-        os.environ.get("LAM_PEER_SYNC", "kernel") == "kernel" and os.environ.get("LAM_PDL", "1") != "0"
+    step_launch = use_step and (engine is None or (args.transport == "peer" and engine.sync == "step"))
+    n_launch = 1 if step_launch else W.layers * W.mb  # decode launches per step and rank
+    pdl = engine is not None and args.transport == "peer" and engine.sync == "kernel" and \
+        os.environ.get("LAM_PDL", "1") != "0"
     pdl = pdl or (engine is None and args.overlap_layers and not args.separate_append)
+    pdl = pdl and not step_launch
     # The timed region carries no per-launch events (an event between two launches adds a gap
     # on the stream: C1's 51 us launches lost 6 %); the decode kernel's own duration is timed by
     # an instrumented pass over the same steps right after (non-PDL modes).
@@ -580,7 +611,9 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
     clocks = sampler.stop() if rank == 0 else None
     ms_total = t0.elapsed_time(t1)
     ms_step = ms_total / max(args.steps, 1)
-    if pdl:
+    if step_launch:  # the launch is the step
+        kern_ms = [ms_step]
+    elif pdl:
         kern_ms = [ms_step / (W.layers * W.mb)]
     else:  # instrumented pass: CUDA events around every decode launch, same steps
         ev = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -596,7 +629,7 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
         ms_step, kern_avg = float(t[0]), float(t[1])
     else:
         kern_avg = statistics.mean(kern_ms)
-    launches = args.steps * W.layers * W.mb * (2 if args.separate_append else 1)
+    launches = args.steps * n_launch * (2 if args.separate_append else 1)
     alone_ms = None
     if pdl:
         # diagnostic: the same step with launches serialised and timed one by one
@@ -655,7 +688,8 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
     peaks = measured_peaks()
     peak = float(peaks.get("hbm_gbs", 6650.0))
     value = W.step_bytes / (ms_step / 1e3) / 1e9
-    achieved = W.decode_bytes_per_launch / (kern_avg / 1e3) / 1e9
+    bytes_per_launch = W.decode_bytes_per_launch * W.layers * W.mb / n_launch
+    achieved = bytes_per_launch / (kern_avg / 1e3) / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
@@ -670,17 +704,21 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
                                    "single GPU" + (", attention-worker engine (2 micro-batches, peer transport)"
                                                    if use_engine else "")),
                    "l2": f"inputs {W.kv_bytes_layer * W.resident / 2**30:.0f} GiB of KV >> 126 MB L2; no flush needed",
-                   "kernel": W.kernel, "splits": W.splits, "split_tokens": W.chunk,
-                   "overlap_layers": bool(args.overlap_layers)},
+                   "kernel": W.kernel, "splits": 1 if step_launch else W.splits,
+                   "split_tokens": W.max_len if step_launch else W.chunk,
+                   "launch": "step" if step_launch else "per layer and micro-batch",
+                   "overlap_layers": bool(args.overlap_layers) and not step_launch},
         "attn_tokens_per_s": W.B / (ms_step / 1e3),
         "frac_of_hbm_roofline": value / world / peak,
         "frac_of_hbm_spec_8tbs": value / world / 8000.0,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650",
-                     "kernel": f"decode_{W.kernel}", "bytes_per_launch": W.decode_bytes_per_launch,
-                     "avg_launch_ms": kern_avg, "traffic": ncu_traffic(args.workload, world),
-                     "launch_timing": ("step time / launches (back-to-back launches overlap under "
+                     "kernel": f"decode_{W.kernel}", "bytes_per_launch": bytes_per_launch,
+                     "avg_launch_ms": kern_avg, "traffic": ncu_traffic(args.workload, world, "step" if step_launch else "layer", W.kernel),
+                     "launch_timing": ("one persistent launch per step (lam_decode_step): the launch "
+                                       "is the step" if step_launch else
+                                       "step time / launches (back-to-back launches overlap under "
                                        "programmatic dependent launch)" if pdl else
                                        "CUDA events around every launch, in an instrumented "
                                        "pass over the same steps right after the timed region"),
@@ -830,6 +868,9 @@ def main():
                     help="lam_kv_append + lam_decode per layer instead of the fused launch")
     ap.add_argument("--scaling", default=None, choices=["strong", "weak"],
                     help="N>1: fixed global batch (strong, the default) or B requests per rank (weak)")
+    ap.add_argument("--launch", default="step", choices=["step", "layer"],
+                    help="one persistent launch per decode step covering every layer and "
+                         "micro-batch (lam_decode_step), or one launch per layer and micro-batch")
     ap.add_argument("--check", type=int, default=1, choices=[0, 1],
                     help="after the timed regions, check the benchmarked launches' outputs against "
                          "the CPU oracle on seeded (request, head) pairs of three layers")

@@ -376,6 +376,35 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
       continue;
     }
     const int i0 = i;  // first stage index of this item
+    // Pool rows of the item's chunks.  The page-table entries are loaded four at a time
+    // (independent loads: one L2 latency per four pages instead of a dependent load per tile),
+    // and a tile's rows are looked up before its stage is acquired, so the lookup overlaps
+    // the wait for a free stage.
+    const int32_t* ptrow =
+        p.page_table ? p.page_table + static_cast<int64_t>(it.b) * p.pt_stride : nullptr;
+    const int64_t blk_rows = static_cast<int64_t>(p.Hkv) * p.page_size;
+    const int64_t head_off =
+        static_cast<int64_t>(it.kvh) * p.page_size +
+        (p.n_lm > 1 ? static_cast<int64_t>((p.layer0 + it.lm / p.n_mb) % p.pool_layers) * p.layer_rows
+                    : 0);
+    int pg_first = -8;
+    int32_t pg0 = 0, pg1 = 0, pg2 = 0, pg3 = 0;
+    auto row_of = [&](int t) -> long long {
+      const int idx = t / p.page_size;
+      int64_t blk = it.b;
+      if (ptrow != nullptr) {
+        if (idx < pg_first || idx >= pg_first + 4) {
+          pg_first = idx;
+          pg0 = __ldg(ptrow + idx);
+          pg1 = idx + 1 < p.pt_stride ? __ldg(ptrow + idx + 1) : 0;
+          pg2 = idx + 2 < p.pt_stride ? __ldg(ptrow + idx + 2) : 0;
+          pg3 = idx + 3 < p.pt_stride ? __ldg(ptrow + idx + 3) : 0;
+        }
+        const int o = idx - pg_first;
+        blk = o == 0 ? pg0 : o == 1 ? pg1 : o == 2 ? pg2 : pg3;
+      }
+      return blk * blk_rows + head_off + t % p.page_size;
+    };
     for (int j = 0; j < it.ntiles; ++j) {
       if (deferring && i >= STAGES) {  // ring full: the inputs must land before any reuse
         inputs_ready();
@@ -383,14 +412,14 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
           issue((i0 + jj) % STAGES, it, jj, &meta_row[(i0 + jj) % META], kIssueInputs);
         deferring = false;
       }
-      const int ms = i % META;
-      const int s = acquire(i++);
       long long rows[NSUB];
 #pragma unroll
       for (int c = 0; c < NSUB; ++c) {
         const int t = it.t_begin + j * TILE + c * (TILE / NSUB);
-        rows[c] = (c == 0 || t < it.t_end) ? kv_row(p, it.b, it.kvh, t, it.lm) : -1;
+        rows[c] = (c == 0 || t < it.t_end) ? row_of(t) : -1;
       }
+      const int ms = i % META;
+      const int s = acquire(i++);
       meta[ms] = make_int4(idx, j, it.len, it.t_end);
       meta_row[ms] = rows[0];
       issue(s, it, j, static_cast<const long long*>(rows), deferring ? kIssueKV : kIssueAll);
@@ -482,7 +511,7 @@ __device__ __forceinline__ int atom_add_acq_rel_gpu(int32_t* p, int v) {
 // but with inputs published ahead a later layer could finish first and must not be announced
 // before the earlier one.
 __device__ __forceinline__ void unit_done(const DecodeParams& p, const Item& it) {
-  if (p.lm_done == nullptr) return;
+  if (p.lm_done == nullptr || p.n_done <= 0) return;  // (nothing to publish)
   __syncwarp();
   if (threadIdx.x % 32 != 0) return;
   __threadfence_system();

@@ -449,7 +449,7 @@ class PeerShardedAttention:
     """
 
     def __init__(self, geo: ShardGeometry, dist, ctx, launch_args: Callable, device: torch.device,
-                 dtype: torch.dtype, sync: str = "kernel"):
+                 dtype: torch.dtype, sync: str = "kernel", step_args: Callable | None = None):
         import ctypes as C
 
         from . import _lib
@@ -534,9 +534,39 @@ class PeerShardedAttention:
         # local flags to wait on: every source's qkv_ready[m][*], every worker's out_ready[m][*]
         self.wait_qkv = [Ptrs(*[fl(j, 0, m, s) for s in range(N)]) for m in range(MB)]
         self.wait_out = [Ptrs(*[fl(j, 1, m, s) for s in range(N)]) for m in range(MB)]
-        if sync not in ("kernel", "stream"):
-            raise ValueError("sync must be 'kernel' or 'stream'")
+        if sync not in ("kernel", "stream", "step"):
+            raise ValueError("sync must be 'kernel', 'stream' or 'step'")
         self.sync = sync
+        if sync == "step":
+            # one persistent lam_decode_step launch per decode step: launch lm = layer * MB + m
+            # of layer 0 / micro-batch 0's addressing, blocks lm * N apart in every model
+            # worker's buffers, flags N apart per micro-batch
+            if step_args is None:
+                raise ValueError("sync='step' needs step_args")
+            a, pool_layers, pool_layer_rows = step_args()
+            a.q_batch_stride = g.W * g.D
+            a.new_batch_stride = g.W * g.D
+            a.lse = None
+            a.overlap_prev = 0
+            io = _lib.PeerIO()
+            io.n_src, io.rows_per_src = N, g.Bh
+            for s in range(N):
+                io.q_src[s] = self.peer[s] + j * qkv_elems_mb * esz
+                io.out_dst[s] = self.peer[s] + self.off_out + j * out_elems_mb * esz
+            io.k_new_offset = g.hq_l * g.D
+            io.v_new_offset = (g.hq_l + g.hkv_l) * g.D
+            io.n_wait = io.n_done = N
+            for i in range(N):
+                io.wait_flags[i] = self.wait_qkv[0][i]
+                io.done_flags[i] = self.sig_out[0][i]
+            from .decode import step_layout
+
+            self.step_a, self.step_io = a, io
+            self.step_st = step_layout(L_ := g.layers, MB, g.B_mb, pool_layers=pool_layers,
+                                       pool_layer_rows=pool_layer_rows,
+                                       lm_q_stride=N * qkv_elems_mb, lm_out_stride=N * out_elems_mb,
+                                       flag_mb_stride=N)
+            del L_
         if sync == "kernel":
             for (layer, m), io in self.io.items():
                 io.n_wait = io.n_done = N
@@ -578,6 +608,13 @@ class PeerShardedAttention:
         if host_out is not None:
             self.d2h.wait_stream(comp)
         ms, cs = model.cuda_stream, comp.cuda_stream
+        if self.sync == "step":  # the whole step in one grid; it waits per (layer, micro-batch)
+            self.step_st.epoch = e0 & 0xFFFFFFFF
+            if ev is not None:
+                ev[0][0].record(comp)
+            _lib.check(lib.lam_decode_step(h, self.step_a, self.step_st, self.step_io, cs))
+            if ev is not None:
+                ev[0][1].record(comp)
         k = 0
         for layer in range(L):
             ep = e0 + layer + 1
@@ -588,7 +625,7 @@ class PeerShardedAttention:
                 if layer > 0:
                     _lib.check(lib.lam_stream_wait(h, self.wait_out[m], N, ep - 1, ms))
                 _lib.check(lib.lam_stream_signal(h, self.sig_qkv[m], N, ep, ms))
-            for m in range(MB):
+            for m in range(MB if self.sync != "step" else 0):
                 io = self.io[layer, m]
                 in_kernel = self.sync == "kernel"
                 if in_kernel:
@@ -604,11 +641,11 @@ class PeerShardedAttention:
                     e[1].record(comp)
                 if not in_kernel:
                     _lib.check(lib.lam_stream_signal(h, self.sig_out[m], N, ep, cs))
-                if host_out is not None:
-                    ds = self.d2h.cuda_stream
-                    _lib.check(lib.lam_stream_wait(h, self.wait_out[m], N, ep, ds))
-                    with torch.cuda.stream(self.d2h):
-                        host_out[layer, m].copy_(self.out[layer, m], non_blocking=True)
+            for m in range(MB if host_out is not None else 0):
+                ds = self.d2h.cuda_stream
+                _lib.check(lib.lam_stream_wait(h, self.wait_out[m], N, ep, ds))
+                with torch.cuda.stream(self.d2h):
+                    host_out[layer, m].copy_(self.out[layer, m], non_blocking=True)
         # the step ends when this rank's outputs of the last layer have all arrived
         for m in range(MB):
             _lib.check(lib.lam_stream_wait(h, self.wait_out[m], N, e0 + L, cs))
