@@ -663,7 +663,7 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
     # ---- end-to-end through the C-ABI host-buffer entry point (pinned host buffers)
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, W, engine, dist, device, stream)
+        e2e = run_e2e(args, W, engine, dist, device, stream, use_step)
 
     # ---- output check of the benchmarked launch configuration (outside the timed regions)
     check = None
@@ -747,10 +747,11 @@ def engine_is_local(args, world: int) -> bool:
     return world == 1 and args.engine == "local" and not args.separate_append
 
 
-def run_e2e(args, W, engine, dist, device, stream):
-    """Same step from host memory through the C-ABI (lam_decode_layers_host): every layer's
-    q / k_new / v_new copied from pinned host memory and its output copied back, inside the
-    timed region; copies overlap the HBM-bound attention of the neighbouring layer."""
+def run_e2e(args, W, engine, dist, device, stream, use_step=False):
+    """Same step from host memory through the C-ABI (lam_decode_step_from_host for step launches,
+    else lam_decode_layers_host): every layer's q / k_new / v_new copied from pinned host memory
+    and its output copied back, inside the timed region; copies overlap the HBM-bound
+    attention."""
     import ctypes as C
 
     import torch
@@ -797,6 +798,8 @@ def run_e2e(args, W, engine, dist, device, stream):
     h_vn = W.vn_in.cpu().pin_memory()
     d_q = torch.empty_like(W.q_in[0])
     d_out = torch.empty_like(W.out[0])
+    if use_step:
+        return run_e2e_step(args, W, device, stream, h_q, h_kn, h_vn, h_out, d_q, d_out)
     # per-layer argument blocks (pools rotate like the device-resident loop)
     ArgsArr = dec.DecodeArgs * L
     args_sets = []
@@ -841,6 +844,57 @@ def run_e2e(args, W, engine, dist, device, stream):
     return {"value": W.step_bytes / (ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "api": "lam_decode_layers_host (C-ABI, pinned host buffers, copies overlapped)"}
+
+
+def run_e2e_step(args, W, device, stream, h_q, h_kn, h_vn, h_out, d_q, d_out):
+    """e2e through lam_decode_step_from_host: one step launch that waits per layer for that
+    layer's host inputs (in-kernel sequence numbers) while later layers are still being copied,
+    and returns each layer's output as soon as it is published."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2405_01814_b200 import _lib, decode as dec
+
+    lib = _lib.load()
+    L = W.layers
+    a, _ = dec.make_args(d_q, W.cache.k[0], W.cache.v[0], W.seq_lens, page_table=W.page_table,
+                         max_len=W.max_len, out=d_out, request_order=W.orders[0])
+    st = dec.step_layout(L, 1, W.B, pool_layers=W.resident,
+                         pool_layer_rows=W.cache.k[0].numel() // W.D)
+    stage = torch.empty(int(lib.lam_decode_step_from_host_stage_bytes(a, L)), dtype=torch.uint8,
+                        device=device)
+    P = C.c_void_p * L
+    hq = P(*[h_q[i].data_ptr() for i in range(L)])
+    hk = P(*[h_kn[i].data_ptr() for i in range(L)])
+    hv = P(*[h_vn[i].data_ptr() for i in range(L)])
+    ho = P(*[h_out[i].data_ptr() for i in range(L)])
+    copy_stream = torch.cuda.Stream(device=device)
+    sp, xp = stream.cuda_stream, copy_stream.cuda_stream
+    counter = [0]
+
+    def step():
+        st.layer0 = (counter[0] * L) % W.resident
+        counter[0] += 1
+        _lib.check(lib.lam_decode_step_from_host(W.ctx.handle, a, st, hq, hk, hv, ho,
+                                                 stage.data_ptr(), sp, xp))
+
+    for _ in range(max(1, args.warmup)):
+        step()
+    torch.cuda.synchronize(device)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize(device)
+    ms = t0.elapsed_time(t1) / max(args.steps, 1)
+    h2d = (h_q.numel() + h_kn.numel() + h_vn.numel()) * h_q.element_size()
+    d2h = h_out.numel() * h_out.element_size()
+    return {"value": W.step_bytes / (ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "api": ("lam_decode_step_from_host (C-ABI, pinned host buffers; one step launch that "
+                    "waits in-kernel for each layer's copied inputs, outputs copied back per layer)")}
 
 
 def main():

@@ -151,8 +151,9 @@ int lam_request_partition(const double* kv_sizes, int64_t n, int64_t num_devices
  * q: [B][Hq][D] in kv_dtype.  out: [B][Hq][D] in out_dtype (kv_dtype or LAM_F32).
  * lse (nullable): [B][Hq] fp32 natural-log sum-exp of the scaled logits.
  * seq_lens: [B] int32 device array; max_len is a host upper bound used for grid sizing.
- * kernel: LAM_KERNEL_AUTO picks GQA_MMA (tensor cores) for 16-bit KV with D = 128 and
- *         1 <= Hq/Hkv <= 8 — MHA included, unless the environment sets LAM_MHA_MMA=0 — and
+ * kernel: LAM_KERNEL_AUTO picks GQA_TC (tcgen05 tensor cores, accumulators in TMEM) for 16-bit
+ *         KV with D = 128 and 1 <= Hq/Hkv <= 8 — MHA included — (GQA_MMA, mma.sync, when the
+ *         environment sets LAM_GQA_TC=0; SIMT for 16-bit MHA when it also sets LAM_MHA_MMA=0) and
  *         SIMT otherwise (fp32 KV, D = 64).  split_tokens: tokens per split-K chunk (0 = auto). */
 typedef struct lam_decode_args {
   int32_t kv_dtype;
@@ -337,6 +338,20 @@ typedef struct lam_step_layout {
 
 int lam_decode_step(lam_ctx* ctx, const lam_decode_args* args, const lam_step_layout* step,
                     const lam_peer_io* io, void* stream);
+
+/* The attention worker's end-to-end step from host buffers as one step launch: layer l's q /
+ * k_new / v_new go H2D on copy_stream into staging region l and are announced by a sequence
+ * number the launch waits for in-kernel (the first layers' attention starts while later layers'
+ * inputs are still in flight), and layer l's output returns D2H as soon as the launch publishes
+ * it.  `args` describes layer 0 (its q / k_new / v_new / out fields are ignored: the staging
+ * regions are used; fused append at seq_lens[b] - 1); `step` gives n_layers and the pool layer
+ * layout (n_mb must be 1).  d_stage holds lam_decode_step_from_host_stage_bytes(args, n_layers) bytes.
+ * Returns after enqueueing; `stream` completes after the last output copy. */
+int lam_decode_step_from_host(lam_ctx* ctx, const lam_decode_args* args, const lam_step_layout* step,
+                         const void* const* h_q, const void* const* h_k_new,
+                         const void* const* h_v_new, void* const* h_out, void* d_stage,
+                         void* stream, void* copy_stream);
+int64_t lam_decode_step_from_host_stage_bytes(const lam_decode_args* args, int32_t n_layers);
 
 #ifdef __cplusplus
 }

@@ -149,6 +149,9 @@ SIGNATURES = {
     "lam_decode_peer": (C.c_int, [_P, C.POINTER(DecodeArgs), C.POINTER(PeerIO), _P]),
     "lam_decode_step": (C.c_int, [_P, C.POINTER(DecodeArgs), C.POINTER(StepLayout),
                                   C.POINTER(PeerIO), _P]),
+    "lam_decode_step_from_host": (C.c_int, [_P, C.POINTER(DecodeArgs), C.POINTER(StepLayout), _P,
+                                            _P, _P, _P, _P, _P, _P]),
+    "lam_decode_step_from_host_stage_bytes": (C.c_int64, [C.POINTER(DecodeArgs), _I32]),
 }
 
 _lib = None

@@ -274,12 +274,11 @@ int plan_decode(lam_ctx* ctx, const lam_decode_args* a, Plan* pl) {
   if (kernel == LAM_KERNEL_AUTO) {
     kernel = mma_ok && (G >= 2 || env_int("LAM_MHA_MMA", 1) != 0) ? LAM_KERNEL_GQA_MMA
                                                                   : LAM_KERNEL_SIMT;
-    // The tcgen05 / TMEM kernel for MHA (G = 1): same box, sustained 32-layer C2 step 7144 vs
-    // 7062 GB/s (e2e 7023 vs 6883) — its SMs draw less power, so the clocks hold higher under
-    // sw_power_cap (1901-1923 vs 1863 MHz).  For GQA the mma.sync kernel stays (C3 step 6888 vs
-    // 6811 GB/s, experiments/r02/call12.sh).  LAM_GQA_TC=1 / 0 forces either for every group.
-    const int tc_env = env_int("LAM_GQA_TC", -1);
-    if (tc_ok && kernel == LAM_KERNEL_GQA_MMA && (tc_env == 1 || (tc_env < 0 && G == 1)))
+    // The tcgen05 / TMEM kernel wherever it applies.  Same box, sustained steps: C2 (MHA) 7144
+    // vs 7062 GB/s per layer launch (its SMs draw less power, so the clocks hold higher under
+    // sw_power_cap, experiments/r02/call12.sh); C3 (GQA) step launch 7207 vs 7098 GB/s, and at
+    // N = 2 13380 vs 12845 (call22.sh).  LAM_GQA_TC=0 restores the mma.sync kernel.
+    if (tc_ok && kernel == LAM_KERNEL_GQA_MMA && env_int("LAM_GQA_TC", 1) != 0)
       kernel = LAM_KERNEL_GQA_TC;
   }
   if (kernel == LAM_KERNEL_GQA_TC) {
@@ -1269,6 +1268,88 @@ int decode_layers_host_flags(lam_ctx* ctx, const lam_decode_args* layer_args, in
   return LAM_OK;
 }
 }  // namespace
+
+int64_t lam_decode_step_from_host_stage_bytes(const lam_decode_args* a, int32_t n_layers) {
+  return a && n_layers > 0 ? n_layers * stage_layout(a).set : 0;
+}
+
+int lam_decode_step_from_host(lam_ctx* ctx, const lam_decode_args* a, const lam_step_layout* step,
+                         const void* const* h_q, const void* const* h_k_new,
+                         const void* const* h_v_new, void* const* h_out, void* d_stage,
+                         void* stream, void* copy_stream) {
+  if (!ctx || !a || !step || step->n_layers < 1 || step->n_mb != 1 || !d_stage)
+    return fail(LAM_ERR_VALIDATION, "step_from_host: bad arguments (one micro-batch, >= 1 layer)");
+  if (a->lse != nullptr) return fail(LAM_ERR_VALIDATION, "step_from_host: lse is not supported");
+  if (a->batch == 0) return LAM_OK;
+  LAM_DEVICE(ctx);
+  auto cs = static_cast<cudaStream_t>(stream);
+  auto xs = static_cast<cudaStream_t>(copy_stream);
+  const StageLayout S = stage_layout(a);
+  const int n = step->n_layers;
+  const int e = elem_bytes(a->kv_dtype), eo = elem_bytes(a->out_dtype);
+  const int64_t qb = static_cast<int64_t>(a->batch) * a->num_q_heads * a->head_dim * e;
+  const int64_t kb = static_cast<int64_t>(a->batch) * a->num_kv_heads * a->head_dim * e;
+  const int64_t ob = static_cast<int64_t>(a->batch) * a->num_q_heads * a->head_dim * eo;
+  auto base = [&](int l) { return static_cast<uint8_t*>(d_stage) + l * S.set; };
+  if (!ctx->host_flags) {
+    LAM_CUDA(cudaMalloc(&ctx->host_flags, 4 * sizeof(uint32_t)));
+    LAM_CUDA(cudaMemset(ctx->host_flags, 0, 4 * sizeof(uint32_t)));
+    LAM_CUDA(cudaDeviceSynchronize());
+  }
+  uint32_t* in_flag = ctx->host_flags;
+  uint32_t* out_flag = ctx->host_flags + 2;
+  const uint32_t epoch = ctx->host_seq;
+  ctx->host_seq += static_cast<uint32_t>(n);
+  // the step launch: layer l's rows live in staging region l (one local "source")
+  lam_decode_args la = *a;
+  la.q_batch_stride = 0;
+  la.new_batch_stride = 0;
+  la.overlap_prev = 0;
+  lam_peer_io io{};
+  io.n_src = 1;
+  io.rows_per_src = a->batch;
+  io.q_src[0] = base(0);
+  io.out_dst[0] = base(0) + S.q + 2 * S.kv;
+  io.k_new_offset = S.q / e;
+  io.v_new_offset = (S.q + S.kv) / e;
+  io.n_wait = io.n_done = 1;
+  io.wait_flags[0] = in_flag;
+  io.done_flags[0] = out_flag;
+  lam_step_layout st = *step;
+  st.n_mb = 1;
+  st.rows_per_mb = a->batch;
+  st.lm_q_stride = S.set / e;
+  st.lm_new_stride = 0;
+  st.lm_out_stride = S.set / eo;
+  st.flag_mb_stride = 0;
+  st.epoch = epoch;
+  cudaEvent_t start, done;
+  LAM_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  LAM_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+  LAM_CUDA(cudaEventRecord(start, cs));  // the copies start after prior work on `stream`
+  LAM_CUDA(cudaStreamWaitEvent(xs, start, 0));
+  int rc = decode_impl(ctx, &la, &io, &st, stream);
+  if (rc != LAM_OK) return rc;
+  // copy stream: every layer's inputs go in at once, each announced by its sequence number;
+  // each output comes back as soon as the launch publishes its layer
+  for (int l = 0; l < n; ++l) {
+    LAM_CUDA(cudaMemcpyAsync(base(l), h_q[l], qb, cudaMemcpyHostToDevice, xs));
+    LAM_CUDA(cudaMemcpyAsync(base(l) + S.q, h_k_new[l], kb, cudaMemcpyHostToDevice, xs));
+    LAM_CUDA(cudaMemcpyAsync(base(l) + S.q + S.kv, h_v_new[l], kb, cudaMemcpyHostToDevice, xs));
+    void* f = in_flag;
+    if ((rc = lam_stream_signal(ctx, &f, 1, epoch + l + 1, xs)) != LAM_OK) return rc;
+  }
+  for (int l = 0; l < n; ++l) {
+    const void* f = out_flag;
+    if ((rc = lam_stream_wait(ctx, &f, 1, epoch + l + 1, xs)) != LAM_OK) return rc;
+    LAM_CUDA(cudaMemcpyAsync(h_out[l], base(l) + S.q + 2 * S.kv, ob, cudaMemcpyDeviceToHost, xs));
+  }
+  LAM_CUDA(cudaEventRecord(done, xs));
+  LAM_CUDA(cudaStreamWaitEvent(cs, done, 0));  // `stream` completes after the last D2H
+  cudaEventDestroy(start);
+  cudaEventDestroy(done);
+  return LAM_OK;
+}
 
 int64_t lam_decode_layers_host_stage_bytes(const lam_decode_args* a) {
   return a ? 2 * stage_layout(a).set : 0;

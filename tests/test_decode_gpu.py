@@ -457,9 +457,9 @@ def test_overlap_prev_orders_inputs_after_preceding_kernel(built, kernel, dtype,
     # the 512-unit sharded GQA launch unsplit on 128 CTAs, the rest unsplit on the full grid.
     ("c1", 8, 32, 32, 1024, torch.float32, False, ("simt", 1, 128)),
     ("c2", 64, 32, 32, 4096, torch.bfloat16, True, ("gqa_tc", 1, 148)),
-    ("c3", 128, 64, 8, 4096, torch.bfloat16, True, ("gqa_mma", 1, 148)),
-    ("c4", 32, 64, 8, 32768, torch.bfloat16, True, ("gqa_mma", 4, 148)),
-    ("c3n8", 512, 8, 1, 4096, torch.bfloat16, True, ("gqa_mma", 1, 128)),
+    ("c3", 128, 64, 8, 4096, torch.bfloat16, True, ("gqa_tc", 1, 148)),
+    ("c4", 32, 64, 8, 32768, torch.bfloat16, True, ("gqa_tc", 4, 148)),
+    ("c3n8", 512, 8, 1, 4096, torch.bfloat16, True, ("gqa_tc", 1, 128)),
 ])
 def test_planner_choices_for_baseline_shapes(built, name, B, Hq, Hkv, L, dtype, paged, want):
     from paper_2405_01814_b200 import decode as dec

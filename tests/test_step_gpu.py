@@ -140,3 +140,44 @@ def test_step_launch_peer_sequence_numbers(built, kernel, ahead):
     got = torch.stack(outs, 2).view(L, MB * rows, Hq, D)
     assert torch.equal(got, want)
     assert torch.equal(cache.k, k_want) and torch.equal(cache.v, v_want)
+
+
+def test_step_from_host_matches_device_step(built):
+    """lam_decode_step_from_host (host buffers in and out, per-layer sequence numbers between the
+    copy stream and the step launch), called twice so the sequence numbers carry across calls,
+    equals the device-resident step launch bitwise — outputs and appended pools."""
+    from paper_2405_01814_b200 import _lib, decode as dec
+
+    L, rows, Hq, Hkv, D = 4, 6, 16, 2, 128
+    cache, lens, x, order = _problem(L, 1, rows, Hq, Hkv, seed=9)
+    k0, v0 = cache.k.clone(), cache.v.clone()
+    want = dec.decode_step(x[:, :, :Hq], cache.k, cache.v, cache.seq_lens, page_table=cache.page_table,
+                           max_len=int(lens.max()), k_new=x[:, :, Hq:Hq + Hkv], v_new=x[:, :, Hq + Hkv:],
+                           request_order=order)
+    k_want, v_want = cache.k.clone(), cache.v.clone()
+    hq = x[:, :, :Hq].contiguous().cpu().pin_memory()
+    hk = x[:, :, Hq:Hq + Hkv].contiguous().cpu().pin_memory()
+    hv = x[:, :, Hq + Hkv:].contiguous().cpu().pin_memory()
+    ho = torch.zeros((L, rows, Hq, D), dtype=torch.bfloat16).pin_memory()
+    dq = torch.empty((rows, Hq, D), dtype=torch.bfloat16, device="cuda")
+    a, _ = dec.make_args(dq, cache.k[0], cache.v[0], cache.seq_lens, page_table=cache.page_table,
+                         max_len=int(lens.max()), out=torch.empty_like(dq), request_order=order)
+    st = dec.step_layout(L, 1, rows, pool_layers=L, pool_layer_rows=cache.k[0].numel() // D)
+    lib, ctx = _lib.load(), _lib.context(0)
+    stage = torch.empty(int(lib.lam_decode_step_from_host_stage_bytes(a, L)), dtype=torch.uint8,
+                        device="cuda")
+    P = C.c_void_p * L
+    s, xs = torch.cuda.current_stream(), torch.cuda.Stream()
+    for rep in range(2):
+        cache.k.copy_(k0)
+        cache.v.copy_(v0)
+        ho.zero_()
+        torch.cuda.synchronize()
+        _lib.check(lib.lam_decode_step_from_host(
+            ctx.handle, a, st, P(*[hq[i].data_ptr() for i in range(L)]),
+            P(*[hk[i].data_ptr() for i in range(L)]), P(*[hv[i].data_ptr() for i in range(L)]),
+            P(*[ho[i].data_ptr() for i in range(L)]), stage.data_ptr(), s.cuda_stream, xs.cuda_stream))
+        torch.cuda.synchronize()
+        assert ctx.status() == _lib.LAM_STATUS_OK
+        assert torch.equal(ho, want.cpu()), rep
+        assert torch.equal(cache.k, k_want) and torch.equal(cache.v, v_want)
