@@ -253,7 +253,7 @@ class Workload:
     per-layer new-token inputs; one GPU's share under KV-head sharding."""
 
     def __init__(self, w: dict, rank: int, world: int, device, engine: bool = False,
-                 strong: bool = False):
+                 strong: bool = False, micro_batches: int = 2):
         import numpy as np
         import torch
 
@@ -273,14 +273,15 @@ class Workload:
 
         try:
             self.B_local = local_batch(w["B"], world, "strong" if strong else "weak",
-                                       2 if (engine or world > 1) else 1)
+                                       micro_batches if (engine or world > 1) else 1)
         except ValueError as e:
             raise SystemExit(str(e))
         self.B = self.B_local * world         # requests whose local heads this rank attends
         self.layers = w["layers"]
-        # the attention-worker engine (always for N > 1): two staggered micro-batches
+        # the attention-worker engine (always for N > 1): staggered micro-batches (two by default,
+        # the paper's schedule)
         engine = engine or world > 1
-        self.mb = 2 if engine else 1
+        self.mb = micro_batches if engine else 1
         self.geo = None
         if engine:
             from paper_2405_01814_b200.dist import ShardGeometry
@@ -464,7 +465,8 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
     if world == 1 and use_engine and args.transport != "peer":  # (NCCL needs N > 1)
         raise SystemExit("--engine peer at one GPU needs --transport peer")
     strong = args.scaling == "strong"
-    W = Workload(w, rank, world, device, engine=use_engine, strong=strong)
+    W = Workload(w, rank, world, device, engine=use_engine, strong=strong,
+                 micro_batches=args.micro_batches)
     if args.overlap_layers is None:
         # consecutive launches of a step are different layers (their pools are disjoint) only
         # when the model has more than one layer; a one-layer stream would have each launch
@@ -922,6 +924,9 @@ def main():
                     help="lam_kv_append + lam_decode per layer instead of the fused launch")
     ap.add_argument("--scaling", default=None, choices=["strong", "weak"],
                     help="N>1: fixed global batch (strong, the default) or B requests per rank (weak)")
+    ap.add_argument("--micro-batches", type=int, default=2,
+                    help="N>1 (and --engine peer): staggered micro-batches of the attention-worker "
+                         "engine (the paper's schedule uses two)")
     ap.add_argument("--launch", default="step", choices=["step", "layer"],
                     help="one persistent launch per decode step covering every layer and "
                          "micro-batch (lam_decode_step), or one launch per layer and micro-batch")

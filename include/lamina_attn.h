@@ -321,7 +321,11 @@ int lam_decode_peer(lam_ctx* ctx, const lam_decode_args* args, const lam_peer_io
  * (uint32 elements) micro-batch mb's; launch lm waits for and publishes epoch + layer + 1 — a CTA
  * waits when it first claims one of lm's items, and lm's flags are published as soon as all its
  * units are stored.  There is no launch boundary between layers: a CTA that runs out of work in
- * one layer goes on with the next.  Splits are not used (S = 1) and args->lse must be NULL. */
+ * one layer goes on with the next, so layers run concurrently — with a fused append, layers of
+ * one step must map to distinct pool layers (else the appended rows of aliased layers race).
+ * The grid is every resident CTA.  split_tokens = 0 picks S = 1 unless io waits for inputs
+ * (n_wait > 0: each launch then depends on the previous layer), in which case a launch is split
+ * until it has two rounds of items on its share of the grid.  args->lse must be NULL. */
 typedef struct lam_step_layout {
   int32_t n_layers;
   int32_t n_mb;

@@ -799,7 +799,7 @@ int decode_impl(lam_ctx* ctx, const lam_decode_args* a_in, const lam_peer_io* io
   lam_decode_args a_step;
   const lam_decode_args* a = a_in;
   int n_lm = 1;
-  if (st != nullptr) {  // plan one launch lm: rows_per_mb requests, no splits
+  if (st != nullptr) {  // plan one launch lm: rows_per_mb requests
     if (st->n_layers < 1 || st->n_mb < 1 || st->rows_per_mb < 1 ||
         static_cast<int64_t>(st->n_mb) * st->rows_per_mb != a_in->batch)
       return fail(LAM_ERR_VALIDATION, "step: need n_layers, n_mb, rows_per_mb >= 1 and batch == "
@@ -811,14 +811,45 @@ int decode_impl(lam_ctx* ctx, const lam_decode_args* a_in, const lam_peer_io* io
       return fail(LAM_ERR_VALIDATION, "step: peer io must describe one micro-batch's rows");
     a_step = *a_in;
     a_step.batch = st->rows_per_mb;
-    a_step.split_tokens = std::max(1, a_in->max_len);  // S = 1
     a = &a_step;
     n_lm = st->n_layers * st->n_mb;
+    if (a_in->split_tokens <= 0) {
+      // Splits: without input dependencies the whole step is one pool of items and S = 1 (fewest
+      // merges).  When every launch lm waits for inputs that follow the previous layer's
+      // outputs, only ~n_mb launches are runnable at a time and a launch's latency is its
+      // longest item: split until a launch has >= 2 rounds of items on its share of the grid
+      // (C4 at N = 2: 64 units of 32 K tokens -> S = 4).
+      a_step.split_tokens = std::max(1, a_in->max_len);
+      Plan p1;
+      int rc1 = plan_decode(ctx, &a_step, &p1);
+      if (rc1 != LAM_OK) return rc1;
+      if (io != nullptr && io->n_wait > 0) {
+        const int64_t units = static_cast<int64_t>(st->rows_per_mb) * a->num_kv_heads * p1.QG;
+        const int occ = p1.kernel == LAM_KERNEL_GQA_TC     ? lam::occupancy_tc(a->kv_dtype)
+                        : p1.kernel == LAM_KERNEL_GQA_MMA ? lam::occupancy_mma(a->kv_dtype, p1.variant)
+                                                           : lam::occupancy_simt(a->kv_dtype, a->head_dim, p1.GQ, p1.variant);
+        const int64_t grid = static_cast<int64_t>(occ) * ctx->num_sms;
+        const int64_t want = 2 * ((grid + st->n_mb - 1) / st->n_mb);
+        const int tiles = std::max(1, (a_in->max_len + p1.tile - 1) / p1.tile);
+        int S = 1;
+        while (units * S < want && S * 2 <= tiles) S *= 2;
+        const int ct = (tiles + S - 1) / S;
+        a_step.split_tokens = ct * p1.tile;
+      }
+    }
   }
   Plan pl;
   int rc = plan_decode(ctx, a, &pl);
   if (rc != LAM_OK) return rc;
   if (a->batch == 0) return LAM_OK;
+  if (st != nullptr) {  // the items of every launch lm share one grid: all resident CTAs
+    const int occ = pl.kernel == LAM_KERNEL_GQA_TC    ? lam::occupancy_tc(a->kv_dtype)
+                    : pl.kernel == LAM_KERNEL_GQA_MMA ? lam::occupancy_mma(a->kv_dtype, pl.variant)
+                                                       : lam::occupancy_simt(a->kv_dtype, a->head_dim, pl.GQ, pl.variant);
+    pl.ctas = std::max(pl.ctas, occ * ctx->num_sms);
+    if (const int force = env_int("LAM_DECODE_CTAS", 0); force > 0)
+      pl.ctas = std::min(force, occ * ctx->num_sms);
+  }
   const int G = a->num_q_heads / a->num_kv_heads;
   const int D = a->head_dim;
   lam::DecodeParams p{};
@@ -945,8 +976,9 @@ int decode_impl(lam_ctx* ctx, const lam_decode_args* a_in, const lam_peer_io* io
   p.scale_log2 = a->scale * 1.4426950408889634f;
   p.out_f32 = a->out_dtype == LAM_F32;
   if (pl.S > 1) {
-    const int64_t rows = static_cast<int64_t>(a->batch) * a->num_q_heads * pl.S;
-    const int64_t cnt = static_cast<int64_t>(a->batch) * a->num_kv_heads * pl.QG;
+    const int64_t all_rows = st != nullptr ? static_cast<int64_t>(st->n_layers) * a_in->batch : a->batch;
+    const int64_t rows = all_rows * a->num_q_heads * pl.S;
+    const int64_t cnt = all_rows * a->num_kv_heads * pl.QG;
     if (rows * D > ctx->ws_acc_cap || rows * 2 > ctx->ws_ml_cap || cnt > ctx->counters_cap) {
       rc = lam_ctx_reserve(ctx, std::max<int64_t>(rows, ctx->ws_ml_cap / 2), D,
                            std::max<int64_t>(cnt, ctx->counters_cap));
@@ -1305,6 +1337,8 @@ int lam_decode_step_from_host(lam_ctx* ctx, const lam_decode_args* a, const lam_
   la.q_batch_stride = 0;
   la.new_batch_stride = 0;
   la.overlap_prev = 0;
+  // layers do not wait for each other's outputs here: one pool of items, no splits
+  if (la.split_tokens <= 0) la.split_tokens = std::max(1, la.max_len);
   lam_peer_io io{};
   io.n_src = 1;
   io.rows_per_src = a->batch;

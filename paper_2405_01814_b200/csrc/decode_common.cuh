@@ -604,11 +604,13 @@ __device__ __forceinline__ void finish_item_warp(const DecodeParams& p, const It
     return;
   }
 
-  // 2. write this split's partial, then count it in.
+  // 2. write this split's partial, then count it in.  (Step launches keep one workspace row
+  //    block per layer: bw = row over every layer.)
+  const int64_t bw = b + (p.n_lm > 1 ? static_cast<int64_t>(it.lm / p.n_mb) * p.B : 0);
 #pragma unroll
   for (int g = 0; g < GQ; ++g) {
     if (g < nvalid) {
-      const int64_t row = (static_cast<int64_t>(b) * p.Hq + qh0 + g) * p.S + it.split;
+      const int64_t row = (bw * p.Hq + qh0 + g) * p.S + it.split;
       float A[DPL];
       merged_acc(g, A);
       st_vec<DPL>(p.ws_acc + row * D + d0, A);
@@ -618,7 +620,7 @@ __device__ __forceinline__ void finish_item_warp(const DecodeParams& p, const It
   }
   release();  // the consumers may refill red_* while this warp counts and merges splits
   __syncwarp();  // every lane's partial stores precede lane 0's release
-  int32_t* counter = p.counters + (static_cast<int64_t>(b) * p.Hkv + it.kvh) * p.QG + it.qg;
+  int32_t* counter = p.counters + (bw * p.Hkv + it.kvh) * p.QG + it.qg;
   int last = 0;
   if (lane == 0) last = (atom_add_acq_rel_gpu(counter, 1) == S_live - 1);
   last = __shfl_sync(0xffffffffu, last, 0);
@@ -633,7 +635,7 @@ __device__ __forceinline__ void finish_item_warp(const DecodeParams& p, const It
     ls[g] = 0.f;
     if (g < nvalid && lane < S_live) {
       const float2 ml = __ldcg(reinterpret_cast<const float2*>(
-          p.ws_ml + ((static_cast<int64_t>(b) * p.Hq + qh0 + g) * p.S + lane) * 2));
+          p.ws_ml + ((bw * p.Hq + qh0 + g) * p.S + lane) * 2));
       ms[g] = ml.x;
       ls[g] = ml.y;
     }
@@ -641,7 +643,7 @@ __device__ __forceinline__ void finish_item_warp(const DecodeParams& p, const It
 #pragma unroll
   for (int g = 0; g < GQ; ++g) {
     if (g >= nvalid) continue;
-    const int64_t row0 = (static_cast<int64_t>(b) * p.Hq + qh0 + g) * p.S;
+    const int64_t row0 = (bw * p.Hq + qh0 + g) * p.S;
     float M = ms[g];
     for (int s0 = 32 + lane; s0 < S_live; s0 += 32) M = fmaxf(M, __ldcg(p.ws_ml + (row0 + s0) * 2));
 #pragma unroll

@@ -153,7 +153,7 @@ def step_layout(n_layers: int, n_mb: int, rows_per_mb: int, *, pool_layers: int 
 
 def decode_step(q, k_pools, v_pools, seq_lens, *, n_mb=1, page_table=None, max_len=None,
                 scale=None, out=None, k_new=None, v_new=None, request_order=None, kernel="auto",
-                layer0=0, ctx=None, stream=None, overlap_prev=False):
+                layer0=0, ctx=None, stream=None, overlap_prev=False, split_tokens=0):
     """Every layer (and micro-batch) of a decode step in one persistent launch (lam_decode_step).
 
     q [L, n_mb * rows, Hq, D] (row stride within a layer allowed), k_pools / v_pools
@@ -166,7 +166,7 @@ def decode_step(q, k_pools, v_pools, seq_lens, *, n_mb=1, page_table=None, max_l
     if out is None:
         out = torch.empty((L,) + tuple(q.shape[1:]), dtype=q.dtype, device=q.device)
     a, _ = make_args(q[0], k_pools[0], v_pools[0], seq_lens, page_table=page_table, max_len=max_len,
-                     scale=scale, out=out[0], kernel=kernel,
+                     scale=scale, out=out[0], kernel=kernel, split_tokens=split_tokens,
                      k_new=k_new[0] if k_new is not None else None,
                      v_new=v_new[0] if v_new is not None else None, request_order=None,
                      overlap_prev=overlap_prev)

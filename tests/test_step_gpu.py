@@ -34,8 +34,8 @@ def _problem(L, MB, rows, Hq, Hkv, D=128, P=64, seed=0, pool_layers=None):
     return cache, lens, x, order
 
 
-def _reference(cache, lens, x, order, L, MB, rows, Hq, Hkv, kernel, layer0=0):
-    """One lam_decode per (layer, micro-batch), S = 1, on cloned pools."""
+def _reference(cache, lens, x, order, L, MB, rows, Hq, Hkv, kernel, layer0=0, split=0):
+    """One lam_decode per (layer, micro-batch), S = 1 (or the given split), on cloned pools."""
     from paper_2405_01814_b200 import decode as dec
 
     k, v = cache.k.clone(), cache.v.clone()
@@ -49,24 +49,26 @@ def _reference(cache, lens, x, order, L, MB, rows, Hq, Hkv, kernel, layer0=0):
                                         page_table=cache.page_table[sl], max_len=int(lens.max()),
                                         k_new=xs[:, Hq:Hq + Hkv], v_new=xs[:, Hq + Hkv:],
                                         request_order=order[sl], kernel=kernel,
-                                        split_tokens=int(lens.max()))
+                                        split_tokens=split or int(lens.max()))
     return out, k, v
 
 
 @pytest.mark.parametrize("kernel,G", [("auto", 8), ("gqa_tc", 8), ("auto", 1), ("gqa_mma", 1),
                                       ("simt", 2)])
-@pytest.mark.parametrize("L,MB,layer0,pool_layers", [(3, 2, 0, None), (4, 1, 2, 3)])
-def test_step_launch_equals_per_layer_launches(built, kernel, G, L, MB, layer0, pool_layers):
+@pytest.mark.parametrize("L,MB,layer0,pool_layers,split", [(3, 2, 0, None, 0), (3, 1, 2, 3, 0),
+                                                           (3, 2, 1, 4, 128)])
+def test_step_launch_equals_per_layer_launches(built, kernel, G, L, MB, layer0, pool_layers, split):
     from paper_2405_01814_b200 import decode as dec
 
     rows, Hkv = 5, 2
     Hq = Hkv * G
     cache, lens, x, order = _problem(L, MB, rows, Hq, Hkv, seed=G + L, pool_layers=pool_layers)
-    want, k_want, v_want = _reference(cache, lens, x, order, L, MB, rows, Hq, Hkv, kernel, layer0)
+    want, k_want, v_want = _reference(cache, lens, x, order, L, MB, rows, Hq, Hkv, kernel, layer0,
+                                      split)
     got = dec.decode_step(x[:, :, :Hq], cache.k, cache.v, cache.seq_lens, n_mb=MB,
                           page_table=cache.page_table, max_len=int(lens.max()),
                           k_new=x[:, :, Hq:Hq + Hkv], v_new=x[:, :, Hq + Hkv:],
-                          request_order=order, kernel=kernel, layer0=layer0)
+                          request_order=order, kernel=kernel, layer0=layer0, split_tokens=split)
     torch.cuda.synchronize()
     assert torch.equal(got, want)
     assert torch.equal(cache.k, k_want) and torch.equal(cache.v, v_want)
