@@ -581,8 +581,13 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
             torch.cuda.synchronize(device)
 
     # ---- warm-up
-    for _ in range(max(args.warmup, 0)):
+    for i in range(max(args.warmup, 0)):
+        tw = time.time()
         step()
+        if os.environ.get("LAM_BENCH_VERBOSE"):
+            torch.cuda.synchronize(device)
+            log(f"[rank {rank}] warm-up step {i}: {1e3 * (time.time() - tw):.1f} ms, "
+                f"status {W.ctx.status(clear=False)}")
     barrier()
 
     # ---- timed region (device-resident inputs)
@@ -726,6 +731,7 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
                                        "pass over the same steps right after the timed region"),
                      "alone_launch_ms": alone_ms},
         "gpu_launches": launches,
+        "device_status": W.ctx.status(clear=False),  # LAM_STATUS_* (0: no bounded wait expired)
         "clocks": clocks,
     }
     if e2e is not None:

@@ -833,6 +833,10 @@ int decode_impl(lam_ctx* ctx, const lam_decode_args* a_in, const lam_peer_io* io
         const int tiles = std::max(1, (a_in->max_len + p1.tile - 1) / p1.tile);
         int S = 1;
         while (units * S < want && S * 2 <= tiles) S *= 2;
+        // and a launch's latency is its longest item: items of at most ~4 K tokens (C5's
+        // 16 K-token requests in a batch of short ones)
+        const int max_tok = env_int("LAM_STEP_ITEM_TOKENS", 4096);
+        while ((a_in->max_len + S - 1) / S > max_tok && S * 2 <= tiles) S *= 2;
         const int ct = (tiles + S - 1) / S;
         a_step.split_tokens = ct * p1.tile;
       }

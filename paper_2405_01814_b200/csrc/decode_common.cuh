@@ -514,8 +514,10 @@ __device__ __forceinline__ void unit_done(const DecodeParams& p, const Item& it)
   if (p.lm_done == nullptr || p.n_done <= 0) return;  // (nothing to publish)
   __syncwarp();
   if (threadIdx.x % 32 != 0) return;
-  __threadfence_system();
-  if (atomicAdd(p.lm_done + it.lm, 1) != p.units_per_lm - 1) return;
+  // this unit's output stores (local or peer) precede its count (release, cumulative over the
+  // warp's stores through the warp barrier); the last unit acquires every count and makes the
+  // outputs visible system-wide before the flags
+  if (atom_add_acq_rel_gpu(p.lm_done + it.lm, 1) != p.units_per_lm - 1) return;
   __threadfence_system();
   const int layer = it.lm / p.n_mb, mb = it.lm % p.n_mb;
   int32_t* published = p.lm_done + p.n_lm + mb;

@@ -397,168 +397,167 @@ __global__ void __launch_bounds__(8 * 32, 1)
   const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
   const float sl2 = p.scale_log2;
   float m[GQ], l[GQ], o[GQ], a_prev[GQ];  // running max (log2 units), sum, output row
-  float m_st[GQ], l_st[GQ];               // the finished item's statistics until its O lands
-  int4 tag{}, tag_st{};                   // {item, len, t_end} of the current / finished item
+  int4 tag{};                             // {item, len, t_end} of the current item
   Item it{};
-  bool prev_real = false, prev_first = false, prev_last = false;
+  bool pending = false, prev_real = false, prev_first = false;  // O(i-1) not folded yet
   int k_item = 0, bpar = 0;
   int nv = 0;  // data-carrying tiles so far (the V ring's counter)
 #pragma unroll
   for (int g = 0; g < GQ; ++g) { m[g] = -INFINITY; l[g] = 0.f; o[g] = 0.f; a_prev[g] = 0.f; }
+  // fold O(j) (tile j's output rows, accumulate = with its rescale factor a) into o
+  auto fold = [&](int j, bool jreal, bool jfirst, const float (&a)[GQ]) {
+    mbar_wait(&obar[j & 1], (j >> 1) & 1);
+    tc_fence_after();
+    if (jreal) {
+      float ot[GQ];
+      tmem_ld8(o_tmem(j & 1) + lane_base, ot);
+#pragma unroll
+      for (int g = 0; g < GQ; ++g) o[g] = jfirst ? ot[g] : fmaf(o[g], a[g], ot[g]);
+    } else {
+#pragma unroll
+      for (int g = 0; g < GQ; ++g) o[g] = 0.f;  // an empty request's zero output
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ofree[j & 1]);
+  };
   for (int i = 0;; ++i) {
     mbar_wait(&sbar[i % NS], (i / NS) & 1);
     tc_fence_after();
     const int4 mt = meta[i % C::META];
-    const bool sentinel = mt.x < 0;
-    bool real = false, first = false, last = false;
+    if (mt.x < 0) {  // end of work (every item was handed over at its last tile)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pbar[i & 1]);  // the O issuer reads the end tag, too
+      break;
+    }
     float a_cur[GQ];
 #pragma unroll
     for (int g = 0; g < GQ; ++g) a_cur[g] = 0.f;
-    if (sentinel || mt.y == 0) {  // an item ends: keep its statistics until its last O lands
+    const bool first = mt.y == 0;
+    if (first) {
+      it = item_from_tag<TILE>(p, mt);
+      tag = make_int4(mt.x, mt.z, mt.w, 0);
 #pragma unroll
-      for (int g = 0; g < GQ; ++g) { m_st[g] = m[g]; l_st[g] = l[g]; m[g] = -INFINITY; l[g] = 0.f; }
-      tag_st = tag;
+      for (int g = 0; g < GQ; ++g) { m[g] = -INFINITY; l[g] = 0.f; }
     }
-    if (!sentinel) {
-      first = mt.y == 0;
-      if (first) {
-        it = item_from_tag<TILE>(p, mt);
-        tag = make_int4(mt.x, mt.z, mt.w, 0);
-      }
-      real = mt.z > 0;
-      last = mt.y == max(it.ntiles, 1) - 1;
-      if (real) {
-        float x[GQ];
-        tmem_ld8(s_tmem(i % NS) + lane_base, x);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sfree[i % NS]);  // the S buffer may take S(i + NS)
-        const int tok = it.t_begin + mt.y * TILE + t;
-        const bool valid = tok < it.t_end;
-#pragma unroll
-        for (int g = 0; g < GQ; ++g) x[g] = valid ? x[g] * sl2 : -INFINITY;
-        // warp max of the 8 columns in 9 shuffles: halve the columns per step, then reduce;
-        // lanes 4g .. 4g+3 end up with column g's max
-        float h4[4], h2[2], h1;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const bool up = lane & 16;
-          const float send = up ? x[j] : x[j + 4];
-          h4[j] = fmaxf(up ? x[j + 4] : x[j], __shfl_xor_sync(0xffffffffu, send, 16));
-        }
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const bool up = lane & 8;
-          const float send = up ? h4[j] : h4[j + 2];
-          h2[j] = fmaxf(up ? h4[j + 2] : h4[j], __shfl_xor_sync(0xffffffffu, send, 8));
-        }
-        {
-          const bool up = lane & 4;
-          const float send = up ? h2[0] : h2[1];
-          h1 = fmaxf(up ? h2[1] : h2[0], __shfl_xor_sync(0xffffffffu, send, 4));
-        }
-        h1 = fmaxf(h1, __shfl_xor_sync(0xffffffffu, h1, 2));
-        h1 = fmaxf(h1, __shfl_xor_sync(0xffffffffu, h1, 1));
-        float* tm = tmax + bpar * 4 * GQ;
-        if ((lane & 3) == 0) tm[warp * GQ + (lane >> 2)] = h1;
-        named_bar_sync(1, 128);
-        bpar ^= 1;
-        uint32_t pw[GQ / 2];
-#pragma unroll
-        for (int g = 0; g < GQ; ++g) {
-          const float mx = fmaxf(fmaxf(tm[g], tm[GQ + g]), fmaxf(tm[2 * GQ + g], tm[3 * GQ + g]));
-          const float mn = fmaxf(m[g], mx);  // finite: the tile has a valid token
-          a_cur[g] = m[g] == -INFINITY ? 0.f : exp2f(m[g] - mn);
-          m[g] = mn;
-        }
-#pragma unroll
-        for (int g = 0; g < GQ; g += 2) {
-          pw[g / 2] = Elem<T>::pack2(exp2f(x[g] - m[g]), exp2f(x[g + 1] - m[g + 1]));
-          float r0, r1;  // the sum uses the rounded weights the MMA sees
-          Elem<T>::unpack2(pw[g / 2], r0, r1);
-          l[g] = l[g] * a_cur[g] + r0;
-          l[g + 1] = l[g + 1] * a_cur[g + 1] + r1;
-        }
-        *reinterpret_cast<uint4*>(pbuf + (i & 1) * C::PBUF_BYTES + t * 16) =
-            make_uint4(pw[0], pw[1], pw[2], pw[3]);
-        // stale rows past the end may hold non-finite values and p = 0 must meet 0: zero them,
-        // once the tile's V half has landed (it is loaded after the previous O MMA read the
-        // slot, so S — and this softmax — can run ahead of it)
-        if (it.t_begin + mt.y * TILE + TILE > it.t_end) mbar_wait(&fullv[nv % VS], (nv / VS) & 1);
-        if (!valid) {
-          uint8_t* vrow = vring + (nv % VS) * C::MAT_BYTES + t * 128;
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            *reinterpret_cast<uint4*>(vrow + c * 16) = make_uint4(0u, 0u, 0u, 0u);
-            *reinterpret_cast<uint4*>(vrow + C::BOX_BYTES + c * 16) = make_uint4(0u, 0u, 0u, 0u);
-          }
-        }
-        fence_proxy_async_smem();
-      }
-      if (real) ++nv;
+    const bool real = mt.z > 0;
+    const bool last = mt.y == max(it.ntiles, 1) - 1;
+    if (real) {
+      float x[GQ];
+      tmem_ld8(s_tmem(i % NS) + lane_base, x);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) {
-        if (!real) mbar_arrive(&sfree[i % NS]);  // (a marker reads no S, but owns the buffer)
-        mbar_arrive(&pbar[i & 1]);
+      if (lane == 0) mbar_arrive(&sfree[i % NS]);  // the S buffer may take S(i + NS)
+      const int tok = it.t_begin + mt.y * TILE + t;
+      const bool valid = tok < it.t_end;
+#pragma unroll
+      for (int g = 0; g < GQ; ++g) x[g] = valid ? x[g] * sl2 : -INFINITY;
+      // warp max of the 8 columns in 9 shuffles: halve the columns per step, then reduce;
+      // lanes 4g .. 4g+3 end up with column g's max
+      float h4[4], h2[2], h1;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const bool up = lane & 16;
+        const float send = up ? x[j] : x[j + 4];
+        h4[j] = fmaxf(up ? x[j + 4] : x[j], __shfl_xor_sync(0xffffffffu, send, 16));
       }
-    } else {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&pbar[i & 1]);  // the O issuer reads the end tag, too
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const bool up = lane & 8;
+        const float send = up ? h4[j] : h4[j + 2];
+        h2[j] = fmaxf(up ? h4[j + 2] : h4[j], __shfl_xor_sync(0xffffffffu, send, 8));
+      }
+      {
+        const bool up = lane & 4;
+        const float send = up ? h2[0] : h2[1];
+        h1 = fmaxf(up ? h2[1] : h2[0], __shfl_xor_sync(0xffffffffu, send, 4));
+      }
+      h1 = fmaxf(h1, __shfl_xor_sync(0xffffffffu, h1, 2));
+      h1 = fmaxf(h1, __shfl_xor_sync(0xffffffffu, h1, 1));
+      float* tm = tmax + bpar * 4 * GQ;
+      if ((lane & 3) == 0) tm[warp * GQ + (lane >> 2)] = h1;
+      named_bar_sync(1, 128);
+      bpar ^= 1;
+      uint32_t pw[GQ / 2];
+#pragma unroll
+      for (int g = 0; g < GQ; ++g) {
+        const float mx = fmaxf(fmaxf(tm[g], tm[GQ + g]), fmaxf(tm[2 * GQ + g], tm[3 * GQ + g]));
+        const float mn = fmaxf(m[g], mx);  // finite: the tile has a valid token
+        a_cur[g] = m[g] == -INFINITY ? 0.f : exp2f(m[g] - mn);
+        m[g] = mn;
+      }
+#pragma unroll
+      for (int g = 0; g < GQ; g += 2) {
+        pw[g / 2] = Elem<T>::pack2(exp2f(x[g] - m[g]), exp2f(x[g + 1] - m[g + 1]));
+        float r0, r1;  // the sum uses the rounded weights the MMA sees
+        Elem<T>::unpack2(pw[g / 2], r0, r1);
+        l[g] = l[g] * a_cur[g] + r0;
+        l[g + 1] = l[g + 1] * a_cur[g + 1] + r1;
+      }
+      *reinterpret_cast<uint4*>(pbuf + (i & 1) * C::PBUF_BYTES + t * 16) =
+          make_uint4(pw[0], pw[1], pw[2], pw[3]);
+      // stale rows past the end may hold non-finite values and p = 0 must meet 0: zero them,
+      // once the tile's V half has landed (it is loaded after the previous O MMA read the
+      // slot, so S — and this softmax — can run ahead of it)
+      if (it.t_begin + mt.y * TILE + TILE > it.t_end) mbar_wait(&fullv[nv % VS], (nv / VS) & 1);
+      if (!valid) {
+        uint8_t* vrow = vring + (nv % VS) * C::MAT_BYTES + t * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          *reinterpret_cast<uint4*>(vrow + c * 16) = make_uint4(0u, 0u, 0u, 0u);
+          *reinterpret_cast<uint4*>(vrow + C::BOX_BYTES + c * 16) = make_uint4(0u, 0u, 0u, 0u);
+        }
+      }
+      fence_proxy_async_smem();
+      ++nv;
     }
-    if (i >= 1) {  // fold O(i-1) into the output rows
-      const int j = i - 1;
-      mbar_wait(&obar[j & 1], (j >> 1) & 1);
-      tc_fence_after();
-      if (prev_real) {
-        float ot[GQ];
-        tmem_ld8(o_tmem(j & 1) + lane_base, ot);
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) {
+      if (!real) mbar_arrive(&sfree[i % NS]);  // (a marker reads no S, but owns the buffer)
+      mbar_arrive(&pbar[i & 1]);
+    }
+    // fold the previous tile's O while this tile's O runs on the tensor core; at an item's last
+    // tile fold its own O right away and hand the item over — never wait for the next item's
+    // tiles (in a step launch the next item may wait for inputs that depend on this item)
+    if (pending) fold(i - 1, prev_real, prev_first, a_prev);
+    pending = !last;
+    if (!last) {
 #pragma unroll
-        for (int g = 0; g < GQ; ++g) o[g] = prev_first ? ot[g] : fmaf(o[g], a_prev[g], ot[g]);
-      } else {
+      for (int g = 0; g < GQ; ++g) a_prev[g] = a_cur[g];
+      prev_real = real;
+      prev_first = first;
+      continue;
+    }
+    fold(i, real, first, a_cur);
+    float ls[GQ];  // hand the finished item to the epilogue warp
 #pragma unroll
-        for (int g = 0; g < GQ; ++g) o[g] = 0.f;  // an empty request's zero output
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&ofree[j & 1]);
-      if (prev_last) {  // hand the finished item to the epilogue warp
-        float ls[GQ];
+    for (int g = 0; g < GQ; ++g) {
+      float v = l[g];
 #pragma unroll
-        for (int g = 0; g < GQ; ++g) {
-          float v = l_st[g];
-#pragma unroll
-          for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-          ls[g] = v;
-        }
-        red_acquire(red, k_item);
-        if (lane == 0) {
-          float4* lw = reinterpret_cast<float4*>(red_lw + warp * GQ);
-          lw[0] = make_float4(ls[0], ls[1], ls[2], ls[3]);
-          lw[1] = make_float4(ls[4], ls[5], ls[6], ls[7]);
-          if (warp == 0) {
-            float4* rm = reinterpret_cast<float4*>(red_m);
-            rm[0] = make_float4(m_st[0], m_st[1], m_st[2], m_st[3]);
-            rm[1] = make_float4(m_st[4], m_st[5], m_st[6], m_st[7]);
-          }
-        }
-#pragma unroll
-        for (int g = 0; g < GQ; ++g) red_acc[g * C::RS + t] = o[g];
-        if (warp == 0 && lane == 0) {
-          red.item[0] = tag_st.x;
-          red.item[1] = tag_st.y;
-          red.item[2] = tag_st.z;
-        }
-        red_commit(red);
-        ++k_item;
+      for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      ls[g] = v;
+    }
+    red_acquire(red, k_item);
+    if (lane == 0) {
+      float4* lw = reinterpret_cast<float4*>(red_lw + warp * GQ);
+      lw[0] = make_float4(ls[0], ls[1], ls[2], ls[3]);
+      lw[1] = make_float4(ls[4], ls[5], ls[6], ls[7]);
+      if (warp == 0) {
+        float4* rm = reinterpret_cast<float4*>(red_m);
+        rm[0] = make_float4(m[0], m[1], m[2], m[3]);
+        rm[1] = make_float4(m[4], m[5], m[6], m[7]);
       }
     }
-    if (sentinel) break;
 #pragma unroll
-    for (int g = 0; g < GQ; ++g) a_prev[g] = real ? a_cur[g] : 0.f;
-    prev_real = real;
-    prev_first = first;
-    prev_last = last;
+    for (int g = 0; g < GQ; ++g) red_acc[g * C::RS + t] = o[g];
+    if (warp == 0 && lane == 0) {
+      red.item[0] = tag.x;
+      red.item[1] = tag.y;
+      red.item[2] = tag.z;
+    }
+    red_commit(red);
+    ++k_item;
   }
   red_acquire(red, k_item);
   if (warp == 0 && lane == 0) red.item[0] = -1;

@@ -498,7 +498,10 @@ class PeerShardedAttention:
         if dist is not None:
             dist.barrier()
         self.compute = torch.cuda.current_stream(device)
-        self.model = torch.cuda.Stream(device=device)   # model-worker side signalling
+        # model-worker side signalling, one stream per micro-batch: a micro-batch waiting for its
+        # previous layer never holds up another micro-batch's signal
+        self.models = [torch.cuda.Stream(device=device) for _ in range(geo.micro_batches)]
+        self.model = self.models[0]
         self.h2d = torch.cuda.Stream(device=device)
         self.d2h = torch.cuda.Stream(device=device)
         self.epoch = 0
@@ -596,7 +599,8 @@ class PeerShardedAttention:
         comp, model = self.compute, self.model
         e0 = self.epoch
         self.epoch += L
-        model.wait_stream(comp)  # the previous step (and any input writes) are complete
+        for ms_ in self.models:
+            ms_.wait_stream(comp)  # the previous step (and any input writes) are complete
         arrived = None
         if host_in is not None:
             self.h2d.wait_stream(comp)
@@ -607,7 +611,7 @@ class PeerShardedAttention:
                     arrived[layer].record(self.h2d)
         if host_out is not None:
             self.d2h.wait_stream(comp)
-        ms, cs = model.cuda_stream, comp.cuda_stream
+        cs = comp.cuda_stream
         if self.sync == "step":  # the whole step in one grid; it waits per (layer, micro-batch)
             self.step_st.epoch = e0 & 0xFFFFFFFF
             if ev is not None:
@@ -618,9 +622,10 @@ class PeerShardedAttention:
         k = 0
         for layer in range(L):
             ep = e0 + layer + 1
-            if arrived is not None:
-                model.wait_event(arrived[layer])
             for m in range(MB):
+                ms = self.models[m].cuda_stream
+                if arrived is not None:
+                    self.models[m].wait_event(arrived[layer])
                 # model worker: layer l's rows need layer l-1's outputs of this micro-batch
                 if layer > 0:
                     _lib.check(lib.lam_stream_wait(h, self.wait_out[m], N, ep - 1, ms))
@@ -649,6 +654,7 @@ class PeerShardedAttention:
         # the step ends when this rank's outputs of the last layer have all arrived
         for m in range(MB):
             _lib.check(lib.lam_stream_wait(h, self.wait_out[m], N, e0 + L, cs))
-        comp.wait_stream(model)
+        for ms_ in self.models:
+            comp.wait_stream(ms_)
         if host_out is not None:
             comp.wait_stream(self.d2h)

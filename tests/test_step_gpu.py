@@ -106,6 +106,7 @@ def test_step_launch_peer_sequence_numbers(built, kernel, ahead):
                          max_len=int(lens.max()), out=qd, kernel=kernel)
     a.q_batch_stride = a.new_batch_stride = W * D
     a.request_order = order.data_ptr()
+    a.split_tokens = int(lens.max())  # S = 1, as the reference (bitwise comparison)
     io = _lib.PeerIO()
     io.n_src, io.rows_per_src = n_src, Bh
     for s in range(n_src):
