@@ -294,6 +294,15 @@ typedef struct lam_peer_io {
   uint32_t done_value;
   const uint32_t* wait_flags[LAM_MAX_PEERS];
   uint32_t* done_flags[LAM_MAX_PEERS];
+  /* Eager q (optional; the reference's prev/new split, attention.cpp:129-139): with
+   * n_wait_kv > 0, wait_flags announce q alone and kv_wait_flags[i] >= kv_wait_value (step
+   * launches: epoch + layer + 1) the new K / V rows.  A CTA then starts attending over the cached
+   * tokens as soon as q is published and waits for the new rows only when it reaches the tile
+   * that holds position seq_len - 1, so the model worker's K/V projection and transfer overlap
+   * the attention over the previous tokens. */
+  int32_t n_wait_kv;
+  uint32_t kv_wait_value;
+  const uint32_t* kv_wait_flags[LAM_MAX_PEERS];
 } lam_peer_io;
 
 /* lam_decode whose q / k_new / v_new / out come from lam_peer_io (args->q, k_new, v_new and out

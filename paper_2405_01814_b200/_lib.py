@@ -84,6 +84,9 @@ class PeerIO(C.Structure):
         ("done_value", C.c_uint32),
         ("wait_flags", C.c_void_p * LAM_MAX_PEERS),
         ("done_flags", C.c_void_p * LAM_MAX_PEERS),
+        ("n_wait_kv", C.c_int32),
+        ("kv_wait_value", C.c_uint32),
+        ("kv_wait_flags", C.c_void_p * LAM_MAX_PEERS),
     ]
 
 

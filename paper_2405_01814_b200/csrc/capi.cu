@@ -955,6 +955,14 @@ int decode_impl(lam_ctx* ctx, const lam_decode_args* a_in, const lam_peer_io* io
     }
     p.n_wait = io->n_wait;
     p.n_done = io->n_done;
+    if (io->n_wait_kv < 0 || io->n_wait_kv > LAM_MAX_PEERS)
+      return fail(LAM_ERR_VALIDATION, "peer io: n_wait_kv out of range");
+    for (int i = 0; i < io->n_wait_kv; ++i) {
+      if (!io->kv_wait_flags[i]) return fail(LAM_ERR_VALIDATION, "peer io: null kv wait flag");
+      p.kv_wait_flag[i] = io->kv_wait_flags[i];
+    }
+    p.n_wait_kv = io->n_wait_kv;
+    p.kv_wait_value = io->kv_wait_value;
     if (st != nullptr && (io->n_wait > 0 || io->n_done > 0) && st->flag_mb_stride < 0)
       return fail(LAM_ERR_VALIDATION, "step: bad flag_mb_stride");
     p.wait_value = io->wait_value;

@@ -85,6 +85,11 @@ struct DecodeParams {
   uint32_t wait_value, done_value;
   const uint32_t* wait_flag[LAM_MAX_PEERS];
   uint32_t* done_flag[LAM_MAX_PEERS];
+  // eager q (optional): wait_flag announces q alone, kv_wait_flag the new K / V rows, awaited
+  // only before the first tile that holds a new token
+  int32_t n_wait_kv;
+  uint32_t kv_wait_value;
+  const uint32_t* kv_wait_flag[LAM_MAX_PEERS];
   // bounded spins (see spin_expired): status word of the context and the timeout (0 = none)
   int32_t* status;
   unsigned long long spin_timeout_ns;
@@ -161,6 +166,25 @@ __device__ __forceinline__ void wait_inputs(const DecodeParams& p, int lm = -1) 
       __nanosleep(200);
       if (spin_expired(p, t0, kStatusInputTimeout)) {
         i = p.n_wait;
+        break;
+      }
+    }
+  }
+  fence_proxy_async_global();
+}
+
+// Eager q: spin until the new K / V rows of launch lm (-1: of this launch) are published.
+__device__ __forceinline__ void wait_new_rows(const DecodeParams& p, int lm) {
+  const unsigned long long t0 = globaltimer_ns();
+  const int mb = lm >= 0 ? lm % p.n_mb : 0;
+  const uint32_t value =
+      lm >= 0 ? p.epoch + static_cast<uint32_t>(lm / p.n_mb) + 1u : p.kv_wait_value;
+  for (int i = 0; i < p.n_wait_kv; ++i) {
+    const uint32_t* f = p.kv_wait_flag[i] + static_cast<int64_t>(mb) * p.flag_mb_stride;
+    while (static_cast<int32_t>(ld_acquire_sys(f) - value) < 0) {
+      __nanosleep(100);
+      if (spin_expired(p, t0, kStatusInputTimeout)) {
+        i = p.n_wait_kv;
         break;
       }
     }
@@ -346,6 +370,7 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
   const bool step = p.n_lm > 1;  // inputs are awaited per launch lm, at its first claim
   if (p.defer_inputs != 2 && !step) wait_inputs(p);
   int waited_lm = -1;
+  int kv_lm = p.n_wait_kv > 0 ? -2 : 0x7fffffff;  // eager q: the last launch whose new rows landed
   int i = 0;
   auto acquire = [&](int k) {
     const int s = k % STAGES;
@@ -417,6 +442,12 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
       for (int c = 0; c < NSUB; ++c) {
         const int t = it.t_begin + j * TILE + c * (TILE / NSUB);
         rows[c] = (c == 0 || t < it.t_end) ? row_of(t) : -1;
+      }
+      // eager q: the tile that holds the new token needs the new K / V rows
+      const int want_lm = step ? it.lm : -1;
+      if (kv_lm != 0x7fffffff && kv_lm < want_lm + 1 && tile_has_new<TILE>(p, it, j)) {
+        wait_new_rows(p, want_lm);
+        kv_lm = want_lm + 1;
       }
       const int ms = i % META;
       const int s = acquire(i++);

@@ -263,3 +263,52 @@ def test_spin_timeout_reports_status_instead_of_trapping(built):
         assert torch.equal(torch.cat(outs, 0), want)
     finally:
         ctx.close()
+
+
+@pytest.mark.parametrize("G", [8, 1])
+def test_eager_q_new_rows_awaited_separately(built, G):
+    """Eager q (lam_peer_io.n_wait_kv): q published alone lets the launch attend over the cached
+    tokens but not finish — it cannot publish its outputs until the new K / V rows are announced;
+    once they are, the result equals the fused launch bitwise."""
+    import time
+
+    from paper_2405_01814_b200 import _lib, decode as dec
+
+    n_src, Bh, Hkv, D = 2, 3, 2, 128
+    Hq = Hkv * G
+    cache, lens, qkv, s = _setup(n_src=n_src, Bh=Bh, Hq=Hq, Hkv=Hkv, D=D, seed=31 + G)
+    W = s["W"]
+    want, k_want, v_want = _reference(cache, lens, qkv, s)
+    outs = [torch.zeros((Bh, Hq, D), dtype=torch.bfloat16, device="cuda") for _ in range(n_src)]
+    flags = torch.zeros(3 * n_src, dtype=torch.int32, device="cuda")  # q ready | kv ready | done
+    qd = torch.empty((n_src * Bh, Hq, D), dtype=torch.bfloat16, device="cuda")
+    a, _ = dec.make_args(qd, cache.k[0], cache.v[0], cache.seq_lens, page_table=cache.page_table,
+                         max_len=int(lens.max()), out=qd)
+    a.q_batch_stride = a.new_batch_stride = W * D
+    io = _peer_io(n_src, Bh, Hq, Hkv, D, qkv, outs)
+    fp = flags.data_ptr()
+    io.n_wait = io.n_done = io.n_wait_kv = n_src
+    io.wait_value = io.done_value = io.kv_wait_value = 5
+    for i in range(n_src):
+        io.wait_flags[i] = fp + 4 * i
+        io.kv_wait_flags[i] = fp + 4 * (n_src + i)
+        io.done_flags[i] = fp + 4 * (2 * n_src + i)
+    lib, ctx = _lib.load(), _lib.context(0)
+    side = torch.cuda.Stream()  # (created before the launch occupies the GPU)
+    P = C.c_void_p * n_src
+    torch.cuda.synchronize()
+    _lib.check(lib.lam_decode_peer(ctx.handle, a, io, torch.cuda.current_stream().cuda_stream))
+    _lib.check(lib.lam_stream_signal(ctx.handle, P(*[fp + 4 * i for i in range(n_src)]), n_src, 5,
+                                     side.cuda_stream))
+    side.synchronize()
+    time.sleep(0.05)
+    with torch.cuda.stream(side):  # (the launch's own stream is still busy)
+        done = flags[2 * n_src:].cpu().tolist()
+    assert done == [0] * n_src  # q alone does not finish the launch
+    _lib.check(lib.lam_stream_signal(ctx.handle, P(*[fp + 4 * (n_src + i) for i in range(n_src)]),
+                                     n_src, 5, side.cuda_stream))
+    torch.cuda.synchronize()
+    assert ctx.status() == _lib.LAM_STATUS_OK
+    assert flags[2 * n_src:].tolist() == [5] * n_src
+    assert torch.equal(torch.cat(outs, 0), want)
+    assert torch.equal(cache.k[0], k_want) and torch.equal(cache.v[0], v_want)
