@@ -79,3 +79,25 @@ def comm_volume(spec: LlmSpec, batch: int) -> float:
 LLAMA_7B_1L_F32 = LlmSpec("llama-7b-1layer-fp32", 4096, 1, 1, 4, 32)
 LLAMA2_7B = LlmSpec("llama-2-7b", 4096, 32, 1, 2, 32)
 LLAMA2_70B = LlmSpec("llama-2-70b", 8192, 80, 8, 2, 64)
+
+
+def max_batch(pool_mem_bytes: float, reserved_weight_bytes: float, spec: LlmSpec, seq_len: int,
+              headroom_frac: float = 0.05) -> int:
+    """Requests of seq_len tokens whose KV fits a memory pool (perf.cpp:130-140):
+    floor((pool - weights - headroom * pool) / (kv_bytes_per_token * seq_len))."""
+    import math
+
+    if seq_len < 1:
+        raise ValueError("seq_len must be >= 1")
+    if not 0 <= headroom_frac < 1:
+        raise ValueError("headroom_frac must be in [0,1)")
+    free = pool_mem_bytes - reserved_weight_bytes - headroom_frac * pool_mem_bytes
+    if free <= 0:
+        raise RuntimeError("model weights plus headroom exceed pool memory")
+    return int(math.floor(free / (kv_bytes_per_token(spec) * seq_len)))
+
+
+# B200 attention-worker memory as the planner sees it (DeviceSpec.mem_bytes, model.hpp:64-74):
+# 180 GB of HBM3e per GPU; the paged pool the bench allocates is what remains after the
+# framework's own buffers (bench.py keeps 6 GiB free).
+B200_MEM_BYTES = 180e9
