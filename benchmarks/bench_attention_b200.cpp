@@ -8,9 +8,18 @@
 //     BASELINE.json shapes, timed with CUDA events on the launching stream, L2-proof (>= 1 GiB
 //     of rotating KV), reported as attn_cost KV GB/s (perf.cpp:77-88).
 //
+//   BM_MultiHeadAttention/C1: BASELINE config 1 (LLaMA-7B, 32 heads, d = 128, l = 1024, fp32),
+//     eight requests, multi_head_attention<float> per request through the reference API.
+//
+// The same source compiled with -DLAM_BENCH_REFERENCE against the reference's own
+// attention.cpp (oracle/Makefile target _ref/bench_attention_ref) times the reference CPU code on
+// the same cases, so the two binaries print comparable lines.
+//
 // google-benchmark is absent in this image (the reference skips its benchmarks then,
 // proj/CMakeLists.txt:23-30), so timing is a plain best-of-N loop printing one line per case.
+#ifndef LAM_BENCH_REFERENCE
 #include <cuda_runtime.h>
+#endif
 
 #include <algorithm>
 #include <chrono>
@@ -22,7 +31,12 @@
 #include <vector>
 
 #include "disagg/attention.hpp"
+#ifndef LAM_BENCH_REFERENCE
 #include "lamina_attn.h"
+#define LAM_WHO "drop-in, host round trip"
+#else
+#define LAM_WHO "reference CPU, 1 thread"
+#endif
 
 using namespace disagg;
 
@@ -58,6 +72,25 @@ double best_seconds(int reps, F f) {
   return best;
 }
 
+MultiHeadInstance<float> make_mh(std::int64_t hq, std::int64_t hkv, std::int64_t d_head,
+                                 std::int64_t l, std::uint64_t seed) {
+  std::mt19937_64 rng(seed);
+  auto uniform = [&] { return float(double(rng() >> 11) * 0x1p-53 * 2 - 1); };
+  MultiHeadInstance<float> mh;
+  mh.scale = 1.0f / std::sqrt(float(d_head));
+  mh.queries.assign(size_t(hq), std::vector<float>(size_t(d_head)));
+  for (auto& row : mh.queries)
+    for (auto& x : row) x = uniform();
+  mh.kv_keys.assign(size_t(hkv), std::vector<std::vector<float>>(size_t(l), std::vector<float>(size_t(d_head))));
+  mh.kv_values = mh.kv_keys;
+  for (auto* kv : {&mh.kv_keys, &mh.kv_values})
+    for (auto& head : *kv)
+      for (auto& row : head)
+        for (auto& x : row) x = uniform();
+  return mh;
+}
+
+#ifndef LAM_BENCH_REFERENCE
 #define CK(x)                                                                      \
   do {                                                                             \
     cudaError_t e_ = (x);                                                          \
@@ -136,7 +169,9 @@ void bench_decode(lam_ctx* ctx, const char* name, int B, int Hq, int Hkv, int L)
   int32_t kernel = 0, splits = 0, chunk = 0;
   lam_decode_plan(ctx, &a, &kernel, &splits, &chunk);
   std::printf("BM_Decode/%-28s %10.1f us  %8.1f GB/s  kernel=%s splits=%d\n", name, per * 1e6,
-              kv_bytes / per / 1e9, kernel == LAM_KERNEL_GQA_MMA ? "gqa_mma" : "simt", splits);
+              kv_bytes / per / 1e9,
+              kernel == LAM_KERNEL_GQA_TC ? "gqa_tc" : kernel == LAM_KERNEL_GQA_MMA ? "gqa_mma" : "simt",
+              splits);
   for (int i = 0; i < nbuf; ++i) {
     cudaFree(kp[i]);
     cudaFree(vp[i]);
@@ -147,6 +182,7 @@ void bench_decode(lam_ctx* ctx, const char* name, int B, int Hq, int Hkv, int L)
   cudaFree(d_out);
   cudaStreamDestroy(s);
 }
+#endif  // LAM_BENCH_REFERENCE
 
 }  // namespace
 
@@ -157,8 +193,8 @@ int main() {
     volatile double sink = 0;
     exact_attention(inst);  // warm
     const double t = best_seconds(20, [&] { sink = exact_attention(inst)[0]; });
-    std::printf("BM_ExactAttention/%d/%-6d %10.1f us  %8.2f Mitems/s (drop-in, host round trip)\n",
-                d, l, t * 1e6, l / t / 1e6);
+    std::printf("BM_ExactAttention/%d/%-6d %10.1f us  %8.2f Mitems/s (" LAM_WHO ")\n", d, l,
+                t * 1e6, l / t / 1e6);
   }
   for (int l : {256, 4096}) {
     const auto inst = make_instance(128, l);
@@ -167,9 +203,22 @@ int main() {
       auto [prev, fresh] = split_prev_new(inst, l - 1);
       sink = finalize(merge(prev, fresh))[0];
     });
-    std::printf("BM_SplitMerge/%-14d %10.1f us  %8.2f Mitems/s (drop-in, host round trip)\n", l,
-                t * 1e6, l / t / 1e6);
+    std::printf("BM_SplitMerge/%-14d %10.1f us  %8.2f Mitems/s (" LAM_WHO ")\n", l, t * 1e6,
+                l / t / 1e6);
   }
+  {  // BASELINE config 1 through the reference API: 8 requests x multi_head_attention<float>
+    std::vector<MultiHeadInstance<float>> reqs;
+    for (int b = 0; b < 8; ++b) reqs.push_back(make_mh(32, 32, 128, 1024, 100 + b));
+    volatile float sink = 0;
+    for (const auto& r : reqs) sink = multi_head_attention(r)[0][0];  // warm
+    const double t = best_seconds(5, [&] {
+      for (const auto& r : reqs) sink = multi_head_attention(r)[0][0];
+    });
+    const double kv_bytes = 2.0 * 4 * 128 * 32 * 1024.0 * 8;  // attn_cost bytes, e = 4
+    std::printf("BM_MultiHeadAttention/C1          %10.1f us  %8.2f GB/s KV (" LAM_WHO ")\n",
+                t * 1e6, kv_bytes / t / 1e9);
+  }
+#ifndef LAM_BENCH_REFERENCE
   // ---- device-timed decode, BASELINE.json shapes (one layer) ----
   lam_ctx* ctx = nullptr;
   if (lam_ctx_create(0, &ctx) != LAM_OK) {
@@ -180,5 +229,6 @@ int main() {
   bench_decode(ctx, "c3_llama2_70b_B128_l4096", 128, 64, 8, 4096);
   bench_decode(ctx, "c4_llama2_70b_B32_l32768", 32, 64, 8, 32768);
   lam_ctx_destroy(ctx);
+#endif
   return 0;
 }

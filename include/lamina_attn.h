@@ -132,6 +132,12 @@ int lam_merge_host(int dtype, int64_t n, int32_t d, const void* a_acc, const voi
 int lam_finalize_host(int dtype, int64_t n, int32_t d, const void* acc, const void* log_denom,
                       const int64_t* count, void* out);
 
+/* Per-thread pinned host staging buffer `slot` (0..3) of at least `bytes` bytes, for callers of
+ * the *_host entry points that marshal nested rows anyway (the C++ drop-in): rows written there
+ * cross PCIe as pinned memory.  Valid until the next call with the same slot on this thread;
+ * NULL on failure (lam_last_error). */
+void* lam_host_buffer(int32_t slot, int64_t bytes);
+
 /* ---- work partitioning (host logic, attention.cpp:164-203) ---------------- */
 
 /* ranges[2*i], ranges[2*i+1] = [begin, end) of device i.  LAM_ERR_VALIDATION with a

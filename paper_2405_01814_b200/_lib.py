@@ -131,6 +131,7 @@ SIGNATURES = {
     "lam_merge_host": (C.c_int, [C.c_int, _I64, _I32] + [_P] * 12),
     "lam_finalize_host": (C.c_int, [C.c_int, _I64, _I32, _P, _P, _P, _P]),
     "lam_head_partition": (C.c_int, [_I64, _I64, _P]),
+    "lam_host_buffer": (C.c_void_p, [_I32, _I64]),
     "lam_request_partition": (C.c_int, [_P, _I64, _I64, _P, _P, _P]),
     "lam_decode": (C.c_int, [_P, C.POINTER(DecodeArgs), _P]),
     "lam_decode_plan": (C.c_int, [_P, C.POINTER(DecodeArgs), _P, _P, _P]),

@@ -375,6 +375,17 @@ struct HostStage {
   }
 };
 
+// per-thread pinned host buffers (lam_host_buffer)
+struct PinnedSlots {
+  void* ptr[4] = {};
+  int64_t cap[4] = {};
+  ~PinnedSlots() {
+    for (void* p : ptr)
+      if (p) cudaFreeHost(p);
+  }
+};
+thread_local PinnedSlots g_pinned;
+
 // one staging area (and context) per device and thread: a thread that moves between devices
 // stages and launches on the device that is current at each call
 HostStage& host_stage() {
@@ -435,6 +446,28 @@ extern "C" {
 int lam_version(void) { return 1; }
 
 const char* lam_last_error(void) { return g_last_error.c_str(); }
+
+void* lam_host_buffer(int32_t slot, int64_t bytes) {
+  if (slot < 0 || slot >= 4 || bytes < 0) {
+    fail(LAM_ERR_VALIDATION, "lam_host_buffer: slot must be 0..3 and bytes >= 0");
+    return nullptr;
+  }
+  if (bytes > g_pinned.cap[slot]) {
+    if (g_pinned.ptr[slot]) cudaFreeHost(g_pinned.ptr[slot]);
+    g_pinned.ptr[slot] = nullptr;
+    g_pinned.cap[slot] = 0;
+    const int64_t want = std::max<int64_t>(bytes + bytes / 4, 1 << 20);  // grow with slack
+    void* p = nullptr;
+    const cudaError_t e = cudaHostAlloc(&p, static_cast<size_t>(want), cudaHostAllocPortable);
+    if (e != cudaSuccess) {
+      cuda_fail(e, "cudaHostAlloc");
+      return nullptr;
+    }
+    g_pinned.ptr[slot] = p;
+    g_pinned.cap[slot] = want;
+  }
+  return g_pinned.ptr[slot];
+}
 
 int lam_ctx_create(int device, lam_ctx** out) {
   if (!out) return fail(LAM_ERR_VALIDATION, "null output pointer");

@@ -109,22 +109,31 @@ __global__ void __launch_bounds__(kThreads) instance_kernel(const InstArgs a) {
     return;
   }
 
-  // pass 1: logits (sequential dot over d, as attention.cpp:16-21) and their max
+  // pass 1: logits and their max — a warp per token row, lanes over d (coalesced row reads),
+  // the dot (attention.cpp:16-21) summed per lane and reduced with xor shuffles
   T mx = neg_inf<T>();
-  for (int64_t k = threadIdx.x; k < n; k += kThreads) {
-    const int64_t j = ix ? ix[k] : k;
-    if (j < 0 || j >= len) {
-      atomicMax(a.err, 2);
-      lg[k] = neg_inf<T>();
-      continue;
+  {
+    const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
+    for (int64_t k = warp; k < n; k += kThreads / 32) {
+      const int64_t j = ix ? ix[k] : k;
+      if (j < 0 || j >= len) {
+        if (lane == 0) {
+          atomicMax(a.err, 2);
+          lg[k] = neg_inf<T>();
+        }
+        continue;
+      }
+      const T* kr = K + j * d;
+      T s = T(0);
+      for (int e = lane; e < d; e += 32) s += q[e] * kr[e];
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      const T x = s * scale;
+      if (lane == 0) lg[k] = x;
+      mx = x > mx ? x : mx;
     }
-    const T* kr = K + j * d;
-    T s = T(0);
-    for (int e = 0; e < d; ++e) s += q[e] * kr[e];
-    const T x = s * scale;
-    lg[k] = x;
-    mx = x > mx ? x : mx;
   }
+  __syncthreads();  // every logit stored before pass 2 reads them by another thread mapping
   mx = block_reduce<T>(mx, scratch, true);
 
   // pass 2: weights and their sum

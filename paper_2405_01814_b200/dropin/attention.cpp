@@ -11,8 +11,10 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <type_traits>
 
 #include "lamina_attn.h"
@@ -40,13 +42,39 @@ constexpr int dtype_of() {
   return std::is_same_v<T, double> ? LAM_F64 : LAM_F32;
 }
 
-// Contiguous [rows][d] copy of a vector-of-rows block; every row must have d entries.
+// Contiguous [rows][d] copy of vector-of-rows blocks (every row must have d entries) into
+// library-owned pinned host memory (lam_host_buffer slot), so the rows cross
+// PCIe at pinned speed; large blocks are copied by several threads.
 template <typename T>
-void append_rows(const std::vector<std::vector<T>>& rows, std::size_t d, std::vector<T>& dst) {
-  for (const auto& r : rows) {
-    require(r.size() == d, "key/value rows must match head dim");
-    dst.insert(dst.end(), r.begin(), r.end());
+T* pinned_rows(int slot, const std::vector<const std::vector<std::vector<T>>*>& blocks,
+               std::size_t d) {
+  std::size_t rows = 0;
+  for (const auto* b : blocks) {
+    for (const auto& r : *b) require(r.size() == d, "key/value rows must match head dim");
+    rows += b->size();
   }
+  T* dst = static_cast<T*>(lam_host_buffer(slot, static_cast<int64_t>(rows * d * sizeof(T))));
+  if (!dst) check(LAM_ERR_CUDA);
+  std::vector<std::pair<const std::vector<T>*, T*>> jobs;
+  jobs.reserve(rows);
+  T* at = dst;
+  for (const auto* b : blocks)
+    for (const auto& r : *b) {
+      jobs.emplace_back(&r, at);
+      at += d;
+    }
+  const std::size_t bytes = rows * d * sizeof(T);
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const std::size_t nt = bytes < (std::size_t{4} << 20) ? 1 : std::min<std::size_t>(hw, 16);
+  auto work = [&](std::size_t t) {
+    for (std::size_t i = t; i < jobs.size(); i += nt)
+      std::memcpy(jobs[i].second, jobs[i].first->data(), d * sizeof(T));
+  };
+  std::vector<std::thread> pool;
+  for (std::size_t t = 1; t < nt; ++t) pool.emplace_back(work, t);
+  work(0);
+  for (auto& th : pool) th.join();
+  return dst;
 }
 
 }  // namespace
@@ -79,15 +107,12 @@ std::vector<T> exact_attention(const AttnInstance<T>& inst) {
   const std::size_t d = inst.query.size();
   require(d > 0, "query must be non-empty");
   require(inst.values.size() == inst.keys.size(), "keys and values must have equal row counts");
-  std::vector<T> k, v;
-  k.reserve(inst.keys.size() * d);
-  v.reserve(inst.keys.size() * d);
-  append_rows(inst.keys, d, k);
-  append_rows(inst.values, d, v);
+  const T* k = pinned_rows<T>(0, {&inst.keys}, d);
+  const T* v = pinned_rows<T>(1, {&inst.values}, d);
   const std::int64_t row0 = 0, len = inst.length();
   std::vector<T> out(d);
   check(lam_exact_attention_host(dtype_of<T>(), 1, static_cast<int32_t>(d), inst.query.data(),
-                                 len, k.data(), v.data(), &row0, &len, &inst.scale, out.data()));
+                                 len, k, v, &row0, &len, &inst.scale, out.data()));
   return out;
 }
 
@@ -100,9 +125,8 @@ std::vector<PartialAttention<T>> partials_of(const AttnInstance<T>& inst,
   const std::size_t d = inst.query.size();
   require(d > 0, "query must be non-empty");
   require(inst.values.size() == inst.keys.size(), "keys and values must have equal row counts");
-  std::vector<T> k, v;
-  append_rows(inst.keys, d, k);
-  append_rows(inst.values, d, v);
+  const T* k = pinned_rows<T>(0, {&inst.keys}, d);
+  const T* v = pinned_rows<T>(1, {&inst.values}, d);
   const std::size_t n = sets.size();
   std::vector<T> q, scale(n, inst.scale);
   std::vector<std::int64_t> row0(n, 0), len(n, inst.length()), idx, off{0};
@@ -114,7 +138,7 @@ std::vector<PartialAttention<T>> partials_of(const AttnInstance<T>& inst,
   std::vector<T> acc(n * d), mx(n), ld(n);
   std::vector<std::int64_t> cnt(n);
   check(lam_partial_attention_host(dtype_of<T>(), static_cast<int64_t>(n), static_cast<int32_t>(d),
-                                   q.data(), inst.length(), k.data(), v.data(), row0.data(),
+                                   q.data(), inst.length(), k, v, row0.data(),
                                    len.data(), idx.data(), off.data(), scale.data(), acc.data(),
                                    mx.data(), ld.data(), cnt.data()));
   std::vector<PartialAttention<T>> out(n);
@@ -200,9 +224,9 @@ std::vector<std::vector<T>> multi_head_attention(const MultiHeadInstance<T>& ins
   require(inst.kv_values.size() == inst.kv_keys.size(), "need one value block per KV head");
   // KV rows are laid out once per KV head; q head h points at block h / group, so the GQA
   // mapping costs no copies (the reference deep-copies per head, attention.cpp:145-147).
-  std::vector<T> k, v;
   std::vector<std::int64_t> block_row0(static_cast<std::size_t>(hkv)),
       block_len(static_cast<std::size_t>(hkv));
+  std::vector<const std::vector<std::vector<T>>*> kblocks, vblocks;
   std::int64_t rows = 0;
   for (std::int64_t h = 0; h < hkv; ++h) {
     const auto& kb = inst.kv_keys[static_cast<std::size_t>(h)];
@@ -211,10 +235,12 @@ std::vector<std::vector<T>> multi_head_attention(const MultiHeadInstance<T>& ins
     block_row0[static_cast<std::size_t>(h)] = rows;
     block_len[static_cast<std::size_t>(h)] = static_cast<std::int64_t>(kb.size());
     if (kb.empty()) throw Error("exact_attention requires a non-empty key set");
-    append_rows(kb, d, k);
-    append_rows(vb, d, v);
+    kblocks.push_back(&kb);
+    vblocks.push_back(&vb);
     rows += static_cast<std::int64_t>(kb.size());
   }
+  const T* k = pinned_rows<T>(0, kblocks, d);
+  const T* v = pinned_rows<T>(1, vblocks, d);
   const std::int64_t group = hq / hkv;
   std::vector<T> q, scale(static_cast<std::size_t>(hq), inst.scale);
   std::vector<std::int64_t> row0(static_cast<std::size_t>(hq)), len(static_cast<std::size_t>(hq));
@@ -227,8 +253,7 @@ std::vector<std::vector<T>> multi_head_attention(const MultiHeadInstance<T>& ins
   }
   std::vector<T> flat(static_cast<std::size_t>(hq) * d);
   check(lam_exact_attention_host(dtype_of<T>(), hq, static_cast<int32_t>(d), q.data(), rows,
-                                 k.data(), v.data(), row0.data(), len.data(), scale.data(),
-                                 flat.data()));
+                                 k, v, row0.data(), len.data(), scale.data(), flat.data()));
   out.reserve(static_cast<std::size_t>(hq));
   for (std::int64_t h = 0; h < hq; ++h)
     out.emplace_back(flat.begin() + static_cast<std::ptrdiff_t>(h * d),

@@ -19,5 +19,6 @@ def test_cpp_bench_runs(built):
     for case in ("BM_ExactAttention/64/256", "BM_ExactAttention/128/8192", "BM_SplitMerge/4096",
                  "BM_Decode/c2_llama2_7b_B64_l4096", "BM_Decode/c3_llama2_70b_B128_l4096"):
         assert case in r.stdout, r.stdout
-    gbs = [float(m) for m in re.findall(r"([0-9.]+) GB/s", r.stdout)]
-    assert gbs and min(gbs) > 1000.0, r.stdout  # device-resident decode streams at TB/s
+    gbs = [float(m) for m in re.findall(r"BM_Decode/\S+\s+[0-9.]+ us\s+([0-9.]+) GB/s", r.stdout)]
+    assert len(gbs) == 3 and min(gbs) > 1000.0, r.stdout  # device-resident decode streams at TB/s
+    assert "BM_MultiHeadAttention/C1" in r.stdout
