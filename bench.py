@@ -518,7 +518,8 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
 
             sync = os.environ.get("LAM_PEER_SYNC", "step" if use_step else "kernel")
             engine = PeerShardedAttention(W.geo, dist, W.ctx, launch_args, device, W.dtype,
-                                          sync=sync, step_args=step_args)
+                                          sync=sync, step_args=step_args,
+                                          relay=args.relay if sync == "step" else "stream")
             engine.qkv_in.copy_(W.qkv_in)
             W.qkv_in = engine.qkv_in
             W.out = engine.out
@@ -667,6 +668,12 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
         torch.cuda.synchronize(device)
         alone_ms = e0.elapsed_time(e1) / reps
 
+    tdir = os.environ.get("LAM_STEP_TRACE")  # diagnostic: the last timed step's stamps
+    if tdir and getattr(engine, "trace_buf", None) is not None:
+        torch.cuda.synchronize(device)
+        os.makedirs(tdir, exist_ok=True)
+        np.save(os.path.join(tdir, f"rank{rank}.npy"), engine.trace_buf.cpu().numpy())
+
     # ---- end-to-end through the C-ABI host-buffer entry point (pinned host buffers)
     e2e = None
     if not args.no_e2e:
@@ -711,10 +718,19 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
                                    "single GPU" + (", attention-worker engine (2 micro-batches, peer transport)"
                                                    if use_engine else "")),
                    "l2": f"inputs {W.kv_bytes_layer * W.resident / 2**30:.0f} GiB of KV >> 126 MB L2; no flush needed",
-                   "kernel": W.kernel, "splits": 1 if step_launch else W.splits,
-                   "split_tokens": W.max_len if step_launch else W.chunk,
+                   "kernel": W.kernel,
+                   "splits": ("lam_decode_step's choice (S = 1 without input waits, else until a "
+                              "launch has >= 2 rounds of items)") if step_launch else W.splits,
+                   "split_tokens": None if step_launch else W.chunk,
                    "launch": "step" if step_launch else "per layer and micro-batch",
-                   "overlap_layers": bool(args.overlap_layers) and not step_launch},
+                   "micro_batches": W.mb,
+                   "overlap_layers": bool(args.overlap_layers) and not step_launch,
+                   **({"model_worker": ("zero-compute stand-in: layer l+1 inputs follow layer l "
+                                        "outputs of all ranks, relayed "
+                                        + ("inside the step launch (lam_peer_io.n_relay)"
+                                           if getattr(engine, "relay", "") == "kernel" and use_step
+                                           else "by stream memory operations"))}
+                      if world > 1 and args.transport == "peer" else {})},
         "attn_tokens_per_s": W.B / (ms_step / 1e3),
         "frac_of_hbm_roofline": value / world / peak,
         "frac_of_hbm_spec_8tbs": value / world / 8000.0,
@@ -936,6 +952,9 @@ def main():
     ap.add_argument("--launch", default="step", choices=["step", "layer"],
                     help="one persistent launch per decode step covering every layer and "
                          "micro-batch (lam_decode_step), or one launch per layer and micro-batch")
+    ap.add_argument("--relay", default="stream", choices=["stream", "kernel"],
+                    help="N > 1: the zero-compute model worker's layer-to-layer relay: stream "
+                         "operations per micro-batch, or forwarded inside the step launch")
     ap.add_argument("--check", type=int, default=1, choices=[0, 1],
                     help="after the timed regions, check the benchmarked launches' outputs against "
                          "the CPU oracle on seeded (request, head) pairs of three layers")
@@ -945,7 +964,10 @@ def main():
     if args.gpus != world and world == 1 and args.gpus > 1:
         log(f"--gpus {args.gpus} requested without torchrun: running one rank")
         args.gpus = 1
-    w = WORKLOADS[args.workload]
+    w = dict(WORKLOADS[args.workload])
+    if os.environ.get("LAM_BENCH_SEQ"):  # diagnostic: shorter contexts (relay latency probes)
+        w["l"] = int(os.environ["LAM_BENCH_SEQ"])
+        w["desc"] += f" [LAM_BENCH_SEQ={w['l']}: diagnostic, not the workload]"
     if args.scaling is None:  # (at N = 1 both mean the same workload)
         args.scaling = "strong"
     if args.impl == "reference":

@@ -309,6 +309,15 @@ typedef struct lam_peer_io {
   int32_t n_wait_kv;
   uint32_t kv_wait_value;
   const uint32_t* kv_wait_flags[LAM_MAX_PEERS];
+  /* Forwarding model worker (optional, step launches only): a model worker whose layer l + 1
+   * inputs need nothing but layer l's outputs (a zero-compute stand-in, as in bench.py's
+   * strong-scaling runs) is relayed by the launch itself.  A CTA waiting for launch
+   * lm = (layer l >= 1, mb) stores epoch + l + 1 to relay_flag (+ mb * flag_mb_stride) once
+   * every relay_wait_flags[i] (+ mb * flag_mb_stride, i < n_relay) >= epoch + l.  Layer 0's
+   * flag is the caller's.  n_relay = 0 disables it. */
+  int32_t n_relay;
+  uint32_t* relay_flag;
+  const uint32_t* relay_wait_flags[LAM_MAX_PEERS];
 } lam_peer_io;
 
 /* lam_decode whose q / k_new / v_new / out come from lam_peer_io (args->q, k_new, v_new and out
@@ -353,6 +362,12 @@ typedef struct lam_step_layout {
   int64_t lm_new_stride;
   int64_t lm_out_stride;
   uint32_t epoch;
+  /* optional diagnostic (NULL: off): 4 * n_layers * n_mb globaltimer stamps (ns), launch
+   * lm = layer * n_mb + mb at [4 lm ..]: first wait for its inputs, inputs seen, last unit
+   * done, flags published; then per CTA (the first 1024) 400 records of its work-item claims:
+   * claim time, inputs seen, item index (3 words each; 4 n_lm + 1228800 words in all).  The
+   * caller fills it with 0xFF bytes before the launch. */
+  uint64_t* trace;
 } lam_step_layout;
 
 int lam_decode_step(lam_ctx* ctx, const lam_decode_args* args, const lam_step_layout* step,

@@ -87,6 +87,9 @@ class PeerIO(C.Structure):
         ("n_wait_kv", C.c_int32),
         ("kv_wait_value", C.c_uint32),
         ("kv_wait_flags", C.c_void_p * LAM_MAX_PEERS),
+        ("n_relay", C.c_int32),
+        ("relay_flag", C.c_void_p),
+        ("relay_wait_flags", C.c_void_p * LAM_MAX_PEERS),
     ]
 
 
@@ -105,6 +108,7 @@ class StepLayout(C.Structure):
         ("lm_new_stride", C.c_int64),
         ("lm_out_stride", C.c_int64),
         ("epoch", C.c_uint32),
+        ("trace", C.c_void_p),
     ]
 
 

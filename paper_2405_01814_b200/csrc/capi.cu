@@ -933,6 +933,7 @@ int decode_impl(lam_ctx* ctx, const lam_decode_args* a_in, const lam_peer_io* io
     p.lm_out_stride = st->lm_out_stride;
     p.flag_mb_stride = st->flag_mb_stride;
     p.epoch = st->epoch;
+    p.trace = reinterpret_cast<unsigned long long*>(st->trace);
   }
   const int slot = static_cast<int>(ctx->seq % kSlots);
   p.slot = ctx->slots + 2 * slot;
@@ -996,6 +997,16 @@ int decode_impl(lam_ctx* ctx, const lam_decode_args* a_in, const lam_peer_io* io
     }
     p.n_wait_kv = io->n_wait_kv;
     p.kv_wait_value = io->kv_wait_value;
+    if (io->n_relay < 0 || io->n_relay > LAM_MAX_PEERS || (io->n_relay > 0 && st == nullptr))
+      return fail(LAM_ERR_VALIDATION, "peer io: n_relay out of range (step launches only)");
+    if (io->n_relay > 0 && io->relay_flag == nullptr)
+      return fail(LAM_ERR_VALIDATION, "peer io: null relay flag");
+    for (int i = 0; i < io->n_relay; ++i) {
+      if (!io->relay_wait_flags[i]) return fail(LAM_ERR_VALIDATION, "peer io: null relay wait flag");
+      p.relay_wait_flag[i] = io->relay_wait_flags[i];
+    }
+    p.n_relay = io->n_relay;
+    p.relay_flag = io->relay_flag;
     if (st != nullptr && (io->n_wait > 0 || io->n_done > 0) && st->flag_mb_stride < 0)
       return fail(LAM_ERR_VALIDATION, "step: bad flag_mb_stride");
     p.wait_value = io->wait_value;
@@ -1161,7 +1172,8 @@ int lam_stream_signal(lam_ctx* ctx, void* const* addrs, int32_t n, uint32_t valu
   if (!fn) return fail(LAM_ERR_CUDA, "cuStreamWriteValue32 unavailable");
   for (int32_t i = 0; i < n; ++i) {
     // default flags: a system-scope memory barrier orders the stream's prior writes (the
-    // decode kernel's peer stores) before the sequence number
+    // decode kernel's peer stores) before the sequence number (B200 rejects
+    // CU_STREAM_WRITE_VALUE_NO_MEMORY_BARRIER with CUDA_ERROR_INVALID_VALUE)
     const CUresult r = fn(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(addrs[i]),
                           value, CU_STREAM_WRITE_VALUE_DEFAULT);
     if (r != CUDA_SUCCESS)

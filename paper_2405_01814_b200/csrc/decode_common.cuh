@@ -90,6 +90,10 @@ struct DecodeParams {
   int32_t n_wait_kv;
   uint32_t kv_wait_value;
   const uint32_t* kv_wait_flag[LAM_MAX_PEERS];
+  // forwarding model worker (lam_peer_io::n_relay, step launches)
+  int32_t n_relay;
+  uint32_t* relay_flag;
+  const uint32_t* relay_wait_flag[LAM_MAX_PEERS];
   // bounded spins (see spin_expired): status word of the context and the timeout (0 = none)
   int32_t* status;
   unsigned long long spin_timeout_ns;
@@ -107,6 +111,7 @@ struct DecodeParams {
   int32_t flag_mb_stride;
   uint32_t epoch;
   int32_t* lm_done;
+  unsigned long long* trace;  // lam_step_layout::trace (diagnostic stamps) or null
 };
 
 // lam_ctx_status codes (include/lamina_attn.h)
@@ -154,21 +159,47 @@ __device__ __forceinline__ void acquire_slot(const DecodeParams& p) {
   }
 }
 
+// lam_step_layout::trace: after the 4 * n_lm launch stamps, kTraceRecords claim records of
+// 3 words per CTA for the first kTraceCtas CTAs
+constexpr int kTraceCtas = 1024;
+constexpr int kTraceRecords = 400;
+
 // Spin until the inputs of this launch (of launch lm of a step launch) are published.
 __device__ __forceinline__ void wait_inputs(const DecodeParams& p, int lm = -1) {
   if (p.n_wait <= 0) return;
   const unsigned long long t0 = globaltimer_ns();
   const int mb = lm >= 0 ? lm % p.n_mb : 0;
   const uint32_t value = lm >= 0 ? p.epoch + static_cast<uint32_t>(lm / p.n_mb) + 1u : p.wait_value;
+  const int64_t moff = static_cast<int64_t>(mb) * p.flag_mb_stride;
+  // forwarding model worker: this rank's inputs of layer l follow once every attention worker
+  // published layer l - 1 of the micro-batch (idempotent: any waiting CTA may forward)
+  bool relay = p.n_relay > 0 && lm >= p.n_mb;
   for (int i = 0; i < p.n_wait; ++i) {
-    const uint32_t* f = p.wait_flag[i] + static_cast<int64_t>(mb) * p.flag_mb_stride;
+    const uint32_t* f = p.wait_flag[i] + moff;
     while (static_cast<int32_t>(ld_acquire_sys(f) - value) < 0) {
+      if (relay) {
+        bool ready = static_cast<int32_t>(ld_acquire_sys(p.relay_flag + moff) - value) >= 0;
+        if (!ready) {
+          ready = true;
+          for (int r = 0; r < p.n_relay && ready; ++r)
+            ready = static_cast<int32_t>(ld_acquire_sys(p.relay_wait_flag[r] + moff) - (value - 1u)) >= 0;
+          if (ready) st_release_sys(p.relay_flag + moff, value);
+        }
+        if (ready) {
+          relay = false;
+          continue;
+        }
+      }
       __nanosleep(200);
       if (spin_expired(p, t0, kStatusInputTimeout)) {
         i = p.n_wait;
         break;
       }
     }
+  }
+  if (p.trace != nullptr && lm >= 0) {
+    atomicMin(p.trace + 4 * lm, t0);
+    atomicMin(p.trace + 4 * lm + 1, globaltimer_ns());
   }
   fence_proxy_async_global();
 }
@@ -203,8 +234,8 @@ __device__ __forceinline__ void finish_cta(const DecodeParams& p) {
     __threadfence();
   const unsigned long long old = atomicAdd(p.slot + 1, 1ull);
   if (p.n_done <= 0 || p.n_lm > 1 || old - p.done_base != gridDim.x - 1) return;
-  __threadfence_system();
-  for (int i = 0; i < p.n_done; ++i) st_release_sys(p.done_flag[i], p.done_value);
+  fence_acq_rel_sys();
+  for (int i = 0; i < p.n_done; ++i) st_relaxed_sys(p.done_flag[i], p.done_value);
 }
 
 // Physical row of token t of (request b, kv head h) of launch lm in a pool viewed as [rows][D].
@@ -378,14 +409,28 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
     return s;
   };
   bool deferring = p.defer_inputs != 0;  // first item: KV now, inputs after griddep_wait
+  // diagnostic claim records (lam_step_layout::trace): [claim time, inputs seen, item index]
+  unsigned long long* rec = p.trace != nullptr && blockIdx.x < kTraceCtas
+                                ? p.trace + 4 * p.n_lm + 3ull * kTraceRecords * blockIdx.x
+                                : nullptr;
+  int n_rec = 0;
+  // (Claiming the next item ahead, ~512 tokens before the boundary, at once or one dependent
+  // access per issued tile, measured 3-4% slower on B200: round 2, calls 50 and 53.)
   for (;;) {
+    const unsigned long long t_claim = rec != nullptr ? globaltimer_ns() : 0ull;
     const long long claim = static_cast<long long>(atomicAdd(p.slot, 1ull) - p.item_base);
     if (claim >= p.n_items) break;
+    const Item it = make_item(p, static_cast<int>(claim), TILE);
     const int idx = static_cast<int>(claim);
-    const Item it = make_item(p, idx, TILE);
     if (step && it.lm != waited_lm) {  // (claims arrive in launch order: lm only grows)
       wait_inputs(p, it.lm);
       waited_lm = it.lm;
+    }
+    if (rec != nullptr && n_rec < kTraceRecords) {
+      rec[3 * n_rec] = t_claim;
+      rec[3 * n_rec + 1] = globaltimer_ns();
+      rec[3 * n_rec + 2] = static_cast<unsigned long long>(idx);
+      ++n_rec;
     }
     if (it.ntiles == 0) {
       if (deferring) {  // nothing to prefetch
@@ -549,7 +594,7 @@ __device__ __forceinline__ void unit_done(const DecodeParams& p, const Item& it)
   // warp's stores through the warp barrier); the last unit acquires every count and makes the
   // outputs visible system-wide before the flags
   if (atom_add_acq_rel_gpu(p.lm_done + it.lm, 1) != p.units_per_lm - 1) return;
-  __threadfence_system();
+  if (p.trace != nullptr) p.trace[4 * it.lm + 2] = globaltimer_ns();
   const int layer = it.lm / p.n_mb, mb = it.lm % p.n_mb;
   int32_t* published = p.lm_done + p.n_lm + mb;
   const unsigned long long t0 = globaltimer_ns();
@@ -559,8 +604,10 @@ __device__ __forceinline__ void unit_done(const DecodeParams& p, const Item& it)
   }
   const uint32_t value = p.epoch + static_cast<uint32_t>(layer) + 1u;
   const int64_t off = static_cast<int64_t>(mb) * p.flag_mb_stride;
-  for (int i = 0; i < p.n_done; ++i) st_release_sys(p.done_flag[i] + off, value);
+  fence_acq_rel_sys();  // every unit's outputs (acquired through the counts) before the flags
+  for (int i = 0; i < p.n_done; ++i) st_relaxed_sys(p.done_flag[i] + off, value);
   st_release_gpu_s32(published, layer + 1);
+  if (p.trace != nullptr) p.trace[4 * it.lm + 3] = globaltimer_ns();
 }
 
 // Split-K epilogue of one work item, run by the CTA's dedicated epilogue warp while the

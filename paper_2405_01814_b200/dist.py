@@ -27,6 +27,7 @@ lam_decode); the CPU gloo test passes the oracle.
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 from typing import Callable
 
@@ -446,10 +447,18 @@ class PeerShardedAttention:
     polls before its first load) and publishes out_ready (the last CTA to finish, after a
     system-scope fence), so the compute stream carries nothing but back-to-back decode
     launches.  sync="stream": the same sequence numbers as stream operations around each launch.
+    sync="step": one lam_decode_step per decode step (every layer and micro-batch).
+
+    The model worker here is a zero-compute stand-in: layer l + 1's qkv_ready follows layer l's
+    out_ready from every attention worker.  relay="stream": stream operations on one model stream
+    per micro-batch (cuStreamWaitValue32 / cuStreamWriteValue32; ~15-20 us from the outputs'
+    publication to the next layer's inputs on B200).  relay="kernel" (sync="step" only, device
+    inputs): the step launch forwards it itself (lam_peer_io::n_relay, a few us).
     """
 
     def __init__(self, geo: ShardGeometry, dist, ctx, launch_args: Callable, device: torch.device,
-                 dtype: torch.dtype, sync: str = "kernel", step_args: Callable | None = None):
+                 dtype: torch.dtype, sync: str = "kernel", step_args: Callable | None = None,
+                 relay: str = "stream"):
         import ctypes as C
 
         from . import _lib
@@ -531,15 +540,29 @@ class PeerShardedAttention:
                 io.v_new_offset = (g.hq_l + g.hkv_l) * g.D
                 self.args[layer, m], self.io[layer, m] = a, io
         fl = lambda r, kind, m, i: self.peer[r] + self.off_flags + ((kind * MB + m) * N + i) * 4  # noqa: E731
-        # qkv_ready[m][rank] on every attention worker / out_ready[m][rank] on every model worker
-        self.sig_qkv = [Ptrs(*[fl(r, 0, m, j) for r in range(N)]) for m in range(MB)]
-        self.sig_out = [Ptrs(*[fl(r, 1, m, j) for r in range(N)]) for m in range(MB)]
-        # local flags to wait on: every source's qkv_ready[m][*], every worker's out_ready[m][*]
-        self.wait_qkv = [Ptrs(*[fl(j, 0, m, s) for s in range(N)]) for m in range(MB)]
-        self.wait_out = [Ptrs(*[fl(j, 1, m, s) for s in range(N)]) for m in range(MB)]
         if sync not in ("kernel", "stream", "step"):
             raise ValueError("sync must be 'kernel', 'stream' or 'step'")
+        # out_ready[m][rank] on every model worker; every worker's out_ready[m][*] is waited on
+        self.sig_out = [Ptrs(*[fl(r, 1, m, j) for r in range(N)]) for m in range(MB)]
+        self.wait_out = [Ptrs(*[fl(j, 1, m, s) for s in range(N)]) for m in range(MB)]
+        if sync == "stream":
+            # qkv_ready[m][rank] written into every attention worker (the compute stream's wait
+            # polls local memory)
+            self.sig_qkv = [Ptrs(*[fl(r, 0, m, j) for r in range(N)]) for m in range(MB)]
+            self.wait_qkv = [Ptrs(*[fl(j, 0, m, s) for s in range(N)]) for m in range(MB)]
+            self.n_sig_qkv = N
+        else:
+            # the model worker writes ONE local qkv_ready[m][rank] (each stream write costs a
+            # system memory barrier, ~3 us on B200) and the kernels poll the sources' flags over
+            # NVLink
+            self.sig_qkv = [Ptrs(fl(j, 0, m, j)) for m in range(MB)]
+            self.wait_qkv = [Ptrs(*[fl(s, 0, m, s) for s in range(N)]) for m in range(MB)]
+            self.n_sig_qkv = 1
         self.sync = sync
+        if relay not in ("stream", "kernel") or (relay == "kernel" and sync != "step"):
+            raise ValueError("relay must be 'stream' or 'kernel' (the latter with sync='step')")
+        self.relay = relay
+        self.ahead = os.environ.get("LAM_PEER_AHEAD", "0") == "1"
         if sync == "step":
             # one persistent lam_decode_step launch per decode step: launch lm = layer * MB + m
             # of layer 0 / micro-batch 0's addressing, blocks lm * N apart in every model
@@ -562,6 +585,10 @@ class PeerShardedAttention:
             for i in range(N):
                 io.wait_flags[i] = self.wait_qkv[0][i]
                 io.done_flags[i] = self.sig_out[0][i]
+            if relay == "kernel":  # this rank's qkv_ready follows its out_ready[*] in-kernel
+                io.relay_flag = self.sig_qkv[0][0]
+                for i in range(N):
+                    io.relay_wait_flags[i] = self.wait_out[0][i]
             from .decode import step_layout
 
             self.step_a, self.step_io = a, io
@@ -570,6 +597,12 @@ class PeerShardedAttention:
                                        lm_q_stride=N * qkv_elems_mb, lm_out_stride=N * out_elems_mb,
                                        flag_mb_stride=N)
             del L_
+            # LAM_STEP_TRACE (diagnostic): per-launch globaltimer stamps of the latest step
+            self.trace_buf = None
+            if os.environ.get("LAM_STEP_TRACE"):
+                self.trace_buf = torch.empty(4 * g.layers * MB + 3 * 400 * 1024, dtype=torch.int64,
+                                             device=device)
+                self.step_st.trace = self.trace_buf.data_ptr()
         if sync == "kernel":
             for (layer, m), io in self.io.items():
                 io.n_wait = io.n_done = N
@@ -614,6 +647,13 @@ class PeerShardedAttention:
         cs = comp.cuda_stream
         if self.sync == "step":  # the whole step in one grid; it waits per (layer, micro-batch)
             self.step_st.epoch = e0 & 0xFFFFFFFF
+            # in-kernel forwarding unless the inputs arrive from the host (their copies order
+            # the model streams' signals)
+            kernel_relay = self.relay == "kernel" and host_in is None
+            self.step_io.n_relay = N if kernel_relay else 0
+            if self.trace_buf is not None:
+                with torch.cuda.stream(comp):
+                    self.trace_buf.fill_(-1)
             if ev is not None:
                 ev[0][0].record(comp)
             _lib.check(lib.lam_decode_step(h, self.step_a, self.step_st, self.step_io, cs))
@@ -622,14 +662,15 @@ class PeerShardedAttention:
         k = 0
         for layer in range(L):
             ep = e0 + layer + 1
-            for m in range(MB):
+            for m in range(MB if layer == 0 or not (self.sync == "step" and kernel_relay) else 0):
                 ms = self.models[m].cuda_stream
                 if arrived is not None:
                     self.models[m].wait_event(arrived[layer])
                 # model worker: layer l's rows need layer l-1's outputs of this micro-batch
-                if layer > 0:
+                # (LAM_PEER_AHEAD=1, a diagnostic: publish every layer at once, no dependency)
+                if layer > 0 and not self.ahead:
                     _lib.check(lib.lam_stream_wait(h, self.wait_out[m], N, ep - 1, ms))
-                _lib.check(lib.lam_stream_signal(h, self.sig_qkv[m], N, ep, ms))
+                _lib.check(lib.lam_stream_signal(h, self.sig_qkv[m], self.n_sig_qkv, ep, ms))
             for m in range(MB if self.sync != "step" else 0):
                 io = self.io[layer, m]
                 in_kernel = self.sync == "kernel"

@@ -166,8 +166,17 @@ def main():
                                  out=qd)
             return a
 
+        def step_args():  # sync="step": every row of every micro-batch, pool layer 0
+            qd = torch.empty((geo.B_attn, geo.hq_l, D), dtype=torch.bfloat16, device=dev)
+            a, _ = dec.make_args(qd, cache.k[0], cache.v[0], cache.seq_lens,
+                                 page_table=cache.page_table, max_len=int(row_lens.max()), out=qd)
+            return a, L, cache.k[0].numel() // D
+
+        sync = os.environ.get("LAM_TEST_SYNC", "kernel")
+        relay = "kernel" if sync == "step-relay" else "stream"
+        sync = "step" if sync == "step-relay" else sync
         eng = PeerShardedAttention(geo, dist, ctx, launch_args, dev, torch.bfloat16,
-                                   sync=os.environ.get("LAM_TEST_SYNC", "kernel"))
+                                   sync=sync, step_args=step_args, relay=relay)
         eng.qkv_in.copy_(qkv_in)
         eng.out.zero_()
         host_io = os.environ.get("LAM_TEST_HOST", "0") == "1"

@@ -14,7 +14,9 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("transport,fused,host,sync", [
     ("nccl", "1", "0", "-"), ("nccl", "0", "0", "-"), ("peer", "1", "0", "kernel"),
-    ("peer", "1", "1", "kernel"), ("peer", "1", "0", "stream"), ("peer", "1", "1", "stream")])
+    ("peer", "1", "1", "kernel"), ("peer", "1", "0", "stream"), ("peer", "1", "1", "stream"),
+    ("peer", "1", "0", "step"), ("peer", "1", "1", "step"), ("peer", "1", "0", "step-relay"),
+    ("peer", "1", "1", "step-relay")])
 @pytest.mark.parametrize("nproc", [2, 4])
 def test_sharded_engine_matches_oracle(built, nproc, transport, fused, host, sync):
     if torch.cuda.device_count() < nproc:

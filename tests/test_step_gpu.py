@@ -82,13 +82,16 @@ def test_step_launch_equals_per_layer_launches(built, kernel, G, L, MB, layer0, 
     assert float(np.abs(got[L - 1, b, h].float().cpu().numpy() - ref[0, 0]).max()) <= 2e-3 + 2 ** -9
 
 
-@pytest.mark.parametrize("ahead", [False, True])
+@pytest.mark.parametrize("mode", ["stream", "ahead", "relay"])
 @pytest.mark.parametrize("kernel", ["auto", "gqa_tc"])
-def test_step_launch_peer_sequence_numbers(built, kernel, ahead):
+def test_step_launch_peer_sequence_numbers(built, kernel, mode):
     """Peer-io step launch: two sources, two micro-batches, three layers.  The kernel is enqueued
     first; a model-worker stream then publishes layer l of micro-batch m only after the kernel
     published layer l - 1 of m (the data dependency through the model) — so the grid must wait
-    per (layer, micro-batch) inside the kernel and publish per (layer, micro-batch)."""
+    per (layer, micro-batch) inside the kernel and publish per (layer, micro-batch).
+    mode="ahead": every layer published before the launch; mode="relay": the launch forwards
+    layers 1.. itself (lam_peer_io.n_relay: one qkv flag, awaited for both sources)."""
+    ahead = mode == "ahead"
     from paper_2405_01814_b200 import _lib, decode as dec
 
     L, MB, n_src, Bh, Hq, Hkv, D = 3, 2, 2, 3, 16, 2, 128
@@ -116,9 +119,15 @@ def test_step_launch_peer_sequence_numbers(built, kernel, ahead):
     io.n_wait = io.n_done = n_src
     fp = flags.data_ptr()
     for s in range(n_src):
-        io.wait_flags[s] = fp + 4 * s                    # qkv_ready[mb 0][s]
+        io.wait_flags[s] = fp + 4 * (s if mode != "relay" else 0)  # qkv_ready[mb 0][s]
         io.done_flags[s] = fp + 4 * (MB * n_src + s)     # out_ready[mb 0][s]
     epoch = 100
+    if mode == "relay":
+        io.n_relay = n_src
+        io.relay_flag = fp
+        for s in range(n_src):
+            io.relay_wait_flags[s] = fp + 4 * (MB * n_src + s)
+        flags[0, :, 0] = epoch + 1  # layer 0's inputs; the launch forwards the rest
     st = dec.step_layout(L, MB, rows, pool_layer_rows=cache.k[0].numel() // D, lm_q_stride=Bh * W * D,
                          lm_out_stride=Bh * Hq * D, flag_mb_stride=n_src, epoch=epoch)
     lib, ctx = _lib.load(), _lib.context(0)
@@ -130,7 +139,7 @@ def test_step_launch_peer_sequence_numbers(built, kernel, ahead):
         flags[0] = epoch + L
     torch.cuda.synchronize()
     _lib.check(lib.lam_decode_step(ctx.handle, a, st, io, torch.cuda.current_stream().cuda_stream))
-    for layer in range(L if not ahead else 0):
+    for layer in range(L if mode == "stream" else 0):
         for m in range(MB):
             if layer > 0:
                 done = P(*[fp + 4 * ((MB + m) * n_src + s) for s in range(n_src)])
@@ -139,7 +148,10 @@ def test_step_launch_peer_sequence_numbers(built, kernel, ahead):
             _lib.check(lib.lam_stream_signal(ctx.handle, ready, n_src, epoch + layer + 1, model.cuda_stream))
     torch.cuda.synchronize()
     assert ctx.status() == _lib.LAM_STATUS_OK
-    assert flags.tolist() == [[[epoch + L] * n_src] * MB] * 2
+    if mode == "relay":
+        assert flags.tolist() == [[[epoch + L, 0]] * MB, [[epoch + L] * n_src] * MB]
+    else:
+        assert flags.tolist() == [[[epoch + L] * n_src] * MB] * 2
     got = torch.stack(outs, 2).view(L, MB * rows, Hq, D)
     assert torch.equal(got, want)
     assert torch.equal(cache.k, k_want) and torch.equal(cache.v, v_want)
