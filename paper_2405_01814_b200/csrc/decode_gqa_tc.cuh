@@ -119,13 +119,16 @@ struct TcCfg {
   static constexpr int OFF_PBUF = OFF_QBUF + NS * QBUF_BYTES;      // [2]
   static constexpr int OFF_SLOT = OFF_PBUF + 2 * PBUF_BYTES;       // [KS]
   static constexpr int OFF_RED = OFF_SLOT + KS * SLOT_BYTES;
-  // red_m[8], red_l[8], red_lw[4][8], red_acc[8][RS], tmax[2][4][8]
-  static constexpr int RED_FLOATS = GQ + GQ + 4 * GQ + GQ * RS + 2 * 4 * GQ;
+  // two hand-off sets {red_m[8], red_l[8], red_lw[4][8], red_acc[8][RS]} (the warpgroup fills
+  // one while the epilogue warp still finishes the other), then tmax[2][4][8]
+  static constexpr int RED_SET = GQ + GQ + 4 * GQ + GQ * RS;
+  static constexpr int RED_FLOATS = 2 * RED_SET + 2 * 4 * GQ;
   static constexpr int OFF_META = OFF_RED + RED_FLOATS * 4;
   static constexpr int META = 16;  // tile tags outlive their K slot (read until the O MMA)
   static constexpr int OFF_BAR = OFF_META + META * 16 + META * 8;
-  // fullK, emptyK [KS]; fullV, emptyV [VS]; s, sfree [NS]; p, o, ofree [2]; red full / empty
-  static constexpr int N_BARS = 2 * KS + 2 * VS + 2 * NS + 8;
+  // fullK, emptyK [KS]; fullV, emptyV [VS]; s, sfree [NS]; p, o, ofree [2]; hand-off full,
+  // empty [2]; hand-off tags (2 x 4 ints); TMEM address
+  static constexpr int N_BARS = 2 * KS + 2 * VS + 2 * NS + 16;
   static constexpr int SMEM_BYTES = OFF_BAR + N_BARS * 8 + 32 + 1024;  // + align slack
   static constexpr int THREADS = 8 * 32;
   static constexpr int TMEM_COLS = 64;  // S[4] and O[2], 8 columns each
@@ -145,11 +148,13 @@ __global__ void __launch_bounds__(8 * 32, 1)
   uint8_t* qbuf = smem + C::OFF_QBUF;
   uint8_t* pbuf = smem + C::OFF_PBUF;
   uint8_t* qslot = smem + C::OFF_SLOT;
-  float* red_m = reinterpret_cast<float*>(smem + C::OFF_RED);
-  float* red_l = red_m + GQ;
-  float* red_lw = red_l + GQ;           // [4 warps][8]
-  float* red_acc = red_lw + 4 * GQ;     // [8][RS]
-  float* tmax = red_acc + GQ * C::RS;   // [2][4 warps][8]
+  // hand-off set b: red_m[8], red_l[8], red_lw[4 warps][8], red_acc[8][RS]
+  float* const red0 = reinterpret_cast<float*>(smem + C::OFF_RED);
+  auto red_m = [&](int b) { return red0 + b * C::RED_SET; };
+  auto red_l = [&](int b) { return red0 + b * C::RED_SET + GQ; };
+  auto red_lw = [&](int b) { return red0 + b * C::RED_SET + 2 * GQ; };
+  auto red_acc = [&](int b) { return red0 + b * C::RED_SET + 6 * GQ; };
+  float* tmax = red0 + 2 * C::RED_SET;  // [2][4 warps][8]
   int4* meta = reinterpret_cast<int4*>(smem + C::OFF_META);
   long long* meta_row = reinterpret_cast<long long*>(meta + C::META);
   // The K and V halves of a tile live in separate rings: K is handed back as soon as S has read
@@ -164,8 +169,10 @@ __global__ void __launch_bounds__(8 * 32, 1)
   uint64_t* pbar = sfree + NS;       // P(i) in smem           [2]
   uint64_t* obar = pbar + 2;         // O(i) in TMEM           [2]
   uint64_t* ofree = obar + 2;        // O(i) read out          [2]
-  RedPipe red{ofree + 2, ofree + 3, reinterpret_cast<int*>(ofree + 4)};
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ofree + 6);
+  uint64_t* rfull = ofree + 2;   // hand-off set b filled      [2]
+  uint64_t* rempty = ofree + 4;  // hand-off set b released    [2]
+  int* ritem = reinterpret_cast<int*>(ofree + 6);  // [2][4]: {item, len, t_end}
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ofree + 10);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int G = p.G;  // real q heads of the group (<= 8); the MMA's other N rows are zero
@@ -189,8 +196,10 @@ __global__ void __launch_bounds__(8 * 32, 1)
       mbar_init(&obar[b], 1);
       mbar_init(&ofree[b], 4);
     }
-    mbar_init(red.full, 4);
-    mbar_init(red.empty, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&rfull[b], 4);
+      mbar_init(&rempty[b], 1);
+    }
     fence_barrier_init();
   }
   if (warp == 5 && lane == 0) {
@@ -265,16 +274,19 @@ __global__ void __launch_bounds__(8 * 32, 1)
   }
   if (warp == 6) {  // ---------------- epilogue ----------------
     for (int k = 0;; ++k) {
-      mbar_wait(red.full, k & 1);
-      const int idx = red.item[0];
+      const int b = k & 1;
+      mbar_wait(&rfull[b], (k >> 1) & 1);
+      const int* tg = ritem + 4 * b;
+      const int idx = tg[0];
       if (idx < 0) break;
-      const Item it = item_from_tag<TILE>(p, make_int4(idx, 0, red.item[1], red.item[2]));
+      const Item it = item_from_tag<TILE>(p, make_int4(idx, 0, tg[1], tg[2]));
+      const float* lw = red_lw(b);
       if (lane < GQ)  // the four warps' partial sums of the softmax denominator
-        red_l[lane] = red_lw[lane] + red_lw[GQ + lane] + red_lw[2 * GQ + lane] + red_lw[3 * GQ + lane];
+        red_l(b)[lane] = lw[lane] + lw[GQ + lane] + lw[2 * GQ + lane] + lw[3 * GQ + lane];
       __syncwarp();
-      finish_item_warp<T, D, GQ, 1, true, C::RS>(p, it, G, red_m, red_l, red_acc, [&] {
+      finish_item_warp<T, D, GQ, 1, true, C::RS>(p, it, G, red_m(b), red_l(b), red_acc(b), [&] {
         __syncwarp();
-        if (lane == 0) mbar_arrive(red.empty);
+        if (lane == 0) mbar_arrive(&rempty[b]);
       });
     }
     finish_cta(p);
@@ -538,30 +550,37 @@ __global__ void __launch_bounds__(8 * 32, 1)
       for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
       ls[g] = v;
     }
-    red_acquire(red, k_item);
+    const int rb = k_item & 1;  // set k_item % 2, free once the epilogue took item k_item - 2
+    if (k_item >= 2) mbar_wait(&rempty[rb], ((k_item - 2) >> 1) & 1);
     if (lane == 0) {
-      float4* lw = reinterpret_cast<float4*>(red_lw + warp * GQ);
+      float4* lw = reinterpret_cast<float4*>(red_lw(rb) + warp * GQ);
       lw[0] = make_float4(ls[0], ls[1], ls[2], ls[3]);
       lw[1] = make_float4(ls[4], ls[5], ls[6], ls[7]);
       if (warp == 0) {
-        float4* rm = reinterpret_cast<float4*>(red_m);
+        float4* rm = reinterpret_cast<float4*>(red_m(rb));
         rm[0] = make_float4(m[0], m[1], m[2], m[3]);
         rm[1] = make_float4(m[4], m[5], m[6], m[7]);
       }
     }
+    float* racc = red_acc(rb);
 #pragma unroll
-    for (int g = 0; g < GQ; ++g) red_acc[g * C::RS + t] = o[g];
+    for (int g = 0; g < GQ; ++g) racc[g * C::RS + t] = o[g];
     if (warp == 0 && lane == 0) {
-      red.item[0] = tag.x;
-      red.item[1] = tag.y;
-      red.item[2] = tag.z;
+      ritem[4 * rb] = tag.x;
+      ritem[4 * rb + 1] = tag.y;
+      ritem[4 * rb + 2] = tag.z;
     }
-    red_commit(red);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&rfull[rb]);
     ++k_item;
   }
-  red_acquire(red, k_item);
-  if (warp == 0 && lane == 0) red.item[0] = -1;
-  red_commit(red);
+  {
+    const int rb = k_item & 1;
+    if (k_item >= 2) mbar_wait(&rempty[rb], ((k_item - 2) >> 1) & 1);
+    if (warp == 0 && lane == 0) ritem[4 * rb] = -1;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&rfull[rb]);
+  }
   named_bar_sync(3, 6 * 32);
 }
 
