@@ -849,27 +849,22 @@ int decode_impl(lam_ctx* ctx, const lam_decode_args* a_in, const lam_peer_io* io
     if (a_in->split_tokens <= 0) {
       // Splits: without input dependencies the whole step is one pool of items and S = 1 (fewest
       // merges).  When every launch lm waits for inputs that follow the previous layer's
-      // outputs, only ~n_mb launches are runnable at a time and a launch's latency is its
-      // longest item: split until a launch has >= 2 rounds of items on its share of the grid
-      // (C4 at N = 2: 64 units of 32 K tokens -> S = 4).
+      // outputs, a launch's latency is its longest item, so items are capped at 8 K tokens
+      // (LAM_STEP_ITEM_TOKENS; C4's 32 K-token requests -> S = 4, C5's 16 K ones -> 2).
+      // Splitting further to give each launch >= 2 rounds of items on its share of the grid
+      // measured slower everywhere: the tcgen05 kernel's per-item cost outweighs the rounding
+      // (C3 at N = 4: 4958 vs 6106 GB/s per GPU; item caps of 4 K / 16 K tokens: C4 6667 / 5414,
+      // C5 5113 / 4128 vs 6802 and 5486 at 8 K; round 2, calls 59-61).
       a_step.split_tokens = std::max(1, a_in->max_len);
       Plan p1;
       int rc1 = plan_decode(ctx, &a_step, &p1);
       if (rc1 != LAM_OK) return rc1;
       if (io != nullptr && io->n_wait > 0) {
-        const int64_t units = static_cast<int64_t>(st->rows_per_mb) * a->num_kv_heads * p1.QG;
-        const int occ = p1.kernel == LAM_KERNEL_GQA_TC     ? lam::occupancy_tc(a->kv_dtype)
-                        : p1.kernel == LAM_KERNEL_GQA_MMA ? lam::occupancy_mma(a->kv_dtype, p1.variant)
-                                                           : lam::occupancy_simt(a->kv_dtype, a->head_dim, p1.GQ, p1.variant);
-        const int64_t grid = static_cast<int64_t>(occ) * ctx->num_sms;
-        const int64_t want = 2 * ((grid + st->n_mb - 1) / st->n_mb);
         const int tiles = std::max(1, (a_in->max_len + p1.tile - 1) / p1.tile);
+        const int max_tok = env_int("LAM_STEP_ITEM_TOKENS", 8192);
         int S = 1;
-        while (units * S < want && S * 2 <= tiles) S *= 2;
-        // and a launch's latency is its longest item: items of at most ~4 K tokens (C5's
-        // 16 K-token requests in a batch of short ones)
-        const int max_tok = env_int("LAM_STEP_ITEM_TOKENS", 4096);
         while ((a_in->max_len + S - 1) / S > max_tok && S * 2 <= tiles) S *= 2;
+        if (const int force = env_int("LAM_STEP_SPLITS", 0); force > 0) S = std::min(force, tiles);
         const int ct = (tiles + S - 1) / S;
         a_step.split_tokens = ct * p1.tile;
       }
