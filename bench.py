@@ -719,8 +719,8 @@ def run_ours(args, w: dict, rank: int, world: int) -> None:
                                                    if use_engine else "")),
                    "l2": f"inputs {W.kv_bytes_layer * W.resident / 2**30:.0f} GiB of KV >> 126 MB L2; no flush needed",
                    "kernel": W.kernel,
-                   "splits": ("lam_decode_step's choice (S = 1 without input waits, else until a "
-                              "launch has >= 2 rounds of items)") if step_launch else W.splits,
+                   "splits": ("lam_decode_step's choice (S = 1 without input waits; with them, "
+                              "items of at most 8 K tokens)") if step_launch else W.splits,
                    "split_tokens": None if step_launch else W.chunk,
                    "launch": "step" if step_launch else "per layer and micro-batch",
                    "micro_batches": W.mb,
