@@ -318,6 +318,13 @@ typedef struct lam_peer_io {
   int32_t n_relay;
   uint32_t* relay_flag;
   const uint32_t* relay_wait_flags[LAM_MAX_PEERS];
+  /* Row map (optional, device memory, int32 per attention row; over every micro-batch of a
+   * step launch): row b reads source row_src[b] >> 24, row row_src[b] & 0xFFFFFF of that
+   * source's block (q / new rows at q_src[s] + row * q_batch_stride, outputs at out_dst[s] +
+   * row * num_q_heads * head_dim).  Rows may then come from the sources in any number and
+   * order — the request-level partition (attention.cpp:179-203) — and batch need not equal
+   * n_src * rows_per_src.  NULL: rows grouped by source, rows_per_src each. */
+  const int32_t* row_src;
 } lam_peer_io;
 
 /* lam_decode whose q / k_new / v_new / out come from lam_peer_io (args->q, k_new, v_new and out

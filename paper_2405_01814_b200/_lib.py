@@ -90,6 +90,7 @@ class PeerIO(C.Structure):
         ("n_relay", C.c_int32),
         ("relay_flag", C.c_void_p),
         ("relay_wait_flags", C.c_void_p * LAM_MAX_PEERS),
+        ("row_src", C.c_void_p),
     ]
 
 

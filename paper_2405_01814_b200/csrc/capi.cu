@@ -840,7 +840,7 @@ int decode_impl(lam_ctx* ctx, const lam_decode_args* a_in, const lam_peer_io* io
     if (st->pool_layers < 1 || st->layer0 < 0 || st->pool_layer_rows < 0)
       return fail(LAM_ERR_VALIDATION, "step: bad pool layer layout");
     if (a_in->lse != nullptr) return fail(LAM_ERR_VALIDATION, "step: lse is not supported");
-    if (io != nullptr && io->rows_per_src * io->n_src != st->rows_per_mb)
+    if (io != nullptr && io->row_src == nullptr && io->rows_per_src * io->n_src != st->rows_per_mb)
       return fail(LAM_ERR_VALIDATION, "step: peer io must describe one micro-batch's rows");
     a_step = *a_in;
     a_step.batch = st->rows_per_mb;
@@ -948,9 +948,9 @@ int decode_impl(lam_ctx* ctx, const lam_decode_args* a_in, const lam_peer_io* io
   }
   if (io != nullptr) {  // rows grouped by source, buffers local or on peers
     if (io->n_src < 1 || io->n_src > LAM_MAX_PEERS || io->rows_per_src < 1 ||
-        static_cast<int64_t>(io->n_src) * io->rows_per_src != a->batch)
+        (io->row_src == nullptr && static_cast<int64_t>(io->n_src) * io->rows_per_src != a->batch))
       return fail(LAM_ERR_VALIDATION, "peer io: need 1 <= n_src <= LAM_MAX_PEERS and batch == "
-                                      "n_src * rows_per_src");
+                                      "n_src * rows_per_src (or a row map)");
     if (a->lse != nullptr) return fail(LAM_ERR_VALIDATION, "peer io: lse is not supported");
     const int e = a->kv_dtype == LAM_F32 ? 4 : 2;
     if ((io->k_new_offset * e) % 16 != 0 || (io->v_new_offset * e) % 16 != 0)
@@ -962,6 +962,7 @@ int decode_impl(lam_ctx* ctx, const lam_decode_args* a_in, const lam_peer_io* io
       p.out_dst[i] = io->out_dst[i];
     }
     p.src_rows = io->rows_per_src;
+    p.row_src = io->row_src;
     p.new_off[0] = io->k_new_offset;
     p.new_off[1] = io->v_new_offset;
     p.q = io->q_src[0];

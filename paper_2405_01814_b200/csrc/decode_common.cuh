@@ -75,6 +75,9 @@ struct DecodeParams {
   // q_src[s] + new_off[0|1] + i * new_stride, and writes its output rows [Hq][D] to
   // out_dst[s] + i * Hq * D — buffers owned by the model worker s, mapped over NVLink.
   int32_t src_rows;
+  // optional row map (lam_peer_io::row_src): row b of the launch (over every micro-batch of a
+  // step launch) is row row_src[b] & 0xFFFFFF of source row_src[b] >> 24
+  const int32_t* row_src;
   const void* q_src[LAM_MAX_PEERS];
   void* out_dst[LAM_MAX_PEERS];
   int64_t new_off[2];
@@ -260,15 +263,28 @@ struct Item {
   int lm;     // launch of a step launch (layer * n_mb + micro-batch); 0 otherwise
 };
 
+// Peer I/O: source rank and row within that source's block of attention row it.b.
+__device__ __forceinline__ int src_row(const DecodeParams& p, const Item& it, int& row) {
+  if (p.row_src != nullptr) {
+    const int v = __ldg(p.row_src + it.b);
+    row = v & 0xFFFFFF;
+    return v >> 24;
+  }
+  const int b = it.b - (it.lm % p.n_mb) * p.mb_rows;  // row within the launch
+  const int s = b / p.src_rows;
+  row = b - s * p.src_rows;
+  return s;
+}
+
 // Start of request it.b's q rows / new k (which = 0) or v (1) rows, local or on a peer.
 template <typename T>
 __device__ __forceinline__ const T* q_rows(const DecodeParams& p, const Item& it) {
   const int b = it.b - (it.lm % p.n_mb) * p.mb_rows;  // row within the launch
   const int64_t lm_off = static_cast<int64_t>(it.lm) * p.lm_q_stride;
   if (p.src_rows > 0) {
-    const int s = b / p.src_rows;
-    return static_cast<const T*>(p.q_src[s]) + lm_off +
-           static_cast<int64_t>(b - s * p.src_rows) * p.q_stride;
+    int i;
+    const int s = src_row(p, it, i);
+    return static_cast<const T*>(p.q_src[s]) + lm_off + static_cast<int64_t>(i) * p.q_stride;
   }
   return static_cast<const T*>(p.q) + lm_off + static_cast<int64_t>(b) * p.q_stride;
 }
@@ -277,9 +293,10 @@ __device__ __forceinline__ const T* new_rows(const DecodeParams& p, int which, c
   const int b = it.b - (it.lm % p.n_mb) * p.mb_rows;
   if (p.src_rows > 0) {  // (the new rows sit in the packed q block)
     const int64_t lm_off = static_cast<int64_t>(it.lm) * p.lm_q_stride;
-    const int s = b / p.src_rows;
+    int i;
+    const int s = src_row(p, it, i);
     return static_cast<const T*>(p.q_src[s]) + lm_off + p.new_off[which] +
-           static_cast<int64_t>(b - s * p.src_rows) * p.new_stride;
+           static_cast<int64_t>(i) * p.new_stride;
   }
   return static_cast<const T*>(which ? p.v_new : p.k_new) +
          static_cast<int64_t>(it.lm) * p.lm_new_stride + static_cast<int64_t>(b) * p.new_stride;
@@ -554,9 +571,8 @@ __device__ __forceinline__ void store_out_vec(const DecodeParams& p, const Item&
   void* base = p.out;
   int b = it.b - (it.lm % p.n_mb) * p.mb_rows;
   if (p.src_rows > 0) {
-    const int s = b / p.src_rows;
+    const int s = src_row(p, it, b);
     base = p.out_dst[s];
-    b -= s * p.src_rows;
   }
   const int64_t idx = static_cast<int64_t>(it.lm) * p.lm_out_stride +
                       (static_cast<int64_t>(b) * p.Hq + h) * D + d;

@@ -699,3 +699,153 @@ class PeerShardedAttention:
             comp.wait_stream(ms_)
         if host_out is not None:
             comp.wait_stream(self.d2h)
+
+
+class PeerRequestShardedAttention:
+    """The request-level partition (RequestGeometry, attention.cpp:179-203) over the zero-copy
+    peer transport: no collective and no copy kernel on the data path.
+
+    Every rank, as model worker, exports qkv_in [L, MB, Bh, Hq + 2 Hkv, D] and out
+    [L, MB, Bh, Hq, D] (both in its send order, `pack_request_inputs` /
+    `unpack_request_outputs`) and a flag block [2][MB][N].  The owner of a request pulls its q /
+    new K/V rows straight from the sender's qkv_in over NVLink, appends, attends with all heads
+    and stores the outputs into the sender's out: one lam_decode_peer per (layer, micro-batch)
+    whose row map (lam_peer_io.row_src) names (source, row in the source's block) for each of the
+    rows the owner received — any number per source.  Sequence numbers as in
+    PeerShardedAttention(sync="kernel"): the model worker writes its own qkv_ready[m] word, the
+    kernel polls every source's word, and the kernel's last CTA stores out_ready[m][owner] into
+    every model worker.
+
+    `launch_args(layer, m)` returns the lam_decode_args of the local launch (pools, page table,
+    seq_lens of micro-batch m's received rows); an owner with no rows in a micro-batch only
+    publishes its out_ready.
+    """
+
+    def __init__(self, geo: RequestGeometry, dist, ctx, launch_args: Callable, device: torch.device,
+                 dtype: torch.dtype):
+        import ctypes as C
+
+        from . import _lib
+
+        g = self.geo = geo
+        if g.world > _lib.LAM_MAX_PEERS:
+            raise ValueError(f"peer transport supports up to {_lib.LAM_MAX_PEERS} ranks")
+        self.lib, self.ctx, self.device, self.dtype = _lib.load(), ctx, device, dtype
+        self._C = C
+        esz = torch.tensor([], dtype=dtype).element_size()
+        align = lambda n: (n + 4095) // 4096 * 4096  # noqa: E731
+        MB, N, L = g.micro_batches, g.world, g.layers
+        n_qkv = L * MB * g.Bh * g.W * g.D
+        n_out = L * MB * g.Bh * g.Hq * g.D
+        self.off_out = align(n_qkv * esz)
+        self.off_flags = self.off_out + align(n_out * esz)
+        total = self.off_flags + align(2 * MB * N * 4)
+        base, handle = C.c_void_p(), (C.c_uint8 * _lib.LAM_IPC_HANDLE_BYTES)()
+        _lib.check(self.lib.lam_peer_alloc(ctx.handle, total, C.byref(base), handle))
+        self.base = base.value
+        raw = torch.as_tensor(_DevView(self.base, total), device=device)
+        self.qkv_in = raw[: n_qkv * esz].view(dtype).view(g.qkv_shape())
+        self.out = raw[self.off_out: self.off_out + n_out * esz].view(dtype).view(g.q_shape())
+        handles = [None] * N
+        if dist is None:
+            if N != 1:
+                raise ValueError("more than one rank needs a process group to exchange handles")
+            handles[0] = bytes(handle)
+        else:
+            dist.all_gather_object(handles, bytes(handle))
+        self.peer = []
+        for r in range(N):
+            if r == g.rank:
+                self.peer.append(self.base)
+                continue
+            hb = (C.c_uint8 * _lib.LAM_IPC_HANDLE_BYTES).from_buffer_copy(handles[r])
+            p = C.c_void_p()
+            _lib.check(self.lib.lam_peer_open(ctx.handle, hb, C.byref(p)))
+            self.peer.append(p.value)
+        if dist is not None:
+            dist.barrier()
+        self.compute = torch.cuda.current_stream(device)
+        self.models = [torch.cuda.Stream(device=device) for _ in range(MB)]
+        self.epoch = 0
+        Ptrs = C.c_void_p * N
+        fl = lambda r, kind, m, i: self.peer[r] + self.off_flags + ((kind * MB + m) * N + i) * 4  # noqa: E731
+        j = g.rank
+        self.sig_qkv = [Ptrs(fl(j, 0, m, j)) for m in range(MB)]          # own word
+        self.wait_qkv = [[fl(s, 0, m, s) for s in range(N)] for m in range(MB)]  # polled remotely
+        self.sig_out = [Ptrs(*[fl(r, 1, m, j) for r in range(N)]) for m in range(MB)]
+        self.wait_out = [Ptrs(*[fl(j, 1, m, s) for s in range(N)]) for m in range(MB)]
+        # row maps: received row k of micro-batch m -> (source, position in its send order)
+        blk_qkv = g.Bh * g.W * g.D * esz
+        blk_out = g.Bh * g.Hq * g.D * esz
+        self.row_maps, self.args, self.io = [], {}, {}
+        for m in range(MB):
+            maps = []
+            for r in g.recv_reqs[m]:
+                s, b = divmod(r, g.B_local)
+                order_s = sorted(range(m * g.Bh, (m + 1) * g.Bh),
+                                 key=lambda x: (g.owner[s * g.B_local + x], x))
+                maps.append((s << 24) | order_s.index(b))
+            self.row_maps.append(torch.tensor(maps or [0], dtype=torch.int32, device=device))
+        for layer in range(L):
+            for m in range(MB):
+                if not g.recv_reqs[m]:
+                    continue
+                a = launch_args(layer, m)
+                a.q_batch_stride = a.new_batch_stride = g.W * g.D
+                a.lse = None
+                a.overlap_prev = 0
+                io = _lib.PeerIO()
+                io.n_src, io.rows_per_src = N, 1
+                for s in range(N):
+                    io.q_src[s] = self.peer[s] + (layer * MB + m) * blk_qkv
+                    io.out_dst[s] = self.peer[s] + self.off_out + (layer * MB + m) * blk_out
+                io.k_new_offset = g.Hq * g.D
+                io.v_new_offset = (g.Hq + g.Hkv) * g.D
+                io.n_wait = io.n_done = N
+                for s in range(N):
+                    io.wait_flags[s] = self.wait_qkv[m][s]
+                    io.done_flags[s] = self.sig_out[m][s]
+                io.row_src = self.row_maps[m].data_ptr()
+                self.args[layer, m], self.io[layer, m] = a, io
+
+    def close(self):
+        if self.peer:
+            torch.cuda.synchronize(self.device)
+            for r, p in enumerate(self.peer):
+                if r != self.geo.rank:
+                    self.lib.lam_peer_close(self.ctx.handle, p)
+            self.lib.lam_peer_free(self.ctx.handle, self.base)
+            self.peer = []
+
+    def step(self):
+        """One decode step over all layers (enqueue only): inputs from self.qkv_in, outputs in
+        self.out of every model worker."""
+        from . import _lib
+
+        g, lib = self.geo, self.lib
+        MB, N, L = g.micro_batches, g.world, g.layers
+        h = self.ctx.handle
+        comp = self.compute
+        e0 = self.epoch
+        self.epoch += L
+        for ms in self.models:
+            ms.wait_stream(comp)
+        cs = comp.cuda_stream
+        for layer in range(L):
+            ep = e0 + layer + 1
+            for m in range(MB):  # model worker: layer l + 1 follows layer l's outputs
+                ms = self.models[m].cuda_stream
+                if layer > 0:
+                    _lib.check(lib.lam_stream_wait(h, self.wait_out[m], N, ep - 1, ms))
+                _lib.check(lib.lam_stream_signal(h, self.sig_qkv[m], 1, ep, ms))
+            for m in range(MB):  # attention worker
+                if (layer, m) in self.io:
+                    io = self.io[layer, m]
+                    io.wait_value = io.done_value = ep
+                    _lib.check(lib.lam_decode_peer(h, self.args[layer, m], io, cs))
+                else:  # nothing received: publish the (empty) outputs at once
+                    _lib.check(lib.lam_stream_signal(h, self.sig_out[m], N, ep, cs))
+        for m in range(MB):
+            _lib.check(lib.lam_stream_wait(h, self.wait_out[m], N, e0 + L, cs))
+        for ms in self.models:
+            comp.wait_stream(ms)

@@ -70,12 +70,36 @@ def main_request():
         dec.decode(qr, cache.k[layer], cache.v[layer], cache.seq_lens[sl],
                    page_table=cache.page_table[sl], max_len=max_len, out=out, k_new=k, v_new=v)
 
-    eng = RequestShardedAttention(geo, dist, None, attend_fused, dev, torch.bfloat16)
     mine = slice(rank * B_LOCAL, (rank + 1) * B_LOCAL)
     qkv_in = pack_request_inputs(geo, q[:, mine], kn[:, mine], vn[:, mine]).to(dev)
-    out = torch.zeros(geo.q_shape(), dtype=torch.bfloat16, device=dev)
-    eng.step(qkv_in, out)
-    torch.cuda.synchronize()
+    if os.environ.get("LAM_TEST_TRANSPORT", "nccl") == "peer":
+        # zero-copy: owners pull whole requests from the senders and store outputs back
+        from paper_2405_01814_b200.dist import PeerRequestShardedAttention
+
+        def launch_args(layer, m):
+            n = len(geo.recv_reqs[m])
+            sl = slice(geo.row_off[m], geo.row_off[m] + n)
+            qd = torch.empty((n, hq, D), dtype=torch.bfloat16, device=dev)
+            a, _ = dec.make_args(qd, cache.k[layer], cache.v[layer], cache.seq_lens[sl],
+                                 page_table=cache.page_table[sl], max_len=max_len, out=qd)
+            return a
+
+        eng = PeerRequestShardedAttention(geo, dist, _lib.context(dev.index), launch_args, dev,
+                                          torch.bfloat16)
+        eng.qkv_in.copy_(qkv_in)
+        eng.out.zero_()
+        torch.cuda.synchronize()
+        dist.barrier()
+        eng.step()
+        torch.cuda.synchronize()
+        out = eng.out.clone()
+        dist.barrier()
+        eng.close()
+    else:
+        eng = RequestShardedAttention(geo, dist, None, attend_fused, dev, torch.bfloat16)
+        out = torch.zeros(geo.q_shape(), dtype=torch.bfloat16, device=dev)
+        eng.step(qkv_in, out)
+        torch.cuda.synchronize()
     got = unpack_request_outputs(geo, out).float().cpu().numpy()
     worst = 0.0
     for layer in range(L):

@@ -32,15 +32,18 @@ def test_sharded_engine_matches_oracle(built, nproc, transport, fused, host, syn
     assert r.stdout.count("OK") == nproc
 
 
+@pytest.mark.parametrize("transport", ["nccl", "peer"])
 @pytest.mark.parametrize("nproc", [2, 4])
-def test_request_sharded_engine_matches_oracle(built, nproc):
-    """request_partition-based pool (KV heads not divisible by N), NCCL, real kernels."""
+def test_request_sharded_engine_matches_oracle(built, nproc, transport):
+    """request_partition-based pool (KV heads not divisible by N), real kernels, over NCCL or
+    the zero-copy peer transport (row map, lam_peer_io.row_src)."""
     if torch.cuda.device_count() < nproc:
         pytest.skip(f"needs {nproc} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1", "--master-port=29532",
            str(ROOT / "tests" / "dist_gpu_worker.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT,
-                       env=dict(os.environ, PYTHONPATH=str(ROOT), LAM_TEST_SHARD="request"))
+                       env=dict(os.environ, PYTHONPATH=str(ROOT), LAM_TEST_SHARD="request",
+                                LAM_TEST_TRANSPORT=transport))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count("OK") == nproc

@@ -226,6 +226,63 @@ def test_decode_peer_vs_oracle(built, n_src, Bh, G):
     assert float(np.abs(got - want).max()) <= 2e-3
 
 
+def test_decode_peer_row_map_vs_oracle(built):
+    """Row map (lam_peer_io.row_src, the request-level partition on the peer transport): the
+    launch's rows come from the sources in any number and order — here 7 of 3 x 3 source rows,
+    shuffled, one source row unused — and each row's q / new K/V are read from, and its output
+    stored to, the (source, row) the map names.  Fused append bit-exact, attention vs the CPU
+    oracle within the bf16 bound."""
+    from oracle import oracle as O
+    from paper_2405_01814_b200 import _lib, decode as dec
+    from tests.helpers import oracle_decode
+
+    n_src, Bh, G, Hkv, D = 3, 3, 8, 2, 128
+    Hq = Hkv * G
+    cache, lens, qkv, s = _setup(n_src=n_src, Bh=Bh, Hq=Hq, Hkv=Hkv, D=D, seed=77)
+    W, P = s["W"], cache.k.shape[3]
+    Bn = 7
+    perm = np.random.default_rng(5).permutation(n_src * Bh)[:Bn]  # row b <- source row perm[b]
+    lens = lens[:Bn]
+    lmax = int(lens.max())
+    pt = cache.page_table.cpu().numpy()[:Bn]
+    k_dense = dec.kv_gather(cache.k[0], cache.page_table[:Bn], cache.seq_lens[:Bn], lmax).cpu()
+    v_dense = dec.kv_gather(cache.v[0], cache.page_table[:Bn], cache.seq_lens[:Bn], lmax).cpu()
+    packed = torch.cat(qkv, 0).cpu()[perm]  # the rows each attention row reads
+    for b in range(Bn):
+        k_dense[b, :, lens[b] - 1] = packed[b, Hq:Hq + Hkv]
+        v_dense[b, :, lens[b] - 1] = packed[b, Hq + Hkv:]
+    outs = [torch.zeros((Bh, Hq, D), dtype=torch.float32, device="cuda") for _ in range(n_src)]
+    flags = torch.zeros(2 * n_src, dtype=torch.int32, device="cuda")
+    qd = torch.empty((Bn, Hq, D), dtype=torch.bfloat16, device="cuda")
+    a, _ = dec.make_args(qd, cache.k[0], cache.v[0], cache.seq_lens[:Bn],
+                         page_table=cache.page_table[:Bn], max_len=lmax,
+                         out=torch.empty((Bn, Hq, D), device="cuda"))
+    a.q_batch_stride = a.new_batch_stride = W * D
+    io = _peer_io(n_src, Bh, Hq, Hkv, D, qkv, outs, flags, value=9)
+    io.rows_per_src = 1  # ignored with a row map
+    row_src = torch.tensor([(int(r) // Bh) << 24 | (int(r) % Bh) for r in perm], dtype=torch.int32,
+                           device="cuda")
+    io.row_src = row_src.data_ptr()
+    lib, ctx = _lib.load(), _lib.context(0)
+    torch.cuda.synchronize()
+    _lib.check(lib.lam_decode_peer(ctx.handle, a, io, torch.cuda.current_stream().cuda_stream))
+    side = torch.cuda.Stream()
+    ready = (C.c_void_p * n_src)(*[flags.data_ptr() + 4 * i for i in range(n_src)])
+    _lib.check(lib.lam_stream_signal(ctx.handle, ready, n_src, 9, side.cuda_stream))
+    torch.cuda.synchronize()
+    assert flags.tolist() == [9] * (2 * n_src)
+    assert ctx.status() == _lib.LAM_STATUS_OK
+    for pool, dense in ((cache.k[0], k_dense), (cache.v[0], v_dense)):
+        pool_bytes = pool.view(torch.uint8).cpu().numpy().reshape(pool.shape[0], Hkv, P, D * 2)
+        got = O.page_gather(pool_bytes, pt, lens, lmax)
+        assert np.array_equal(got, dense.view(torch.uint8).numpy().reshape(got.shape))
+    want = oracle_decode(packed[:, :Hq], k_dense, v_dense, lens, 1 / math.sqrt(D))
+    got_src = torch.cat(outs, 0).cpu().numpy()
+    assert float(np.abs(got_src[perm] - want).max()) <= 2e-3
+    unused = sorted(set(range(n_src * Bh)) - set(int(r) for r in perm))
+    assert not got_src[unused].any()  # rows no attention row maps to are never written
+
+
 def test_spin_timeout_reports_status_instead_of_trapping(built):
     """A launch whose inputs are never published gives up after the context's spin timeout:
     it records LAM_STATUS_INPUT_TIMEOUT, still publishes its done flags, and the context stays
