@@ -305,6 +305,21 @@ class RequestGeometry:
         """attention-side KV rows: global request of every row of this rank's store"""
         return [r for reqs in self.recv_reqs for r in reqs]
 
+    def send_order_of(self, s: int, m: int) -> list:
+        """model worker s's micro-batch m requests (local indices) grouped by destination"""
+        return sorted(range(m * self.Bh, (m + 1) * self.Bh),
+                      key=lambda b: (self.owner[s * self.B_local + b], b))
+
+    @property
+    def R(self) -> int:
+        """rows per micro-batch of a step launch: the largest micro-batch's received rows"""
+        return max(1, max(len(x) for x in self.recv_reqs))
+
+    def padded_rows(self) -> list:
+        """the step launch's rows: micro-batch m's received requests in rows
+        [m * R, m * R + n_recv[m]), then -1 (an empty row: length 0, no work, a scratch output)"""
+        return [r for reqs in self.recv_reqs for r in reqs + [-1] * (self.R - len(reqs))]
+
     def q_shape(self):
         return (self.layers, self.micro_batches, self.Bh, self.Hq, self.D)
 
@@ -707,22 +722,26 @@ class PeerRequestShardedAttention:
 
     Every rank, as model worker, exports qkv_in [L, MB, Bh, Hq + 2 Hkv, D] and out
     [L, MB, Bh, Hq, D] (both in its send order, `pack_request_inputs` /
-    `unpack_request_outputs`) and a flag block [2][MB][N].  The owner of a request pulls its q /
-    new K/V rows straight from the sender's qkv_in over NVLink, appends, attends with all heads
-    and stores the outputs into the sender's out: one lam_decode_peer per (layer, micro-batch)
-    whose row map (lam_peer_io.row_src) names (source, row in the source's block) for each of the
-    rows the owner received — any number per source.  Sequence numbers as in
-    PeerShardedAttention(sync="kernel"): the model worker writes its own qkv_ready[m] word, the
-    kernel polls every source's word, and the kernel's last CTA stores out_ready[m][owner] into
-    every model worker.
+    `unpack_request_outputs`; each (layer, micro-batch) block has one more scratch row) and a
+    flag block [2][MB][N].  The owner of a request pulls its q / new K/V rows straight from the
+    sender's qkv_in over NVLink, appends, attends with all heads and stores the outputs into the
+    sender's out.  The launch's row map (lam_peer_io.row_src) names (source, row in the source's
+    block) for each received row — any number per source.  The model worker writes its own
+    qkv_ready[m] word, the kernels poll every source's word, and the last unit of a launch stores
+    out_ready[m][owner] into every model worker.
 
-    `launch_args(layer, m)` returns the lam_decode_args of the local launch (pools, page table,
-    seq_lens of micro-batch m's received rows); an owner with no rows in a micro-batch only
-    publishes its out_ready.
+    sync="step" (default): one lam_decode_step per decode step; every micro-batch has geo.R rows
+    (geo.padded_rows(): pads are empty rows whose zero output goes to the owner's scratch row).
+    `step_args()` returns (lam_decode_args over all MB * R rows — pools of layer 0, page table,
+    seq_lens with 0 for pads, request_order local to each micro-batch —, pool_layers,
+    pool_layer_rows).  sync="kernel": one lam_decode_peer per (layer, micro-batch) from
+    `launch_args(layer, m)` over micro-batch m's received rows (an owner with none only
+    publishes).
     """
 
-    def __init__(self, geo: RequestGeometry, dist, ctx, launch_args: Callable, device: torch.device,
-                 dtype: torch.dtype):
+    def __init__(self, geo: RequestGeometry, dist, ctx, launch_args: Callable | None,
+                 device: torch.device, dtype: torch.dtype, sync: str = "step",
+                 step_args: Callable | None = None):
         import ctypes as C
 
         from . import _lib
@@ -730,13 +749,18 @@ class PeerRequestShardedAttention:
         g = self.geo = geo
         if g.world > _lib.LAM_MAX_PEERS:
             raise ValueError(f"peer transport supports up to {_lib.LAM_MAX_PEERS} ranks")
+        if sync not in ("step", "kernel") or (sync == "step" and step_args is None) or \
+                (sync == "kernel" and launch_args is None):
+            raise ValueError("sync='step' needs step_args, sync='kernel' needs launch_args")
+        self.sync = sync
         self.lib, self.ctx, self.device, self.dtype = _lib.load(), ctx, device, dtype
         self._C = C
         esz = torch.tensor([], dtype=dtype).element_size()
         align = lambda n: (n + 4095) // 4096 * 4096  # noqa: E731
         MB, N, L = g.micro_batches, g.world, g.layers
-        n_qkv = L * MB * g.Bh * g.W * g.D
-        n_out = L * MB * g.Bh * g.Hq * g.D
+        Bb = g.Bh + 1  # rows per (layer, micro-batch) block: the requests and one scratch row
+        n_qkv = L * MB * Bb * g.W * g.D
+        n_out = L * MB * Bb * g.Hq * g.D
         self.off_out = align(n_qkv * esz)
         self.off_flags = self.off_out + align(n_out * esz)
         total = self.off_flags + align(2 * MB * N * 4)
@@ -744,8 +768,9 @@ class PeerRequestShardedAttention:
         _lib.check(self.lib.lam_peer_alloc(ctx.handle, total, C.byref(base), handle))
         self.base = base.value
         raw = torch.as_tensor(_DevView(self.base, total), device=device)
-        self.qkv_in = raw[: n_qkv * esz].view(dtype).view(g.qkv_shape())
-        self.out = raw[self.off_out: self.off_out + n_out * esz].view(dtype).view(g.q_shape())
+        qkv = raw[: n_qkv * esz].view(dtype).view(L, MB, Bb, g.W, g.D)
+        out = raw[self.off_out: self.off_out + n_out * esz].view(dtype).view(L, MB, Bb, g.Hq, g.D)
+        self.qkv_in, self.out = qkv[:, :, : g.Bh], out[:, :, : g.Bh]  # (strided views)
         handles = [None] * N
         if dist is None:
             if N != 1:
@@ -774,39 +799,55 @@ class PeerRequestShardedAttention:
         self.wait_qkv = [[fl(s, 0, m, s) for s in range(N)] for m in range(MB)]  # polled remotely
         self.sig_out = [Ptrs(*[fl(r, 1, m, j) for r in range(N)]) for m in range(MB)]
         self.wait_out = [Ptrs(*[fl(j, 1, m, s) for s in range(N)]) for m in range(MB)]
-        # row maps: received row k of micro-batch m -> (source, position in its send order)
-        blk_qkv = g.Bh * g.W * g.D * esz
-        blk_out = g.Bh * g.Hq * g.D * esz
-        self.row_maps, self.args, self.io = [], {}, {}
-        for m in range(MB):
-            maps = []
-            for r in g.recv_reqs[m]:
-                s, b = divmod(r, g.B_local)
-                order_s = sorted(range(m * g.Bh, (m + 1) * g.Bh),
-                                 key=lambda x: (g.owner[s * g.B_local + x], x))
-                maps.append((s << 24) | order_s.index(b))
-            self.row_maps.append(torch.tensor(maps or [0], dtype=torch.int32, device=device))
-        for layer in range(L):
-            for m in range(MB):
-                if not g.recv_reqs[m]:
-                    continue
-                a = launch_args(layer, m)
-                a.q_batch_stride = a.new_batch_stride = g.W * g.D
-                a.lse = None
-                a.overlap_prev = 0
-                io = _lib.PeerIO()
-                io.n_src, io.rows_per_src = N, 1
-                for s in range(N):
-                    io.q_src[s] = self.peer[s] + (layer * MB + m) * blk_qkv
-                    io.out_dst[s] = self.peer[s] + self.off_out + (layer * MB + m) * blk_out
-                io.k_new_offset = g.Hq * g.D
-                io.v_new_offset = (g.Hq + g.Hkv) * g.D
-                io.n_wait = io.n_done = N
-                for s in range(N):
-                    io.wait_flags[s] = self.wait_qkv[m][s]
-                    io.done_flags[s] = self.sig_out[m][s]
-                io.row_src = self.row_maps[m].data_ptr()
-                self.args[layer, m], self.io[layer, m] = a, io
+        blk_qkv, blk_out = Bb * g.W * g.D, Bb * g.Hq * g.D  # elements per (layer, mb) block
+
+        def src_row(r):  # global request -> (source, row in the source's block)
+            s, b = divmod(r, g.B_local)
+            m = b // g.Bh
+            return (s << 24) | g.send_order_of(s, m).index(b)
+
+        def io_for(layer, m, rows_map):
+            io = _lib.PeerIO()
+            io.n_src, io.rows_per_src = N, 1
+            for s in range(N):
+                io.q_src[s] = self.peer[s] + (layer * MB + m) * blk_qkv * esz
+                io.out_dst[s] = self.peer[s] + self.off_out + (layer * MB + m) * blk_out * esz
+            io.k_new_offset = g.Hq * g.D
+            io.v_new_offset = (g.Hq + g.Hkv) * g.D
+            io.n_wait = io.n_done = N
+            for s in range(N):
+                io.wait_flags[s] = self.wait_qkv[m][s]
+                io.done_flags[s] = self.sig_out[m][s]
+            io.row_src = rows_map.data_ptr()
+            return io
+
+        self.args, self.io = {}, {}
+        if sync == "step":
+            scratch = (j << 24) | g.Bh
+            rmap = [src_row(r) if r >= 0 else scratch for r in g.padded_rows()]
+            self.row_map = torch.tensor(rmap, dtype=torch.int32, device=device)
+            a, pool_layers, pool_layer_rows = step_args()
+            a.q_batch_stride = a.new_batch_stride = g.W * g.D
+            a.lse = None
+            a.overlap_prev = 0
+            self.step_a, self.step_io = a, io_for(0, 0, self.row_map)
+            from .decode import step_layout
+
+            self.step_st = step_layout(L, MB, g.R, pool_layers=pool_layers,
+                                       pool_layer_rows=pool_layer_rows, lm_q_stride=blk_qkv,
+                                       lm_out_stride=blk_out, flag_mb_stride=N)
+        else:
+            self.row_maps = [torch.tensor([src_row(r) for r in g.recv_reqs[m]] or [0],
+                                          dtype=torch.int32, device=device) for m in range(MB)]
+            for layer in range(L):
+                for m in range(MB):
+                    if not g.recv_reqs[m]:
+                        continue
+                    a = launch_args(layer, m)
+                    a.q_batch_stride = a.new_batch_stride = g.W * g.D
+                    a.lse = None
+                    a.overlap_prev = 0
+                    self.args[layer, m], self.io[layer, m] = a, io_for(layer, m, self.row_maps[m])
 
     def close(self):
         if self.peer:
@@ -831,6 +872,9 @@ class PeerRequestShardedAttention:
         for ms in self.models:
             ms.wait_stream(comp)
         cs = comp.cuda_stream
+        if self.sync == "step":
+            self.step_st.epoch = e0 & 0xFFFFFFFF
+            _lib.check(lib.lam_decode_step(h, self.step_a, self.step_st, self.step_io, cs))
         for layer in range(L):
             ep = e0 + layer + 1
             for m in range(MB):  # model worker: layer l + 1 follows layer l's outputs
@@ -838,7 +882,7 @@ class PeerRequestShardedAttention:
                 if layer > 0:
                     _lib.check(lib.lam_stream_wait(h, self.wait_out[m], N, ep - 1, ms))
                 _lib.check(lib.lam_stream_signal(h, self.sig_qkv[m], 1, ep, ms))
-            for m in range(MB):  # attention worker
+            for m in range(MB if self.sync == "kernel" else 0):  # attention worker
                 if (layer, m) in self.io:
                     io = self.io[layer, m]
                     io.wait_value = io.done_value = ep

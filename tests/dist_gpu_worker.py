@@ -46,8 +46,11 @@ def main_request():
     q = bf(rng.uniform(-1, 1, (L, B, hq, D)).astype(np.float32))
     kn = bf(rng.uniform(-1, 1, (L, B, hkv, D)).astype(np.float32))
     vn = bf(rng.uniform(-1, 1, (L, B, hkv, D)).astype(np.float32))
-    rows = np.array(geo.rows, np.int64)
-    row_lens = lens[rows] + 1
+    peer = os.environ.get("LAM_TEST_TRANSPORT", "nccl") == "peer"
+    req_sync = os.environ.get("LAM_TEST_SYNC", "step") if peer else "-"
+    # the step launch's rows are micro-batch-major with R rows each (-1: an empty pad row)
+    rows = np.array(geo.padded_rows() if req_sync == "step" else geo.rows, np.int64)
+    row_lens = np.where(rows >= 0, lens[np.maximum(rows, 0)] + 1, 0)
     n_rows = max(len(rows), 1)
     cache = PagedKVCache(L, hkv, D, P, int((-(-row_lens // P)).sum()) + 2, n_rows,
                          int(-(-row_lens.max() // P)) if len(rows) else 1, dtype=torch.bfloat16,
@@ -58,6 +61,8 @@ def main_request():
     pt = cache.page_table_host
     for layer in range(L):
         for r, req in enumerate(rows):
+            if req < 0:
+                continue
             n = int(lens[req])
             for p0 in range(0, n, P):
                 t1 = min(n, p0 + P)
@@ -72,7 +77,7 @@ def main_request():
 
     mine = slice(rank * B_LOCAL, (rank + 1) * B_LOCAL)
     qkv_in = pack_request_inputs(geo, q[:, mine], kn[:, mine], vn[:, mine]).to(dev)
-    if os.environ.get("LAM_TEST_TRANSPORT", "nccl") == "peer":
+    if peer:
         # zero-copy: owners pull whole requests from the senders and store outputs back
         from paper_2405_01814_b200.dist import PeerRequestShardedAttention
 
@@ -84,8 +89,14 @@ def main_request():
                                  page_table=cache.page_table[sl], max_len=max_len, out=qd)
             return a
 
+        def step_args():
+            qd = torch.empty((len(rows), hq, D), dtype=torch.bfloat16, device=dev)
+            a, _ = dec.make_args(qd, cache.k[0], cache.v[0], cache.seq_lens,
+                                 page_table=cache.page_table, max_len=max_len, out=qd)
+            return a, L, cache.k[0].numel() // D
+
         eng = PeerRequestShardedAttention(geo, dist, _lib.context(dev.index), launch_args, dev,
-                                          torch.bfloat16)
+                                          torch.bfloat16, sync=req_sync, step_args=step_args)
         eng.qkv_in.copy_(qkv_in)
         eng.out.zero_()
         torch.cuda.synchronize()

@@ -32,9 +32,9 @@ def test_sharded_engine_matches_oracle(built, nproc, transport, fused, host, syn
     assert r.stdout.count("OK") == nproc
 
 
-@pytest.mark.parametrize("transport", ["nccl", "peer"])
+@pytest.mark.parametrize("transport,sync", [("nccl", "-"), ("peer", "kernel"), ("peer", "step")])
 @pytest.mark.parametrize("nproc", [2, 4])
-def test_request_sharded_engine_matches_oracle(built, nproc, transport):
+def test_request_sharded_engine_matches_oracle(built, nproc, transport, sync):
     """request_partition-based pool (KV heads not divisible by N), real kernels, over NCCL or
     the zero-copy peer transport (row map, lam_peer_io.row_src)."""
     if torch.cuda.device_count() < nproc:
@@ -44,6 +44,6 @@ def test_request_sharded_engine_matches_oracle(built, nproc, transport):
            str(ROOT / "tests" / "dist_gpu_worker.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT,
                        env=dict(os.environ, PYTHONPATH=str(ROOT), LAM_TEST_SHARD="request",
-                                LAM_TEST_TRANSPORT=transport))
+                                LAM_TEST_TRANSPORT=transport, LAM_TEST_SYNC=sync))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count("OK") == nproc
