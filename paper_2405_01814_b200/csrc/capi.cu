@@ -340,9 +340,11 @@ int plan_decode(lam_ctx* ctx, const lam_decode_args* a, Plan* pl) {
 struct HostStage {
   lam_ctx* ctx = nullptr;
   cudaStream_t stream = nullptr;
+  int32_t* err = nullptr;  // pinned: the instance kernels' error word, read after the sync
   std::vector<void*> bufs;
   std::vector<int64_t> caps;
   ~HostStage() {
+    if (err) cudaFreeHost(err);
     for (void* p : bufs)
       if (p) cudaFree(p);
     if (stream) cudaStreamDestroy(stream);
@@ -355,6 +357,7 @@ struct HostStage {
     int rc = lam_ctx_create(dev, &ctx);
     if (rc != LAM_OK) return rc;
     LAM_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    LAM_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&err), sizeof(int32_t), cudaHostAllocDefault));
     return LAM_OK;
   }
   // buffer slot i with at least `bytes`
@@ -406,11 +409,15 @@ int check_err_word(lam_ctx* ctx, cudaStream_t stream, const char* empty_msg) {
   return LAM_OK;
 }
 
+// host_total >= 0: the caller knows the logit count (the host-buffer entry points sum the
+// lengths on the host), so the scan's result is not read back; err_out != null: the error word
+// is copied there asynchronously and the caller checks it after its own synchronisation.
+// Together they leave one host synchronisation per host-buffer call instead of three.
 int run_instances(lam_ctx* ctx, int dtype, int64_t n_inst, int32_t d, const void* q,
                   const void* k, const void* v, const int64_t* kv_row0, const int64_t* kv_len,
                   const int64_t* idx, const int64_t* idx_off, const void* scale, void* acc,
                   void* max_logit, void* log_denom, int64_t* count, int exact,
-                  cudaStream_t stream) {
+                  cudaStream_t stream, int64_t host_total = -1, int32_t* err_out = nullptr) {
   if (!ctx) return fail(LAM_ERR_VALIDATION, "null context");
   if (dtype != LAM_F32 && dtype != LAM_F64)
     return fail(LAM_ERR_VALIDATION, "instance API supports f32 and f64");
@@ -420,10 +427,12 @@ int run_instances(lam_ctx* ctx, int dtype, int64_t n_inst, int32_t d, const void
   LAM_DEVICE(ctx);
   LAM_CUDA(grow(&ctx->offs, &ctx->offs_cap, n_inst + 1, false));
   LAM_CUDA(lam::launch_count_scan(n_inst, kv_len, exact ? nullptr : idx_off, ctx->offs, stream));
-  int64_t total = 0;
-  LAM_CUDA(cudaMemcpyAsync(&total, ctx->offs + n_inst, sizeof(total), cudaMemcpyDeviceToHost,
-                           stream));
-  LAM_CUDA(cudaStreamSynchronize(stream));
+  int64_t total = host_total;
+  if (total < 0) {
+    LAM_CUDA(cudaMemcpyAsync(&total, ctx->offs + n_inst, sizeof(total), cudaMemcpyDeviceToHost,
+                             stream));
+    LAM_CUDA(cudaStreamSynchronize(stream));
+  }
   const int64_t need = std::max<int64_t>(total, 1) * elem_bytes(dtype);
   if (ctx->scratch_cap < need) {
     if (ctx->scratch) cudaFree(ctx->scratch);
@@ -436,7 +445,18 @@ int run_instances(lam_ctx* ctx, int dtype, int64_t n_inst, int32_t d, const void
   LAM_CUDA(lam::launch_instances(dtype, n_inst, d, q, k, v, kv_row0, kv_len, exact ? nullptr : idx,
                                  exact ? nullptr : idx_off, scale, ctx->scratch, ctx->offs, acc,
                                  max_logit, log_denom, count, exact, ctx->err, stream));
+  if (err_out != nullptr) {
+    LAM_CUDA(cudaMemcpyAsync(err_out, ctx->err, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+    return LAM_OK;
+  }
   return check_err_word(ctx, stream, "exact_attention requires a non-empty key set");
+}
+
+// The deferred error word of run_instances(err_out), after the caller's synchronisation.
+int deferred_err(int32_t h) {
+  if (h == 2) return fail(LAM_ERR_ERROR, "token index out of range");
+  if (h == 1) return fail(LAM_ERR_ERROR, "exact_attention requires a non-empty key set");
+  return LAM_OK;
 }
 
 }  // namespace
@@ -646,13 +666,16 @@ int lam_exact_attention_host(int dtype, int64_t n_inst, int32_t d, const void* q
                  {nullptr, n_inst * d * e}},
                 dv);
   if (rc != LAM_OK) return rc;
-  rc = lam_exact_attention(host_stage().ctx, dtype, n_inst, d, dv[0], dv[1], dv[2],
-                           static_cast<int64_t*>(dv[3]), static_cast<int64_t*>(dv[4]), dv[5], dv[6],
-                           host_stage().stream);
+  int64_t total = 0;  // logits the kernel stores (the host knows the lengths)
+  for (int64_t i = 0; i < n_inst && total >= 0; ++i) total = kv_len[i] < 0 ? -1 : total + kv_len[i];
+  HostStage& hs = host_stage();
+  rc = run_instances(hs.ctx, dtype, n_inst, d, dv[0], dv[1], dv[2], static_cast<int64_t*>(dv[3]),
+                     static_cast<int64_t*>(dv[4]), nullptr, nullptr, dv[5], dv[6], nullptr,
+                     nullptr, nullptr, 1, hs.stream, total, hs.err);
   if (rc != LAM_OK) return rc;
-  LAM_CUDA(cudaMemcpyAsync(out, dv[6], n_inst * d * e, cudaMemcpyDeviceToHost, host_stage().stream));
-  LAM_CUDA(cudaStreamSynchronize(host_stage().stream));
-  return LAM_OK;
+  LAM_CUDA(cudaMemcpyAsync(out, dv[6], n_inst * d * e, cudaMemcpyDeviceToHost, hs.stream));
+  LAM_CUDA(cudaStreamSynchronize(hs.stream));
+  return deferred_err(*hs.err);
 }
 
 int lam_partial_attention_host(int dtype, int64_t n_inst, int32_t d, const void* q,
@@ -683,18 +706,22 @@ int lam_partial_attention_host(int dtype, int64_t n_inst, int32_t d, const void*
                  {nullptr, n_inst * 8}},
                 dv);
   if (rc != LAM_OK) return rc;
-  rc = lam_partial_attention(host_stage().ctx, dtype, n_inst, d, dv[0], dv[1], dv[2],
-                             static_cast<int64_t*>(dv[3]), static_cast<int64_t*>(dv[4]),
-                             static_cast<int64_t*>(dv[5]), static_cast<int64_t*>(dv[6]), dv[7],
-                             dv[8], dv[9], dv[10], static_cast<int64_t*>(dv[11]), host_stage().stream);
+  int64_t total = 0;  // index entries: the logits the kernel stores
+  for (int64_t i = 0; i < n_inst && total >= 0; ++i)
+    total = idx_off[i + 1] < idx_off[i] ? -1 : total + (idx_off[i + 1] - idx_off[i]);
+  HostStage& hs = host_stage();
+  rc = run_instances(hs.ctx, dtype, n_inst, d, dv[0], dv[1], dv[2], static_cast<int64_t*>(dv[3]),
+                     static_cast<int64_t*>(dv[4]), static_cast<int64_t*>(dv[5]),
+                     static_cast<int64_t*>(dv[6]), dv[7], dv[8], dv[9], dv[10],
+                     static_cast<int64_t*>(dv[11]), 0, hs.stream, total, hs.err);
   if (rc != LAM_OK) return rc;
-  auto s = host_stage().stream;
+  auto s = hs.stream;
   LAM_CUDA(cudaMemcpyAsync(acc, dv[8], n_inst * d * e, cudaMemcpyDeviceToHost, s));
   LAM_CUDA(cudaMemcpyAsync(max_logit, dv[9], n_inst * e, cudaMemcpyDeviceToHost, s));
   LAM_CUDA(cudaMemcpyAsync(log_denom, dv[10], n_inst * e, cudaMemcpyDeviceToHost, s));
   LAM_CUDA(cudaMemcpyAsync(token_count, dv[11], n_inst * 8, cudaMemcpyDeviceToHost, s));
   LAM_CUDA(cudaStreamSynchronize(s));
-  return LAM_OK;
+  return deferred_err(*hs.err);
 }
 
 int lam_merge_host(int dtype, int64_t n, int32_t d, const void* a_acc, const void* a_max,
