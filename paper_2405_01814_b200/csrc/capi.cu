@@ -1429,6 +1429,8 @@ int lam_decode_step_from_host(lam_ctx* ctx, const lam_decode_args* a, const lam_
   io.n_wait = io.n_done = 1;
   io.wait_flags[0] = in_flag;
   io.done_flags[0] = out_flag;
+  // (a one-layer step is an ordinary launch: it waits for and publishes these values)
+  io.wait_value = io.done_value = epoch + 1;
   lam_step_layout st = *step;
   st.n_mb = 1;
   st.rows_per_mb = a->batch;

@@ -157,13 +157,15 @@ def test_step_launch_peer_sequence_numbers(built, kernel, mode):
     assert torch.equal(cache.k, k_want) and torch.equal(cache.v, v_want)
 
 
-def test_step_from_host_matches_device_step(built):
+@pytest.mark.parametrize("L", [1, 4])
+def test_step_from_host_matches_device_step(built, L):
     """lam_decode_step_from_host (host buffers in and out, per-layer sequence numbers between the
     copy stream and the step launch), called twice so the sequence numbers carry across calls,
-    equals the device-resident step launch bitwise — outputs and appended pools."""
+    equals the device-resident step launch bitwise — outputs and appended pools.  L = 1 is an
+    ordinary launch that waits for, and publishes, the same sequence numbers."""
     from paper_2405_01814_b200 import _lib, decode as dec
 
-    L, rows, Hq, Hkv, D = 4, 6, 16, 2, 128
+    rows, Hq, Hkv, D = 6, 16, 2, 128
     cache, lens, x, order = _problem(L, 1, rows, Hq, Hkv, seed=9)
     k0, v0 = cache.k.clone(), cache.v.clone()
     want = dec.decode_step(x[:, :, :Hq], cache.k, cache.v, cache.seq_lens, page_table=cache.page_table,
