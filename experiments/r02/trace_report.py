@@ -52,7 +52,7 @@ for f in sorted(glob.glob(f"{d}/rank*.npy"))[:1]:
           f"input waits per CTA: mean {w.mean():.0f} us ({100 * w.mean() / span:.1f}% of span); "
           f"claim-to-claim median {np.median(durs):.1f} us, p10 {np.percentile(durs, 10):.1f}, p90 {np.percentile(durs, 90):.1f}")
     # the waits by launch lm (sum over CTAs, us) for a few layers in the middle
-    lm_of = lambda i: i // items_per_lm  # noqa: E731
+    lm_of = lambda i: min(int(i) // items_per_lm, n_lm - 1)  # noqa: E731  (approximate with splits)
     per_lm = np.zeros(n_lm)
     for c in range(ctas):
         r = recs[c][valid[c]]
