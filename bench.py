@@ -871,11 +871,17 @@ def run_e2e(args, W, engine, dist, device, stream, use_step=False):
     t1.record(stream)
     torch.cuda.synchronize(device)
     ms = t0.elapsed_time(t1) / max(args.steps, 1)
+    # the library takes the zero-copy path for a one-layer step (LAM_HOST_ZERO_COPY overrides)
+    zc = os.environ.get("LAM_HOST_ZERO_COPY", "-1")
+    zero_copy = zc == "1" or (zc not in ("0", "1") and L == 1)
     h2d = (h_q.numel() + h_kn.numel() + h_vn.numel()) * h_q.element_size()
     d2h = h_out.numel() * h_out.element_size()
     return {"value": W.step_bytes / (ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "api": "lam_decode_layers_host (C-ABI, pinned host buffers, copies overlapped)"}
+            "api": ("lam_decode_layers_host (C-ABI, pinned host buffers, zero-copy: the launch reads "
+                    "q / k_new / v_new from and stores the outputs into the mapped host buffers "
+                    "over PCIe)" if zero_copy else
+                    "lam_decode_layers_host (C-ABI, pinned host buffers, copies overlapped)")}
 
 
 def run_e2e_step(args, W, device, stream, h_q, h_kn, h_vn, h_out, d_q, d_out):
@@ -921,6 +927,9 @@ def run_e2e_step(args, W, device, stream, h_q, h_kn, h_vn, h_out, d_q, d_out):
     t1.record(stream)
     torch.cuda.synchronize(device)
     ms = t0.elapsed_time(t1) / max(args.steps, 1)
+    # the library takes the zero-copy path for a one-layer step (LAM_HOST_ZERO_COPY overrides)
+    zc = os.environ.get("LAM_HOST_ZERO_COPY", "-1")
+    zero_copy = zc == "1" or (zc not in ("0", "1") and L == 1)
     h2d = (h_q.numel() + h_kn.numel() + h_vn.numel()) * h_q.element_size()
     d2h = h_out.numel() * h_out.element_size()
     return {"value": W.step_bytes / (ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": ms,

@@ -1379,6 +1379,62 @@ int decode_layers_host_flags(lam_ctx* ctx, const lam_decode_args* layer_args, in
   cudaEventDestroy(done);
   return LAM_OK;
 }
+// lam_decode_layers_host with zero-copy I/O: every layer is one lam_decode_peer launch whose
+// single "source" is the caller's pinned host memory (mapped into the device address space).
+// The producer warps load each item's q and new K / V rows from host memory over PCIe with the
+// same TMA copies that read peer memory over NVLink, hidden under the item's KV streaming, and
+// the epilogue stores the outputs straight into h_out.  No staging copies, no copy-stream
+// events: one launch per layer on `stream`.
+bool host_mapped(const void* ptr) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost && at.devicePointer == ptr;
+}
+
+int decode_layers_host_mapped(lam_ctx* ctx, const lam_decode_args* layer_args, int32_t n_layers,
+                              const void* const* h_q, const void* const* h_k_new,
+                              const void* const* h_v_new, void* const* h_out, cudaStream_t cs) {
+  for (int l = 0; l < n_layers; ++l) {
+    lam_decode_args a = layer_args[l];
+    const int e = elem_bytes(a.kv_dtype);
+    const auto* q = static_cast<const uint8_t*>(h_q[l]);
+    a.q_batch_stride = 0;     // dense [B][Hq][D] host rows
+    a.new_batch_stride = 0;   // dense [B][Hkv][D]
+    a.overlap_prev = 0;
+    lam_peer_io io{};
+    io.n_src = 1;
+    io.rows_per_src = a.batch;
+    io.q_src[0] = h_q[l];
+    io.out_dst[0] = h_out[l];
+    io.k_new_offset = (static_cast<const uint8_t*>(h_k_new[l]) - q) / e;
+    io.v_new_offset = (static_cast<const uint8_t*>(h_v_new[l]) - q) / e;
+    const int rc = lam_decode_peer(ctx, &a, &io, cs);
+    if (rc != LAM_OK) return rc;
+  }
+  return LAM_OK;
+}
+
+// zero-copy applies when every host buffer is pinned, mapped and 16-byte aligned relative to q
+bool host_mapped_ok(const lam_decode_args* layer_args, int32_t n_layers, const void* const* h_q,
+                    const void* const* h_k_new, const void* const* h_v_new, void* const* h_out) {
+  for (int l = 0; l < n_layers; ++l) {
+    if (layer_args[l].lse != nullptr || layer_args[l].batch < 1) return false;
+    const auto q = reinterpret_cast<uintptr_t>(h_q[l]);
+    const uintptr_t ptrs[3] = {reinterpret_cast<uintptr_t>(h_k_new[l]),
+                               reinterpret_cast<uintptr_t>(h_v_new[l]),
+                               reinterpret_cast<uintptr_t>(h_out[l])};
+    if (q % 16 != 0) return false;
+    for (uintptr_t p : ptrs)
+      if (p % 16 != 0) return false;
+    if (!host_mapped(h_q[l]) || !host_mapped(h_k_new[l]) || !host_mapped(h_v_new[l]) ||
+        !host_mapped(h_out[l]))
+      return false;
+  }
+  return true;
+}
 }  // namespace
 
 int64_t lam_decode_step_from_host_stage_bytes(const lam_decode_args* a, int32_t n_layers) {
@@ -1487,6 +1543,13 @@ int lam_decode_layers_host(lam_ctx* ctx, const lam_decode_args* layer_args, int3
       return fail(LAM_ERR_VALIDATION, "layer " + std::to_string(l) +
                                           ": q / k_new / v_new / out larger than layer 0's staging");
   }
+  // Zero-copy I/O (decode_layers_host_mapped) for a one-layer step — there the staged path's
+  // H2D -> decode -> D2H chain is serial, nothing hides it — and wherever LAM_HOST_ZERO_COPY=1;
+  // LAM_HOST_ZERO_COPY=0 always stages.
+  const int zc = env_int("LAM_HOST_ZERO_COPY", -1);
+  if ((zc == 1 || (zc < 0 && n_layers == 1)) &&
+      host_mapped_ok(layer_args, n_layers, h_q, h_k_new, h_v_new, h_out))
+    return decode_layers_host_mapped(ctx, layer_args, n_layers, h_q, h_k_new, h_v_new, h_out, cs);
   auto base = [&](int set) { return static_cast<uint8_t*>(d_stage) + set * L.set; };
   // LAM_HOST_FLAGS=1: launches synchronised by sequence numbers instead of events.  Measured
   // equal for C2 / C3 and slower for one-layer C1 (experiments/r01/call63.sh), so events stay default.

@@ -258,18 +258,20 @@ def test_packed_qkv_strides(built, G):
     assert torch.equal(a, b)
 
 
-@pytest.mark.parametrize("flags", ["0", "1"])
+@pytest.mark.parametrize("mode", ["events", "flags", "zero_copy"])
 @pytest.mark.parametrize("L", [1, 3, 6])
-def test_decode_layers_host_matches_device_path(built, monkeypatch, L, flags):
-    """lam_decode_layers_host (host buffers, overlapped copies, launches synchronised by
-    sequence numbers) == append + decode per layer; called twice, so the sequence numbers
+def test_decode_layers_host_matches_device_path(built, monkeypatch, L, mode):
+    """lam_decode_layers_host (host buffers: staged copies synchronised by events or by sequence
+    numbers, or zero-copy launches that read q / new rows from and store outputs into the
+    pinned host buffers) == append + decode per layer; called twice, so the sequence numbers
     carry across calls."""
     import ctypes as C
 
     from paper_2405_01814_b200 import _lib
     from paper_2405_01814_b200 import decode as dec
 
-    monkeypatch.setenv("LAM_HOST_FLAGS", flags)  # events (0) or sequence numbers (1)
+    monkeypatch.setenv("LAM_HOST_FLAGS", "1" if mode == "flags" else "0")
+    monkeypatch.setenv("LAM_HOST_ZERO_COPY", "1" if mode == "zero_copy" else "0")
     B, Hq, Hkv, D, P = 4, 16, 2, 128, 64
     lens = [130, 64, 300, 1]
     pt, npages = page_table_for(lens, P, seed=2)
