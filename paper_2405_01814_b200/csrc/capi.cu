@@ -306,6 +306,11 @@ int plan_decode(lam_ctx* ctx, const lam_decode_args* a, Plan* pl) {
     pl->GQ = G % 4 == 0 ? 4 : (G % 2 == 0 ? 2 : 1);
     pl->QG = G / pl->GQ;
     pl->variant = (a->head_dim == 128 && pl->GQ == 1) ? simt_variant() : 0;
+    // fp32 MHA: 64-token tiles and two 16-byte vectors per lane and row (variant 7) — C1 0.874
+    // vs 0.860 of the copy peak, same box (experiments/r02/call84.sh); needs 64-token pages
+    if (pl->variant == 0 && kvd == LAM_F32 && a->head_dim == 128 && pl->GQ == 1 &&
+        (!paged || a->page_size % 64 == 0))
+      pl->variant = 7;
     pl->tile = lam::simt_variant_tile(kvd, a->head_dim, pl->GQ, pl->variant);
     if (pl->tile == 0) return fail(LAM_ERR_VALIDATION, "unsupported SIMT decode shape");
     if (paged && a->page_size % pl->tile != 0)
@@ -1099,7 +1104,8 @@ int decode_impl(lam_ctx* ctx, const lam_decode_args* a_in, const lam_peer_io* io
   }
   // the slot's next launch starts where this one ends (every CTA claims until one claim past
   // the last item, and counts itself out once)
-  ctx->item_base[slot] += static_cast<uint64_t>(p.n_items) + pl.ctas;
+  // (producer_loop: the first min(grid, n_items) items are assigned without a claim)
+  ctx->item_base[slot] += static_cast<uint64_t>(std::max<int64_t>(p.n_items, pl.ctas));
   ctx->done_base[slot] += static_cast<uint64_t>(pl.ctas);
   ++ctx->seq;
   return LAM_OK;

@@ -46,23 +46,23 @@ cudaError_t launch_k(K kernel, const DecodeParams& p, int ctas, int threads, int
   return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
-template <typename T, int D, int GQ, int NW, int TILE, int STAGES>
+template <typename T, int D, int GQ, int NW, int TILE, int STAGES, int NV = 1>
 cudaError_t simt_launch(const DecodeParams& p, int ctas, cudaStream_t stream) {
-  using C = SimtCfg<T, D, GQ, NW, TILE, STAGES>;
+  using C = SimtCfg<T, D, GQ, NW, TILE, STAGES, NV>;
   static std::atomic<uint64_t> done{0};
-  auto* k = decode_simt_kernel<T, D, GQ, NW, TILE, STAGES>;
+  auto* k = decode_simt_kernel<T, D, GQ, NW, TILE, STAGES, NV>;
   cudaError_t e = ensure_smem_attr(k, C::SMEM_BYTES, done);
   if (e != cudaSuccess) return e;
   return launch_k(k, p, ctas, C::THREADS, C::SMEM_BYTES, stream, p);
 }
 
-template <typename T, int D, int GQ, int NW, int TILE, int STAGES>
+template <typename T, int D, int GQ, int NW, int TILE, int STAGES, int NV = 1>
 int simt_occ() {
-  using C = SimtCfg<T, D, GQ, NW, TILE, STAGES>;
+  using C = SimtCfg<T, D, GQ, NW, TILE, STAGES, NV>;
   static std::atomic<uint64_t> done{0};
   static std::atomic<int> cached{0};  // queried once per process (one device model)
   if (const int c = cached.load(std::memory_order_relaxed); c > 0) return c;
-  auto* k = decode_simt_kernel<T, D, GQ, NW, TILE, STAGES>;
+  auto* k = decode_simt_kernel<T, D, GQ, NW, TILE, STAGES, NV>;
   if (ensure_smem_attr(k, C::SMEM_BYTES, done) != cudaSuccess) return 0;
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, C::THREADS, C::SMEM_BYTES) !=
@@ -172,24 +172,27 @@ int mma_occ(int variant) {
   return 0;
 }
 
-// SIMT variants (consumer warps, tokens per stage for 32-bit / 16-bit KV, stages).  Variant 0
-// is the default for every (dtype, D, GQ); the others exist for D = 128, GQ = 1 (tuning).
+// SIMT variants (consumer warps, tokens per stage for 32-bit / 16-bit KV, stages, 16-byte
+// vectors per lane and row).  Variant 0 is the default for every (dtype, D, GQ); the others
+// exist for D = 128, GQ = 1 (tuning).
 #define LAM_SIMT_VARIANTS(X) \
-  X(1, 8, 32, 64, 6) X(2, 8, 32, 64, 3) X(3, 4, 32, 32, 4) X(4, 16, 32, 64, 4)
+  X(1, 8, 32, 64, 6, 1) X(2, 8, 32, 64, 3, 1) X(3, 4, 32, 32, 4, 1) X(4, 16, 32, 64, 4, 1) \
+  X(5, 16, 64, 64, 3, 1) X(6, 8, 64, 64, 3, 1) X(7, 16, 64, 64, 3, 2) X(8, 8, 64, 64, 3, 2) \
+  X(9, 16, 64, 128, 3, 4)
 
 struct SimtLaunchF {
   const DecodeParams& p;
   int ctas;
   cudaStream_t s;
-  template <typename T, int DD, int GG, int NW, int TILE, int ST>
-  cudaError_t operator()() const { return simt_launch<T, DD, GG, NW, TILE, ST>(p, ctas, s); }
+  template <typename T, int DD, int GG, int NW, int TILE, int ST, int NV = 1>
+  cudaError_t operator()() const { return simt_launch<T, DD, GG, NW, TILE, ST, NV>(p, ctas, s); }
 };
 struct SimtOccF {
-  template <typename T, int DD, int GG, int NW, int TILE, int ST>
-  int operator()() const { return simt_occ<T, DD, GG, NW, TILE, ST>(); }
+  template <typename T, int DD, int GG, int NW, int TILE, int ST, int NV = 1>
+  int operator()() const { return simt_occ<T, DD, GG, NW, TILE, ST, NV>(); }
 };
 struct SimtTileF {
-  template <typename T, int DD, int GG, int NW, int TILE, int ST>
+  template <typename T, int DD, int GG, int NW, int TILE, int ST, int NV = 1>
   int operator()() const { return TILE; }
 };
 
@@ -199,8 +202,8 @@ auto simt_variant(int variant, F f) {
   // default: 16 consumer warps (measured best on B200 for MHA), 8 when GQ = 4 (smem)
   if (variant == 0) return f.template operator()<T, D, GQ, GQ <= 2 ? 16 : 8, wide ? 32 : 64, 6>();
   if constexpr (D == 128 && GQ == 1) {
-#define X(id, nw, t32, t16, st) \
-    if (variant == id) return f.template operator()<T, D, GQ, nw, wide ? t32 : t16, st>();
+#define X(id, nw, t32, t16, st, nv) \
+    if (variant == id) return f.template operator()<T, D, GQ, nw, wide ? t32 : t16, st, nv>();
     LAM_SIMT_VARIANTS(X)
 #undef X
   }

@@ -41,7 +41,7 @@ struct DecodeParams {
   int32_t* counters;        // [B*Hkv*QG] split arrival counters (self-resetting)
   // Launch slot (one of a small ring, so overlapping launches never share state): slot[0]
   // counts item claims, slot[1] finished epilogues, both monotonic.  This launch owns claims
-  // [item_base, item_base + n_items + grid) and arrivals [done_base, done_base + grid); it
+  // [item_base, item_base + max(n_items, grid)) and arrivals [done_base, done_base + grid); it
   // starts only once the slot's previous launch has fully finished (slot[1] >= done_base).
   unsigned long long* slot;
   unsigned long long item_base, done_base;
@@ -433,9 +433,18 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
   int n_rec = 0;
   // (Claiming the next item ahead, ~512 tokens before the boundary, at once or one dependent
   // access per issued tile, measured 3-4% slower on B200: round 2, calls 50 and 53.)
+  // The first min(grid, n_items) items go to CTAs 0, 1, ... without a claim (one global round
+  // trip less before a launch's first loads); the counter hands out the rest, offset by them.
+  // Claims on the counter per launch: max(n_items, grid) (capi.cu's item_base accounting).
+  const int n_static = min(static_cast<int>(gridDim.x), p.n_items);
+  bool first_claim = true;
   for (;;) {
     const unsigned long long t_claim = rec != nullptr ? globaltimer_ns() : 0ull;
-    const long long claim = static_cast<long long>(atomicAdd(p.slot, 1ull) - p.item_base);
+    const long long claim =
+        first_claim && static_cast<int>(blockIdx.x) < n_static
+            ? static_cast<long long>(blockIdx.x)
+            : static_cast<long long>(atomicAdd(p.slot, 1ull) - p.item_base) + n_static;
+    first_claim = false;
     if (claim >= p.n_items) break;
     const Item it = make_item(p, static_cast<int>(claim), TILE);
     const int idx = static_cast<int>(claim);

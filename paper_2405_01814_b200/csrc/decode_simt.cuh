@@ -23,13 +23,15 @@
 namespace lam {
 
 template <typename T, int D, int GQ, int NW_ = 8, int TILE_ = (sizeof(T) == 4 ? 32 : 64),
-          int STAGES_ = 6>
+          int STAGES_ = 6, int NV_ = 1>
 struct SimtCfg {
   static constexpr int NW = NW_;                     // consumer warps
   static constexpr int TILE = TILE_;                 // tokens per stage
   static constexpr int STAGES = STAGES_;
   static constexpr int VEC = 16 / sizeof(T);         // elements per 16-byte vector
-  static constexpr int LPR = D / VEC;                // lanes per K/V row
+  static constexpr int NV = NV_;                     // 16-byte vectors per lane and row
+  static constexpr int EPL = VEC * NV;               // elements per lane and row
+  static constexpr int LPR = D / EPL;                // lanes per K/V row
   static constexpr int RPI = 32 / LPR;               // rows per warp instruction
   static constexpr int TPW = TILE / NW;              // tokens per warp per tile
   static constexpr int ITER = TPW / RPI;
@@ -47,11 +49,12 @@ struct SimtCfg {
   static_assert(TPW % RPI == 0 && ITER >= 1, "warp slice must be whole instructions");
 };
 
-template <typename T, int D, int GQ, int NW, int TILE, int STAGES>
+template <typename T, int D, int GQ, int NW, int TILE, int STAGES, int NV = 1>
 __global__ void __launch_bounds__((NW + 2) * 32, 1)
     decode_simt_kernel(const DecodeParams p) {
-  using C = SimtCfg<T, D, GQ, NW, TILE, STAGES>;
+  using C = SimtCfg<T, D, GQ, NW, TILE, STAGES, NV>;
   constexpr int VEC = C::VEC, LPR = C::LPR, RPI = C::RPI, TPW = C::TPW, ITER = C::ITER;
+  constexpr int EPL = C::EPL;
   extern __shared__ __align__(128) uint8_t smem[];
   T* ring = reinterpret_cast<T*>(smem);  // [STAGES][2][TILE][D]
   uint8_t* qslot = smem + C::RING_BYTES;  // [STAGES][q rows GQ | new k | new v][D]
@@ -117,13 +120,18 @@ __global__ void __launch_bounds__((NW + 2) * 32, 1)
   }
 
   // ---------------- consumers ----------------
-  const int sub = lane % LPR;  // which 16-byte vector of the row
+  // Lane `sub` of a row group owns the NV 16-byte vectors sub, sub + LPR, ... of each K / V row
+  // (element offsets voff(v)): a quarter-warp phase of 16-byte shared loads reads 128
+  // contiguous bytes of one row (no bank conflicts), and NV > 1 shortens the q·k shuffle
+  // reduction to log2(LPR) steps per RPI rows.
+  const int sub = lane % LPR;  // first 16-byte vector of the row owned by this lane
   const int rg = lane / LPR;   // row group within one instruction
   const float sc = C::kLog2 ? p.scale_log2 : p.scale;
   const uint32_t ring_addr = smem_u32(ring);
   const uint32_t q_addr = smem_u32(qslot);
 
-  float q[GQ][VEC], m[GQ], l[GQ], acc[GQ][VEC];
+  auto voff = [&](int v) { return (v * LPR + sub) * VEC; };  // element offset of vector v
+  float q[GQ][EPL], m[GQ], l[GQ], acc[GQ][EPL];
   Item it{};
   int k_item = 0;  // hand-offs to the epilogue warp
   for (int i = 0;; ++i) {
@@ -140,12 +148,19 @@ __global__ void __launch_bounds__((NW + 2) * 32, 1)
       it = item_from_tag<TILE>(p, mt);
 #pragma unroll
       for (int g = 0; g < GQ; ++g) {
-        if (it.ntiles > 0)
-          Elem<T>::unpack(lds128(q_addr + s * C::SLOT_BYTES + (g * D + sub * VEC) * sizeof(T)), q[g]);
+        if (it.ntiles > 0) {
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            float f[VEC];
+            Elem<T>::unpack(lds128(q_addr + s * C::SLOT_BYTES + (g * D + voff(v)) * sizeof(T)), f);
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) q[g][v * VEC + e] = f[e];
+          }
+        }
         m[g] = -INFINITY;
         l[g] = 0.f;
 #pragma unroll
-        for (int e = 0; e < VEC; ++e) acc[g][e] = 0.f;
+        for (int e = 0; e < EPL; ++e) acc[g][e] = 0.f;
       }
     }
     if (it.ntiles > 0 && !(p.flags & 16)) {  // (flags bit 4: streaming-only diagnostic)
@@ -154,7 +169,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, 1)
       const uint32_t v_addr = k_addr + C::TILE_BYTES;
       // fused append: the request's new token is read from the slot, not from the pool
       const int new_r = tile_has_new<TILE>(p, it, mt.y) ? it.len - 1 - tile_tok : -1;
-      const uint32_t kn_addr = q_addr + s * C::SLOT_BYTES + C::Q_BYTES + sub * VEC * sizeof(T);
+      const uint32_t kn_addr = q_addr + s * C::SLOT_BYTES + C::Q_BYTES;
 
       // q·k for this warp's TPW tokens.
       float logit[ITER][GQ];
@@ -163,20 +178,27 @@ __global__ void __launch_bounds__((NW + 2) * 32, 1)
       for (int r8 = 0; r8 < ITER; ++r8) {
         const int r = warp * TPW + r8 * RPI + rg;  // row within the tile
         valid[r8] = tile_tok + r < it.t_end;
-        float kf[VEC];
-        const uint4 kraw = lds128(r == new_r ? kn_addr : k_addr + (r * D + sub * VEC) * sizeof(T));
-        if (r == new_r) {  // write the new token into the pool for later steps
-          const uint4 vraw = lds128(kn_addr + C::ROW_BYTES);
-          const int64_t dst = (meta_row[s] + r) * D + sub * VEC;
-          *reinterpret_cast<uint4*>(static_cast<T*>(p.k_pool_w) + dst) = kraw;
-          *reinterpret_cast<uint4*>(static_cast<T*>(p.v_pool_w) + dst) = vraw;
+        float kf[EPL];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const uint32_t vb = voff(v) * sizeof(T);
+          const uint4 kraw = lds128(r == new_r ? kn_addr + vb : k_addr + r * D * sizeof(T) + vb);
+          if (r == new_r) {  // write the new token into the pool for later steps
+            const uint4 vraw = lds128(kn_addr + C::ROW_BYTES + vb);
+            const int64_t dst = (meta_row[s] + r) * D + voff(v);
+            *reinterpret_cast<uint4*>(static_cast<T*>(p.k_pool_w) + dst) = kraw;
+            *reinterpret_cast<uint4*>(static_cast<T*>(p.v_pool_w) + dst) = vraw;
+          }
+          float f[VEC];
+          Elem<T>::unpack(kraw, f);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) kf[v * VEC + e] = f[e];
         }
-        Elem<T>::unpack(kraw, kf);
 #pragma unroll
         for (int g = 0; g < GQ; ++g) {
           float d0 = 0.f;
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) d0 = fmaf(q[g][e], kf[e], d0);
+          for (int e = 0; e < EPL; ++e) d0 = fmaf(q[g][e], kf[e], d0);
           logit[r8][g] = d0;
         }
       }
@@ -207,7 +229,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, 1)
               m[g] == -INFINITY ? 0.f : (C::kLog2 ? exp2f(m[g] - m_new) : expf(m[g] - m_new));
           l[g] *= alpha;
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) acc[g][e] *= alpha;
+          for (int e = 0; e < EPL; ++e) acc[g][e] *= alpha;
           m[g] = m_new;
         }
       }
@@ -217,15 +239,22 @@ __global__ void __launch_bounds__((NW + 2) * 32, 1)
       for (int r8 = 0; r8 < ITER; ++r8) {
         if (!valid[r8]) continue;
         const int r = warp * TPW + r8 * RPI + rg;
-        float vf[VEC];
-        Elem<T>::unpack(lds128(r == new_r ? kn_addr + C::ROW_BYTES
-                                          : v_addr + (r * D + sub * VEC) * sizeof(T)), vf);
+        float vf[EPL];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const uint32_t vb = voff(v) * sizeof(T);
+          float f[VEC];
+          Elem<T>::unpack(lds128(r == new_r ? kn_addr + C::ROW_BYTES + vb
+                                            : v_addr + r * D * sizeof(T) + vb), f);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) vf[v * VEC + e] = f[e];
+        }
 #pragma unroll
         for (int g = 0; g < GQ; ++g) {
           const float pr = C::kLog2 ? exp2f(logit[r8][g] - m[g]) : expf(logit[r8][g] - m[g]);
           l[g] += pr;
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) acc[g][e] = fmaf(pr, vf[e], acc[g][e]);
+          for (int e = 0; e < EPL; ++e) acc[g][e] = fmaf(pr, vf[e], acc[g][e]);
         }
       }
     }
@@ -241,7 +270,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, 1)
         for (int g = 0; g < GQ; ++g) {
           l[g] += __shfl_xor_sync(0xffffffffu, l[g], off);
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) acc[g][e] += __shfl_xor_sync(0xffffffffu, acc[g][e], off);
+          for (int e = 0; e < EPL; ++e) acc[g][e] += __shfl_xor_sync(0xffffffffu, acc[g][e], off);
         }
       }
       red_acquire(red, k_item);
@@ -249,8 +278,8 @@ __global__ void __launch_bounds__((NW + 2) * 32, 1)
 #pragma unroll
         for (int g = 0; g < GQ; ++g) {
 #pragma unroll
-          for (int e = 0; e < VEC; e += 4)
-            *reinterpret_cast<float4*>(red_acc + (warp * GQ + g) * D + sub * VEC + e) =
+          for (int e = 0; e < EPL; e += 4)
+            *reinterpret_cast<float4*>(red_acc + (warp * GQ + g) * D + voff(e / VEC) + e % VEC) =
                 make_float4(acc[g][e], acc[g][e + 1], acc[g][e + 2], acc[g][e + 3]);
           if (sub == 0) {
             red_m[warp * GQ + g] = m[g];
