@@ -219,8 +219,11 @@ void choose_splits(Plan& pl, int64_t units, int max_len, int max_ctas, int split
     const int64_t items = std::max<int64_t>(1, units * s_eff);
     const int64_t k = (items + max_ctas - 1) / max_ctas;
     int ctas = static_cast<int>((items + k - 1) / k);
-    // shrink only when it evens the rounds out by a margin (C3: 147 CTAs lose 0.6 % to 148)
-    if (ctas > max_ctas * 95 / 100) ctas = max_ctas;
+    // shrink only when it evens the rounds out by a margin (C3: 147 CTAs lose 0.6 % to 148);
+    // the SIMT kernel with 64-token fp32 tiles keeps the full grid (C1: 148 CTAs 0.878 vs 128
+    // CTAs 0.874 of the copy peak, experiments/r02/call84.sh)
+    if (ctas > max_ctas * 95 / 100 || (pl.kernel == LAM_KERNEL_SIMT && pl.variant == 7))
+      ctas = max_ctas;
     const double rate = std::min(BW_CHIP / ctas, RATE_SM * occ_per_sm);
     const double t = static_cast<double>(k) * (item_bytes / rate + C_ITEM);
     // more splits must win by >= 1.5 % (model noise)

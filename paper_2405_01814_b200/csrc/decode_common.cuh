@@ -406,6 +406,15 @@ template <int STAGES, int TILE, int NSUB = 1, int META = STAGES, class Issue>
 __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* full,
                                               uint64_t* empty, int4* meta, long long* meta_row,
                                               Issue issue) {
+  // The first min(grid, n_items) items go to CTAs 0, 1, ... without a claim (one global round
+  // trip less before a launch's first loads); the counter hands out the rest, offset by them.
+  // Claims on the counter per launch: max(n_items, grid) (capi.cu's item_base accounting).
+  // Without input sequence numbers the static item's bounds (seq_lens) are read while the
+  // slot is acquired: the two loads overlap.
+  const int n_static = min(static_cast<int>(gridDim.x), p.n_items);
+  const bool pre = p.n_wait == 0 && static_cast<int>(blockIdx.x) < n_static;
+  Item it_pre{};
+  if (pre) it_pre = make_item(p, static_cast<int>(blockIdx.x), TILE);
   acquire_slot(p);
   // peer transport: the inputs' sequence numbers are awaited like the preceding grid of an
   // overlap_prev launch — after the first KV tiles are in flight (p.defer_inputs = 2)
@@ -433,20 +442,16 @@ __device__ __forceinline__ void producer_loop(const DecodeParams& p, uint64_t* f
   int n_rec = 0;
   // (Claiming the next item ahead, ~512 tokens before the boundary, at once or one dependent
   // access per issued tile, measured 3-4% slower on B200: round 2, calls 50 and 53.)
-  // The first min(grid, n_items) items go to CTAs 0, 1, ... without a claim (one global round
-  // trip less before a launch's first loads); the counter hands out the rest, offset by them.
-  // Claims on the counter per launch: max(n_items, grid) (capi.cu's item_base accounting).
-  const int n_static = min(static_cast<int>(gridDim.x), p.n_items);
   bool first_claim = true;
   for (;;) {
     const unsigned long long t_claim = rec != nullptr ? globaltimer_ns() : 0ull;
+    const bool is_static = first_claim && static_cast<int>(blockIdx.x) < n_static;
     const long long claim =
-        first_claim && static_cast<int>(blockIdx.x) < n_static
-            ? static_cast<long long>(blockIdx.x)
-            : static_cast<long long>(atomicAdd(p.slot, 1ull) - p.item_base) + n_static;
+        is_static ? static_cast<long long>(blockIdx.x)
+                  : static_cast<long long>(atomicAdd(p.slot, 1ull) - p.item_base) + n_static;
     first_claim = false;
     if (claim >= p.n_items) break;
-    const Item it = make_item(p, static_cast<int>(claim), TILE);
+    const Item it = is_static && pre ? it_pre : make_item(p, static_cast<int>(claim), TILE);
     const int idx = static_cast<int>(claim);
     if (step && it.lm != waited_lm) {  // (claims arrive in launch order: lm only grows)
       wait_inputs(p, it.lm);

@@ -455,9 +455,10 @@ def test_overlap_prev_orders_inputs_after_preceding_kernel(built, kernel, dtype,
 
 @pytest.mark.parametrize("name,B,Hq,Hkv,L,dtype,paged,want", [
     # (kernel, splits, CTAs) the planner picks for the BASELINE launch shapes, measured best on
-    # B200 (profiles/r01b/SUMMARY.md §2, §7): C1 on 128 CTAs (2 even rounds), C4 split 4 ways,
-    # the 512-unit sharded GQA launch unsplit on 128 CTAs, the rest unsplit on the full grid.
-    ("c1", 8, 32, 32, 1024, torch.float32, False, ("simt", 1, 128)),
+    # B200 (profiles/r01b/SUMMARY.md §2, §7): C4 split 4 ways, the 512-unit sharded GQA launch
+    # unsplit on 128 CTAs (2 even rounds), the rest unsplit on the full grid — C1 too since its
+    # 64-token fp32 tiles (profiles/r02/final3/c1_simt_variants.txt).
+    ("c1", 8, 32, 32, 1024, torch.float32, False, ("simt", 1, 148)),
     ("c2", 64, 32, 32, 4096, torch.bfloat16, True, ("gqa_tc", 1, 148)),
     ("c3", 128, 64, 8, 4096, torch.bfloat16, True, ("gqa_tc", 1, 148)),
     ("c4", 32, 64, 8, 32768, torch.bfloat16, True, ("gqa_tc", 4, 148)),
