@@ -783,13 +783,28 @@ __device__ __forceinline__ void finish_item_warp(const DecodeParams& p, const It
         for (int e = 0; e < DPL; ++e) A[e] = fmaf(wj, v[j][e], A[e]);
       }
     } else {
+      // 9..32 splits: kBatch independent partial loads per L2 round trip, accumulated in split
+      // order (an S = 16 unit: 2 round trips per head instead of 16)
       const int n = min(32, S_live);
-      for (int j = 0; j < n; ++j) {
-        const float wj = __shfl_sync(0xffffffffu, w, j);
-        float v[DPL];
-        ldcg_vec<DPL>(p.ws_acc + (row0 + j) * D + d0, v);
+      for (int j0 = 0; j0 < n; j0 += kBatch) {
+        float v[kBatch][DPL];
 #pragma unroll
-        for (int e = 0; e < DPL; ++e) A[e] = fmaf(wj, v[e], A[e]);
+        for (int j = 0; j < kBatch; ++j) {
+          if (j0 + j < n) {
+            ldcg_vec<DPL>(p.ws_acc + (row0 + j0 + j) * D + d0, v[j]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < DPL; ++e) v[j][e] = 0.f;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {
+          const float wj = __shfl_sync(0xffffffffu, w, (j0 + j) & 31);
+          if (j0 + j < n) {
+#pragma unroll
+            for (int e = 0; e < DPL; ++e) A[e] = fmaf(wj, v[j][e], A[e]);
+          }
+        }
       }
     }
     for (int s0 = 32; s0 < S_live; s0 += 32) {  // more than 32 splits (rare)
