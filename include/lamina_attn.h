@@ -245,7 +245,11 @@ int lam_decode_step_host(lam_ctx* ctx, const lam_decode_args* args, const void* 
  * attention.  layer_args[l] describes layer l's pools (its q/out fields are ignored: the staging
  * set is used).  d_stage must hold 2 * (q + k_new + v_new + out) bytes of one layer, each part
  * 256-byte aligned (lam_decode_layers_host_stage_bytes).  Returns after enqueueing; the caller
- * synchronises `stream`. */
+ * synchronises `stream`.
+ * Zero-copy: for a one-layer call (or any call with LAM_HOST_ZERO_COPY=1) whose host buffers are
+ * all pinned, device-mapped and 16-byte aligned, each layer is a single launch that reads q /
+ * k_new / v_new straight from the host buffers and stores the output into h_out (no staging
+ * copies; d_stage and copy_stream are unused).  LAM_HOST_ZERO_COPY=0 always stages. */
 int lam_decode_layers_host(lam_ctx* ctx, const lam_decode_args* layer_args, int32_t n_layers,
                            const void* const* h_q, const void* const* h_k_new,
                            const void* const* h_v_new, void* const* h_out, void* d_stage,
