@@ -60,7 +60,8 @@ struct DecodeParams {
   float scale_log2;         // scale * log2(e)
   int32_t out_f32;
   int32_t flags;            // diagnostics: bit 4 = consumers skip the math (streaming only),
-                            // bit 5 = the epilogue warp skips its work
+                            // bit 5 = the epilogue warp skips its work, bit 6 = the last split
+                            // skips the merge (single launches only: outputs are not written)
   // fused append (optional): the new token of request b (position seq_lens[b] - 1) comes from
   // k_new/v_new (request b, kv head h at + b * new_stride + h * D); the kernel attends over it
   // from shared memory and writes it into the pools for later steps.
@@ -735,9 +736,32 @@ __device__ __forceinline__ void finish_item_warp(const DecodeParams& p, const It
   if (lane == 0) last = (atom_add_acq_rel_gpu(counter, 1) == S_live - 1);
   last = __shfl_sync(0xffffffffu, last, 0);
   if (!last) return;
+  if (p.flags & 64) {  // diagnostic: the last split skips the merge (outputs are not written)
+    if (lane == 0) *counter = 0;
+    return;
+  }
 
   // 3. last split of this unit: merge the live partials in split order and finalize.  Lane s
   //    holds split s's statistics; every live split's slice of a head is loaded before use.
+  //    In a streaming SM a dependent global load waits behind the TMA data in flight (µs), so
+  //    the loads are issued ahead: up to 4 splits, head g + 1's partials are in flight while
+  //    head g is merged, and head 0's with the statistics (2 round trips instead of 9 for 8
+  //    heads).
+  constexpr int kPre = 4;
+  float pre[2][kPre][DPL];
+  auto load_head = [&](int g, float (&v)[kPre][DPL]) {
+    const int64_t row0 = (bw * p.Hq + qh0 + g) * p.S;
+#pragma unroll
+    for (int j = 0; j < kPre; ++j) {
+      if (g < nvalid && j < S_live) {
+        ldcg_vec<DPL>(p.ws_acc + (row0 + j) * D + d0, v[j]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) v[j][e] = 0.f;
+      }
+    }
+  };
+  if (S_live <= kPre) load_head(0, pre[0]);
   float ms[GQ], ls[GQ];
 #pragma unroll
   for (int g = 0; g < GQ; ++g) {
@@ -749,6 +773,38 @@ __device__ __forceinline__ void finish_item_warp(const DecodeParams& p, const It
       ms[g] = ml.x;
       ls[g] = ml.y;
     }
+  }
+  if (S_live <= kPre) {
+#pragma unroll
+    for (int g = 0; g < GQ; ++g) {
+      if (g + 1 < GQ) load_head(g + 1, pre[(g + 1) & 1]);
+      if (g >= nvalid) continue;
+      float M = ms[g];
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+      const float w = ms[g] == -INFINITY ? 0.f : expf(ms[g] - M);  // lanes >= S_live: 0
+      float L = w * ls[g];
+      float A[DPL];
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) A[e] = 0.f;
+#pragma unroll
+      for (int j = 0; j < kPre; ++j) {  // split order, as the general path below
+        const float wj = __shfl_sync(0xffffffffu, w, j);
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) A[e] = fmaf(wj, pre[g & 1][j][e], A[e]);
+      }
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
+      const float inv = L > 0.f ? 1.f / L : 0.f;
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) A[e] *= inv;
+      store_out_vec<T, D, DPL>(p, it, qh0 + g, d0, A);
+      if (lane == 0 && p.lse != nullptr)
+        p.lse[static_cast<int64_t>(b) * p.Hq + qh0 + g] = L > 0.f ? M + logf(L) : -INFINITY;
+    }
+    if (lane == 0) *counter = 0;  // ready for the next launch
+    unit_done(p, it);
+    return;
   }
 #pragma unroll
   for (int g = 0; g < GQ; ++g) {

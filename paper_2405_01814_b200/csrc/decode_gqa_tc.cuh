@@ -22,7 +22,8 @@
 //             (Two issuers, so neither stream of MMAs ever waits behind the other's inputs.)
 //   warp 5    TMA producer (decode_common.cuh:producer_loop): 128-token tiles as two 64-row
 //             chunks (a page each at page_size 64), K and V into separate rings.
-//   warp 6    epilogue (decode_common.cuh:finish_item_warp): output, LSE or split partials.
+//   warps 6, 8  epilogue (decode_common.cuh:finish_item_warp): output, LSE or split partials
+//             and the last split's merge; one warp per hand-off buffer (even / odd items).
 //
 // S is four-buffered and O^T double-buffered in TMEM (48 of 64 allocated columns), P
 // double-buffered in shared memory.  Online softmax semantics are those of the reference's
@@ -130,12 +131,12 @@ struct TcCfg {
   // empty [2]; hand-off tags (2 x 4 ints); TMEM address
   static constexpr int N_BARS = 2 * KS + 2 * VS + 2 * NS + 16;
   static constexpr int SMEM_BYTES = OFF_BAR + N_BARS * 8 + 32 + 1024;  // + align slack
-  static constexpr int THREADS = 8 * 32;
+  static constexpr int THREADS = 9 * 32;
   static constexpr int TMEM_COLS = 64;  // S[4] and O[2], 8 columns each
 };
 
 template <typename T, int KS_, int VS_>
-__global__ void __launch_bounds__(8 * 32, 1)
+__global__ void __launch_bounds__(9 * 32, 1)
     decode_gqa_tc_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap kmap,
                          const __grid_constant__ CUtensorMap vmap) {
   using C = TcCfg<KS_, VS_>;
@@ -272,10 +273,13 @@ __global__ void __launch_bounds__(8 * 32, 1)
     }
     return;
   }
-  if (warp == 6) {  // ---------------- epilogue ----------------
+  if (warp == 6 || warp == 8) {  // ---------------- epilogue ----------------
+    // two epilogue warps, one per hand-off buffer: warp 6 finishes the even items, warp 8 the
+    // odd ones, so each has two items' time for an item's split partial and the last split's
+    // merge (L2 round trips that are slow under full HBM load) before its buffer is needed again
+    const int b = warp == 6 ? 0 : 1;
     for (int k = 0;; ++k) {
-      const int b = k & 1;
-      mbar_wait(&rfull[b], (k >> 1) & 1);
+      mbar_wait(&rfull[b], k & 1);
       const int* tg = ritem + 4 * b;
       const int idx = tg[0];
       if (idx < 0) break;
@@ -284,12 +288,17 @@ __global__ void __launch_bounds__(8 * 32, 1)
       if (lane < GQ)  // the four warps' partial sums of the softmax denominator
         red_l(b)[lane] = lw[lane] + lw[GQ + lane] + lw[2 * GQ + lane] + lw[3 * GQ + lane];
       __syncwarp();
+      if (p.flags & 32) {  // diagnostic: no epilogue work (outputs are not written)
+        if (lane == 0) mbar_arrive(&rempty[b]);
+        continue;
+      }
       finish_item_warp<T, D, GQ, 1, true, C::RS>(p, it, G, red_m(b), red_l(b), red_acc(b), [&] {
         __syncwarp();
         if (lane == 0) mbar_arrive(&rempty[b]);
       });
     }
-    finish_cta(p);
+    named_bar_sync(5, 2 * 32);  // both epilogue warps' stores precede the CTA's count
+    if (warp == 6) finish_cta(p);
     return;
   }
 
@@ -574,9 +583,9 @@ __global__ void __launch_bounds__(8 * 32, 1)
     if (lane == 0) mbar_arrive(&rfull[rb]);
     ++k_item;
   }
-  {
-    const int rb = k_item & 1;
-    if (k_item >= 2) mbar_wait(&rempty[rb], ((k_item - 2) >> 1) & 1);
+  for (int e = 0; e < 2; ++e) {  // end of work, to both epilogue warps
+    const int k = k_item + e, rb = k & 1;
+    if (k >= 2) mbar_wait(&rempty[rb], ((k - 2) >> 1) & 1);
     if (warp == 0 && lane == 0) ritem[4 * rb] = -1;
     __syncwarp();
     if (lane == 0) mbar_arrive(&rfull[rb]);
